@@ -1,0 +1,428 @@
+"""Benchmark: pair-interactions/s and s/iteration of the SPARKLING hot path.
+
+Workload (BASELINE.json configs[1], "C2"): 3D, 1024 shots x 1024 samples (p = 2^20),
+129^3 density grid (N = 64, "128^3"), exact attraction (north star), eps_rep = 1e-3,
+eps_att = 1/(2N), full3d hardware limits, pin at N_s/2, perturbed radial init
+(P = 0.25, seed 0).  One step = one optimize() iteration on the device: fused K1+K2
+N-body, gradient combine + BB dots, step + K3 projection (FISTA 100 it + polish),
+feasibility residuals, position all-gather.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's CPU path (the
+bit-exact C port in oracle/, all host threads) on bounded row samples of the same
+workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_C, N_S, GRID_N, DIMS = 1024, 1024, 64, 3
+EPS_REP = 1e-3
+FLOPS_REP_3D, FLOPS_ATT_3D = 17, 19  # per pair
+METRIC = "pair-interactions/s"
+
+
+def workload_config():
+    return {"workload": "C2: 3D SPARKLING 1024 shots x 1024 samples, 129^3 density grid "
+                        "(exact attraction + exact repulsion + projection)",
+            "n_c": N_C, "n_s": N_S, "p": N_C * N_S, "grid": [2 * GRID_N + 1] * 3,
+            "grad_mode": "exact", "eps_rep": EPS_REP, "eps_att": 1.0 / (2 * GRID_N),
+            "n_pit": 100, "hardware": "full3d.cfg limits (G 40 mT/m, S 180 T/m/s)",
+            "l2": "flushed between steps (256 MiB memset outside the per-step events)"}
+
+
+def hardware():
+    import paper_2108_02991_b200 as spk
+
+    return spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                            dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
+                            dims=3)
+
+
+def start_pattern():
+    import paper_2108_02991_b200 as spk
+
+    return spk.perturb(spk.init_radial(N_C, N_S, DIMS), 0.25, 0)
+
+
+def proj_config():
+    import paper_2108_02991_b200 as spk
+
+    lim = spk.normalized_limits(hardware())
+    pin = spk.LinearConstraint(pinned_index=N_S // 2, pinned_value=np.zeros(DIMS))
+    return spk.ProjectionConfig(alpha=lim.alpha, beta=lim.beta, raster_dt=1e-5, n_pit=100,
+                                pin=pin)
+
+
+def pairs_per_step():
+    p = N_C * N_S
+    g = (2 * GRID_N + 1) ** DIMS
+    return p, g, p * p, p * g
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- helpers
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def fp32_peak_tflops(sm_mhz):
+    # 148 SMs x 128 FP32 lanes x 2 flop (FMA) x clock
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def committed_traffic():
+    path = os.path.join(REPO, "profiles", "nbody_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference_sample(rows: int, threads: int = 0):
+    """Reference CPU path (bit-exact C port of direct_sums / the weighted attraction sum
+    / _project_all, OpenMP over all host threads) on bounded row samples of the workload.
+    Returns pairs/s and an extrapolated s/iteration."""
+    from oracle import oracle as orc
+    import paper_2108_02991_b200 as spk
+
+    pts = start_pattern().points().copy()
+    rho = spk.discretize(spk.DensityParams(0.25, 2.0), GRID_N, DIMS)
+    p, g, rep_pairs, att_pairs = pairs_per_step()
+    idx = np.linspace(0, p - 1, rows).astype(np.int64)
+    t0 = time.perf_counter()
+    orc.direct_sums_subset(pts, idx, EPS_REP * EPS_REP, threads)
+    t_rep = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.grid_sums(pts[idx], rho.grid, (1.0 / (2 * GRID_N)) ** 2, threads)
+    t_att = time.perf_counter() - t0
+    rate = (rows * p + rows * g) / (t_rep + t_att)
+    # projection: a bounded shot sample at full size, scaled to all shots
+    cfg = proj_config()
+    n_sh = 16
+    shots = start_pattern().coords[:n_sh]
+    tau = 1.0 / spk.projection.stacked_operator_norm(N_S, N_S // 2)
+    t0 = time.perf_counter()
+    orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, N_S // 2, np.zeros(3), 100,
+                    tau, 0.1 * cfg.feas_tol, nthreads=threads)
+    t_proj = (time.perf_counter() - t0) * (N_C / n_sh)
+    s_per_it = rep_pairs / (rows * p / t_rep) + att_pairs / (rows * g / t_att) + t_proj
+    return {"pairs_per_s": rate, "s_per_iteration": s_per_it, "t_sample": t_rep + t_att,
+            "rows": rows, "proj_s_extrapolated": t_proj}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import _native, engine
+    from paper_2108_02991_b200.optimizer import _bb_step, default_eta0
+
+    class TimedOps(engine.CudaOps):
+        def __init__(self):
+            super().__init__()
+            self.record = False
+            self.ev = []
+
+        def sums(self, *a, **k):
+            if not self.record:
+                return super().sums(*a, **k)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            out = super().sums(*a, **k)
+            e.record()
+            self.ev.append((s, e))
+            return out
+
+    hw = hardware()
+    cfg = spk.OptimizerConfig(n_c=N_C, n_s=N_S, dims=DIMS, n_pit=100, grad_mode="exact",
+                              grid_n=GRID_N, seed=0, perturbation=0.25)
+    rho = spk.discretize(cfg.density, GRID_N, DIMS)
+    fld = spk.precompute_field(rho)
+    pcfg = proj_config()
+    ops = TimedOps()
+    run = engine.ShardedRun(np.ascontiguousarray(start_pattern().coords), cfg, fld, ops=ops)
+    run.project(pcfg)
+    eta0 = default_eta0(run.p, EPS_REP)
+    state = {"eta": eta0, "it": 0, "have": False}
+
+    def step():
+        state["it"] += 1
+        att, rep, bad, dots = run.evaluate()
+        if bad or not np.isfinite(att - rep):
+            raise RuntimeError("non-finite during bench")
+        state["eta"] = _bb_step(state["it"], state["eta"], dots[0], dots[1], state["have"],
+                                eta0, cfg.fixed_step_iters)
+        state["have"] = True
+        run.step_project(pcfg, state["eta"])
+        run.residual_max(pcfg)
+        return att - rep
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ops.record = True
+    _native.reset_launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step()
+            e.record()
+            times.append((s, e))
+        torch.cuda.synchronize()
+    launches = _native.launch_count()
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(s.elapsed_time(e) for s, e in times)
+    nb_ms = [s.elapsed_time(e) for s, e in ops.ev]
+    if world > 1:
+        t = torch.tensor([total_ms, float(np.mean(nb_ms))], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, nb_mean = float(t[0]), float(t[1])
+    else:
+        nb_mean = float(np.mean(nb_ms))
+    p, g, rep_pairs, att_pairs = pairs_per_step()
+    value = (rep_pairs + att_pairs) * args.steps / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (fused K1+K2 launch on this rank)
+    local_t = run.local * N_S
+    flops = local_t * p * FLOPS_REP_3D + local_t * g * FLOPS_ATT_3D
+    achieved = flops / (nb_mean / 1e3) / 1e12
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = fp32_peak_tflops(sm_max)
+    clocks = clk.summary()
+
+    # end-to-end through the public drop-in API with host buffers
+    e2e = run_e2e(args, spk, fld, pcfg) if rank == 0 and world == 1 else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "s_per_iteration": total_ms / args.steps / 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
+            "config": workload_config() | {"parallelism": f"shots sharded over {world} GPU(s)"},
+            "roofline": {"bound": "fp32+sfu", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "frac_at_measured_clock": (achieved / fp32_peak_tflops(clocks["sm_mhz"])
+                                                    if clocks.get("sm_mhz") else None),
+                         "traffic": committed_traffic(),
+                         "kernel": "nbody_kernel (fused K1+K2) + finalize",
+                         "flops_per_pair": {"repulsion": FLOPS_REP_3D, "attraction": FLOPS_ATT_3D},
+                         "launch_ms": nb_mean,
+                         "peak_source": f"148 SM x 128 FP32 lanes x 2 x sm_max_mhz {sm_max} "
+                                        f"(MEASURED_PEAKS.json clock)"},
+            "clocks": clocks,
+            "gpu_launches": launches,
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if not args.no_cpu_baseline and world == 1:
+            cb = cpu_reference_sample(args.cpu_rows)
+            line["cpu_baseline"] = {
+                "value": cb["pairs_per_s"], "unit": "pairs/s", "cores": os.cpu_count(),
+                "kind": "port", "cpu": cpu_model(),
+                "sample": f"{cb['rows']} target rows x all p={p} sources (repulsion) + "
+                          f"{cb['rows']} rows x all {g} grid cells (attraction), fp64, "
+                          f"{cb['t_sample']:.1f} s; projection 16 shots scaled to {N_C}",
+                "s_per_iteration_extrapolated": cb["s_per_iteration"]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, spk, fld, pcfg):
+    """The reference's loop body (optimizer.py:301-344) through the public API with numpy
+    host arrays; every call copies its inputs H2D and results D2H."""
+    import torch
+    from paper_2108_02991_b200.optimizer import default_eta0, step_size
+
+    pattern = spk.project_pattern(start_pattern(), pcfg)
+    rcfg = spk.RepulsionConfig(kernel_eps=EPS_REP)
+    eta0 = default_eta0(pattern.n_samples, EPS_REP)
+    prev_c = prev_g = None
+    eta = eta0
+    steps = max(1, min(args.steps, args.e2e_steps))
+    bi = bo = 0
+    nbytes = pattern.coords.nbytes
+    for it in range(1, steps + 2):  # first iteration is warm-up
+        if it == 2:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+        att = spk.eval_attraction(pattern, fld, "exact")
+        rep_cost, rep_grad = spk.eval_repulsion(pattern, rcfg)
+        grad = (att.grad - rep_grad).reshape(pattern.coords.shape)
+        dk = None if prev_c is None else pattern.coords - prev_c
+        dg = None if prev_g is None else grad - prev_g
+        eta = step_size(it, eta, dk, dg, eta0, 20)
+        prev_c, prev_g = pattern.coords.copy(), grad
+        pattern = spk.project_pattern(spk.SamplingPattern(pattern.coords - eta * grad), pcfg)
+        spk.feasibility_residuals(pattern, pcfg)
+        if it >= 2:
+            bi += 4 * nbytes          # coords to att, rep, project, residuals
+            bo += 3 * nbytes + 2 * pattern.n_samples * 8 + 40  # grads, vals, coords, resid
+    dt = time.perf_counter() - t0
+    p, g, rep_pairs, att_pairs = pairs_per_step()
+    return {"value": (rep_pairs + att_pairs) * steps / dt, "unit": "pairs/s",
+            "s_per_iteration": dt / steps, "steps": steps,
+            "h2d_bytes_per_step": bi // steps, "d2h_bytes_per_step": bo // steps,
+            "api": "eval_attraction(exact) + eval_repulsion + step_size + project_pattern + "
+                   "feasibility_residuals on numpy host arrays"}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+
+    orc.build()
+    threads = orc.max_threads()
+    samples = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_reference_sample(args.ref_rows, threads)
+        if i >= args.warmup:
+            samples.append(cb)
+    rate = float(np.mean([c["pairs_per_s"] for c in samples]))
+    p, g, _, _ = pairs_per_step()
+    s_it = float(np.mean([c["s_per_iteration"] for c in samples]))
+    line = {
+        "metric": METRIC, "value": rate, "unit": "pairs/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": s_it * 1e3, "s_per_iteration": s_it, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config() | {"parallelism": "host CPU threads"},
+        "cpu_baseline": {"value": rate, "unit": "pairs/s", "cores": threads, "kind": "port",
+                         "cpu": cpu_model(),
+                         "sample": f"per step {args.ref_rows} target rows x all {p} sources "
+                                   f"+ {args.ref_rows} rows x {g} grid cells, fp64, plus 16 "
+                                   f"shots of projection; s/iteration extrapolated"},
+        "e2e": {"value": rate, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=4096)
+    ap.add_argument("--ref-rows", type=int, default=2048)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

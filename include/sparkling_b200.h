@@ -1,0 +1,143 @@
+/*
+ * sparkling_b200.h -- C ABI of the B200 (sm_100a) SPARKLING hot path.
+ *
+ * Every entry point is stream-ordered, never allocates or frees, and takes caller-owned
+ * DEVICE pointers (torch tensors' data_ptr() on the Python side), sizes as int64_t,
+ * scalars by value and an explicit cudaStream_t.  Scratch memory is a caller-provided
+ * workspace whose size is given by the matching *_workspace_bytes() query.  Each call
+ * returns SPK_OK (0) or a nonzero SPK_ERR_* code; spk_last_error() then holds a
+ * one-line message.  No C++ exception crosses this boundary.
+ *
+ * Positions used by the N-body kernels are float4 records {x, y, z, w}: for sample
+ * positions w is ignored (z = 0 in 2D); for density-grid sources w is the weight rho.
+ * Trajectories are fp64 (n_shots, n_s, dims) row-major, shot-major, axis-innermost,
+ * exactly the SamplingPattern.coords layout (reference src/core.py:141-186).
+ *
+ * Reference paths below are relative to /root/reference/pkg/src/vdtraj/.
+ */
+#ifndef SPARKLING_B200_H
+#define SPARKLING_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* spk_stream_t; /* == cudaStream_t */
+
+enum {
+    SPK_OK = 0,
+    SPK_ERR_ARG = 1,       /* invalid shape / argument (reference raises ValueError) */
+    SPK_ERR_LAUNCH = 2,    /* kernel launch failure */
+    SPK_ERR_WORKSPACE = 3, /* workspace too small */
+    SPK_ERR_CUDA = 4       /* other CUDA runtime error */
+};
+
+int spk_version(void);
+const char* spk_last_error(void);
+
+/* ---------------------------------------------------------------- K1 / K2 N-body */
+
+/* Workspace for one spk_*_sums call with n_tgt targets and two source segments. */
+size_t spk_nbody_workspace_bytes(int64_t n_tgt, int64_t n_src0, int64_t n_src1);
+
+/* Repulsion raw sums.  Replaces _treecode.direct_sums (_treecode.py:506-534) and
+ * direct_sums_subset (:474-503): for every target i,
+ *   val[i]  = sum_j sqrt(|t_i - s_j|^2 + eps2)
+ *   grad[i] = sum_j (t_i - s_j) / sqrt(|t_i - s_j|^2 + eps2)   (term skipped when 0)
+ * over the n_src sources (i == j included, as the reference does).  fp32 pair math on
+ * the FMA + MUFU pipes, fp64 accumulation across source tiles.  val: [n_tgt] f64,
+ * grad: [n_tgt, dims] f64.  Called by eval_repulsion_direct (repulsion.py:72-87). */
+int spk_direct_sums(const void* tgt, int64_t n_tgt, const void* src, int64_t n_src,
+                    int dims, float eps2, double* val, double* grad, void* ws,
+                    size_t ws_bytes, spk_stream_t stream);
+
+/* Attraction raw sums over weighted grid sources (north-star attraction):
+ *   val[i]  = sum_y w_y sqrt(|t_i - y|^2 + eps2),  grad[i] = sum_y w_y (t_i - y)/h.
+ * With the grid nodes themselves as targets this is precompute_field's potential and
+ * force (attraction.py:62-113). */
+int spk_grid_sums(const void* tgt, int64_t n_tgt, const void* grid_src, int64_t n_cells,
+                  int dims, float eps2, double* val, double* grad, void* ws,
+                  size_t ws_bytes, spk_stream_t stream);
+
+/* Both sums in ONE launch (the optimize() hot loop, optimizer.py:302-303): segment 0 =
+ * weighted grid sources (attraction), segment 1 = unweighted positions (repulsion).
+ * Either segment may be empty (n = 0, outputs untouched). */
+int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const void* grid_src,
+                   int64_t n_cells, float eps2_att, const void* pos_src, int64_t n_pos,
+                   float eps2_rep, double* val_att, double* grad_att, double* val_rep,
+                   double* grad_rep, void* ws, size_t ws_bytes, spk_stream_t stream);
+
+/* Pack fp64 (p, dims) coordinates into float4 {x, y, z|0, 1}. */
+int spk_pack_positions(const double* coords, int64_t p, int dims, void* pos4,
+                       spk_stream_t stream);
+
+/* Grid sources {x, y, z|0, rho} for a (side0 x side1 [x side2]) node grid, node i on axis
+ * a at (i - N_a)/N_a with side_a = 2 N_a + 1 (density.py:58-67).  rho: fp64 row-major. */
+int spk_build_grid_sources(const double* rho, int dims, const int64_t* side, void* out,
+                           spk_stream_t stream);
+
+/* Combine raw sums into the optimizer gradient and scalars (optimizer.py:302-321):
+ *   grad[i] = grad_att[i] / p_att - grad_rep[i] / (p_rep * p_rep)
+ * (either term may be absent: pass NULL), and scalars written to out[0..5]:
+ *   out[0] = sum val_att, out[1] = sum val_rep,
+ *   out[2] = <coords - prev_coords, grad - prev_grad>, out[3] = <grad - prev_grad, ..>,
+ *   out[4] = count of non-finite gradient entries, out[5] = 0.
+ * prev_* may be NULL (then out[2..3] = 0).  Deterministic fixed-order reductions. */
+size_t spk_combine_workspace_bytes(int64_t n);
+int spk_combine_gradient(int64_t n_tgt, int dims, const double* val_att,
+                         const double* grad_att, double p_att, const double* val_rep,
+                         const double* grad_rep, double p_rep, const double* coords,
+                         const double* prev_coords, const double* prev_grad, double* grad,
+                         double* out, void* ws, size_t ws_bytes, spk_stream_t stream);
+
+/* ---------------------------------------------------------------- K3 projection */
+
+size_t spk_project_workspace_bytes(int64_t n_shots, int n_s, int dims, int with_trace);
+
+/* Batched shot projection.  Replaces _project_all (projection.py:376-382): per shot,
+ * n_pit iterations of dual FISTA with gradient restart (_project_shot, :169-284), then
+ * the relaxed cyclic feasibility polish (_feasibility_polish, :287-373) to tol with at
+ * most max_sweeps sweeps.  fp64, bit-identical to the reference.
+ *   in:  shots (n_shots, n_s, dims) f64; if grad != NULL the projected point is
+ *        in - eta * grad (the optimizer step, optimizer.py:326).
+ *   out: projected shots; pos4 (nullable) receives float4 positions of the result;
+ *        sweeps (nullable) the polish sweep count per shot; trace (nullable,
+ *        n_shots * n_pit f64) the dual objective per iteration (project_shot
+ *        return_trace=True, :394-418); nonfinite (nullable, 1 int32) is set to 1 when
+ *        the stepped input is not finite (SamplingPattern check, core.py:157).
+ *   pin_idx < 0 means no pin; pin_val: host array of dims doubles. */
+int spk_project_all(const double* in, const double* grad, double eta, double* out,
+                    int64_t n_shots, int n_s, int dims, double a, double b, int pin_idx,
+                    const double* pin_val, int n_pit, double tau, int monotone, double tol,
+                    int max_sweeps, void* pos4, int32_t* sweeps, double* trace,
+                    int32_t* nonfinite, void* ws, size_t ws_bytes, spk_stream_t stream);
+
+/* feasibility_residuals (projection.py:435-452): out[0..4] = amplitude, speed,
+ * acceleration, pin (0 if no pin), max -- each already clipped at 0 like the reference. */
+size_t spk_residuals_workspace_bytes(int64_t n_shots);
+int spk_feasibility_residuals(const double* coords, int64_t n_shots, int n_s, int dims,
+                              double a, double b, int pin_idx, const double* pin_val,
+                              double* out, void* ws, size_t ws_bytes, spk_stream_t stream);
+
+/* upsample_shots (optimizer.py:183-199): (n_shots, n_s, d) -> (n_shots, 2 n_s, d). */
+int spk_upsample_shots(const double* in, double* out, int64_t n_shots, int n_s, int dims,
+                       spk_stream_t stream);
+
+/* ------------------------------------------------------- field-path attraction */
+
+/* eval_attraction's interpolation path (attraction.py:116-308), fp64:
+ * mode 0 = "consistent" (_cell_grad2/3), 1 = "smooth" (interpolated force grids).
+ * pts (p, dims) f64; potential (2N+1)^d f64; force (dims, (2N+1)^d) f64 (mode 1).
+ * vals [p] = interpolated potential, grad [p, dims] (NOT divided by p),
+ * n_clamped (device int64, 1) = count of clamped samples. */
+int spk_field_eval(const double* pts, int64_t p, int dims, const double* potential,
+                   const double* force, int64_t grid_n, int mode, double* vals,
+                   double* grad, int64_t* n_clamped, spk_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARKLING_B200_H */

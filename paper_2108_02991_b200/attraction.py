@@ -1,0 +1,214 @@
+"""Attraction term on the B200: exact density-weighted N-body (K2) and the reference's
+interpolated-field path.
+
+Two evaluations share one ``KernelField``:
+
+* ``grad_mode="exact"`` -- the north-star attraction:
+  cost = (1/p) sum_i sum_y rho(y) sqrt(|x_i - y|^2 + eps^2),
+  grad_i = (1/p) sum_y rho(y) (x_i - y) / sqrt(...),
+  summed directly over every density node by ``spk_grid_sums`` (csrc/nbody.cu).
+* ``grad_mode="consistent"`` / ``"smooth"`` -- the reference's semantics
+  (/root/reference/pkg/src/vdtraj/attraction.py:267-308): multilinear interpolation of
+  the potential (and force) grids, fp64, in ``spk_field_eval`` (csrc/project.cu),
+  bit-identical to the numba kernels for the same grids.  The grids
+  (``precompute_field``, attraction.py:62-113) are produced by K2 with the grid nodes as
+  targets -- the same linear convolution the reference evaluates by FFT -- and are
+  computed lazily on first use.
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .core import SamplingPattern
+from .density import TargetDensity
+
+DEFAULT_MEM_CAP_BYTES = 6 * 1024**3
+GRAD_MODES = ("consistent", "smooth", "exact")
+
+
+class AttractionResult(NamedTuple):
+    cost: float
+    grad: np.ndarray
+    n_clamped: int
+
+
+def field_workspace_bytes(grid_n: int, dims: int) -> int:
+    """Device bytes needed to build the field: node sources (16 B), potential + force
+    (8 (1 + d) B) and the K2 partial-sum slots (<= 64 chunks x 32 B) per node."""
+    nodes = (2 * grid_n + 1) ** dims
+    return nodes * (16 + 8 * (1 + dims) + 64 * 32)
+
+
+class KernelField:
+    """Attraction potential/force grids on the (2N+1)^d density grid (attraction.py:26-43).
+
+    Constructed either with explicit ``potential`` / ``force`` arrays (drop-in) or from a
+    ``density`` by :func:`precompute_field`, in which case the grids are evaluated by K2
+    the first time they are needed.  ``density`` also feeds ``grad_mode="exact"``.
+    """
+
+    def __init__(self, potential=None, force=None, grid_n: int | None = None,
+                 kernel_eps: float | None = None, density: TargetDensity | None = None):
+        if potential is None and density is None:
+            raise ValueError("KernelField needs grids or a density")
+        self._potential = None if potential is None else np.asarray(potential, np.float64)
+        self._force = None if force is None else np.asarray(force, np.float64)
+        self.density = density
+        if grid_n is None:
+            grid_n = density.grid_n if density is not None else (self._potential.shape[0] - 1) // 2
+        self.grid_n = int(grid_n)
+        self.kernel_eps = float(kernel_eps if kernel_eps is not None else 1.0 / (2.0 * grid_n))
+        self._dev = {}
+
+    # -- grids ---------------------------------------------------------------------
+    @property
+    def dims(self) -> int:
+        if self._potential is not None:
+            return self._potential.ndim
+        return self.density.dims
+
+    def _evaluate_grids(self) -> None:
+        pot, force = self.device_grids()
+        side = 2 * self.grid_n + 1
+        shape = (side,) * self.dims
+        self._potential = _device.d2h(pot).reshape(shape)
+        self._force = _device.d2h(force).reshape((self.dims,) + shape)
+
+    @property
+    def potential(self) -> np.ndarray:
+        if self._potential is None:
+            self._evaluate_grids()
+        return self._potential
+
+    @property
+    def force(self) -> np.ndarray:
+        if self._force is None:
+            self._evaluate_grids()
+        return self._force
+
+    def device_sources(self) -> torch.Tensor:
+        """float4 {x, y, z, rho} records of every density node (the K2 sources)."""
+        if "src" not in self._dev:
+            if self.density is None:
+                raise ValueError("exact attraction needs the density grid (precompute_field)")
+            rho = _device.h2d(self.density.grid)
+            side = 2 * self.grid_n + 1
+            out = torch.empty((rho.numel(), 4), dtype=torch.float32, device=rho.device)
+            sides = _native.i64_array([side] * self.dims)
+            _native.call("spk_build_grid_sources", rho.data_ptr(), self.dims, sides,
+                         out.data_ptr(), _device.stream())
+            self._dev["src"] = out
+        return self._dev["src"]
+
+    def device_grids(self):
+        """(potential [G] f64, force [d, G] f64) on the device."""
+        if "pot" not in self._dev:
+            if self._potential is not None and self._force is not None:
+                self._dev["pot"] = _device.h2d(self._potential.reshape(-1))
+                self._dev["force"] = _device.h2d(self._force.reshape(self.dims, -1))
+            else:
+                src = self.device_sources()
+                g = src.shape[0]
+                val = torch.empty(g, dtype=torch.float64, device=src.device)
+                grad = torch.empty((g, self.dims), dtype=torch.float64, device=src.device)
+                grid_sums_device(src, src, self.dims, self.kernel_eps ** 2, val, grad)
+                self._dev["pot"] = val
+                self._dev["force"] = grad.t().contiguous()
+        return self._dev["pot"], self._dev["force"]
+
+
+def grid_sums_device(tgt4, src4, dims, eps2, val=None, grad=None):
+    """Raw K2 sums: val_i = sum_y w_y h, grad_i = sum_y w_y (t_i - y)/h (fp64 out)."""
+    n_t, n_c = tgt4.shape[0], src4.shape[0]
+    if val is None:
+        val = torch.empty(n_t, dtype=torch.float64, device=tgt4.device)
+    if grad is None:
+        grad = torch.empty((n_t, dims), dtype=torch.float64, device=tgt4.device)
+    nbytes = _native.query("spk_nbody_workspace_bytes", n_t, n_c, 0)
+    ws = _device.workspace(nbytes, "nbody")
+    _native.call("spk_grid_sums", tgt4.data_ptr(), n_t, src4.data_ptr(), n_c, dims,
+                 float(eps2), val.data_ptr(), grad.data_ptr(), ws.data_ptr(), ws.numel(),
+                 _device.stream())
+    return val, grad
+
+
+def precompute_field(rho: TargetDensity, kernel_eps: float | None = None,
+                     mem_cap_bytes: int = DEFAULT_MEM_CAP_BYTES) -> KernelField:
+    """Kernel-density convolution grids (attraction.py:62-113); eps defaults to 1/(2N).
+
+    Raises MemoryError with sizing guidance when the device workspace would exceed
+    ``mem_cap_bytes``, like the reference's FFT guard."""
+    n = rho.grid_n
+    dims = rho.dims
+    if kernel_eps is None:
+        kernel_eps = 1.0 / (2.0 * n)
+    if kernel_eps <= 0:
+        raise ValueError("kernel_eps must be positive")
+    need = field_workspace_bytes(n, dims)
+    if need > mem_cap_bytes:
+        raise MemoryError(
+            f"attraction field for grid_n={n}, dims={dims} needs ~{need / 1e9:.1f} GB of "
+            f"device workspace; reduce the density grid size or raise mem_cap_bytes")
+    return KernelField(grid_n=n, kernel_eps=float(kernel_eps), density=rho)
+
+
+def field_eval_device(coords: torch.Tensor, field: KernelField, mode: str,
+                      vals: torch.Tensor | None = None, grad: torch.Tensor | None = None):
+    """Interpolated attraction at fp64 device coords (p, d): (vals, grad, n_clamped dev)."""
+    dims = field.dims
+    p = coords.numel() // dims
+    pot, force = field.device_grids()
+    if vals is None:
+        vals = torch.empty(p, dtype=torch.float64, device=coords.device)
+    if grad is None:
+        grad = torch.empty((p, dims), dtype=torch.float64, device=coords.device)
+    ncl = torch.zeros(1, dtype=torch.int64, device=coords.device)
+    _native.call("spk_field_eval", coords.data_ptr(), p, dims, pot.data_ptr(),
+                 force.data_ptr(), field.grid_n, 0 if mode == "consistent" else 1,
+                 vals.data_ptr(), grad.data_ptr(), ncl.data_ptr(), _device.stream())
+    return vals, grad, ncl
+
+
+def interpolate(grid: np.ndarray, points: np.ndarray, grid_n: int) -> np.ndarray:
+    """Multilinear interpolation of a (2N+1)^d grid at points (attraction.py:258-264)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    g = np.asarray(grid, dtype=np.float64)
+    fld = KernelField(potential=g, force=np.zeros((g.ndim,) + g.shape), grid_n=grid_n,
+                      kernel_eps=1.0)
+    vals, _, _ = field_eval_device(_device.h2d(pts), fld, "consistent")
+    return _device.d2h(vals)
+
+
+def _n_outside(pts: np.ndarray) -> int:
+    return int(np.count_nonzero((np.abs(pts) > 1.0).any(axis=1)))
+
+
+def eval_attraction(k: SamplingPattern, field: KernelField,
+                    grad_mode: str = "consistent") -> AttractionResult:
+    """Attraction cost, gradient and clamp count (attraction.py:267-308)."""
+    if k.dims != field.dims:
+        raise ValueError(f"pattern dims {k.dims} != field dims {field.dims}")
+    if grad_mode not in GRAD_MODES:
+        raise ValueError(f"unknown grad_mode {grad_mode!r}")
+    pts = k.points()
+    p = pts.shape[0]
+    coords = _device.h2d(pts)
+    if grad_mode == "exact":
+        src = field.device_sources()
+        tgt = _device.pack_positions(coords)
+        val, grad = grid_sums_device(tgt, src, k.dims, field.kernel_eps ** 2)
+        vals_h = _device.d2h(val)
+        n_clamped = _n_outside(pts)
+    else:
+        val, grad, ncl = field_eval_device(coords, field, grad_mode)
+        vals_h = _device.d2h(val)
+        n_clamped = int(ncl.item())
+    grad_h = _device.d2h(grad)
+    cost = float(vals_h.sum() / p)
+    grad_h /= p
+    return AttractionResult(cost=cost, grad=grad_h, n_clamped=n_clamped)

@@ -1,0 +1,524 @@
+// nbody.cu -- K1 (repulsion) and K2 (attraction) all-pairs sums for sm_100a.
+//
+// Replaces the reference's O(p^2) numba loops: direct_sums / direct_sums_subset
+// (/root/reference/pkg/src/vdtraj/_treecode.py:474-534) and, for the north-star exact
+// attraction, the density-weighted sum that precompute_field evaluates by FFT
+// (attraction.py:62-113).
+//
+// Design:
+//  * Work unit = (target block of NB_TB targets) x (source chunk).  Units are sized on
+//    the host so that their count fills 148 SMs evenly; every unit writes its fp64
+//    partial sums to its own workspace slot and a second kernel adds the slots in a
+//    fixed order => bitwise run-to-run determinism without float atomics.
+//  * Source tiles (NB_TILE float4 records) are staged into shared memory with 1-D bulk
+//    TMA (cp.async.bulk + mbarrier complete_tx), NB_STAGES deep.  Every thread reads
+//    each source record with one broadcast LDS.128.
+//  * Each thread owns NB_TPT targets as NB_TPT/2 packed f32x2 pairs: one FADD2/FFMA2/
+//    FMUL2 instruction advances two pair-interactions; the reciprocal square root runs
+//    on the SFU (MUFU.RSQ).  Per pair (3D, unweighted): 3 FADD + 3 FFMA (r^2) + 1 MUFU
+//    + 1 FFMA (value) + 3 FFMA (gradient) = 17 flops, 10 FP32 lane-ops, 1 MUFU.
+//  * fp32 accumulation inside a tile, folded into fp64 per tile (relative gradient
+//    error vs the fp64 reference ~1e-6, well inside the 1e-4 north-star bound).
+#include <algorithm>
+#include <cfloat>
+#include <cstdarg>
+#include <cstring>
+
+#include "spk_common.cuh"
+
+namespace spk {
+
+constexpr int NB_THREADS = 256;
+constexpr int NB_TPT = 8;                   // targets per thread
+constexpr int NB_PAIRS = NB_TPT / 2;        // f32x2 pairs per thread
+constexpr int NB_TB = NB_THREADS * NB_TPT;  // targets per CTA
+constexpr int NB_TILE = 512;                // sources per shared-memory stage
+constexpr int NB_STAGES = 4;
+constexpr int NB_SMEM = NB_STAGES * NB_TILE * 16;
+constexpr int NB_MAX_CHUNKS = 192;
+
+struct SegDesc {
+    const float4* src;
+    long long n;      // source records
+    long long tiles;  // ceil(n / NB_TILE)
+    int n_chunks;     // chunks this segment is split into (0 if empty)
+    int weighted;     // 1: multiply by w (grid density); 0: w ignored (positions)
+    float eps2;
+};
+
+struct NBParams {
+    const float4* tgt;
+    long long n_tgt;
+    long long n_tb;
+    SegDesc seg[2];
+    double* part;  // [chunk][4][n_tgt]: value, gx, gy, gz
+};
+
+__device__ __forceinline__ float rsqrt_sfu(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// One shared-memory tile against this thread's NB_TPT targets.  W: weighted sources;
+// G: guard r2 == 0 (eps2 == 0 => coincident points contribute value 0, gradient 0,
+// like the reference's `if h > 0` at _treecode.py:525).
+template <int D, bool W, bool G>
+__device__ __forceinline__ void tile_pairs(const float4* __restrict__ tile, int cnt,
+                                           const float2 (&X)[NB_PAIRS],
+                                           const float2 (&Y)[NB_PAIRS],
+                                           const float2 (&Z)[NB_PAIRS], float2 e2,
+                                           float2 (&av)[NB_PAIRS], float2 (&ax)[NB_PAIRS],
+                                           float2 (&ay)[NB_PAIRS],
+                                           float2 (&az)[NB_PAIRS]) {
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+        const float4 s = tile[j];
+        const float2 nsx = make_float2(-s.x, -s.x);
+        const float2 nsy = make_float2(-s.y, -s.y);
+        const float2 nsz = make_float2(-s.z, -s.z);
+#pragma unroll
+        for (int k = 0; k < NB_PAIRS; ++k) {
+            const float2 dx = __fadd2_rn(X[k], nsx);
+            const float2 dy = __fadd2_rn(Y[k], nsy);
+            float2 r2 = __ffma2_rn(dx, dx, e2);
+            r2 = __ffma2_rn(dy, dy, r2);
+            float2 dz;
+            if (D == 3) {
+                dz = __fadd2_rn(Z[k], nsz);
+                r2 = __ffma2_rn(dz, dz, r2);
+            }
+            float2 inv;
+            inv.x = rsqrt_sfu(r2.x);
+            inv.y = rsqrt_sfu(r2.y);
+            if (G) {
+                inv.x = r2.x > 0.0f ? inv.x : 0.0f;
+                inv.y = r2.y > 0.0f ? inv.y : 0.0f;
+            }
+            if (W) inv = __fmul2_rn(inv, make_float2(s.w, s.w));
+            av[k] = __ffma2_rn(r2, inv, av[k]);  // sum w*h = sum r2 * (w/h)
+            ax[k] = __ffma2_rn(dx, inv, ax[k]);
+            ay[k] = __ffma2_rn(dy, inv, ay[k]);
+            if (D == 3) az[k] = __ffma2_rn(dz, inv, az[k]);
+        }
+    }
+}
+
+template <int D, bool W, bool G>
+__device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, long long t_end,
+                                          float4* tiles, uint64_t* bars,
+                                          const float2 (&X)[NB_PAIRS],
+                                          const float2 (&Y)[NB_PAIRS],
+                                          const float2 (&Z)[NB_PAIRS], double (&acc)[NB_TPT][4]) {
+    const int tid = threadIdx.x;
+    const float2 e2 = make_float2(S.eps2, S.eps2);
+    auto issue = [&](long long t, int stage) {
+        const long long first = t * NB_TILE;
+        const long long cnt = min((long long)NB_TILE, S.n - first);
+        const uint32_t bytes = (uint32_t)(cnt * 16);
+        mbar_expect_tx(&bars[stage], bytes);
+        tma_load_1d(tiles + stage * NB_TILE, S.src + first, bytes, &bars[stage]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < NB_STAGES; ++s)
+            if (t_begin + s < t_end) issue(t_begin + s, s);
+    }
+    for (long long t = t_begin; t < t_end; ++t) {
+        const long long i = t - t_begin;
+        const int stage = (int)(i % NB_STAGES);
+        const uint32_t parity = (uint32_t)((i / NB_STAGES) & 1);
+        const int cnt = (int)min((long long)NB_TILE, S.n - t * NB_TILE);
+        float2 av[NB_PAIRS], ax[NB_PAIRS], ay[NB_PAIRS], az[NB_PAIRS];
+#pragma unroll
+        for (int k = 0; k < NB_PAIRS; ++k) {
+            av[k] = ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
+        }
+        mbar_wait(&bars[stage], parity);
+        tile_pairs<D, W, G>(tiles + stage * NB_TILE, cnt, X, Y, Z, e2, av, ax, ay, az);
+#pragma unroll
+        for (int k = 0; k < NB_PAIRS; ++k) {
+            acc[2 * k][0] += av[k].x;
+            acc[2 * k + 1][0] += av[k].y;
+            acc[2 * k][1] += ax[k].x;
+            acc[2 * k + 1][1] += ax[k].y;
+            acc[2 * k][2] += ay[k].x;
+            acc[2 * k + 1][2] += ay[k].y;
+            if (D == 3) {
+                acc[2 * k][3] += az[k].x;
+                acc[2 * k + 1][3] += az[k].y;
+            }
+        }
+        __syncthreads();  // every warp is done with this stage
+        if (tid == 0 && t + NB_STAGES < t_end) issue(t + NB_STAGES, stage);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(NB_THREADS, 1) nbody_kernel(const NBParams P) {
+    extern __shared__ __align__(128) float4 tiles[];
+    __shared__ __align__(8) uint64_t bars[NB_STAGES];
+    const int tid = threadIdx.x;
+    const long long unit = blockIdx.x;
+    const long long tb = unit % P.n_tb;
+    const int chunk = (int)(unit / P.n_tb);
+    const bool first = chunk < P.seg[0].n_chunks;
+    const SegDesc S = first ? P.seg[0] : P.seg[1];
+    const long long lc = first ? chunk : chunk - P.seg[0].n_chunks;
+    const long long t_begin = lc * S.tiles / S.n_chunks;
+    const long long t_end = (lc + 1) * S.tiles / S.n_chunks;
+
+    float2 X[NB_PAIRS], Y[NB_PAIRS], Z[NB_PAIRS];
+    const long long base = tb * NB_TB + tid;
+#pragma unroll
+    for (int k = 0; k < NB_PAIRS; ++k) {
+        const long long i0 = min(base + (2 * k) * NB_THREADS, P.n_tgt - 1);
+        const long long i1 = min(base + (2 * k + 1) * NB_THREADS, P.n_tgt - 1);
+        const float4 a = P.tgt[i0];
+        const float4 b = P.tgt[i1];
+        X[k] = make_float2(a.x, b.x);
+        Y[k] = make_float2(a.y, b.y);
+        Z[k] = make_float2(D == 3 ? a.z : 0.f, D == 3 ? b.z : 0.f);
+    }
+    double acc[NB_TPT][4];
+#pragma unroll
+    for (int k = 0; k < NB_TPT; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
+
+    if (tid == 0) {
+        for (int s = 0; s < NB_STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const bool guard = !(S.eps2 >= FLT_MIN);
+    if (S.weighted) {
+        if (guard) run_chunk<D, true, true>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
+        else run_chunk<D, true, false>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
+    } else {
+        if (guard) run_chunk<D, false, true>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
+        else run_chunk<D, false, false>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
+    }
+
+    double* slot = P.part + (size_t)chunk * 4 * P.n_tgt;
+#pragma unroll
+    for (int k = 0; k < NB_TPT; ++k) {
+        const long long i = base + k * NB_THREADS;
+        if (i < P.n_tgt) {
+            slot[i] = acc[k][0];
+            slot[P.n_tgt + i] = acc[k][1];
+            slot[2 * P.n_tgt + i] = acc[k][2];
+            if (D == 3) slot[3 * P.n_tgt + i] = acc[k][3];
+        }
+    }
+}
+
+// Fixed-order sum over the chunk slots of one segment.
+__global__ void nbody_finalize(const double* __restrict__ part, long long n_tgt, int c_begin,
+                               int c_end, int dims, double* __restrict__ val,
+                               double* __restrict__ grad) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_tgt) return;
+    double v = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    for (int c = c_begin; c < c_end; ++c) {
+        const double* slot = part + (size_t)c * 4 * n_tgt;
+        v += slot[i];
+        gx += slot[n_tgt + i];
+        gy += slot[2 * n_tgt + i];
+        if (dims == 3) gz += slot[3 * n_tgt + i];
+    }
+    if (val) val[i] = v;
+    if (grad) {
+        grad[i * dims] = gx;
+        grad[i * dims + 1] = gy;
+        if (dims == 3) grad[i * dims + 2] = gz;
+    }
+}
+
+struct Plan {
+    long long n_tb = 0;
+    int nc0 = 0, nc1 = 0;
+    size_t ws_bytes = 0;
+};
+
+static int nbody_slots() {
+    static int slots = 0;
+    if (slots == 0) {
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbody_kernel<3>, NB_THREADS,
+                                                          NB_SMEM) != cudaSuccess ||
+            occ <= 0) {
+            cudaGetLastError();
+            occ = 1;
+        }
+        slots = num_sms() * occ;
+    }
+    return slots;
+}
+
+// Choose the chunk counts: minimise (waves x longest unit) + per-chunk reduction cost,
+// with the two segments split in proportion to their tile counts.
+static Plan make_plan(long long n_tgt, long long n0, long long n1) {
+    Plan pl;
+    if (n_tgt <= 0) return pl;
+    pl.n_tb = (n_tgt + NB_TB - 1) / NB_TB;
+    const long long t0 = (n0 + NB_TILE - 1) / NB_TILE;
+    const long long t1 = (n1 + NB_TILE - 1) / NB_TILE;
+    const long long slots = nbody_slots();
+    double best = 1e300;
+    const int cmin = (t0 > 0) + (t1 > 0);
+    for (int c = std::max(cmin, 1); c <= NB_MAX_CHUNKS; ++c) {
+        int c0 = 0, c1 = 0;
+        if (t0 > 0 && t1 > 0) {
+            c0 = (int)std::llround((double)c * t0 / (double)(t0 + t1));
+            c0 = std::max(1, std::min(c - 1, c0));
+            c1 = c - c0;
+        } else if (t0 > 0) {
+            c0 = c;
+        } else {
+            c1 = c;
+        }
+        if ((t0 > 0 && c0 > t0) || (t1 > 0 && c1 > t1)) break;
+        const long long l0 = c0 ? (t0 + c0 - 1) / c0 : 0;
+        const long long l1 = c1 ? (t1 + c1 - 1) / c1 : 0;
+        const long long units = pl.n_tb * c;
+        const long long waves = (units + slots - 1) / slots;
+        const double cost = (double)waves * (double)std::max(l0, l1) +
+                            0.03 * (double)c * (double)pl.n_tb / (double)slots;
+        if (cost < best * 0.999) {
+            best = cost;
+            pl.nc0 = c0;
+            pl.nc1 = c1;
+        }
+    }
+    pl.ws_bytes = (size_t)(pl.nc0 + pl.nc1) * 4 * (size_t)n_tgt * sizeof(double);
+    return pl;
+}
+
+static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float4* s0,
+                       long long n0, float e0, int w0, const float4* s1, long long n1,
+                       float e1, int w1, double* val0, double* grad0, double* val1,
+                       double* grad1, void* ws, size_t ws_bytes, cudaStream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(n_tgt >= 0 && n0 >= 0 && n1 >= 0, SPK_ERR_ARG, "negative size");
+    if (n_tgt == 0 || (n0 == 0 && n1 == 0)) {
+        // Empty sums: zero the outputs like a loop that never runs.
+        if (n_tgt > 0) {
+            if (val0) cudaMemsetAsync(val0, 0, n_tgt * 8, stream);
+            if (grad0) cudaMemsetAsync(grad0, 0, n_tgt * dims * 8, stream);
+            if (val1) cudaMemsetAsync(val1, 0, n_tgt * 8, stream);
+            if (grad1) cudaMemsetAsync(grad1, 0, n_tgt * dims * 8, stream);
+        }
+        return SPK_OK;
+    }
+    SPK_REQUIRE(tgt != nullptr, SPK_ERR_ARG, "null target pointer");
+    SPK_REQUIRE(((uintptr_t)s0 & 15) == 0 && ((uintptr_t)s1 & 15) == 0, SPK_ERR_ARG,
+                "source arrays must be 16-byte aligned");
+    const Plan pl = make_plan(n_tgt, n0, n1);
+    SPK_REQUIRE(ws != nullptr && ws_bytes >= pl.ws_bytes, SPK_ERR_WORKSPACE,
+                "nbody workspace too small: need %zu bytes, got %zu", pl.ws_bytes, ws_bytes);
+    NBParams P;
+    P.tgt = tgt;
+    P.n_tgt = n_tgt;
+    P.n_tb = pl.n_tb;
+    P.seg[0] = SegDesc{s0, n0, (n0 + NB_TILE - 1) / NB_TILE, pl.nc0, w0, e0};
+    P.seg[1] = SegDesc{s1, n1, (n1 + NB_TILE - 1) / NB_TILE, pl.nc1, w1, e1};
+    P.part = static_cast<double*>(ws);
+    const long long grid = pl.n_tb * (pl.nc0 + pl.nc1);
+    if (dims == 3)
+        nbody_kernel<3><<<(unsigned)grid, NB_THREADS, NB_SMEM, stream>>>(P);
+    else
+        nbody_kernel<2><<<(unsigned)grid, NB_THREADS, NB_SMEM, stream>>>(P);
+    SPK_CHECK_LAUNCH("nbody_kernel");
+    const unsigned fb = (unsigned)((n_tgt + 255) / 256);
+    if (pl.nc0 > 0 && (val0 || grad0))
+        nbody_finalize<<<fb, 256, 0, stream>>>(P.part, n_tgt, 0, pl.nc0, dims, val0, grad0);
+    if (pl.nc1 > 0 && (val1 || grad1))
+        nbody_finalize<<<fb, 256, 0, stream>>>(P.part, n_tgt, pl.nc0, pl.nc0 + pl.nc1, dims,
+                                               val1, grad1);
+    SPK_CHECK_LAUNCH("nbody_finalize");
+    return SPK_OK;
+}
+
+// ------------------------------------------------------------------ packing kernels
+__global__ void pack_positions_kernel(const double* __restrict__ c, long long p, int dims,
+                                      float4* __restrict__ out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const double* r = c + i * dims;
+    out[i] = make_float4((float)r[0], (float)r[1], dims == 3 ? (float)r[2] : 0.f, 1.f);
+}
+
+__global__ void grid_sources_kernel(const double* __restrict__ rho, long long s0,
+                                    long long s1, long long s2, int dims,
+                                    float4* __restrict__ out) {
+    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long n = s0 * s1 * s2;
+    if (c >= n) return;
+    const long long k = c % s2;
+    const long long j = (c / s2) % s1;
+    const long long i = c / (s1 * s2);
+    const long long h0 = (s0 - 1) / 2, h1 = (s1 - 1) / 2, h2 = (s2 - 1) / 2;
+    const double x = (double)(i - h0) / (double)h0;
+    const double y = (double)(j - h1) / (double)h1;
+    const double z = dims == 3 ? (double)(k - h2) / (double)h2 : 0.0;
+    out[c] = make_float4((float)x, (float)y, (float)z, (float)rho[c]);
+}
+
+// ------------------------------------------------------------ gradient combination
+constexpr int CB_THREADS = 256;
+
+__global__ void combine_kernel(long long n, int dims, const double* __restrict__ va,
+                               const double* __restrict__ ga, double pa,
+                               const double* __restrict__ vr, const double* __restrict__ gr,
+                               double pr, const double* __restrict__ coords,
+                               const double* __restrict__ prev_c,
+                               const double* __restrict__ prev_g, double* __restrict__ grad,
+                               double* __restrict__ block_out) {
+    __shared__ double red[5][CB_THREADS];
+    const long long i = blockIdx.x * (long long)CB_THREADS + threadIdx.x;
+    double s_va = 0, s_vr = 0, s_kg = 0, s_gg = 0, s_nf = 0;
+    if (i < n) {
+        if (va) s_va = va[i];
+        if (vr) s_vr = vr[i];
+        const double prr = pr * pr;
+        for (int l = 0; l < dims; ++l) {
+            const long long e = i * dims + l;
+            double g = 0.0;
+            if (ga) g = ga[e] / pa;
+            if (gr) g = g - gr[e] / prr;
+            grad[e] = g;
+            if (!isfinite(g)) s_nf += 1.0;
+            if (prev_c && prev_g) {
+                const double dk = coords[e] - prev_c[e];
+                const double dg = g - prev_g[e];
+                s_kg += dk * dg;
+                s_gg += dg * dg;
+            }
+        }
+    }
+    red[0][threadIdx.x] = s_va;
+    red[1][threadIdx.x] = s_vr;
+    red[2][threadIdx.x] = s_kg;
+    red[3][threadIdx.x] = s_gg;
+    red[4][threadIdx.x] = s_nf;
+    __syncthreads();
+    for (int w = CB_THREADS / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int q = 0; q < 5; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 5) block_out[blockIdx.x * 5 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void combine_final_kernel(const double* __restrict__ block_out, long long nb,
+                                     double* __restrict__ out) {
+    __shared__ double red[5][CB_THREADS];
+    double s[5] = {0, 0, 0, 0, 0};
+    for (long long b = threadIdx.x; b < nb; b += CB_THREADS)
+        for (int q = 0; q < 5; ++q) s[q] += block_out[b * 5 + q];
+    for (int q = 0; q < 5; ++q) red[q][threadIdx.x] = s[q];
+    __syncthreads();
+    for (int w = CB_THREADS / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int q = 0; q < 5; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 5) out[threadIdx.x] = red[threadIdx.x][0];
+    if (threadIdx.x == 5) out[5] = 0.0;
+}
+
+// --------------------------------------------------------------------- error text
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+}  // namespace spk
+
+using namespace spk;
+
+extern "C" {
+
+int spk_version(void) { return 1; }
+
+const char* spk_last_error(void) { return g_err; }
+
+size_t spk_nbody_workspace_bytes(int64_t n_tgt, int64_t n_src0, int64_t n_src1) {
+    return make_plan(n_tgt, n_src0, n_src1).ws_bytes + 256;
+}
+
+int spk_direct_sums(const void* tgt, int64_t n_tgt, const void* src, int64_t n_src, int dims,
+                    float eps2, double* val, double* grad, void* ws, size_t ws_bytes,
+                    spk_stream_t stream) {
+    return launch_sums((const float4*)tgt, n_tgt, dims, nullptr, 0, 0.f, 0,
+                       (const float4*)src, n_src, eps2, 0, nullptr, nullptr, val, grad, ws,
+                       ws_bytes, (cudaStream_t)stream);
+}
+
+int spk_grid_sums(const void* tgt, int64_t n_tgt, const void* grid_src, int64_t n_cells,
+                  int dims, float eps2, double* val, double* grad, void* ws, size_t ws_bytes,
+                  spk_stream_t stream) {
+    return launch_sums((const float4*)tgt, n_tgt, dims, (const float4*)grid_src, n_cells,
+                       eps2, 1, nullptr, 0, 0.f, 0, val, grad, nullptr, nullptr, ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const void* grid_src,
+                   int64_t n_cells, float eps2_att, const void* pos_src, int64_t n_pos,
+                   float eps2_rep, double* val_att, double* grad_att, double* val_rep,
+                   double* grad_rep, void* ws, size_t ws_bytes, spk_stream_t stream) {
+    return launch_sums((const float4*)tgt, n_tgt, dims, (const float4*)grid_src, n_cells,
+                       eps2_att, 1, (const float4*)pos_src, n_pos, eps2_rep, 0, val_att,
+                       grad_att, val_rep, grad_rep, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int spk_pack_positions(const double* coords, int64_t p, int dims, void* pos4,
+                       spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    if (p <= 0) return SPK_OK;
+    pack_positions_kernel<<<(unsigned)((p + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        coords, p, dims, (float4*)pos4);
+    SPK_CHECK_LAUNCH("pack_positions");
+    return SPK_OK;
+}
+
+int spk_build_grid_sources(const double* rho, int dims, const int64_t* side, void* out,
+                           spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    const long long s0 = side[0], s1 = side[1], s2 = dims == 3 ? side[2] : 1;
+    SPK_REQUIRE(s0 >= 3 && s1 >= 3 && s2 >= 1 && (s0 & 1) && (s1 & 1) && (s2 & 1),
+                SPK_ERR_ARG, "grid sides must be odd (2N+1) and >= 3");
+    const long long n = s0 * s1 * s2;
+    grid_sources_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        rho, s0, s1, s2, dims, (float4*)out);
+    SPK_CHECK_LAUNCH("grid_sources");
+    return SPK_OK;
+}
+
+size_t spk_combine_workspace_bytes(int64_t n) {
+    return (size_t)((n + CB_THREADS - 1) / CB_THREADS) * 5 * sizeof(double) + 256;
+}
+
+int spk_combine_gradient(int64_t n_tgt, int dims, const double* val_att,
+                         const double* grad_att, double p_att, const double* val_rep,
+                         const double* grad_rep, double p_rep, const double* coords,
+                         const double* prev_coords, const double* prev_grad, double* grad,
+                         double* out, void* ws, size_t ws_bytes, spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    SPK_REQUIRE(n_tgt > 0, SPK_ERR_ARG, "n_tgt must be positive");
+    SPK_REQUIRE(ws_bytes >= spk_combine_workspace_bytes(n_tgt), SPK_ERR_WORKSPACE,
+                "combine workspace too small");
+    const long long nb = (n_tgt + CB_THREADS - 1) / CB_THREADS;
+    double* bo = static_cast<double*>(ws);
+    combine_kernel<<<(unsigned)nb, CB_THREADS, 0, (cudaStream_t)stream>>>(
+        n_tgt, dims, val_att, grad_att, p_att, val_rep, grad_rep, p_rep, coords, prev_coords,
+        prev_grad, grad, bo);
+    combine_final_kernel<<<1, CB_THREADS, 0, (cudaStream_t)stream>>>(bo, nb, out);
+    SPK_CHECK_LAUNCH("combine_gradient");
+    return SPK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,911 @@
+// project.cu -- K3 batched shot projection (fp64) and the per-shot helpers around it.
+//
+// Compiled with -fmad=false: every fp64 expression is evaluated with the reference's
+// operation order and no FMA contraction, so results are bit-identical to the numba
+// kernels of /root/reference/pkg/src/vdtraj/projection.py (IEEE div/sqrt on both sides).
+//
+//  * fista_kernel: one CTA per shot, one thread per sample (strided), n_pit iterations
+//    of dual FISTA with gradient restart (_project_shot, projection.py:169-284).  s and
+//    the first/second-difference duals live in shared memory (neighbour access); the
+//    remaining per-sample state lives in an L2-resident workspace.  The restart test
+//    sign(<y - z, z - q>) uses a block tree reduction plus a rounding-error bound; if the
+//    bound cannot certify the sign, thread 0 re-sums the terms in the reference's
+//    sequential order, so restart decisions are identical to the reference.
+//  * polish_kernel: the relaxed cyclic projections (_feasibility_polish, :287-373),
+//    a Gauss-Seidel recurrence.  One warp per shot, wavefront-pipelined: lane k runs
+//    sweep (base + k) four samples behind lane k-1, so 32 sweeps advance together with
+//    exactly the reference's per-element operation sequence; a checkpoint + replay
+//    reproduces the reference's stopping sweep.
+#include <cfloat>
+#include <cmath>
+
+#include "spk_common.cuh"
+
+namespace spk {
+
+constexpr int PJ_THREADS = 256;
+constexpr int PJ_SMEM_LIMIT = 200 * 1024;
+
+struct ProjArgs {
+    const double* in;
+    const double* grad;
+    double eta;
+    double* out;
+    long long n_shots;
+    int ns;
+    double a, b;
+    int pin;
+    double pv[3];
+    int n_pit;
+    double tau;
+    int monotone;
+    double* trace;
+    int32_t* nonfinite;
+    double* ws;         // per-shot state, stride = ws_stride doubles
+    long long ws_stride;
+    int smem_arrays;    // 1: s/y1/y2 in shared memory
+};
+
+// Workspace layout per shot (units of ns*D doubles): k, q0, q1, q2, y0, z0, z1, z2, s_obj,
+// [s, y1, y2 when they do not fit in shared memory].
+constexpr int PJ_WS_ARRAYS = 12;
+
+__device__ __forceinline__ double clamp_unit(double z) {
+    const double m = (z > -1.0) ? z : -1.0;  // max(z, -1.0)
+    return (m < 1.0) ? m : 1.0;              // min(., 1.0)
+}
+
+// s = k - (A0^T q0 + A1^T q1 + A2^T q2) for one row n (_dual_to_primal,
+// projection.py:103-123); the pinned row is handled by the caller.
+template <int D>
+__device__ __forceinline__ void primal_row(const double* k, const double* q0, const double* q1,
+                                           const double* q2, int ns, int n, double* s) {
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        double r = q0[n * D + l];
+        if (n <= ns - 2) r -= q1[n * D + l];
+        if (n >= 1) r += q1[(n - 1) * D + l];
+        if (n <= ns - 3) r += q2[n * D + l];
+        if (1 <= n && n <= ns - 2) r -= 2.0 * q2[(n - 1) * D + l];
+        if (n >= 2) r += q2[(n - 2) * D + l];
+        s[n * D + l] = k[n * D + l] - r;
+    }
+}
+
+// Dual objective of (q0, q1, q2) in the reference's sequential order (_dual_objective,
+// projection.py:126-166).  Requires s = primal(q) already written for all rows; run by
+// a single thread.
+template <int D>
+__device__ double dual_objective_serial(const double* s, const double* q0, const double* q1,
+                                        const double* q2, int ns, int pin, const double* pv,
+                                        double a, double b) {
+    double obj = 0.0;
+    for (int n = 0; n < ns; ++n) {
+        if (n == pin) continue;
+        for (int l = 0; l < D; ++l) obj += 0.5 * s[n * D + l] * s[n * D + l];
+    }
+    for (int i = 0; i < ns * D; ++i) obj += fabs(q0[i]);
+    for (int n = 0; n < ns - 1; ++n) {
+        double nrm = 0.0;
+        for (int l = 0; l < D; ++l) nrm += q1[n * D + l] * q1[n * D + l];
+        obj += a * sqrt(nrm);
+    }
+    for (int n = 0; n < ns - 2; ++n) {
+        double nrm = 0.0;
+        for (int l = 0; l < D; ++l) nrm += q2[n * D + l] * q2[n * D + l];
+        obj += b * sqrt(nrm);
+    }
+    if (pin >= 0) {
+        const int p = pin;
+        for (int l = 0; l < D; ++l) {
+            obj -= q0[p * D + l] * pv[l];
+            if (p <= ns - 2) obj -= q1[p * D + l] * pv[l];
+            if (p >= 1) obj += q1[(p - 1) * D + l] * pv[l];
+            if (p <= ns - 3) obj += q2[p * D + l] * pv[l];
+            if (1 <= p && p <= ns - 2) obj -= 2.0 * q2[(p - 1) * D + l] * pv[l];
+            if (p >= 2) obj += q2[(p - 2) * D + l] * pv[l];
+        }
+    }
+    return obj;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide (sum, sum of |.|) with a fixed reduction tree; result broadcast.
+__device__ __forceinline__ void block_sum2(double& x, double& y, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    x = warp_sum(x);
+    y = warp_sum(y);
+    if (lane == 0) {
+        red[w] = x;
+        red[32 + w] = y;
+    }
+    __syncthreads();
+    if (w == 0) {
+        double a = lane < nw ? red[lane] : 0.0;
+        double b = lane < nw ? red[32 + lane] : 0.0;
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (lane == 0) {
+            red[64] = a;
+            red[65] = b;
+        }
+    }
+    __syncthreads();
+    x = red[64];
+    y = red[65];
+}
+
+template <int D>
+__global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ double red[72];
+    __shared__ int flag_sh[2];
+    const int ns = A.ns;
+    const int nd = ns * D;
+    const long long c = blockIdx.x;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    double* W = A.ws + c * A.ws_stride;
+    double* k = W;
+    double* q0 = W + 1 * (size_t)nd;
+    double* q1 = W + 2 * (size_t)nd;
+    double* q2 = W + 3 * (size_t)nd;
+    double* y0 = W + 4 * (size_t)nd;
+    double* z0 = W + 5 * (size_t)nd;
+    double* z1 = W + 6 * (size_t)nd;
+    double* z2 = W + 7 * (size_t)nd;
+    double* so = W + 8 * (size_t)nd;  // scratch primal for objectives
+    double *s, *y1, *y2;
+    if (A.smem_arrays) {
+        s = smem;
+        y1 = smem + nd;
+        y2 = smem + 2 * nd;
+    } else {
+        s = W + 9 * (size_t)nd;
+        y1 = W + 10 * (size_t)nd;
+        y2 = W + 11 * (size_t)nd;
+    }
+    const double* pv = A.pv;
+    const double a = A.a, b = A.b, tau = A.tau;
+    const double inv_tau = 1.0 / tau;
+    const double* in = A.in + c * (size_t)nd;
+    const double* gr = A.grad ? A.grad + c * (size_t)nd : nullptr;
+
+    if (tid == 0) flag_sh[0] = 0;
+    __syncthreads();
+    int bad = 0;
+    for (int i = tid; i < nd; i += nt) {
+        double kv = in[i];
+        if (gr) kv = kv - A.eta * gr[i];  // pattern.coords - eta * grad (optimizer.py:326)
+        if (!isfinite(kv)) bad = 1;
+        k[i] = kv;
+        q0[i] = 0.0;
+        q1[i] = 0.0;
+        q2[i] = 0.0;
+        y0[i] = 0.0;
+        y1[i] = 0.0;
+        y2[i] = 0.0;
+    }
+    if (bad) flag_sh[0] = 1;
+    __syncthreads();
+    if (tid == 0 && flag_sh[0] && A.nonfinite) atomicExch(A.nonfinite, 1);
+
+    const int n1 = (ns - 1) * D, n2 = (ns - 2) * D;
+    const int nterms = nd + (n1 > 0 ? n1 : 0) + (n2 > 0 ? n2 : 0);
+    const double ebound = 2.02 * (double)nterms * 1.1102230246251565e-16;
+    double t = 1.0, best = INFINITY;
+
+    for (int it = 0; it < A.n_pit; ++it) {
+        // ---- s = primal(y)
+        for (int n = tid; n < ns; n += nt) {
+            primal_row<D>(k, y0, y1, y2, ns, n, s);
+            if (n == A.pin)
+                for (int l = 0; l < D; ++l) s[n * D + l] = pv[l];
+        }
+        __syncthreads();
+        // ---- dual prox -> z, restart terms
+        double gd = 0.0, ga = 0.0;
+        for (int n = tid; n < ns; n += nt) {
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                const int e = n * D + l;
+                const double yv = y0[e];
+                const double z = yv * inv_tau + s[e];
+                const double pz = clamp_unit(z);
+                const double zz = tau * (z - pz);
+                z0[e] = zz;
+                const double term = (yv - zz) * (zz - q0[e]);
+                gd += term;
+                ga += fabs(term);
+            }
+            if (n <= ns - 2) {
+                double zv[D];
+                double nrm = 0.0;
+#pragma unroll
+                for (int l = 0; l < D; ++l) {
+                    const int e = n * D + l;
+                    const double z = y1[e] * inv_tau + (s[e + D] - s[e]);
+                    zv[l] = z;
+                    nrm += z * z;
+                }
+                nrm = sqrt(nrm);
+                const double scale = (nrm <= a) ? 0.0 : 1.0 - a / nrm;
+#pragma unroll
+                for (int l = 0; l < D; ++l) {
+                    const int e = n * D + l;
+                    const double zz = tau * zv[l] * scale;
+                    z1[e] = zz;
+                    const double term = (y1[e] - zz) * (zz - q1[e]);
+                    gd += term;
+                    ga += fabs(term);
+                }
+            }
+            if (n <= ns - 3) {
+                double zv[D];
+                double nrm = 0.0;
+#pragma unroll
+                for (int l = 0; l < D; ++l) {
+                    const int e = n * D + l;
+                    const double z =
+                        y2[e] * inv_tau + (s[e + 2 * D] - 2.0 * s[e + D] + s[e]);
+                    zv[l] = z;
+                    nrm += z * z;
+                }
+                nrm = sqrt(nrm);
+                const double scale = (nrm <= b) ? 0.0 : 1.0 - b / nrm;
+#pragma unroll
+                for (int l = 0; l < D; ++l) {
+                    const int e = n * D + l;
+                    const double zz = tau * zv[l] * scale;
+                    z2[e] = zz;
+                    const double term = (y2[e] - zz) * (zz - q2[e]);
+                    gd += term;
+                    ga += fabs(term);
+                }
+            }
+        }
+        block_sum2(gd, ga, red);  // contains __syncthreads: z*, y* visible block-wide
+        int restart;
+        if (fabs(gd) > ebound * ga) {
+            restart = gd > 0.0;
+        } else {
+            // Sign not certified: reproduce the reference's sequential sum exactly.
+            if (tid == 0) {
+                double g = 0.0;
+                for (int i = 0; i < nd; ++i) g += (y0[i] - z0[i]) * (z0[i] - q0[i]);
+                for (int i = 0; i < n1; ++i) g += (y1[i] - z1[i]) * (z1[i] - q1[i]);
+                for (int i = 0; i < n2; ++i) g += (y2[i] - z2[i]) * (z2[i] - q2[i]);
+                flag_sh[1] = g > 0.0;
+            }
+            __syncthreads();
+            restart = flag_sh[1];
+        }
+        int accept = 1;
+        if (A.monotone) {
+            // objective of the candidate z (projection.py:221-227)
+            for (int n = tid; n < ns; n += nt) {
+                primal_row<D>(k, z0, z1, z2, ns, n, so);
+                if (n == A.pin)
+                    for (int l = 0; l < D; ++l) so[n * D + l] = pv[l];
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const double obj = dual_objective_serial<D>(so, z0, z1, z2, ns, A.pin, pv, a, b);
+                int acc = 1;
+                if (obj > best) acc = 0;
+                else best = obj;
+                flag_sh[0] = acc;
+                red[70] = best;
+            }
+            __syncthreads();
+            accept = flag_sh[0];
+            best = red[70];
+        }
+        if (restart) t = 1.0;
+        const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+        if (A.monotone) {
+            const double mom_z = t / t_next;
+            const double mom_q = (t - 1.0) / t_next;
+            for (int n = tid; n < ns; n += nt) {
+#pragma unroll
+                for (int l = 0; l < D; ++l) {
+                    const int e = n * D + l;
+                    double nq = accept ? z0[e] : q0[e];
+                    y0[e] = nq + mom_z * (z0[e] - nq) + mom_q * (nq - q0[e]);
+                    q0[e] = nq;
+                    if (n <= ns - 2) {
+                        nq = accept ? z1[e] : q1[e];
+                        y1[e] = nq + mom_z * (z1[e] - nq) + mom_q * (nq - q1[e]);
+                        q1[e] = nq;
+                    }
+                    if (n <= ns - 3) {
+                        nq = accept ? z2[e] : q2[e];
+                        y2[e] = nq + mom_z * (z2[e] - nq) + mom_q * (nq - q2[e]);
+                        q2[e] = nq;
+                    }
+                }
+            }
+        } else {
+            const double mom = (t - 1.0) / t_next;
+            for (int n = tid; n < ns; n += nt) {
+#pragma unroll
+                for (int l = 0; l < D; ++l) {
+                    const int e = n * D + l;
+                    double zz = z0[e];
+                    y0[e] = zz + mom * (zz - q0[e]);
+                    q0[e] = zz;
+                    if (n <= ns - 2) {
+                        zz = z1[e];
+                        y1[e] = zz + mom * (zz - q1[e]);
+                        q1[e] = zz;
+                    }
+                    if (n <= ns - 3) {
+                        zz = z2[e];
+                        y2[e] = zz + mom * (zz - q2[e]);
+                        q2[e] = zz;
+                    }
+                }
+            }
+        }
+        t = t_next;
+        __syncthreads();
+        if (A.trace) {
+            for (int n = tid; n < ns; n += nt) {
+                primal_row<D>(k, q0, q1, q2, ns, n, so);
+                if (n == A.pin)
+                    for (int l = 0; l < D; ++l) so[n * D + l] = pv[l];
+            }
+            __syncthreads();
+            if (tid == 0)
+                A.trace[c * A.n_pit + it] =
+                    dual_objective_serial<D>(so, q0, q1, q2, ns, A.pin, pv, a, b);
+            __syncthreads();
+        }
+    }
+    // ---- out = primal(q)
+    double* out = A.out + c * (size_t)nd;
+    for (int n = tid; n < ns; n += nt) {
+        primal_row<D>(k, q0, q1, q2, ns, n, out);
+        if (n == A.pin)
+            for (int l = 0; l < D; ++l) out[n * D + l] = pv[l];
+    }
+}
+
+// ------------------------------------------------------------------- feasibility polish
+// Wavefront layout: lane L runs sweep (base + L).  At step t a lane
+//   (1) boxes sample t + 1 (and sets the pin first when t + 1 == pin),
+//   (2) applies the speed pair (t, t+1),
+//   (3) applies the acceleration triple (t-2, t-1, t),
+// which is exactly the reference's box -> speed -> accel order restricted to the samples
+// those operations touch.  Lane L runs LAG steps behind lane L-1; with LAG >= 4 the
+// samples touched by adjacent lanes in the same step are disjoint and every sample a lane
+// reads was finalised by the previous sweep.  Box at sample 0 happens at step -1.
+constexpr int PL_LAG = 4;
+
+template <int D>
+__device__ __forceinline__ void box_sample(double* s, int n, double& worst) {
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        const double v = s[n * D + l];
+        if (v > 1.0) {
+            if (v - 1.0 > worst) worst = v - 1.0;
+            s[n * D + l] = 1.0;
+        } else if (v < -1.0) {
+            if (-1.0 - v > worst) worst = -1.0 - v;
+            s[n * D + l] = -1.0;
+        }
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void speed_pair(double* s, int n, double a, int pin, double& worst) {
+    const double omega = 1.8;
+    double nrm = 0.0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        const double df = s[(n + 1) * D + l] - s[n * D + l];
+        nrm += df * df;
+    }
+    nrm = sqrt(nrm);
+    if (n == pin || n + 1 == pin) {
+        const int fr = (n == pin) ? n + 1 : n;
+        const double sign = (fr == n + 1) ? 1.0 : -1.0;
+        if (nrm > a) {
+            if (nrm - a > worst) worst = nrm - a;
+            const double shrink = omega * (nrm - a) / nrm;
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                const double df = s[(n + 1) * D + l] - s[n * D + l];
+                s[fr * D + l] -= sign * shrink * df;
+            }
+        }
+        return;
+    }
+    if (nrm > a) {
+        if (nrm - a > worst) worst = nrm - a;
+        const double shrink = omega * 0.5 * (nrm - a) / nrm;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            const double df = s[(n + 1) * D + l] - s[n * D + l];
+            s[n * D + l] += shrink * df;
+            s[(n + 1) * D + l] -= shrink * df;
+        }
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void accel_triple(double* s, int n, double b, int pin,
+                                             double& worst) {
+    const double omega = 1.8;
+    double nrm = 0.0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        const double w = s[n * D + l] - 2.0 * s[(n + 1) * D + l] + s[(n + 2) * D + l];
+        nrm += w * w;
+    }
+    nrm = sqrt(nrm);
+    if (nrm > b) {
+        if (nrm - b > worst) worst = nrm - b;
+        double c0 = 1.0, c1 = -2.0, c2 = 1.0;
+        if (pin == n) c0 = 0.0;
+        else if (pin == n + 1) c1 = 0.0;
+        else if (pin == n + 2) c2 = 0.0;
+        const double denom = c0 * c0 + c1 * c1 + c2 * c2;
+        if (denom > 0.0) {
+            const double step = omega * (nrm - b) / (denom * nrm);
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                const double w = s[n * D + l] - 2.0 * s[(n + 1) * D + l] + s[(n + 2) * D + l];
+                s[n * D + l] -= step * c0 * w;
+                s[(n + 1) * D + l] -= step * c1 * w;
+                s[(n + 2) * D + l] -= step * c2 * w;
+            }
+        }
+    }
+}
+
+// Run `nsw` consecutive sweeps (1..32) wavefront-pipelined on s; worst per sweep is
+// returned in lane order (lane L -> sweep L).  Called by the whole warp.
+template <int D>
+__device__ double pipelined_sweeps(double* s, int ns, double a, double b, int pin,
+                                   const double* pv, int nsw) {
+    const int lane = threadIdx.x & 31;
+    const bool active = lane < nsw;
+    double worst = 0.0;
+    const int t_first = -1;                    // box of sample 0
+    const int t_last = ns - 1 + 0;             // last step that does any work
+    const int n_steps = t_last - t_first + 1 + PL_LAG * (nsw - 1);
+    for (int step = 0; step < n_steps; ++step) {
+        const int t = t_first + step - PL_LAG * lane;
+        if (active && t >= t_first && t <= t_last) {
+            const int nb = t + 1;
+            if (nb < ns) {
+                if (nb == pin)
+                    for (int l = 0; l < D; ++l) s[nb * D + l] = pv[l];
+                box_sample<D>(s, nb, worst);
+            }
+            if (t >= 0 && t <= ns - 2) speed_pair<D>(s, t, a, pin, worst);
+            if (t - 2 >= 0 && t - 2 <= ns - 3) accel_triple<D>(s, t - 2, b, pin, worst);
+        }
+        __syncwarp();
+    }
+    return worst;
+}
+
+template <int D>
+__global__ void __launch_bounds__(32) polish_kernel(double* shots, long long n_shots, int ns,
+                                                    double a, double b, int pin, double pv0,
+                                                    double pv1, double pv2, double tol,
+                                                    int max_sweeps, double* ckpt_ws,
+                                                    int use_smem, int32_t* sweeps_out,
+                                                    float4* pos4) {
+    extern __shared__ __align__(16) double sm[];
+    const long long c = blockIdx.x;
+    const int lane = threadIdx.x;
+    const int nd = ns * D;
+    const double pv[3] = {pv0, pv1, pv2};
+    double* g = shots + c * (size_t)nd;
+    double* s = use_smem ? sm : g;
+    double* ck = use_smem ? sm + nd : ckpt_ws + c * (size_t)nd;
+    if (use_smem)
+        for (int i = lane; i < nd; i += 32) s[i] = g[i];
+    __syncwarp();
+    int done = 0;
+    int total = 0;
+    while (total < max_sweeps) {
+        const int nsw = min(32, max_sweeps - total);
+        for (int i = lane; i < nd; i += 32) ck[i] = s[i];
+        __syncwarp();
+        const double worst = pipelined_sweeps<D>(s, ns, a, b, pin, pv, nsw);
+        const unsigned ok = __ballot_sync(0xffffffffu, lane < nsw && worst <= tol);
+        if (ok) {
+            const int first = __ffs(ok) - 1;  // sweep index within the batch (0-based)
+            if (first != nsw - 1) {
+                // Roll back and replay only the sweeps up to the stopping one.
+                for (int i = lane; i < nd; i += 32) s[i] = ck[i];
+                __syncwarp();
+                pipelined_sweeps<D>(s, ns, a, b, pin, pv, first + 1);
+            }
+            total += first + 1;
+            done = 1;
+            break;
+        }
+        total += nsw;
+    }
+    (void)done;
+    __syncwarp();
+    for (int i = lane; i < nd; i += 32) g[i] = s[i];
+    if (pos4) {
+        for (int n = lane; n < ns; n += 32) {
+            const double* r = s + n * D;
+            pos4[c * ns + n] = make_float4((float)r[0], (float)r[1], D == 3 ? (float)r[2] : 0.f,
+                                           1.f);
+        }
+    }
+    if (lane == 0 && sweeps_out) sweeps_out[c] = total;
+}
+
+// ------------------------------------------------------------------ residuals
+constexpr int RS_THREADS = 256;
+
+template <int D>
+__global__ void residual_kernel(const double* __restrict__ co, int ns, int pin, double pv0,
+                                double pv1, double pv2, double* __restrict__ per_shot) {
+    __shared__ double red[4][RS_THREADS];
+    const long long c = blockIdx.x;
+    const double* x = co + c * (size_t)ns * D;
+    const double pv[3] = {pv0, pv1, pv2};
+    double amp = 0.0, sp = -INFINITY, ac = -INFINITY, pe = 0.0;
+    for (int n = threadIdx.x; n < ns; n += RS_THREADS) {
+        for (int l = 0; l < D; ++l) amp = fmax(amp, fabs(x[n * D + l]));
+        if (n <= ns - 2) {
+            double q = 0.0;
+            for (int l = 0; l < D; ++l) {
+                const double df = x[(n + 1) * D + l] - x[n * D + l];
+                q = (l == 0) ? df * df : q + df * df;
+            }
+            sp = fmax(sp, sqrt(q));
+        }
+        if (n <= ns - 3) {
+            double q = 0.0;
+            for (int l = 0; l < D; ++l) {
+                // np.diff(coords, 2) = diff of diffs
+                const double d2 = (x[(n + 2) * D + l] - x[(n + 1) * D + l]) -
+                                  (x[(n + 1) * D + l] - x[n * D + l]);
+                q = (l == 0) ? d2 * d2 : q + d2 * d2;
+            }
+            ac = fmax(ac, sqrt(q));
+        }
+        if (n == pin)
+            for (int l = 0; l < D; ++l) pe = fmax(pe, fabs(x[n * D + l] - pv[l]));
+    }
+    red[0][threadIdx.x] = amp;
+    red[1][threadIdx.x] = sp;
+    red[2][threadIdx.x] = ac;
+    red[3][threadIdx.x] = pe;
+    __syncthreads();
+    for (int w = RS_THREADS / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int q = 0; q < 4; ++q)
+                red[q][threadIdx.x] = fmax(red[q][threadIdx.x], red[q][threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) per_shot[c * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void residual_final_kernel(const double* __restrict__ per_shot, long long n_shots,
+                                      double a, double b, int has_pin,
+                                      double* __restrict__ out) {
+    __shared__ double red[4][RS_THREADS];
+    double m[4] = {0.0, -INFINITY, -INFINITY, 0.0};
+    for (long long c = threadIdx.x; c < n_shots; c += RS_THREADS)
+        for (int q = 0; q < 4; ++q) m[q] = fmax(m[q], per_shot[c * 4 + q]);
+    for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = m[q];
+    __syncthreads();
+    for (int w = RS_THREADS / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int q = 0; q < 4; ++q)
+                red[q][threadIdx.x] = fmax(red[q][threadIdx.x], red[q][threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        // feasibility_residuals (projection.py:435-452)
+        const double amp = fmax(red[0][0] - 1.0, 0.0);
+        const double sp = fmax(red[1][0] - a, 0.0);
+        const double ac = fmax(red[2][0] - b, 0.0);
+        const double pe = has_pin ? red[3][0] : 0.0;
+        out[0] = amp;
+        out[1] = sp;
+        out[2] = ac;
+        out[3] = pe;
+        out[4] = fmax(fmax(amp, sp), fmax(ac, pe));
+    }
+}
+
+// ------------------------------------------------------------------ upsample
+__global__ void upsample_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                long long n_shots, int ns, int dims) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long total = n_shots * 2 * ns * dims;
+    if (idx >= total) return;
+    const int l = (int)(idx % dims);
+    const long long m = (idx / dims) % (2 * ns);
+    const long long c = idx / ((long long)dims * 2 * ns);
+    const double* x = in + c * (long long)ns * dims;
+    double v;
+    if ((m & 1) == 0) {
+        v = x[(m / 2) * dims + l];
+    } else if (m < 2 * ns - 1) {
+        const long long j = m / 2;
+        v = 0.5 * (x[j * dims + l] + x[(j + 1) * dims + l]);
+    } else {
+        const double last = x[(ns - 1) * dims + l];
+        v = last + 0.5 * (last - x[(ns - 2) * dims + l]);
+    }
+    v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);  // np.clip
+    out[idx] = v;
+}
+
+// ------------------------------------------------------- field-path attraction
+// Mirrors attraction.py:116-255 (_clamp_points, _interp2/3, _cell_grad2/3), fp64.
+__global__ void field_eval_kernel(const double* __restrict__ pts, long long p, int dims,
+                                  const double* __restrict__ pot,
+                                  const double* __restrict__ force, long long n, int mode,
+                                  double* __restrict__ vals, double* __restrict__ grad,
+                                  unsigned long long* __restrict__ n_clamped) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const long long side = 2 * n + 1;
+    const double hi = 2.0 * (double)n;
+    double u[3] = {0, 0, 0};
+    bool bad = false;
+    for (int l = 0; l < dims; ++l) {
+        double v = (pts[i * dims + l] + 1.0) * (double)n;
+        if (v < 0.0) {
+            v = 0.0;
+            bad = true;
+        } else if (v > hi) {
+            v = hi;
+            bad = true;
+        }
+        u[l] = v;
+    }
+    if (bad) atomicAdd(n_clamped, 1ull);
+    long long i0 = (long long)u[0], j0 = (long long)u[1], k0 = dims == 3 ? (long long)u[2] : 0;
+    i0 = i0 < side - 2 ? i0 : side - 2;
+    j0 = j0 < side - 2 ? j0 : side - 2;
+    k0 = k0 < side - 2 ? k0 : side - 2;
+    const double fx = u[0] - (double)i0, fy = u[1] - (double)j0;
+    const double fz = dims == 3 ? u[2] - (double)k0 : 0.0;
+    const double scale = (double)n;
+    if (dims == 2) {
+        auto G = [&](const double* g, long long a, long long bb) { return g[a * side + bb]; };
+        auto interp2 = [&](const double* g) {
+            return (1 - fx) * (1 - fy) * G(g, i0, j0) + fx * (1 - fy) * G(g, i0 + 1, j0) +
+                   (1 - fx) * fy * G(g, i0, j0 + 1) + fx * fy * G(g, i0 + 1, j0 + 1);
+        };
+        vals[i] = interp2(pot);
+        if (mode == 0) {
+            double gx0 = G(pot, i0 + 1, j0) - G(pot, i0, j0);
+            double gx1 = G(pot, i0 + 1, j0 + 1) - G(pot, i0, j0 + 1);
+            if (fx == 0.0 && i0 > 0) {
+                gx0 = 0.5 * (G(pot, i0 + 1, j0) - G(pot, i0 - 1, j0));
+                gx1 = 0.5 * (G(pot, i0 + 1, j0 + 1) - G(pot, i0 - 1, j0 + 1));
+            }
+            grad[i * 2] = scale * ((1 - fy) * gx0 + fy * gx1);
+            double gy0 = G(pot, i0, j0 + 1) - G(pot, i0, j0);
+            double gy1 = G(pot, i0 + 1, j0 + 1) - G(pot, i0 + 1, j0);
+            if (fy == 0.0 && j0 > 0) {
+                gy0 = 0.5 * (G(pot, i0, j0 + 1) - G(pot, i0, j0 - 1));
+                gy1 = 0.5 * (G(pot, i0 + 1, j0 + 1) - G(pot, i0 + 1, j0 - 1));
+            }
+            grad[i * 2 + 1] = scale * ((1 - fx) * gy0 + fx * gy1);
+        } else {
+            const long long plane = side * side;
+            grad[i * 2] = interp2(force);
+            grad[i * 2 + 1] = interp2(force + plane);
+        }
+        return;
+    }
+    auto G3 = [&](const double* g, long long a, long long bb, long long cc) {
+        return g[(a * side + bb) * side + cc];
+    };
+    auto interp3 = [&](const double* g) {
+        double v = 0.0;
+        for (int ii = 0; ii < 2; ++ii) {
+            const double wx = ii == 1 ? fx : 1 - fx;
+            for (int jj = 0; jj < 2; ++jj) {
+                const double wy = jj == 1 ? fy : 1 - fy;
+                for (int kk = 0; kk < 2; ++kk) {
+                    const double wz = kk == 1 ? fz : 1 - fz;
+                    v += wx * wy * wz * G3(g, i0 + ii, j0 + jj, k0 + kk);
+                }
+            }
+        }
+        return v;
+    };
+    vals[i] = interp3(pot);
+    if (mode == 0) {
+        for (int ax = 0; ax < 3; ++ax) {
+            const double f_ax = ax == 0 ? fx : (ax == 1 ? fy : fz);
+            const long long a0 = ax == 0 ? i0 : (ax == 1 ? j0 : k0);
+            const bool central = f_ax == 0.0 && a0 > 0;
+            double g = 0.0;
+            for (int jj = 0; jj < 2; ++jj) {
+                for (int kk = 0; kk < 2; ++kk) {
+                    double w, hv, lv;
+                    if (ax == 0) {
+                        w = (jj == 1 ? fy : 1 - fy) * (kk == 1 ? fz : 1 - fz);
+                        hv = G3(pot, i0 + 1, j0 + jj, k0 + kk);
+                        lv = central ? G3(pot, i0 - 1, j0 + jj, k0 + kk)
+                                     : G3(pot, i0, j0 + jj, k0 + kk);
+                    } else if (ax == 1) {
+                        w = (jj == 1 ? fx : 1 - fx) * (kk == 1 ? fz : 1 - fz);
+                        hv = G3(pot, i0 + jj, j0 + 1, k0 + kk);
+                        lv = central ? G3(pot, i0 + jj, j0 - 1, k0 + kk)
+                                     : G3(pot, i0 + jj, j0, k0 + kk);
+                    } else {
+                        w = (jj == 1 ? fx : 1 - fx) * (kk == 1 ? fy : 1 - fy);
+                        hv = G3(pot, i0 + jj, j0 + kk, k0 + 1);
+                        lv = central ? G3(pot, i0 + jj, j0 + kk, k0 - 1)
+                                     : G3(pot, i0 + jj, j0 + kk, k0);
+                    }
+                    g += w * (hv - lv);
+                }
+            }
+            if (central) g *= 0.5;
+            grad[i * 3 + ax] = scale * g;
+        }
+    } else {
+        const long long vol = side * side * side;
+        for (int ax = 0; ax < 3; ++ax) grad[i * 3 + ax] = interp3(force + ax * vol);
+    }
+}
+
+}  // namespace spk
+
+using namespace spk;
+
+static size_t proj_state_doubles(int n_s, int dims) {
+    return (size_t)PJ_WS_ARRAYS * (size_t)n_s * dims;
+}
+
+extern "C" {
+
+size_t spk_project_workspace_bytes(int64_t n_shots, int n_s, int dims, int with_trace) {
+    (void)with_trace;
+    return (size_t)n_shots * proj_state_doubles(n_s, dims) * sizeof(double) + 256;
+}
+
+int spk_project_all(const double* in, const double* grad, double eta, double* out,
+                    int64_t n_shots, int n_s, int dims, double a, double b, int pin_idx,
+                    const double* pin_val, int n_pit, double tau, int monotone, double tol,
+                    int max_sweeps, void* pos4, int32_t* sweeps, double* trace,
+                    int32_t* nonfinite, void* ws, size_t ws_bytes, spk_stream_t stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(n_s >= 2, SPK_ERR_ARG, "projection needs at least 2 samples per shot");
+    SPK_REQUIRE(n_pit >= 1, SPK_ERR_ARG, "n_pit must be >= 1");
+    SPK_REQUIRE(pin_idx < n_s, SPK_ERR_ARG, "pinned_index %d out of range for N_s=%d",
+                pin_idx, n_s);
+    SPK_REQUIRE(max_sweeps >= 1, SPK_ERR_ARG, "max_sweeps must be >= 1");
+    if (n_shots <= 0) return SPK_OK;
+    const size_t need = spk_project_workspace_bytes(n_shots, n_s, dims, trace != nullptr);
+    SPK_REQUIRE(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE,
+                "projection workspace too small: need %zu, got %zu", need, ws_bytes);
+    ProjArgs A;
+    A.in = in;
+    A.grad = grad;
+    A.eta = eta;
+    A.out = out;
+    A.n_shots = n_shots;
+    A.ns = n_s;
+    A.a = a;
+    A.b = b;
+    A.pin = pin_idx < 0 ? -1 : pin_idx;
+    for (int l = 0; l < 3; ++l) A.pv[l] = (pin_idx >= 0 && l < dims) ? pin_val[l] : 0.0;
+    A.n_pit = n_pit;
+    A.tau = tau;
+    A.monotone = monotone;
+    A.trace = trace;
+    A.nonfinite = nonfinite;
+    A.ws = static_cast<double*>(ws);
+    A.ws_stride = (long long)proj_state_doubles(n_s, dims);
+    const size_t smem3 = (size_t)3 * n_s * dims * sizeof(double);
+    A.smem_arrays = smem3 <= (size_t)PJ_SMEM_LIMIT;
+    const size_t dyn = A.smem_arrays ? smem3 : 0;
+    int nt = PJ_THREADS;
+    if (n_s < PJ_THREADS) nt = ((n_s + 31) / 32) * 32;
+    if (dims == 3) {
+        cudaFuncSetAttribute(fista_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dyn);
+        fista_kernel<3><<<(unsigned)n_shots, nt, dyn, stream>>>(A);
+    } else {
+        cudaFuncSetAttribute(fista_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dyn);
+        fista_kernel<2><<<(unsigned)n_shots, nt, dyn, stream>>>(A);
+    }
+    SPK_CHECK_LAUNCH("fista_kernel");
+    // polish: state + checkpoint in shared memory when they fit (2 arrays)
+    const size_t psm = (size_t)2 * n_s * dims * sizeof(double);
+    const int use_smem = psm <= (size_t)PJ_SMEM_LIMIT;
+    double* ck = static_cast<double*>(ws);  // FISTA state is dead by now: reuse it
+    const size_t pdyn = use_smem ? psm : 0;
+    if (dims == 3) {
+        cudaFuncSetAttribute(polish_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pdyn);
+        polish_kernel<3><<<(unsigned)n_shots, 32, pdyn, stream>>>(
+            out, n_shots, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, ck,
+            use_smem, sweeps, (float4*)pos4);
+    } else {
+        cudaFuncSetAttribute(polish_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pdyn);
+        polish_kernel<2><<<(unsigned)n_shots, 32, pdyn, stream>>>(
+            out, n_shots, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, ck,
+            use_smem, sweeps, (float4*)pos4);
+    }
+    SPK_CHECK_LAUNCH("polish_kernel");
+    return SPK_OK;
+}
+
+size_t spk_residuals_workspace_bytes(int64_t n_shots) {
+    return (size_t)n_shots * 4 * sizeof(double) + 256;
+}
+
+int spk_feasibility_residuals(const double* coords, int64_t n_shots, int n_s, int dims,
+                              double a, double b, int pin_idx, const double* pin_val,
+                              double* out, void* ws, size_t ws_bytes, spk_stream_t stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    SPK_REQUIRE(n_shots >= 1 && n_s >= 1, SPK_ERR_ARG, "empty pattern");
+    SPK_REQUIRE(ws_bytes >= spk_residuals_workspace_bytes(n_shots), SPK_ERR_WORKSPACE,
+                "residual workspace too small");
+    double pv[3] = {0, 0, 0};
+    if (pin_idx >= 0)
+        for (int l = 0; l < dims; ++l) pv[l] = pin_val[l];
+    double* per = static_cast<double*>(ws);
+    if (dims == 3)
+        residual_kernel<3><<<(unsigned)n_shots, RS_THREADS, 0, stream>>>(
+            coords, n_s, pin_idx, pv[0], pv[1], pv[2], per);
+    else
+        residual_kernel<2><<<(unsigned)n_shots, RS_THREADS, 0, stream>>>(
+            coords, n_s, pin_idx, pv[0], pv[1], pv[2], per);
+    residual_final_kernel<<<1, RS_THREADS, 0, stream>>>(per, n_shots, a, b, pin_idx >= 0, out);
+    SPK_CHECK_LAUNCH("feasibility_residuals");
+    return SPK_OK;
+}
+
+int spk_upsample_shots(const double* in, double* out, int64_t n_shots, int n_s, int dims,
+                       spk_stream_t stream) {
+    SPK_REQUIRE(n_s >= 2, SPK_ERR_ARG, "need at least 2 samples to upsample");
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    const long long total = n_shots * 2LL * n_s * dims;
+    if (total == 0) return SPK_OK;
+    upsample_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        in, out, n_shots, n_s, dims);
+    SPK_CHECK_LAUNCH("upsample_shots");
+    return SPK_OK;
+}
+
+int spk_field_eval(const double* pts, int64_t p, int dims, const double* potential,
+                   const double* force, int64_t grid_n, int mode, double* vals, double* grad,
+                   int64_t* n_clamped, spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    SPK_REQUIRE(mode == 0 || mode == 1, SPK_ERR_ARG, "unknown grad mode %d", mode);
+    SPK_REQUIRE(grid_n >= 1, SPK_ERR_ARG, "grid_n must be >= 1");
+    SPK_REQUIRE(mode == 0 || force != nullptr, SPK_ERR_ARG, "smooth mode needs force grids");
+    cudaMemsetAsync(n_clamped, 0, sizeof(int64_t), (cudaStream_t)stream);
+    if (p <= 0) return SPK_OK;
+    field_eval_kernel<<<(unsigned)((p + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        pts, p, dims, potential, force, grid_n, mode, vals, grad,
+        reinterpret_cast<unsigned long long*>(n_clamped));
+    SPK_CHECK_LAUNCH("field_eval");
+    return SPK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,237 @@
+"""Device-resident state of one optimisation run, sharded over ranks.
+
+``ShardedRun`` owns the fp64 shot coordinates of this rank's contiguous block of shots,
+the float4 positions of ALL samples (the K1 sources), and the gradient buffers.  Each
+optimizer iteration is:
+
+  evaluate()      fused K1 + K2 (or field interpolation + K1) -> combine kernel
+                  -> 6 scalars -> all-gather, summed in rank order (deterministic)
+  step_project()  K3 with the step k - eta*grad in its prologue; the polish epilogue
+                  writes this rank's float4 positions straight into its slice of the
+                  gather buffer; NCCL all-gather of positions over NVLink
+  residual_max()  feasibility reduction -> all-gather max
+
+The device operations come from an ``ops`` object; the product uses :class:`CudaOps`
+(the sm_100a kernels).  Tests substitute CPU ops to exercise the multi-rank logic with
+the gloo backend.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _device, _native
+from .attraction import field_eval_device
+from .projection import project_device, residuals_device
+from .repulsion import direct_sums_device
+
+
+class CudaOps:
+    """The product device operations: every call is one of our sm_100a kernels."""
+
+    def __init__(self):
+        self.device = _device.device()
+
+    def empty(self, shape, dtype=torch.float64):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def to_device(self, arr: np.ndarray) -> torch.Tensor:
+        return _device.h2d(arr)
+
+    def pack(self, coords, out):
+        return _device.pack_positions(coords, out)
+
+    def sums(self, tgt4, src4, coords_local, fld, cfg):
+        """Raw attraction (val, grad) and repulsion (val, grad) sums for local targets."""
+        n_t = tgt4.shape[0]
+        d = cfg.dims
+        eps2_rep = cfg.repulsion.kernel_eps ** 2
+        vr = self.empty(n_t)
+        gr = self.empty((n_t, d))
+        if cfg.grad_mode == "exact":
+            va = self.empty(n_t)
+            ga = self.empty((n_t, d))
+            src = fld.device_sources()
+            n_cells = src.shape[0]
+            nbytes = _native.query("spk_nbody_workspace_bytes", n_t, n_cells, src4.shape[0])
+            ws = _device.workspace(nbytes, "nbody")
+            _native.call("spk_fused_sums", tgt4.data_ptr(), n_t, d, src.data_ptr(), n_cells,
+                         float(fld.kernel_eps ** 2), src4.data_ptr(), src4.shape[0],
+                         float(eps2_rep), va.data_ptr(), ga.data_ptr(), vr.data_ptr(),
+                         gr.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
+        else:
+            va, ga, _ = field_eval_device(coords_local.reshape(-1, d), fld, cfg.grad_mode)
+            vr, gr = direct_sums_device(tgt4, src4, d, eps2_rep)
+        return va, ga, vr, gr
+
+    def combine(self, va, ga, vr, gr, p, coords, prev_c, prev_g, grad_out):
+        n_t, d = ga.shape
+        out = self.empty(6)
+        ws = _device.workspace(_native.query("spk_combine_workspace_bytes", n_t), "combine")
+        _native.call("spk_combine_gradient", n_t, d, va.data_ptr(), ga.data_ptr(), float(p),
+                     vr.data_ptr(), gr.data_ptr(), float(p), coords.data_ptr(),
+                     _device.ptr(prev_c), _device.ptr(prev_g), grad_out.data_ptr(),
+                     out.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
+        return out
+
+    def project(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite):
+        return project_device(coords, proj_cfg, grad=grad, eta=eta, out=out, pos4=pos4,
+                              nonfinite=nonfinite)
+
+    def residuals(self, coords, proj_cfg):
+        return residuals_device(coords, proj_cfg)
+
+    def upsample(self, coords):
+        n_c, n_s, d = coords.shape
+        out = self.empty((n_c, 2 * n_s, d))
+        _native.call("spk_upsample_shots", coords.data_ptr(), out.data_ptr(), n_c, n_s, d,
+                     _device.stream())
+        return out
+
+
+class ShardedRun:
+    """Per-rank device state for :func:`optimize` (see module docstring)."""
+
+    def __init__(self, start: np.ndarray, cfg, fld, ops=None, group=None):
+        self.cfg = cfg
+        self.fld = fld
+        self.ops = ops if ops is not None else CudaOps()
+        if group is None and dist.is_available() and dist.is_initialized():
+            group = dist.group.WORLD
+        self.group = group
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
+        n_c, n_s, d = start.shape
+        base, extra = divmod(n_c, self.world)
+        self.counts = [base + (1 if r < extra else 0) for r in range(self.world)]
+        self.offsets = [sum(self.counts[:r]) for r in range(self.world)]
+        self.even = extra == 0
+        self.n_c, self.d = n_c, d
+        lo = self.offsets[self.rank]
+        self.local = self.counts[self.rank]
+        self.coords = self.ops.to_device(np.ascontiguousarray(start[lo:lo + self.local]))
+        self._level_buffers(n_s)
+
+    # ------------------------------------------------------------------ buffers
+    def _level_buffers(self, n_s: int):
+        ops, d = self.ops, self.d
+        self.n_s = n_s
+        self.p = self.n_c * n_s
+        self.pos4_all = ops.empty((self.p, 4), torch.float32)
+        if self.world == 1 or self.even:
+            off = self.offsets[self.rank] * n_s
+            self.pos4_local = self.pos4_all.narrow(0, off, self.local * n_s)
+        else:
+            self.pos4_local = ops.empty((max(self.counts) * n_s, 4), torch.float32)
+        self.next = ops.empty((self.local, n_s, d))
+        self.prev = ops.empty((self.local, n_s, d))
+        self.grad = ops.empty((self.local, n_s, d))
+        self.prev_grad = ops.empty((self.local, n_s, d))
+        self.flag = ops.empty(1, torch.int32)
+        self.have_prev = False
+        self.host_prev = None
+
+    # ------------------------------------------------------------ communication
+    def _gather_pos4(self):
+        if self.world == 1:
+            return
+        if self.even:
+            dist.all_gather_into_tensor(self.pos4_all, self.pos4_local, group=self.group)
+            return
+        m = max(self.counts) * self.n_s
+        pad = self.ops.empty((self.world * m, 4), torch.float32)
+        dist.all_gather_into_tensor(pad, self.pos4_local, group=self.group)
+        for r in range(self.world):
+            n = self.counts[r] * self.n_s
+            self.pos4_all[self.offsets[r] * self.n_s:self.offsets[r] * self.n_s + n] = \
+                pad[r * m:r * m + n]
+
+    def _all_scalars(self, t: torch.Tensor) -> np.ndarray:
+        """(world, k) host array of every rank's scalar vector, rank order."""
+        if self.world == 1:
+            return t.detach().to("cpu").numpy()[None]
+        buf = self.ops.empty((self.world, t.numel()), t.dtype)
+        dist.all_gather_into_tensor(buf, t.reshape(1, -1), group=self.group)
+        return buf.to("cpu").numpy()
+
+    # --------------------------------------------------------------- iteration
+    def project(self, proj_cfg):
+        """Level-start projection (no step)."""
+        out = self.ops.project(self.coords, proj_cfg, None, 0.0, self.next,
+                               self._pos4_target(), None)
+        self.coords, self.next = out, self.coords
+        self._gather_pos4()
+        self.have_prev = False
+        self.host_prev = None
+
+    def _pos4_target(self):
+        n = self.local * self.n_s
+        return self.pos4_local if self.pos4_local.shape[0] == n else self.pos4_local[:n]
+
+    def evaluate(self):
+        """Fused device evaluation -> (att_cost, rep_cost, n_nonfinite, (dkdg, dgdg))."""
+        tgt = self._pos4_target()
+        va, ga, vr, gr = self.ops.sums(tgt, self.pos4_all, self.coords, self.fld, self.cfg)
+        prev_c = self.prev if self.have_prev else None
+        prev_g = self.prev_grad if self.have_prev else None
+        scal = self.ops.combine(va, ga, vr, gr, self.p, self.coords, prev_c, prev_g,
+                                self.grad.view(-1, self.d))
+        allv = self._all_scalars(scal)
+        tot = np.zeros(allv.shape[1])
+        for r in range(allv.shape[0]):
+            tot = tot + allv[r]
+        p = self.p
+        att_cost = float(tot[0] / p)
+        rep_cost = float(tot[1] / (2.0 * p * p))
+        return att_cost, rep_cost, int(tot[4]), (float(tot[2]), float(tot[3]))
+
+    def set_host_gradient(self, grad: np.ndarray):
+        """Patched-evaluator path (single rank): install a host gradient, return the BB
+        dot products computed with numpy exactly as step_size does."""
+        coords = self.gather_coords()
+        dots = (0.0, 0.0)
+        if self.host_prev is not None:
+            pc, pg = self.host_prev
+            dk = coords - pc
+            dg = grad - pg
+            dots = (float(np.vdot(dk, dg)), float(np.vdot(dg, dg)))
+        self.host_prev = (coords.copy(), grad)
+        self.grad.copy_(torch.from_numpy(np.ascontiguousarray(grad, dtype=np.float64)))
+        return dots
+
+    def step_project(self, proj_cfg, eta: float) -> bool:
+        """coords <- P(coords - eta * grad); returns False if the step was non-finite."""
+        self.flag.zero_()
+        out = self.ops.project(self.coords, proj_cfg, self.grad, float(eta), self.next,
+                               self._pos4_target(), self.flag)
+        # rotate: prev <- coords, coords <- out, next <- old prev
+        self.prev, self.coords, self.next = self.coords, out, self.prev
+        self.prev_grad, self.grad = self.grad, self.prev_grad
+        self.have_prev = True
+        bad = self._all_scalars(self.flag.to(torch.float64))
+        self._gather_pos4()
+        return not bool(bad.max() > 0)
+
+    def residual_max(self, proj_cfg) -> float:
+        r = self.ops.residuals(self.coords, proj_cfg)
+        allv = self._all_scalars(r)
+        return float(allv[:, 4].max())
+
+    def upsample(self):
+        self.coords = self.ops.upsample(self.coords)
+        self._level_buffers(self.coords.shape[1])
+
+    def gather_coords(self) -> np.ndarray:
+        """All ranks' fp64 coordinates, global shot order, on the host."""
+        if self.world == 1:
+            return self.coords.detach().to("cpu").numpy().copy()
+        m = max(self.counts)
+        loc = self.ops.empty((m, self.n_s, self.d))
+        loc[:self.local] = self.coords
+        buf = self.ops.empty((self.world * m, self.n_s, self.d))
+        dist.all_gather_into_tensor(buf, loc, group=self.group)
+        host = buf.to("cpu").numpy()
+        parts = [host[r * m:r * m + self.counts[r]] for r in range(self.world)]
+        return np.ascontiguousarray(np.concatenate(parts, axis=0))

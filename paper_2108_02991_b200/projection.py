@@ -1,0 +1,184 @@
+"""Constraint projection K3 on the B200 (fp64, one CTA per shot + warp wavefront polish).
+
+Projects each shot onto {|s| <= 1, ||s[n+1]-s[n]|| <= alpha dt, ||s[n+2]-2s[n+1]+s[n]||
+<= beta dt^2, s[pin] = v} with the reference's algorithm
+(/root/reference/pkg/src/vdtraj/projection.py): dual FISTA with gradient restart
+(:169-284) then the over-relaxed cyclic feasibility polish (:287-373).  The kernels are
+bit-identical to the reference on the same inputs and step size tau (csrc/project.cu).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .core import FEAS_TOL, LinearConstraint, NormalizedLimits, SamplingPattern
+
+MAX_POLISH_SWEEPS = 50000
+_LAMBDA_CACHE: dict = {}
+
+
+@dataclass
+class ProjectionConfig:
+    """Same fields, defaults and validation as the reference (projection.py:28-68)."""
+
+    alpha: float
+    beta: float
+    raster_dt: float
+    n_pit: int = 100
+    feas_tol: float = FEAS_TOL
+    pin: LinearConstraint | None = None
+    monotone: bool = False
+
+    def __post_init__(self):
+        if self.n_pit < 1:
+            raise ValueError("n_pit must be >= 1")
+        if self.feas_tol <= 0:
+            raise ValueError("feas_tol must be positive")
+        if self.raster_dt <= 0:
+            raise ValueError("raster_dt must be positive")
+        if self.alpha < 0 or self.beta < 0:
+            raise ValueError("alpha and beta must be non-negative")
+
+    @classmethod
+    def from_limits(cls, limits: NormalizedLimits, raster_dt: float, **kw):
+        return cls(alpha=limits.alpha, beta=limits.beta, raster_dt=raster_dt, **kw)
+
+    @property
+    def speed_bound(self) -> float:
+        return self.alpha * self.raster_dt
+
+    @property
+    def accel_bound(self) -> float:
+        return self.beta * self.raster_dt**2
+
+
+def _gram_apply(x: np.ndarray, pin_idx: int) -> np.ndarray:
+    """(I + D1^T D1 + D2^T D2) x with the pinned coordinate removed, evaluated with the
+    same elementwise sequence as projection.py:86-95 (so lambda is bit-identical)."""
+    n = x.shape[0]
+    first = np.diff(x)
+    second = np.diff(x, 2)
+    out = x.copy()
+    out[:-1] -= first
+    out[1:] += first
+    out[: n - 2] += second
+    out[1 : n - 1] -= 2 * second
+    out[2:] += second
+    if pin_idx >= 0:
+        out[pin_idx] = 0.0
+    return out
+
+
+def stacked_operator_norm(n_s: int, pin_idx: int) -> float:
+    """lambda_max of the stacked constraint operator by 50 power iterations from
+    default_rng(12345) (projection.py:71-100); cached per (n_s, pin_idx).  tau = 1/lambda."""
+    key = (int(n_s), int(pin_idx))
+    hit = _LAMBDA_CACHE.get(key)
+    if hit is not None:
+        return hit
+    x = np.random.default_rng(12345).standard_normal(n_s)
+    if pin_idx >= 0:
+        x[pin_idx] = 0.0
+    for _ in range(50):
+        x /= np.linalg.norm(x)
+        x = _gram_apply(x, pin_idx)
+    lam = float(np.linalg.norm(x))
+    _LAMBDA_CACHE[key] = lam
+    return lam
+
+
+_stacked_operator_norm = stacked_operator_norm  # reference-private name
+
+
+def _pin_arrays(cfg: ProjectionConfig, dims: int):
+    if cfg.pin is None:
+        return -1, np.zeros(dims)
+    value = np.asarray(cfg.pin.pinned_value, dtype=np.float64)
+    if value.shape != (dims,):
+        raise ValueError(f"pinned_value must have {dims} components")
+    return int(cfg.pin.pinned_index), value
+
+
+def project_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad=None, eta=0.0,
+                   out: torch.Tensor | None = None, pos4=None, sweeps=None, trace=None,
+                   nonfinite=None, tau: float | None = None,
+                   max_sweeps: int = MAX_POLISH_SWEEPS) -> torch.Tensor:
+    """K3 on device buffers: out = P(coords - eta * grad) for every shot.
+
+    ``coords``/``grad``/``out``: (n_shots, n_s, d) fp64 CUDA tensors.  ``pos4`` (optional)
+    receives the float4 positions of the result (the next N-body's sources)."""
+    n_c, n_s, dims = coords.shape
+    pin_idx, pin_val = _pin_arrays(cfg, dims)
+    if pin_idx >= n_s:
+        raise ValueError(f"pinned_index {pin_idx} out of range for N_s={n_s}")
+    if n_s < 2:
+        raise ValueError("projection needs at least 2 samples per shot")
+    if tau is None:
+        tau = 1.0 / stacked_operator_norm(n_s, pin_idx)
+    if out is None:
+        out = torch.empty_like(coords)
+    nbytes = _native.query("spk_project_workspace_bytes", n_c, n_s, dims, int(trace is not None))
+    ws = _device.workspace(nbytes, "project")
+    pv = _native.f64_array(list(pin_val) + [0.0] * (3 - dims))
+    _native.call("spk_project_all", coords.data_ptr(), _device.ptr(grad), float(eta),
+                 out.data_ptr(), n_c, n_s, dims, cfg.speed_bound, cfg.accel_bound, pin_idx,
+                 pv, cfg.n_pit, float(tau), int(bool(cfg.monotone)), 0.1 * cfg.feas_tol,
+                 int(max_sweeps), _device.ptr(pos4), _device.ptr(sweeps), _device.ptr(trace),
+                 _device.ptr(nonfinite), ws.data_ptr(), ws.numel(), _device.stream())
+    return out
+
+
+def project_shot(shot: np.ndarray, cfg: ProjectionConfig, return_trace: bool = False):
+    """Project one (N_s, d) shot (projection.py:394-418); optionally the dual objective
+    after every FISTA iteration."""
+    shot = np.ascontiguousarray(shot, dtype=np.float64)
+    if shot.ndim != 2:
+        raise ValueError("shot must be (N_s, d)")
+    dev_in = _device.h2d(shot[None])
+    trace = None
+    if return_trace:
+        trace = torch.empty(cfg.n_pit, dtype=torch.float64, device=dev_in.device)
+    out = project_device(dev_in, cfg, trace=trace)
+    res = _device.d2h(out)[0]
+    if return_trace:
+        return res, _device.d2h(trace)
+    return res
+
+
+def project_pattern(k: SamplingPattern, cfg: ProjectionConfig) -> SamplingPattern:
+    """Project every shot independently (projection.py:421-432); bit-exact shot
+    independence holds because each shot is one CTA / one warp with no cross-shot
+    state."""
+    coords = np.ascontiguousarray(k.coords)
+    out = project_device(_device.h2d(coords), cfg)
+    return SamplingPattern(_device.d2h(out))
+
+
+def residuals_device(coords: torch.Tensor, cfg: ProjectionConfig,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device feasibility residuals -> tensor [amplitude, speed, accel, pin, max]."""
+    n_c, n_s, dims = coords.shape
+    pin_idx, pin_val = _pin_arrays(cfg, dims)
+    if out is None:
+        out = torch.empty(5, dtype=torch.float64, device=coords.device)
+    ws = _device.workspace(_native.query("spk_residuals_workspace_bytes", n_c), "resid")
+    pv = _native.f64_array(list(pin_val) + [0.0] * (3 - dims))
+    _native.call("spk_feasibility_residuals", coords.data_ptr(), n_c, n_s, dims,
+                 cfg.speed_bound, cfg.accel_bound, pin_idx, pv, out.data_ptr(),
+                 ws.data_ptr(), ws.numel(), _device.stream())
+    return out
+
+
+def feasibility_residuals(k: SamplingPattern, cfg: ProjectionConfig) -> dict:
+    """Max violation per constraint (projection.py:435-452)."""
+    vals = _device.d2h(residuals_device(_device.h2d(k.coords), cfg))
+    res = {"amplitude": float(vals[0]), "speed": float(vals[1]),
+           "acceleration": float(vals[2])}
+    if cfg.pin is not None:
+        res["pin"] = float(vals[3])
+    res["max"] = max(res.values())
+    return res

@@ -1,0 +1,282 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE itself.
+
+Run in the authoring container only (the reference does not exist on the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+It imports ``vdtraj`` from /root/reference/pkg/src (read-only, never copied) and writes
+small ``.npz`` files of seeded inputs and the reference's outputs.  The tests compare
+the CPU oracle (bitwise), the host-side mirror (bitwise) and the CUDA kernels (bitwise
+for fp64 projection, tolerance for fp32 N-body) against these vectors.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+from vdtraj import _treecode as tc  # noqa: E402
+from vdtraj import attraction as at  # noqa: E402
+from vdtraj import core, density, optimizer as om, projection as pr  # noqa: E402
+from vdtraj.repulsion import eval_repulsion_direct  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def radial_cloud(rng, p, d):
+    r = rng.uniform(0, 1, p) ** 2
+    v = rng.normal(size=(p, d))
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    return np.ascontiguousarray(r[:, None] * v)
+
+
+def repulsion_fixtures():
+    rng = np.random.default_rng(20260101)
+    cases = {}
+    inputs = {
+        "u2d": (rng.uniform(-1, 1, (257, 2)), 1e-6),
+        "r3d": (radial_cloud(rng, 300, 3), 1e-6),
+        "pair0": (np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]]), 0.0),
+        "coinc": (np.zeros((3, 2)), 0.01),
+        "spokes3d": (om.perturb(om.init_radial(16, 64, 3), 0.25, 0).points().copy(), 1e-6),
+        "spokes2d": (om.perturb(om.init_radial(8, 128, 2), 0.25, 0).points().copy(), 1e-6),
+        "dup3d": (np.repeat(rng.uniform(-0.5, 0.5, (40, 3)), 3, axis=0), 1e-6),
+    }
+    for name, (pts, eps2) in inputs.items():
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        val = np.empty(pts.shape[0])
+        grad = np.empty_like(pts)
+        tc.direct_sums(pts, eps2, val, grad)
+        cases[f"{name}_pos"] = pts
+        cases[f"{name}_eps2"] = np.float64(eps2)
+        cases[f"{name}_val"] = val
+        cases[f"{name}_grad"] = grad
+        c, g = eval_repulsion_direct(pts, float(np.sqrt(eps2)))
+        cases[f"{name}_cost"] = np.float64(c)
+        cases[f"{name}_gnorm"] = g
+    # subset rows
+    pts = cases["spokes3d_pos"]
+    tg = np.arange(0, pts.shape[0], 7, dtype=np.int64)
+    val = np.empty(tg.shape[0])
+    grad = np.empty((tg.shape[0], 3))
+    tc.direct_sums_subset(pts, tg, 1e-6, val, grad)
+    cases["subset_targets"] = tg
+    cases["subset_val"] = val
+    cases["subset_grad"] = grad
+    cases["names"] = np.array(list(inputs.keys()))
+    np.savez_compressed(os.path.join(OUT, "repulsion.npz"), **cases)
+
+
+def attraction_fixtures():
+    rng = np.random.default_rng(20260202)
+    out = {}
+    # (name, grid, grid_n, eps)
+    specs = [
+        ("d2", density.discretize(density.DensityParams(0.25, 2.0), 8, 2).grid, 8, 0.05),
+        ("d3", density.discretize(density.DensityParams(0.25, 2.0), 4, 3).grid, 4, None),
+        ("r2", density.TargetDensity(rng.uniform(0, 1, (13, 13)), 6).grid, 6, 0.1),
+        ("delta2", None, 8, 0.05),
+    ]
+    for name, grid, n, eps in specs:
+        if grid is None:
+            grid = np.zeros((2 * n + 1,) * 2)
+            grid[n, n] = 1.0
+        rho = density.TargetDensity(grid=grid, grid_n=n)
+        fld = at.precompute_field(rho, kernel_eps=eps)
+        out[f"{name}_rho"] = rho.grid
+        out[f"{name}_n"] = np.int64(n)
+        out[f"{name}_eps"] = np.float64(fld.kernel_eps)
+        out[f"{name}_potential"] = fld.potential
+        out[f"{name}_force"] = fld.force
+        d = rho.dims
+        pts = rng.uniform(-1.05, 1.05, (37, d))
+        pts[0] = 0.0
+        pts[1] = np.array([1.0, -1.0, 0.5][:d])  # on the boundary / a node
+        pat = core.SamplingPattern(pts[None])
+        for mode in ("consistent", "smooth"):
+            res = at.eval_attraction(pat, fld, mode)
+            out[f"{name}_{mode}_cost"] = np.float64(res.cost)
+            out[f"{name}_{mode}_grad"] = res.grad
+            out[f"{name}_{mode}_nclamp"] = np.int64(res.n_clamped)
+        out[f"{name}_pts"] = pts
+        out[f"{name}_interp"] = at.interpolate(fld.potential, pts, n)
+    out["names"] = np.array([s[0] for s in specs])
+    np.savez_compressed(os.path.join(OUT, "attraction.npz"), **out)
+
+
+def _project_case(shot, cfg, want_trace=False):
+    if want_trace:
+        o, tr = pr.project_shot(shot, cfg, return_trace=True)
+        return o, tr
+    return pr.project_shot(shot, cfg), None
+
+
+def projection_fixtures():
+    rng = np.random.default_rng(20260303)
+    out = {}
+    names = []
+
+    def add(name, shots, cfg, trace=False):
+        names.append(name)
+        pin_idx, pin_val = pr._pin_arrays(cfg, shots.shape[2])
+        out[f"{name}_in"] = shots
+        out[f"{name}_a"] = np.float64(cfg.speed_bound)
+        out[f"{name}_b"] = np.float64(cfg.accel_bound)
+        out[f"{name}_pin"] = np.int64(pin_idx)
+        out[f"{name}_pinval"] = pin_val
+        out[f"{name}_npit"] = np.int64(cfg.n_pit)
+        out[f"{name}_mono"] = np.int64(cfg.monotone)
+        out[f"{name}_tol"] = np.float64(0.1 * cfg.feas_tol)
+        out[f"{name}_lam"] = np.float64(pr._stacked_operator_norm(shots.shape[1], pin_idx))
+        if trace:
+            o, tr = pr.project_shot(shots[0], cfg, return_trace=True)
+            out[f"{name}_out"] = o[None]
+            out[f"{name}_trace"] = tr
+        else:
+            out[f"{name}_out"] = pr.project_pattern(core.SamplingPattern(shots), cfg).coords
+        # FISTA-only output (n_pit iterations, no polish) via the numba kernel
+        fo = np.empty_like(shots)
+        for c in range(shots.shape[0]):
+            pr._project_shot(shots[c], cfg.speed_bound, cfg.accel_bound, pin_idx, pin_val,
+                             cfg.n_pit, 1.0 / out[f"{name}_lam"], cfg.monotone, fo[c],
+                             np.empty(0))
+        out[f"{name}_fista"] = fo
+
+    desk = dict(alpha=10216.0, beta=4.6e7, raster_dt=1e-5)
+    add("desk2d", rng.uniform(-1.1, 1.1, (6, 24, 2)), pr.ProjectionConfig(n_pit=60, **desk))
+    add("qp2d", rng.uniform(-1.5, 1.5, (3, 8, 2)),
+        pr.ProjectionConfig(alpha=0.3, beta=0.15, raster_dt=1.0, n_pit=1000))
+    pin = core.LinearConstraint(pinned_index=3, pinned_value=np.array([0.1, -0.2]))
+    add("pin2d", rng.uniform(-1.2, 1.2, (2, 9, 2)),
+        pr.ProjectionConfig(alpha=0.4, beta=0.2, raster_dt=1.0, n_pit=200, pin=pin))
+    add("mono2d", rng.uniform(-1.4, 1.4, (1, 32, 2)),
+        pr.ProjectionConfig(alpha=0.3, beta=0.15, raster_dt=1.0, n_pit=150, monotone=True),
+        trace=True)
+    add("trace3d", rng.uniform(-1.2, 1.2, (1, 20, 3)),
+        pr.ProjectionConfig(alpha=0.5, beta=0.3, raster_dt=1.0, n_pit=80), trace=True)
+    add("clamp2d", np.full((1, 12, 2), 1.5),
+        pr.ProjectionConfig(alpha=1e9, beta=1e12, raster_dt=1.0, n_pit=200))
+    add("tiny", rng.uniform(-1.5, 1.5, (3, 2, 3)),
+        pr.ProjectionConfig(alpha=0.3, beta=0.1, raster_dt=1.0, n_pit=30))
+    # In-loop 3D shots at full3d hardware limits (scale 4): projected init + a step.
+    hw = core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                           dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
+                           dims=3)
+    lim = core.normalized_limits(hw).scaled(4.0)
+    ns = 512
+    pin3 = core.LinearConstraint(pinned_index=ns // 2, pinned_value=np.zeros(3))
+    cfg3 = pr.ProjectionConfig(alpha=lim.alpha, beta=lim.beta, raster_dt=1e-5, n_pit=100,
+                               pin=pin3)
+    base = om.perturb(om.init_radial(9, ns, 3), 0.75, 0)
+    feas = pr.project_pattern(base, cfg3)
+    stepped = feas.coords[:4] + rng.uniform(-2e-3, 2e-3, (4, ns, 3))
+    add("inloop3d", stepped, cfg3)
+    add("fresh3d", base.coords[:2].copy(), cfg3)
+    # 2D in-loop shots at desk limits, N_s=256 (config-1-like)
+    hw2 = core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                            dwell_dt=2e-6, fov=0.192, matrix=64, dims=2)
+    lim2 = core.normalized_limits(hw2)
+    pin2 = core.LinearConstraint(pinned_index=128, pinned_value=np.zeros(2))
+    cfg2 = pr.ProjectionConfig(alpha=lim2.alpha, beta=lim2.beta, raster_dt=1e-5, n_pit=100,
+                               pin=pin2)
+    base2 = om.perturb(om.init_radial(8, 256, 2), 0.25, 1)
+    feas2 = pr.project_pattern(base2, cfg2)
+    add("inloop2d", feas2.coords[:3] + rng.uniform(-5e-3, 5e-3, (3, 256, 2)), cfg2)
+
+    # Polish-only cases with sweep counts (reference kernel called directly).
+    pol_in = out["inloop3d_fista"][:2].copy()
+    pol_out = pol_in.copy()
+    for c in range(2):
+        pr._feasibility_polish(pol_out[c], cfg3.speed_bound, cfg3.accel_bound, ns // 2,
+                               np.zeros(3), 1e-7, 50000)
+    out["polish_in"] = pol_in
+    out["polish_out"] = pol_out
+    out["polish_a"] = np.float64(cfg3.speed_bound)
+    out["polish_b"] = np.float64(cfg3.accel_bound)
+    out["polish_pin"] = np.int64(ns // 2)
+    # max_sweeps-capped polish
+    capped = pol_in.copy()
+    for c in range(2):
+        pr._feasibility_polish(capped[c], cfg3.speed_bound, cfg3.accel_bound, ns // 2,
+                               np.zeros(3), 1e-7, 37)
+    out["polish_capped37"] = capped
+
+    # operator norms
+    lam_keys = [(32, 16), (1024, 512), (2048, 1024), (256, -1), (9, 3), (2, -1), (3, 1)]
+    out["lam_keys"] = np.array(lam_keys, dtype=np.int64)
+    out["lam_vals"] = np.array([pr._stacked_operator_norm(n, p) for n, p in lam_keys])
+    # feasibility residuals
+    fr = pr.feasibility_residuals(core.SamplingPattern(out["inloop3d_in"]), cfg3)
+    out["feas_inloop3d_in"] = np.array([fr["amplitude"], fr["speed"], fr["acceleration"],
+                                        fr["pin"], fr["max"]])
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "projection.npz"), **out)
+
+
+def host_fixtures():
+    out = {}
+    for n_c, n_s, d in ((8, 33, 2), (16, 32, 3), (4096, 4, 3), (1, 9, 2)):
+        out[f"init_{n_c}_{n_s}_{d}"] = om.init_radial(n_c, n_s, d).coords
+    base = om.init_radial(16, 64, 3)
+    out["perturb_3d_s7"] = om.perturb(base, 0.5, 7).coords
+    out["perturb_2d_s0"] = om.perturb(om.init_radial(64, 512, 2), 0.25, 0).coords
+    rng = np.random.default_rng(5)
+    c = rng.uniform(-0.9, 0.9, (3, 16, 3))
+    out["ups_in"] = c
+    out["ups_out"] = om.upsample_shots(core.SamplingPattern(c)).coords
+    hw = core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                           dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
+                           dims=3)
+    lim = core.normalized_limits(hw)
+    out["lim_full3d"] = np.array([lim.alpha, lim.beta])
+    out["dens_2d_16"] = density.discretize(density.DensityParams(0.25, 2.0), 16, 2).grid
+    out["dens_3d_6"] = density.discretize(density.DensityParams(0.3, 1.0), 6, 3).grid
+    dk = rng.normal(size=40)
+    dg = rng.normal(size=40)
+    out["bb_dk"] = dk
+    out["bb_dg"] = dg
+    out["bb_eta"] = np.float64(om.step_size(25, 0.5, dk, dg, 0.01, 20))
+    np.savez_compressed(os.path.join(OUT, "host.npz"), **out)
+
+
+def optimize_fixture():
+    """A tiny stock ``optimize`` run (2D, direct backend) for end-to-end drift checks."""
+    hw = core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                           dwell_dt=1e-5, fov=0.192, matrix=32, dims=2)
+    out = {}
+    for mode in ("consistent", "smooth"):
+        cfg = om.OptimizerConfig(n_c=8, n_s=64, dims=2, n_decim=1, n_git=6, n_pit=100,
+                                 perturbation=0.25, seed=3, grad_mode=mode,
+                                 repulsion=om.RepulsionConfig(backend="direct"))
+        res = om.optimize(cfg, hw)
+        out[f"{mode}_coords"] = res.pattern.coords
+        out[f"{mode}_costs"] = res.trace.costs()
+        out[f"{mode}_steps"] = np.array([r.step for r in res.trace.records])
+        out[f"{mode}_att"] = np.array([r.attraction for r in res.trace.records])
+        out[f"{mode}_rep"] = np.array([r.repulsion for r in res.trace.records])
+        out[f"{mode}_feas"] = np.array([r.feas_residual for r in res.trace.records])
+    cfg = om.OptimizerConfig(n_c=4, n_s=32, dims=2, n_decim=0, n_git=0, perturbation=0.2,
+                             seed=5, repulsion=om.RepulsionConfig(backend="direct"))
+    res = om.optimize(cfg, core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6,
+                                             raster_dt=1e-5, dwell_dt=1e-5, fov=0.192,
+                                             matrix=64, dims=2))
+    out["ngit0_coords"] = res.pattern.coords
+    out["ngit0_initial"] = res.initial.coords
+    np.savez_compressed(os.path.join(OUT, "optimize.npz"), **out)
+
+
+if __name__ == "__main__":
+    repulsion_fixtures()
+    attraction_fixtures()
+    projection_fixtures()
+    host_fixtures()
+    optimize_fixture()
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))

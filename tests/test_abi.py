@@ -1,0 +1,66 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports exactly the
+entry points include/sparkling_b200.h declares (no compute calls here)."""
+
+import os
+import re
+import subprocess
+
+import paper_2108_02991_b200 as spk
+from paper_2108_02991_b200 import _build, _native
+
+HEADER = os.path.join(_build.INCLUDE, "sparkling_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(spk_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = _native.load()
+    names = declared_symbols()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _native.SIGNATURES, name
+    assert lib.spk_version() == 1
+    nm = subprocess.run(["nm", "-D", "--defined-only", _build.LIB_PATH], capture_output=True,
+                        text=True, check=True).stdout
+    exported = set(re.findall(r" T (spk_\w+)", nm))
+    assert exported == set(names)
+
+
+def test_sass_is_sm100a_and_uses_blackwell_paths():
+    """The N-body kernel is compiled for sm_100a with FFMA2/FADD2 packed f32x2 math, MUFU
+    rsqrt and UBLKCP bulk copies (cp.async.bulk)."""
+    out = subprocess.run(["cuobjdump", "-sass", _build.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    assert "sm_100a" in out
+    nb = out[out.index("nbody_kernel"):]
+    for mnemonic in ("FFMA2", "FADD2", "MUFU.RSQ", "UBLKCP", "SYNCS"):
+        assert mnemonic in nb, mnemonic
+
+
+def test_public_surface_mirrors_reference_names():
+    needed = {"optimize", "step_size", "eval_repulsion", "eval_repulsion_direct",
+              "eval_repulsion_tree", "eval_attraction", "precompute_field", "project_pattern",
+              "project_shot", "feasibility_residuals", "SamplingPattern", "HardwareSpec",
+              "OptimizerConfig", "RepulsionConfig", "ProjectionConfig", "KernelField",
+              "TargetDensity", "DensityParams", "discretize", "init_radial", "perturb",
+              "upsample_shots", "normalized_limits", "LinearConstraint", "RunTrace"}
+    assert needed <= set(spk.__all__)
+
+
+def test_no_cpu_fallback_without_cuda(monkeypatch):
+    import torch
+
+    from paper_2108_02991_b200 import _device
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    import numpy as np
+    import pytest
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        spk.eval_repulsion_direct(np.zeros((4, 3)))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _device.device()

@@ -1,0 +1,129 @@
+"""Field-path attraction (bitwise with the reference's grids) and the GPU-resident
+optimize loop (drop-in behaviour, determinism, guards, drift vs the reference)."""
+
+import numpy as np
+import pytest
+
+from spk_golden import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spk():
+    import paper_2108_02991_b200 as m
+
+    return m
+
+
+def desk_hw(spk, dims=2, matrix=64):
+    return spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                            dwell_dt=1e-5, fov=0.192, matrix=matrix, dims=dims)
+
+
+def test_field_eval_bitwise_with_reference_grids(spk):
+    att = golden("attraction")
+    for name in att["names"]:
+        fld = spk.KernelField(potential=att[f"{name}_potential"], force=att[f"{name}_force"],
+                              grid_n=int(att[f"{name}_n"]), kernel_eps=float(att[f"{name}_eps"]))
+        pat = spk.SamplingPattern(att[f"{name}_pts"][None])
+        for mode in ("consistent", "smooth"):
+            res = spk.eval_attraction(pat, fld, mode)
+            assert res.cost == float(att[f"{name}_{mode}_cost"]), (name, mode)
+            assert np.array_equal(res.grad, att[f"{name}_{mode}_grad"]), (name, mode)
+            assert res.n_clamped == int(att[f"{name}_{mode}_nclamp"])
+        from paper_2108_02991_b200.attraction import interpolate
+
+        vals = interpolate(att[f"{name}_potential"], att[f"{name}_pts"], int(att[f"{name}_n"]))
+        assert np.array_equal(vals, att[f"{name}_interp"])
+
+
+def test_n_git_zero_is_projected_init(spk):
+    g = golden("optimize")
+    cfg = spk.OptimizerConfig(n_c=4, n_s=32, dims=2, n_decim=0, n_git=0, perturbation=0.2,
+                              seed=5, repulsion=spk.RepulsionConfig(backend="direct"))
+    res = spk.optimize(cfg, desk_hw(spk))
+    assert np.array_equal(res.initial.coords, g["ngit0_initial"])
+    assert np.array_equal(res.pattern.coords, g["ngit0_coords"])
+    assert len(res.trace.records) == 0
+
+
+def test_deterministic(spk):
+    cfg = spk.OptimizerConfig(n_c=4, n_s=32, dims=2, n_decim=1, n_git=5, perturbation=0.2,
+                              seed=5, repulsion=spk.RepulsionConfig(backend="direct"))
+    a = spk.optimize(cfg, desk_hw(spk))
+    b = spk.optimize(cfg, desk_hw(spk))
+    assert np.array_equal(a.pattern.coords, b.pattern.coords)
+
+
+@pytest.mark.parametrize("mode", ["consistent", "smooth"])
+def test_drift_vs_reference_optimize(spk, mode):
+    """Same config / seed as the reference run in tests/golden/optimize.npz.  The only
+    numeric difference is the fp32 repulsion sums (rel 1e-6); report the drift."""
+    g = golden("optimize")
+    hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                          dwell_dt=1e-5, fov=0.192, matrix=32, dims=2)
+    cfg = spk.OptimizerConfig(n_c=8, n_s=64, dims=2, n_decim=1, n_git=6, n_pit=100,
+                              perturbation=0.25, seed=3, grad_mode=mode,
+                              repulsion=spk.RepulsionConfig(backend="direct"))
+    res = spk.optimize(cfg, hw)
+    costs = res.trace.costs()
+    assert np.abs(costs - g[f"{mode}_costs"]).max() <= 1e-6 * np.abs(g[f"{mode}_costs"]).max()
+    drift = np.abs(res.pattern.coords - g[f"{mode}_coords"]).max()
+    print(f"[drift] {mode}: max |coords - reference| = {drift:.3e}")
+    assert drift <= 1e-4
+
+
+def test_final_pattern_feasible(spk):
+    hw = desk_hw(spk)
+    cfg = spk.OptimizerConfig(n_c=8, n_s=64, dims=2, n_decim=2, n_git=8, perturbation=0.25,
+                              seed=2, repulsion=spk.RepulsionConfig(backend="direct"))
+    res = spk.optimize(cfg, hw)
+    lim = spk.normalized_limits(hw)
+    pc = spk.ProjectionConfig(alpha=lim.alpha, beta=lim.beta, raster_dt=hw.raster_dt)
+    assert spk.feasibility_residuals(res.pattern, pc)["max"] <= pc.feas_tol
+    assert res.pattern.samples_per_shot == 64
+
+
+def test_exact_mode_runs_3d(spk):
+    hw = desk_hw(spk, dims=3, matrix=16)
+    cfg = spk.OptimizerConfig(n_c=16, n_s=64, dims=3, n_decim=1, n_git=4, grad_mode="exact",
+                              seed=2)
+    res = spk.optimize(cfg, hw)
+    assert np.all(np.isfinite(res.trace.costs()))
+    assert len(res.trace.records) == 8
+
+
+def test_divergence_guard_with_patched_evaluator(spk, monkeypatch):
+    import paper_2108_02991_b200.optimizer as om
+
+    calls = {"n": 0}
+
+    def exploding(k, cfg2):
+        calls["n"] += 1
+        return -(10.0 ** calls["n"]), np.zeros((k.n_samples, k.dims))
+
+    monkeypatch.setattr(om, "eval_repulsion", exploding)
+    cfg = spk.OptimizerConfig(n_c=4, n_s=32, dims=2, n_decim=0, n_git=10, perturbation=0.2,
+                              seed=1, repulsion=spk.RepulsionConfig(backend="direct"))
+    with pytest.raises(spk.DivergenceError, match="divergence guard"):
+        spk.optimize(cfg, desk_hw(spk))
+
+
+def test_non_finite_aborts(spk, monkeypatch):
+    import paper_2108_02991_b200.optimizer as om
+
+    monkeypatch.setattr(om, "eval_repulsion",
+                        lambda k, c: (np.nan, np.zeros((k.n_samples, k.dims))))
+    cfg = spk.OptimizerConfig(n_c=4, n_s=32, dims=2, n_decim=0, n_git=5, perturbation=0.2,
+                              seed=1)
+    with pytest.raises(spk.DivergenceError, match="non-finite"):
+        spk.optimize(cfg, desk_hw(spk))
+
+
+def test_fixed_phase_monotone(spk):
+    cfg = spk.OptimizerConfig(n_c=8, n_s=64, dims=2, n_decim=0, n_git=20, n_pit=400,
+                              perturbation=0.25, seed=3,
+                              repulsion=spk.RepulsionConfig(backend="direct"))
+    res = spk.optimize(cfg, desk_hw(spk))
+    assert np.max(np.diff(res.trace.costs())) <= 1e-8

@@ -1,0 +1,146 @@
+"""K3 projection kernels vs the reference's golden vectors: BIT-IDENTICAL.
+
+tau is taken from the fixture (the reference's lambda) so that the comparison does not
+depend on the host BLAS used for the power iteration on the GPU box."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from spk_golden import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spk():
+    import paper_2108_02991_b200 as m
+
+    return m
+
+
+@pytest.fixture(scope="module")
+def proj():
+    return golden("projection")
+
+
+def cfg_of(spk, proj, name):
+    a, b = float(proj[f"{name}_a"]), float(proj[f"{name}_b"])
+    pin = int(proj[f"{name}_pin"])
+    pc = None if pin < 0 else spk.LinearConstraint(pin, proj[f"{name}_pinval"])
+    # raster_dt = 1 so that speed_bound == a and accel_bound == b exactly
+    cfg = spk.ProjectionConfig(alpha=a, beta=b, raster_dt=1.0, n_pit=int(proj[f"{name}_npit"]),
+                               pin=pc, monotone=bool(proj[f"{name}_mono"]))
+    return cfg, 1.0 / float(proj[f"{name}_lam"])
+
+
+def run(spk, shots, cfg, tau, trace=False, max_sweeps=50000):
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.projection import project_device
+
+    dev = _device.h2d(shots)
+    tr = None
+    if trace:
+        tr = torch.empty(shots.shape[0] * cfg.n_pit, dtype=torch.float64, device=dev.device)
+    sweeps = torch.empty(shots.shape[0], dtype=torch.int32, device=dev.device)
+    out = project_device(dev, cfg, tau=tau, trace=tr, sweeps=sweeps, max_sweeps=max_sweeps)
+    return (_device.d2h(out), None if tr is None else _device.d2h(tr), _device.d2h(sweeps))
+
+
+def test_bounds_roundtrip(spk, proj):
+    # speed_bound/accel_bound with raster_dt=1 reproduce the fixture's a, b exactly
+    for name in proj["names"]:
+        cfg, _ = cfg_of(spk, proj, name)
+        assert cfg.speed_bound == float(proj[f"{name}_a"])
+        assert cfg.accel_bound == float(proj[f"{name}_b"])
+
+
+def test_project_all_bitwise(spk, proj):
+    for name in proj["names"]:
+        cfg, tau = cfg_of(spk, proj, name)
+        out, _, _ = run(spk, proj[f"{name}_in"], cfg, tau)
+        ref = proj[f"{name}_out"]
+        assert np.array_equal(out, ref), (name, np.abs(out - ref).max())
+
+
+def test_trace_bitwise(spk, proj):
+    for name in ("mono2d", "trace3d"):
+        cfg, tau = cfg_of(spk, proj, name)
+        out, tr, _ = run(spk, proj[f"{name}_in"], cfg, tau, trace=True)
+        assert np.array_equal(tr, proj[f"{name}_trace"]), name
+        assert np.array_equal(out, proj[f"{name}_out"]), name
+
+
+def test_polish_sweeps_and_cap(spk, proj):
+    """Wavefront polish reproduces the sequential stopping sweep and the max_sweeps cap."""
+    name = "inloop3d"
+    cfg, tau = cfg_of(spk, proj, name)
+    shots = proj[f"{name}_in"]
+    _, ref_sweeps = orc.project_all(shots, cfg.speed_bound, cfg.accel_bound,
+                                    cfg.pin.pinned_index, np.zeros(3), cfg.n_pit, tau,
+                                    0.1 * cfg.feas_tol)
+    out, _, sweeps = run(spk, shots, cfg, tau)
+    assert np.array_equal(sweeps, ref_sweeps)
+    assert np.array_equal(out, proj[f"{name}_out"])
+    for cap in (1, 31, 32, 33, 37):
+        ref_c, _ = orc.project_all(shots, cfg.speed_bound, cfg.accel_bound,
+                                   cfg.pin.pinned_index, np.zeros(3), cfg.n_pit, tau,
+                                   0.1 * cfg.feas_tol, max_sweeps=cap)
+        out_c, _, sw = run(spk, shots, cfg, tau, max_sweeps=cap)
+        assert np.all(sw == cap)
+        assert np.array_equal(out_c, ref_c), cap
+
+
+def test_random_cases_vs_oracle(spk):
+    rng = np.random.default_rng(99)
+    for d in (2, 3):
+        for ns, pin in ((5, 2), (64, -1), (300, 150), (1024, 512)):
+            shots = rng.uniform(-1.3, 1.3, (3, ns, d))
+            pc = None if pin < 0 else spk.LinearConstraint(pin, np.full(d, 0.05))
+            cfg = spk.ProjectionConfig(alpha=0.05, beta=0.01, raster_dt=1.0, n_pit=50, pin=pc)
+            tau = 1.0 / spk.projection.stacked_operator_norm(ns, pin)
+            out, _, sw = run(spk, shots, cfg, tau)
+            ref, rsw = orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, pin,
+                                       np.full(d, 0.05), 50, tau, 0.1 * cfg.feas_tol)
+            assert np.array_equal(sw, rsw), (d, ns)
+            assert np.array_equal(out, ref), (d, ns, np.abs(out - ref).max())
+
+
+def test_public_api(spk, proj):
+    rng = np.random.default_rng(4)
+    cfg = spk.ProjectionConfig(alpha=10216.0, beta=4.6e7, raster_dt=1e-5, n_pit=80)
+    shot = rng.uniform(-1.1, 1.1, (32, 2))
+    single = spk.project_shot(shot, cfg)
+    pat = spk.project_pattern(spk.SamplingPattern(shot[None]), cfg)
+    assert np.array_equal(pat.coords[0], single)
+    coords = rng.uniform(-1.1, 1.1, (6, 24, 2))
+    out = spk.project_pattern(spk.SamplingPattern(coords), cfg)
+    perm = rng.permutation(6)
+    out_p = spk.project_pattern(spk.SamplingPattern(coords[perm]), cfg)
+    assert np.array_equal(out_p.coords, out.coords[perm])
+    pin = spk.LinearConstraint(pinned_index=4, pinned_value=np.array([0.1, -0.2]))
+    c2 = spk.ProjectionConfig(alpha=0.4, beta=0.2, raster_dt=1.0, n_pit=200, pin=pin)
+    o = spk.project_shot(rng.uniform(-1, 1, (9, 2)), c2)
+    assert np.array_equal(o[4], pin.pinned_value)
+    with pytest.raises(ValueError):
+        spk.project_shot(rng.uniform(-1, 1, (3, 2)), c2)  # pin out of range
+
+
+def test_feasibility_residuals(spk, proj):
+    name = "inloop3d"
+    cfg, _ = cfg_of(spk, proj, name)
+    res = spk.feasibility_residuals(spk.SamplingPattern(proj[f"{name}_in"]), cfg)
+    ref = proj["feas_inloop3d_in"]
+    got = np.array([res["amplitude"], res["speed"], res["acceleration"], res["pin"],
+                    res["max"]])
+    assert np.array_equal(got, ref)
+
+
+def test_upsample_device_bitwise(spk):
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.engine import CudaOps
+
+    h = golden("host")
+    out = CudaOps().upsample(_device.h2d(h["ups_in"]))
+    assert np.array_equal(_device.d2h(out), h["ups_out"])
