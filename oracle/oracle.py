@@ -46,6 +46,8 @@ def _load():
         lib.or_direct_sums_subset.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int, _i64p,
                                               ctypes.c_int64, ctypes.c_double, _f64p, _f64p,
                                               ctypes.c_int]
+        lib.or_cross_sums.argtypes = [_f64p, ctypes.c_int64, _f64p, ctypes.c_int64,
+                                      ctypes.c_int, ctypes.c_double, _f64p, _f64p, ctypes.c_int]
         lib.or_grid_sums.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int, _f64p, _i64p,
                                      ctypes.c_double, _f64p, _f64p, ctypes.c_int]
         lib.or_project_shot.argtypes = [_f64p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
@@ -92,6 +94,18 @@ def direct_sums_subset(pos, targets, eps2, nthreads=0):
     grad = np.empty((m, d))
     _load().or_direct_sums_subset(_p(pos), p, d, _p(targets, _i64p), m, float(eps2),
                                   _p(val), _p(grad), int(nthreads))
+    return val, grad
+
+
+def cross_sums(targets, sources, eps2, nthreads=0):
+    """direct_sums rows for separate target points (sharded form of _treecode.py:506)."""
+    tgt = np.ascontiguousarray(targets, dtype=np.float64)
+    src = np.ascontiguousarray(sources, dtype=np.float64)
+    m, d = tgt.shape
+    val = np.empty(m)
+    grad = np.empty((m, d))
+    _load().or_cross_sums(_p(tgt), m, _p(src), src.shape[0], d, float(eps2), _p(val),
+                          _p(grad), int(nthreads))
     return val, grad
 
 

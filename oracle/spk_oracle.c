@@ -47,16 +47,15 @@ int or_max_threads(void) {
 #define ROW_BLOCK 8
 #define SRC_TILE 2048
 
-static void rows_block(const double* pos, int64_t p, int d, const int64_t* rows, int nr,
+static void rows_block(const double* pos, int64_t p, int d, const double* tcoords, int nr,
                        double eps2, double* val, double* grad) {
     double v[ROW_BLOCK] = {0}, gx[ROW_BLOCK] = {0}, gy[ROW_BLOCK] = {0}, gz[ROW_BLOCK] = {0};
     for (int64_t j0 = 0; j0 < p; j0 += SRC_TILE) {
         const int64_t j1 = (j0 + SRC_TILE < p) ? j0 + SRC_TILE : p;
         for (int r = 0; r < nr; ++r) {
-            const int64_t i = rows[r];
-            const double xi = pos[i * d + 0];
-            const double yi = pos[i * d + 1];
-            const double zi = (d == 3) ? pos[i * d + 2] : 0.0;
+            const double xi = tcoords[r * d + 0];
+            const double yi = tcoords[r * d + 1];
+            const double zi = (d == 3) ? tcoords[r * d + 2] : 0.0;
             double vv = v[r], ax = gx[r], ay = gy[r], az = gz[r];
             if (d == 3) {
                 for (int64_t j = j0; j < j1; ++j) {
@@ -104,16 +103,23 @@ static void rows_block(const double* pos, int64_t p, int d, const int64_t* rows,
     }
 }
 
-static void rows_all(const double* pos, int64_t p, int d, const int64_t* targets, int64_t m,
-                     double eps2, double* val, double* grad) {
+/* Target rows come from `tcoords` (m, d) when given, else from pos[targets[r]] (or
+ * pos[r] when targets is NULL). */
+static void rows_all(const double* pos, int64_t p, int d, const int64_t* targets,
+                     const double* tcoords, int64_t m, double eps2, double* val,
+                     double* grad) {
     const int64_t nblk = (m + ROW_BLOCK - 1) / ROW_BLOCK;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t b = 0; b < nblk; ++b) {
-        int64_t rows[ROW_BLOCK];
+        double tc[ROW_BLOCK * 3];
         const int64_t r0 = b * ROW_BLOCK;
         const int nr = (int)((m - r0 < ROW_BLOCK) ? m - r0 : ROW_BLOCK);
-        for (int r = 0; r < nr; ++r) rows[r] = targets ? targets[r0 + r] : r0 + r;
-        rows_block(pos, p, d, rows, nr, eps2, val + r0, grad + r0 * d);
+        for (int r = 0; r < nr; ++r) {
+            const double* src = tcoords ? tcoords + (r0 + r) * d
+                                        : pos + (targets ? targets[r0 + r] : r0 + r) * d;
+            for (int l = 0; l < d; ++l) tc[r * d + l] = src[l];
+        }
+        rows_block(pos, p, d, tc, nr, eps2, val + r0, grad + r0 * d);
     }
 }
 
@@ -121,7 +127,7 @@ static void rows_all(const double* pos, int64_t p, int d, const int64_t* targets
 void or_direct_sums(const double* pos, int64_t p, int d, double eps2,
                     double* val, double* grad, int nthreads) {
     set_threads(nthreads);
-    rows_all(pos, p, d, NULL, p, eps2, val, grad);
+    rows_all(pos, p, d, NULL, NULL, p, eps2, val, grad);
 }
 
 /* direct_sums_subset (_treecode.py:474-503): rows for a list of targets.  Also used
@@ -129,7 +135,15 @@ void or_direct_sums(const double* pos, int64_t p, int d, double eps2,
 void or_direct_sums_subset(const double* pos, int64_t p, int d, const int64_t* targets,
                            int64_t m, double eps2, double* val, double* grad, int nthreads) {
     set_threads(nthreads);
-    rows_all(pos, p, d, targets, m, eps2, val, grad);
+    rows_all(pos, p, d, targets, NULL, m, eps2, val, grad);
+}
+
+/* Rows for arbitrary target points against the sources `pos` (the sharded form:
+ * this rank's samples as targets, all samples as sources). */
+void or_cross_sums(const double* tgt, int64_t m, const double* pos, int64_t p, int d,
+                   double eps2, double* val, double* grad, int nthreads) {
+    set_threads(nthreads);
+    rows_all(pos, p, d, NULL, tgt, m, eps2, val, grad);
 }
 
 /* Exact density-weighted attraction sums over a (2N_a+1)-per-axis node grid.

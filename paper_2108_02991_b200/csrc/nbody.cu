@@ -34,7 +34,11 @@ constexpr int NB_PAIRS = NB_TPT / 2;        // f32x2 pairs per thread
 constexpr int NB_TB = NB_THREADS * NB_TPT;  // targets per CTA
 constexpr int NB_TILE = 512;                // sources per shared-memory stage
 constexpr int NB_STAGES = 4;
-constexpr int NB_SMEM = NB_STAGES * NB_TILE * 16;
+constexpr int NB_TILE_BYTES = NB_STAGES * NB_TILE * 16;
+// fp64 per-target accumulators live in shared memory (per-thread slots) so that the
+// kernel fits 128 registers and two CTAs (16 warps) share an SM.
+constexpr int NB_ACC_BYTES = NB_TPT * 4 * NB_THREADS * 8;
+constexpr int NB_SMEM = NB_TILE_BYTES + NB_ACC_BYTES;
 constexpr int NB_MAX_CHUNKS = 192;
 
 struct SegDesc {
@@ -109,7 +113,7 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
                                           float4* tiles, uint64_t* bars,
                                           const float2 (&X)[NB_PAIRS],
                                           const float2 (&Y)[NB_PAIRS],
-                                          const float2 (&Z)[NB_PAIRS], double (&acc)[NB_TPT][4]) {
+                                          const float2 (&Z)[NB_PAIRS], double* acc) {
     const int tid = threadIdx.x;
     const float2 e2 = make_float2(S.eps2, S.eps2);
     auto issue = [&](long long t, int stage) {
@@ -135,17 +139,18 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
         }
         mbar_wait(&bars[stage], parity);
         tile_pairs<D, W, G>(tiles + stage * NB_TILE, cnt, X, Y, Z, e2, av, ax, ay, az);
+#define NB_ACC(k, c) acc[((k) * 4 + (c)) * NB_THREADS + tid]
 #pragma unroll
         for (int k = 0; k < NB_PAIRS; ++k) {
-            acc[2 * k][0] += av[k].x;
-            acc[2 * k + 1][0] += av[k].y;
-            acc[2 * k][1] += ax[k].x;
-            acc[2 * k + 1][1] += ax[k].y;
-            acc[2 * k][2] += ay[k].x;
-            acc[2 * k + 1][2] += ay[k].y;
+            NB_ACC(2 * k, 0) += av[k].x;
+            NB_ACC(2 * k + 1, 0) += av[k].y;
+            NB_ACC(2 * k, 1) += ax[k].x;
+            NB_ACC(2 * k + 1, 1) += ax[k].y;
+            NB_ACC(2 * k, 2) += ay[k].x;
+            NB_ACC(2 * k + 1, 2) += ay[k].y;
             if (D == 3) {
-                acc[2 * k][3] += az[k].x;
-                acc[2 * k + 1][3] += az[k].y;
+                NB_ACC(2 * k, 3) += az[k].x;
+                NB_ACC(2 * k + 1, 3) += az[k].y;
             }
         }
         __syncthreads();  // every warp is done with this stage
@@ -154,8 +159,9 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
 }
 
 template <int D>
-__global__ void __launch_bounds__(NB_THREADS, 1) nbody_kernel(const NBParams P) {
+__global__ void __launch_bounds__(NB_THREADS, 2) nbody_kernel(const NBParams P) {
     extern __shared__ __align__(128) float4 tiles[];
+    double* acc = reinterpret_cast<double*>(reinterpret_cast<char*>(tiles) + NB_TILE_BYTES);
     __shared__ __align__(8) uint64_t bars[NB_STAGES];
     const int tid = threadIdx.x;
     const long long unit = blockIdx.x;
@@ -179,9 +185,8 @@ __global__ void __launch_bounds__(NB_THREADS, 1) nbody_kernel(const NBParams P) 
         Y[k] = make_float2(a.y, b.y);
         Z[k] = make_float2(D == 3 ? a.z : 0.f, D == 3 ? b.z : 0.f);
     }
-    double acc[NB_TPT][4];
 #pragma unroll
-    for (int k = 0; k < NB_TPT; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
+    for (int k = 0; k < NB_TPT * 4; ++k) acc[k * NB_THREADS + tid] = 0.0;
 
     if (tid == 0) {
         for (int s = 0; s < NB_STAGES; ++s) mbar_init(&bars[s], 1);
@@ -203,10 +208,10 @@ __global__ void __launch_bounds__(NB_THREADS, 1) nbody_kernel(const NBParams P) 
     for (int k = 0; k < NB_TPT; ++k) {
         const long long i = base + k * NB_THREADS;
         if (i < P.n_tgt) {
-            slot[i] = acc[k][0];
-            slot[P.n_tgt + i] = acc[k][1];
-            slot[2 * P.n_tgt + i] = acc[k][2];
-            if (D == 3) slot[3 * P.n_tgt + i] = acc[k][3];
+            slot[i] = NB_ACC(k, 0);
+            slot[P.n_tgt + i] = NB_ACC(k, 1);
+            slot[2 * P.n_tgt + i] = NB_ACC(k, 2);
+            if (D == 3) slot[3 * P.n_tgt + i] = NB_ACC(k, 3);
         }
     }
 }
@@ -243,6 +248,10 @@ static int nbody_slots() {
     static int slots = 0;
     if (slots == 0) {
         int occ = 0;
+        cudaFuncSetAttribute(nbody_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             NB_SMEM);
+        cudaFuncSetAttribute(nbody_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             NB_SMEM);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbody_kernel<3>, NB_THREADS,
                                                           NB_SMEM) != cudaSuccess ||
             occ <= 0) {

@@ -377,177 +377,253 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
 }
 
 // ------------------------------------------------------------------- feasibility polish
-// Wavefront layout: lane L runs sweep (base + L).  At step t a lane
-//   (1) boxes sample t + 1 (and sets the pin first when t + 1 == pin),
-//   (2) applies the speed pair (t, t+1),
-//   (3) applies the acceleration triple (t-2, t-1, t),
-// which is exactly the reference's box -> speed -> accel order restricted to the samples
-// those operations touch.  Lane L runs LAG steps behind lane L-1; with LAG >= 4 the
-// samples touched by adjacent lanes in the same step are disjoint and every sample a lane
-// reads was finalised by the previous sweep.  Box at sample 0 happens at step -1.
+// The polish (_feasibility_polish, projection.py:287-373) is a Gauss-Seidel recurrence:
+// every sweep is box(all) -> speed pairs n = 0..ns-2 -> accel triples n = 0..ns-3, and
+// sweeps repeat until the worst violation of a sweep is <= tol.  It is run as a
+// SYSTOLIC WAVEFRONT: lane g of the CTA executes sweep (base + g).  At its local step t a
+// lane applies
+//     S(t)     speed pair (t, t+1)
+//     A(t-2)   accel triple (t-2, t-1, t)       -> sample t-2 is now final for this sweep
+//     B(t+2)   box of sample t+2 (pin set first) on the value handed over by lane g-1
+// which touches each sample in exactly the reference's per-sample operation order.  The
+// samples a lane is working on live in registers (a 4-sample window); finished samples
+// are handed to the next sweep with a warp shuffle (shared memory across warp
+// boundaries, one extra step of lag).  Lane g runs 4 steps behind lane g-1, the minimum
+// for which the windows of consecutive sweeps never overlap out of order.  A batch of
+// B = 32 W sweeps reads the state from one shared buffer and the last sweep writes the
+// other, so the batch input doubles as the checkpoint: if sweep j < B-1 is the stopping
+// sweep, the batch is replayed with j + 1 lanes.  Every element sees the same IEEE fp64
+// operations in the same order as the reference => bit-identical results and sweep count.
 constexpr int PL_LAG = 4;
 
 template <int D>
-__device__ __forceinline__ void box_sample(double* s, int n, double& worst) {
+struct Sample {
+    double v[D];
+};
+
+template <int D>
+__device__ __forceinline__ void box_sample(Sample<D>& s, double& worst) {
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double v = s[n * D + l];
+        const double v = s.v[l];
         if (v > 1.0) {
             if (v - 1.0 > worst) worst = v - 1.0;
-            s[n * D + l] = 1.0;
+            s.v[l] = 1.0;
         } else if (v < -1.0) {
             if (-1.0 - v > worst) worst = -1.0 - v;
-            s[n * D + l] = -1.0;
+            s.v[l] = -1.0;
         }
     }
 }
 
+// Speed pair (n, n+1) on registers x0 = s[n], x1 = s[n+1] (projection.py:313-345).
 template <int D>
-__device__ __forceinline__ void speed_pair(double* s, int n, double a, int pin, double& worst) {
+__device__ __forceinline__ void speed_pair(Sample<D>& x0, Sample<D>& x1, int n, double a,
+                                           int pin, double& worst) {
     const double omega = 1.8;
     double nrm = 0.0;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double df = s[(n + 1) * D + l] - s[n * D + l];
+        const double df = x1.v[l] - x0.v[l];
         nrm += df * df;
     }
     nrm = sqrt(nrm);
+    if (!(nrm > a)) return;
+    if (nrm - a > worst) worst = nrm - a;
     if (n == pin || n + 1 == pin) {
-        const int fr = (n == pin) ? n + 1 : n;
-        const double sign = (fr == n + 1) ? 1.0 : -1.0;
-        if (nrm > a) {
-            if (nrm - a > worst) worst = nrm - a;
-            const double shrink = omega * (nrm - a) / nrm;
+        // move only the free endpoint of a pinned pair
+        const double shrink = omega * (nrm - a) / nrm;
+        if (n == pin) {
 #pragma unroll
             for (int l = 0; l < D; ++l) {
-                const double df = s[(n + 1) * D + l] - s[n * D + l];
-                s[fr * D + l] -= sign * shrink * df;
+                const double df = x1.v[l] - x0.v[l];
+                x1.v[l] -= 1.0 * shrink * df;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                const double df = x1.v[l] - x0.v[l];
+                x0.v[l] -= -1.0 * shrink * df;
             }
         }
         return;
     }
-    if (nrm > a) {
-        if (nrm - a > worst) worst = nrm - a;
-        const double shrink = omega * 0.5 * (nrm - a) / nrm;
+    const double shrink = omega * 0.5 * (nrm - a) / nrm;
 #pragma unroll
-        for (int l = 0; l < D; ++l) {
-            const double df = s[(n + 1) * D + l] - s[n * D + l];
-            s[n * D + l] += shrink * df;
-            s[(n + 1) * D + l] -= shrink * df;
-        }
+    for (int l = 0; l < D; ++l) {
+        const double df = x1.v[l] - x0.v[l];
+        x0.v[l] += shrink * df;
+        x1.v[l] -= shrink * df;
     }
 }
 
+// Accel triple (n, n+1, n+2) (projection.py:346-371).
 template <int D>
-__device__ __forceinline__ void accel_triple(double* s, int n, double b, int pin,
-                                             double& worst) {
+__device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sample<D>& x2, int n,
+                                             double b, int pin, double& worst) {
     const double omega = 1.8;
     double nrm = 0.0;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double w = s[n * D + l] - 2.0 * s[(n + 1) * D + l] + s[(n + 2) * D + l];
+        const double w = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
         nrm += w * w;
     }
     nrm = sqrt(nrm);
-    if (nrm > b) {
-        if (nrm - b > worst) worst = nrm - b;
-        double c0 = 1.0, c1 = -2.0, c2 = 1.0;
-        if (pin == n) c0 = 0.0;
-        else if (pin == n + 1) c1 = 0.0;
-        else if (pin == n + 2) c2 = 0.0;
-        const double denom = c0 * c0 + c1 * c1 + c2 * c2;
-        if (denom > 0.0) {
-            const double step = omega * (nrm - b) / (denom * nrm);
+    if (!(nrm > b)) return;
+    if (nrm - b > worst) worst = nrm - b;
+    double c0 = 1.0, c1 = -2.0, c2 = 1.0;
+    if (pin == n) c0 = 0.0;
+    else if (pin == n + 1) c1 = 0.0;
+    else if (pin == n + 2) c2 = 0.0;
+    const double denom = c0 * c0 + c1 * c1 + c2 * c2;
+    if (denom > 0.0) {
+        const double step = omega * (nrm - b) / (denom * nrm);
 #pragma unroll
-            for (int l = 0; l < D; ++l) {
-                const double w = s[n * D + l] - 2.0 * s[(n + 1) * D + l] + s[(n + 2) * D + l];
-                s[n * D + l] -= step * c0 * w;
-                s[(n + 1) * D + l] -= step * c1 * w;
-                s[(n + 2) * D + l] -= step * c2 * w;
-            }
+        for (int l = 0; l < D; ++l) {
+            const double w = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
+            x0.v[l] -= step * c0 * w;
+            x1.v[l] -= step * c1 * w;
+            x2.v[l] -= step * c2 * w;
         }
     }
 }
 
-// Run `nsw` consecutive sweeps (1..32) wavefront-pipelined on s; worst per sweep is
-// returned in lane order (lane L -> sweep L).  Called by the whole warp.
+__device__ __forceinline__ int lane_offset(int g) { return PL_LAG * g + (g >> 5); }
+
+// One batch of `nsw` (1..blockDim) sweeps from s_in to s_out; returns this lane's worst.
 template <int D>
-__device__ double pipelined_sweeps(double* s, int ns, double a, double b, int pin,
-                                   const double* pv, int nsw) {
-    const int lane = threadIdx.x & 31;
-    const bool active = lane < nsw;
+__device__ double systolic_batch(const double* __restrict__ s_in, double* __restrict__ s_out,
+                                 double* xfer, int ns, double a, double b, int pin,
+                                 const double* pv, int nsw) {
+    const int g = threadIdx.x;
+    const int lane = g & 31;
+    const int warp = g >> 5;
+    const bool active = g < nsw;
+    const bool last = g == nsw - 1;
+    const int off = lane_offset(g);
+    const int n_steps = ns + 4 + lane_offset(nsw - 1);
     double worst = 0.0;
-    const int t_first = -1;                    // box of sample 0
-    const int t_last = ns - 1 + 0;             // last step that does any work
-    const int n_steps = t_last - t_first + 1 + PL_LAG * (nsw - 1);
-    for (int step = 0; step < n_steps; ++step) {
-        const int t = t_first + step - PL_LAG * lane;
-        if (active && t >= t_first && t <= t_last) {
-            const int nb = t + 1;
-            if (nb < ns) {
-                if (nb == pin)
-                    for (int l = 0; l < D; ++l) s[nb * D + l] = pv[l];
-                box_sample<D>(s, nb, worst);
+    Sample<D> w0, w1, w2, w3;
+#pragma unroll
+    for (int l = 0; l < D; ++l) w0.v[l] = w1.v[l] = w2.v[l] = w3.v[l] = 0.0;
+    for (int st = 0; st < n_steps; ++st) {
+        const int t = st - 2 - off;
+        const bool on = active && t >= -2 && t <= ns + 1;
+        Sample<D> emit;
+#pragma unroll
+        for (int l = 0; l < D; ++l) emit.v[l] = 0.0;
+        if (on) {
+            if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, worst);
+            if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, worst);
+            emit = w0;  // sample t-2, final for this sweep when t >= 2
+            if (last && t >= 2) {
+#pragma unroll
+                for (int l = 0; l < D; ++l) s_out[(t - 2) * D + l] = emit.v[l];
             }
-            if (t >= 0 && t <= ns - 2) speed_pair<D>(s, t, a, pin, worst);
-            if (t - 2 >= 0 && t - 2 <= ns - 3) accel_triple<D>(s, t - 2, b, pin, worst);
         }
-        __syncwarp();
+        // hand finished samples to the next sweep
+        Sample<D> recv;
+#pragma unroll
+        for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, emit.v[l], 1);
+        if (lane == 31) {
+            double* x = xfer + ((warp * 2 + (st & 1)) * D);
+#pragma unroll
+            for (int l = 0; l < D; ++l) x[l] = emit.v[l];
+        }
+        if (on) {
+            const int m = t + 2;
+            if (m <= ns - 1) {
+                if (g == 0) {
+#pragma unroll
+                    for (int l = 0; l < D; ++l) recv.v[l] = s_in[m * D + l];
+                } else if (lane == 0) {
+                    const double* x = xfer + (((warp - 1) * 2 + ((st - 1) & 1)) * D);
+#pragma unroll
+                    for (int l = 0; l < D; ++l) recv.v[l] = x[l];
+                }
+                if (m == pin) {
+#pragma unroll
+                    for (int l = 0; l < D; ++l) recv.v[l] = pv[l];
+                }
+                box_sample<D>(recv, worst);
+            }
+            w0 = w1;
+            w1 = w2;
+            w2 = w3;
+            w3 = recv;
+        }
+        if (blockDim.x > 32) __syncthreads();
+        else __syncwarp();
     }
     return worst;
 }
 
 template <int D>
-__global__ void __launch_bounds__(32) polish_kernel(double* shots, long long n_shots, int ns,
-                                                    double a, double b, int pin, double pv0,
-                                                    double pv1, double pv2, double tol,
-                                                    int max_sweeps, double* ckpt_ws,
-                                                    int use_smem, int32_t* sweeps_out,
-                                                    float4* pos4) {
+__global__ void __launch_bounds__(256) polish_kernel(double* shots, int ns, double a, double b,
+                                                     int pin, double pv0, double pv1,
+                                                     double pv2, double tol, int max_sweeps,
+                                                     int32_t* sweeps_out, float4* pos4) {
     extern __shared__ __align__(16) double sm[];
+    __shared__ unsigned masks[8];
+    __shared__ int first_sh;
     const long long c = blockIdx.x;
-    const int lane = threadIdx.x;
+    const int g = threadIdx.x;
+    const int nb = blockDim.x;
     const int nd = ns * D;
     const double pv[3] = {pv0, pv1, pv2};
-    double* g = shots + c * (size_t)nd;
-    double* s = use_smem ? sm : g;
-    double* ck = use_smem ? sm + nd : ckpt_ws + c * (size_t)nd;
-    if (use_smem)
-        for (int i = lane; i < nd; i += 32) s[i] = g[i];
-    __syncwarp();
-    int done = 0;
+    double* gsh = shots + c * (size_t)nd;
+    double* buf0 = sm;
+    double* buf1 = sm + nd;
+    double* xfer = sm + 2 * nd;  // [warps][2][D]
+    for (int i = g; i < nd; i += nb) buf0[i] = gsh[i];
+    __syncthreads();
     int total = 0;
+    double* cur = buf0;
+    double* nxt = buf1;
     while (total < max_sweeps) {
-        const int nsw = min(32, max_sweeps - total);
-        for (int i = lane; i < nd; i += 32) ck[i] = s[i];
-        __syncwarp();
-        const double worst = pipelined_sweeps<D>(s, ns, a, b, pin, pv, nsw);
-        const unsigned ok = __ballot_sync(0xffffffffu, lane < nsw && worst <= tol);
-        if (ok) {
-            const int first = __ffs(ok) - 1;  // sweep index within the batch (0-based)
-            if (first != nsw - 1) {
-                // Roll back and replay only the sweeps up to the stopping one.
-                for (int i = lane; i < nd; i += 32) s[i] = ck[i];
-                __syncwarp();
-                pipelined_sweeps<D>(s, ns, a, b, pin, pv, first + 1);
-            }
+        const int nsw = min(nb, max_sweeps - total);
+        const double worst = systolic_batch<D>(cur, nxt, xfer, ns, a, b, pin, pv, nsw);
+        const unsigned ok = __ballot_sync(0xffffffffu, g < nsw && worst <= tol);
+        if ((g & 31) == 0) masks[g >> 5] = ok;
+        __syncthreads();
+        if (g == 0) {
+            int f = -1;
+            for (int w = 0; w < (nb >> 5) && f < 0; ++w)
+                if (masks[w]) f = w * 32 + __ffs(masks[w]) - 1;
+            first_sh = f;
+        }
+        __syncthreads();
+        const int first = first_sh;
+        if (first >= 0) {
+            if (first != nsw - 1) systolic_batch<D>(cur, nxt, xfer, ns, a, b, pin, pv, first + 1);
             total += first + 1;
-            done = 1;
+            __syncthreads();
+            double* tmp = cur;
+            cur = nxt;
+            nxt = tmp;
             break;
         }
         total += nsw;
+        __syncthreads();
+        double* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
     }
-    (void)done;
-    __syncwarp();
-    for (int i = lane; i < nd; i += 32) g[i] = s[i];
+    __syncthreads();
+    for (int i = g; i < nd; i += nb) gsh[i] = cur[i];
     if (pos4) {
-        for (int n = lane; n < ns; n += 32) {
-            const double* r = s + n * D;
-            pos4[c * ns + n] = make_float4((float)r[0], (float)r[1], D == 3 ? (float)r[2] : 0.f,
-                                           1.f);
+        for (int n = g; n < ns; n += nb) {
+            const double* r = cur + n * D;
+            pos4[c * ns + n] =
+                make_float4((float)r[0], (float)r[1], D == 3 ? (float)r[2] : 0.f, 1.f);
         }
     }
-    if (lane == 0 && sweeps_out) sweeps_out[c] = total;
+    if (g == 0 && sweeps_out) sweeps_out[c] = total;
+}
+
+inline int polish_warps(int ns) {
+    int w = ns / 128;
+    return w < 1 ? 1 : (w > 8 ? 8 : w);
 }
 
 // ------------------------------------------------------------------ residuals
@@ -831,23 +907,23 @@ int spk_project_all(const double* in, const double* grad, double eta, double* ou
         fista_kernel<2><<<(unsigned)n_shots, nt, dyn, stream>>>(A);
     }
     SPK_CHECK_LAUNCH("fista_kernel");
-    // polish: state + checkpoint in shared memory when they fit (2 arrays)
-    const size_t psm = (size_t)2 * n_s * dims * sizeof(double);
-    const int use_smem = psm <= (size_t)PJ_SMEM_LIMIT;
-    double* ck = static_cast<double*>(ws);  // FISTA state is dead by now: reuse it
-    const size_t pdyn = use_smem ? psm : 0;
+    // polish: ping-pong state buffers + warp hand-over slots in shared memory
+    const int pw = polish_warps(n_s);
+    const size_t psm = ((size_t)2 * n_s * dims + (size_t)pw * 2 * dims) * sizeof(double);
+    SPK_REQUIRE(psm <= (size_t)(227 * 1024), SPK_ERR_ARG,
+                "N_s=%d too large for the shared-memory polish", n_s);
     if (dims == 3) {
         cudaFuncSetAttribute(polish_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pdyn);
-        polish_kernel<3><<<(unsigned)n_shots, 32, pdyn, stream>>>(
-            out, n_shots, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, ck,
-            use_smem, sweeps, (float4*)pos4);
+                             (int)psm);
+        polish_kernel<3><<<(unsigned)n_shots, 32 * pw, psm, stream>>>(
+            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, sweeps,
+            (float4*)pos4);
     } else {
         cudaFuncSetAttribute(polish_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pdyn);
-        polish_kernel<2><<<(unsigned)n_shots, 32, pdyn, stream>>>(
-            out, n_shots, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, ck,
-            use_smem, sweeps, (float4*)pos4);
+                             (int)psm);
+        polish_kernel<2><<<(unsigned)n_shots, 32 * pw, psm, stream>>>(
+            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, sweeps,
+            (float4*)pos4);
     }
     SPK_CHECK_LAUNCH("polish_kernel");
     return SPK_OK;

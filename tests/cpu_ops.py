@@ -1,0 +1,94 @@
+"""CPU stand-in for paper_2108_02991_b200.engine.CudaOps, built on the oracle.  TEST ONLY:
+lets the multi-rank engine (sharding, all-gathers, rank-ordered reductions, guards) run
+under the gloo backend in a GPU-less container.  Mirrors the kernels' semantics: float32
+positions for the N-body, fp64 everything else."""
+
+import numpy as np
+import torch
+
+from oracle import oracle as orc
+from paper_2108_02991_b200.projection import stacked_operator_norm
+
+
+class OracleOps:
+    def __init__(self):
+        self.device = torch.device("cpu")
+
+    def empty(self, shape, dtype=torch.float64):
+        return torch.empty(shape, dtype=dtype)
+
+    def to_device(self, arr):
+        return torch.from_numpy(np.array(arr, dtype=np.float64, copy=True))
+
+    @staticmethod
+    def _fill_pos4(coords, pos4):
+        d = coords.shape[-1]
+        flat = coords.reshape(-1, d)
+        pos4.zero_()
+        pos4[:, :d] = flat.to(torch.float32)
+        pos4[:, 3] = 1.0
+
+    def pack(self, coords, out):
+        self._fill_pos4(coords, out)
+        return out
+
+    def sums(self, tgt4, src4, coords_local, fld, cfg):
+        d = cfg.dims
+        assert cfg.grad_mode == "exact", "OracleOps covers the exact (north-star) mode"
+        t = tgt4[:, :d].double().numpy()
+        s = src4[:, :d].double().numpy()
+        va, ga = orc.grid_sums(t, fld.density.grid, fld.kernel_eps ** 2)
+        vr, gr = orc.cross_sums(t, s, cfg.repulsion.kernel_eps ** 2)
+        return tuple(torch.from_numpy(x) for x in (va, ga, vr, gr))
+
+    def combine(self, va, ga, vr, gr, p, coords, prev_c, prev_g, grad_out):
+        g = ga.numpy() / float(p) - gr.numpy() / (float(p) * float(p))
+        grad_out.copy_(torch.from_numpy(g))
+        out = np.zeros(6)
+        out[0] = va.numpy().sum()
+        out[1] = vr.numpy().sum()
+        if prev_c is not None:
+            dk = coords.numpy().reshape(g.shape) - prev_c.numpy().reshape(g.shape)
+            dg = g - prev_g.numpy().reshape(g.shape)
+            out[2] = np.vdot(dk, dg)
+            out[3] = np.vdot(dg, dg)
+        out[4] = np.count_nonzero(~np.isfinite(g))
+        return torch.from_numpy(out)
+
+    def project(self, coords, cfg, grad, eta, out, pos4, nonfinite):
+        k = coords.numpy()
+        if grad is not None:
+            k = k - eta * grad.numpy()
+        if nonfinite is not None and not np.isfinite(k).all():
+            nonfinite.fill_(1)
+        n_c, n_s, d = k.shape
+        pin = -1 if cfg.pin is None else cfg.pin.pinned_index
+        pv = np.zeros(d) if cfg.pin is None else cfg.pin.pinned_value
+        tau = 1.0 / stacked_operator_norm(n_s, pin)
+        res, _ = orc.project_all(k, cfg.speed_bound, cfg.accel_bound, pin, pv, cfg.n_pit,
+                                 tau, 0.1 * cfg.feas_tol, monotone=cfg.monotone)
+        out.copy_(torch.from_numpy(res))
+        if pos4 is not None:
+            self._fill_pos4(out, pos4)
+        return out
+
+    def residuals(self, coords, cfg):
+        c = coords.numpy()
+        amp = max(np.abs(c).max() - 1.0, 0.0)
+        d1 = np.linalg.norm(np.diff(c, axis=1), axis=2)
+        d2 = np.linalg.norm(np.diff(c, 2, axis=1), axis=2)
+        sp = max(d1.max() - cfg.speed_bound, 0.0) if d1.size else 0.0
+        ac = max(d2.max() - cfg.accel_bound, 0.0) if d2.size else 0.0
+        pe = 0.0
+        if cfg.pin is not None:
+            pe = float(np.abs(c[:, cfg.pin.pinned_index, :] - cfg.pin.pinned_value).max())
+        return torch.tensor([amp, sp, ac, pe, max(amp, sp, ac, pe)], dtype=torch.float64)
+
+    def upsample(self, coords):
+        c = coords.numpy()
+        n_c, n_s, d = c.shape
+        up = np.empty((n_c, 2 * n_s, d))
+        up[:, 0::2] = c
+        up[:, 1:-1:2] = 0.5 * (c[:, :-1] + c[:, 1:])
+        up[:, -1] = c[:, -1] + 0.5 * (c[:, -1] - c[:, -2])
+        return torch.from_numpy(np.clip(up, -1.0, 1.0))

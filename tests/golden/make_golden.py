@@ -261,6 +261,9 @@ def optimize_fixture():
         out[f"{mode}_att"] = np.array([r.attraction for r in res.trace.records])
         out[f"{mode}_rep"] = np.array([r.repulsion for r in res.trace.records])
         out[f"{mode}_feas"] = np.array([r.feas_residual for r in res.trace.records])
+        out["field_potential"] = res.field.potential
+        out["field_force"] = res.field.force
+        out["field_eps"] = np.float64(res.field.kernel_eps)
     cfg = om.OptimizerConfig(n_c=4, n_s=32, dims=2, n_decim=0, n_git=0, perturbation=0.2,
                              seed=5, repulsion=om.RepulsionConfig(backend="direct"))
     res = om.optimize(cfg, core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6,
