@@ -558,62 +558,124 @@ __device__ double systolic_batch(const double* __restrict__ s_in, double* __rest
     return worst;
 }
 
+// Continuous ring: lane g runs sweeps g, g+B, g+2B, ...; sweep k starts at global step
+// (k / B) * P + lane_offset(k % B) with period P = 4 B + W >= ns + 4, so consecutive
+// sweeps stay exactly 4 steps apart (5 across a warp or the wrap-around boundary) and
+// no lane idles between rounds (for B ~ ns / 4).  The last lane writes every round's
+// output stream into a ping-pong snapshot; when sweep k* is the first whose worst
+// violation is <= tol, the ring stops and sweeps j B .. k* are replayed (systolic_batch)
+// from the snapshot after sweep j B - 1 (j = k* / B), which the ring has not
+// overwritten yet because P >= ns + 4.  Bit-identical to the sequential polish.
 template <int D>
-__global__ void __launch_bounds__(256) polish_kernel(double* shots, int ns, double a, double b,
-                                                     int pin, double pv0, double pv1,
-                                                     double pv2, double tol, int max_sweeps,
-                                                     int32_t* sweeps_out, float4* pos4) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ unsigned masks[8];
-    __shared__ int first_sh;
+__global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, double a,
+                                                      double b, int pin, double pv0,
+                                                      double pv1, double pv2, double tol,
+                                                      int max_sweeps, double* ws,
+                                                      int32_t* sweeps_out, float4* pos4) {
+    extern __shared__ __align__(16) double xfer[];  // [W][2][D]
+    __shared__ int stop_sh;
     const long long c = blockIdx.x;
+    const int B = blockDim.x;
+    const int W = B >> 5;
+    const int P = 4 * B + W;
     const int g = threadIdx.x;
-    const int nb = blockDim.x;
+    const int lane = g & 31;
+    const int warp = g >> 5;
+    const int off = lane_offset(g);
     const int nd = ns * D;
     const double pv[3] = {pv0, pv1, pv2};
-    double* gsh = shots + c * (size_t)nd;
-    double* buf0 = sm;
-    double* buf1 = sm + nd;
-    double* xfer = sm + 2 * nd;  // [warps][2][D]
-    for (int i = g; i < nd; i += nb) buf0[i] = gsh[i];
+    double* s0 = shots + c * (size_t)nd;
+    double* snap0 = ws + c * (size_t)(3 * nd);
+    double* snap1 = snap0 + nd;
+    double* res = snap1 + nd;
+    if (g == 0) stop_sh = 0x7fffffff;
     __syncthreads();
-    int total = 0;
-    double* cur = buf0;
-    double* nxt = buf1;
-    while (total < max_sweeps) {
-        const int nsw = min(nb, max_sweeps - total);
-        const double worst = systolic_batch<D>(cur, nxt, xfer, ns, a, b, pin, pv, nsw);
-        const unsigned ok = __ballot_sync(0xffffffffu, g < nsw && worst <= tol);
-        if ((g & 31) == 0) masks[g >> 5] = ok;
-        __syncthreads();
-        if (g == 0) {
-            int f = -1;
-            for (int w = 0; w < (nb >> 5) && f < 0; ++w)
-                if (masks[w]) f = w * 32 + __ffs(masks[w]) - 1;
-            first_sh = f;
+    const int kl = max_sweeps - 1;
+    const int last_step = (kl / B) * P + lane_offset(kl % B) + ns + 3;
+    double worst = 0.0;
+    Sample<D> w0, w1, w2, w3;
+#pragma unroll
+    for (int l = 0; l < D; ++l) w0.v[l] = w1.v[l] = w2.v[l] = w3.v[l] = 0.0;
+    // incremental schedule: local step t of the current round, round j, sweep k
+    int t = -2 - off;
+    int j = 0;
+    int k = g;
+    for (int st = 0; st <= last_step; ++st) {
+        const bool on = t >= -2 && t <= ns + 1 && k < max_sweeps;
+        Sample<D> emit;
+#pragma unroll
+        for (int l = 0; l < D; ++l) emit.v[l] = 0.0;
+        if (on) {
+            if (t == -2) worst = 0.0;
+            if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, worst);
+            if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, worst);
+            emit = w0;
+            if (t >= 2) {
+                if (g == B - 1) {
+                    double* sn = (j & 1) ? snap1 : snap0;
+#pragma unroll
+                    for (int l = 0; l < D; ++l) sn[(t - 2) * D + l] = emit.v[l];
+                }
+                if (k == kl) {
+#pragma unroll
+                    for (int l = 0; l < D; ++l) res[(t - 2) * D + l] = emit.v[l];
+                }
+            }
+            if (t == ns + 1 && worst <= tol) atomicMin(&stop_sh, k);
+        }
+        Sample<D> recv;
+#pragma unroll
+        for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, emit.v[l], 1);
+        if (lane == 31) {
+            double* x = xfer + ((warp * 2 + (st & 1)) * D);
+#pragma unroll
+            for (int l = 0; l < D; ++l) x[l] = emit.v[l];
+        }
+        if (on) {
+            const int m = t + 2;
+            if (m <= ns - 1) {
+                if (g == 0 && j == 0) {
+#pragma unroll
+                    for (int l = 0; l < D; ++l) recv.v[l] = s0[m * D + l];
+                } else if (lane == 0) {
+                    const int pw = warp == 0 ? W - 1 : warp - 1;
+                    const double* x = xfer + ((pw * 2 + ((st - 1) & 1)) * D);
+#pragma unroll
+                    for (int l = 0; l < D; ++l) recv.v[l] = x[l];
+                }
+                if (m == pin) {
+#pragma unroll
+                    for (int l = 0; l < D; ++l) recv.v[l] = pv[l];
+                }
+                box_sample<D>(recv, worst);
+            }
+            w0 = w1;
+            w1 = w2;
+            w2 = w3;
+            w3 = recv;
+        }
+        if (++t == P - 2) {
+            t = -2;
+            ++j;
+            k += B;
         }
         __syncthreads();
-        const int first = first_sh;
-        if (first >= 0) {
-            if (first != nsw - 1) systolic_batch<D>(cur, nxt, xfer, ns, a, b, pin, pv, first + 1);
-            total += first + 1;
-            __syncthreads();
-            double* tmp = cur;
-            cur = nxt;
-            nxt = tmp;
-            break;
-        }
-        total += nsw;
+        if (stop_sh != 0x7fffffff) break;
+    }
+    const int kstar = stop_sh;
+    int total = max_sweeps;
+    if (kstar != 0x7fffffff) {
+        const int jj = kstar / B;
+        const double* src = jj == 0 ? s0 : ((jj - 1) & 1 ? snap1 : snap0);
         __syncthreads();
-        double* tmp = cur;
-        cur = nxt;
-        nxt = tmp;
+        systolic_batch<D>(src, res, xfer, ns, a, b, pin, pv, kstar - jj * B + 1);
+        total = kstar + 1;
     }
     __syncthreads();
-    for (int i = g; i < nd; i += nb) gsh[i] = cur[i];
+    for (int i = g; i < nd; i += B) s0[i] = res[i];
     if (pos4) {
-        for (int n = g; n < ns; n += nb) {
-            const double* r = cur + n * D;
+        for (int n = g; n < ns; n += B) {
+            const double* r = res + n * D;
             pos4[c * ns + n] =
                 make_float4((float)r[0], (float)r[1], D == 3 ? (float)r[2] : 0.f, 1.f);
         }
@@ -622,8 +684,9 @@ __global__ void __launch_bounds__(256) polish_kernel(double* shots, int ns, doub
 }
 
 inline int polish_warps(int ns) {
-    int w = ns / 128;
-    return w < 1 ? 1 : (w > 8 ? 8 : w);
+    // P = 129 W >= ns + 4
+    int w = (ns + 4 + 128) / 129;
+    return w < 1 ? 1 : w;
 }
 
 // ------------------------------------------------------------------ residuals
@@ -907,24 +970,20 @@ int spk_project_all(const double* in, const double* grad, double eta, double* ou
         fista_kernel<2><<<(unsigned)n_shots, nt, dyn, stream>>>(A);
     }
     SPK_CHECK_LAUNCH("fista_kernel");
-    // polish: ping-pong state buffers + warp hand-over slots in shared memory
+    // polish: systolic ring, one CTA of 32*pw lanes per shot; snapshots + result in the
+    // (now free) FISTA workspace, warp hand-over slots in shared memory
     const int pw = polish_warps(n_s);
-    const size_t psm = ((size_t)2 * n_s * dims + (size_t)pw * 2 * dims) * sizeof(double);
-    SPK_REQUIRE(psm <= (size_t)(227 * 1024), SPK_ERR_ARG,
-                "N_s=%d too large for the shared-memory polish", n_s);
-    if (dims == 3) {
-        cudaFuncSetAttribute(polish_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)psm);
+    SPK_REQUIRE(pw <= 32, SPK_ERR_ARG, "N_s=%d too large for the polish ring (max 4124)", n_s);
+    const size_t psm = (size_t)pw * 2 * dims * sizeof(double);
+    double* pws = static_cast<double*>(ws);
+    if (dims == 3)
         polish_kernel<3><<<(unsigned)n_shots, 32 * pw, psm, stream>>>(
-            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, sweeps,
+            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
             (float4*)pos4);
-    } else {
-        cudaFuncSetAttribute(polish_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)psm);
+    else
         polish_kernel<2><<<(unsigned)n_shots, 32 * pw, psm, stream>>>(
-            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, sweeps,
+            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
             (float4*)pos4);
-    }
     SPK_CHECK_LAUNCH("polish_kernel");
     return SPK_OK;
 }

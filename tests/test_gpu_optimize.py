@@ -77,7 +77,10 @@ def test_drift_vs_reference_optimize(spk, mode):
     drift = np.abs(res.pattern.coords - g[f"{mode}_coords"]).max()
     print(f"[drift] {mode}: cost rel {cdrift:.3e}, max |coords - reference| = {drift:.3e}")
     assert cdrift <= 1e-4
-    assert drift <= 1e-3
+    # The reference itself drifts by 2.0e-2 (consistent: the interpolant gradient is
+    # discontinuous across cells) and 7.1e-6 (smooth) under 1e-6 relative noise in the
+    # repulsion gradient (scripts/drift_sensitivity.py); bound at ~2.5x / 140x that.
+    assert drift <= (5e-2 if mode == "consistent" else 1e-3)
 
 
 def test_final_pattern_feasible(spk):
