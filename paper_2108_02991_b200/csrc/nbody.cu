@@ -28,18 +28,35 @@
 
 namespace spk {
 
-constexpr int NB_THREADS = 256;
-constexpr int NB_TPT = 8;                   // targets per thread
+// Tuning knobs (overridable at compile time for scripts/micro/nbody_variants.sh).
+#ifndef NB_THREADS_CFG
+#define NB_THREADS_CFG 256
+#endif
+#ifndef NB_TPT_CFG
+#define NB_TPT_CFG 8
+#endif
+#ifndef NB_UNROLL_CFG
+#define NB_UNROLL_CFG 2
+#endif
+#ifndef NB_MINBLOCKS_CFG
+#define NB_MINBLOCKS_CFG 2
+#endif
+#ifndef NB_STAGES_CFG
+#define NB_STAGES_CFG 4
+#endif
+constexpr int NB_THREADS = NB_THREADS_CFG;
+constexpr int NB_TPT = NB_TPT_CFG;          // targets per thread
 constexpr int NB_PAIRS = NB_TPT / 2;        // f32x2 pairs per thread
 constexpr int NB_TB = NB_THREADS * NB_TPT;  // targets per CTA
 constexpr int NB_TILE = 512;                // sources per shared-memory stage
-constexpr int NB_STAGES = 4;
+constexpr int NB_STAGES = NB_STAGES_CFG;
+constexpr int NB_UNROLL = NB_UNROLL_CFG;
 constexpr int NB_TILE_BYTES = NB_STAGES * NB_TILE * 16;
 // fp64 per-target accumulators live in shared memory (per-thread slots) so that the
 // kernel fits 128 registers and two CTAs (16 warps) share an SM.
 constexpr int NB_ACC_BYTES = NB_TPT * 4 * NB_THREADS * 8;
 constexpr int NB_SMEM = NB_TILE_BYTES + NB_ACC_BYTES;
-constexpr int NB_MAX_CHUNKS = 192;
+constexpr int NB_MAX_CHUNKS = 64;
 
 struct SegDesc {
     const float4* src;
@@ -75,7 +92,7 @@ __device__ __forceinline__ void tile_pairs(const float4* __restrict__ tile, int 
                                            float2 (&av)[NB_PAIRS], float2 (&ax)[NB_PAIRS],
                                            float2 (&ay)[NB_PAIRS],
                                            float2 (&az)[NB_PAIRS]) {
-#pragma unroll 2
+#pragma unroll NB_UNROLL
     for (int j = 0; j < cnt; ++j) {
         const float4 s = tile[j];
         const float2 nsx = make_float2(-s.x, -s.x);
@@ -159,7 +176,7 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
 }
 
 template <int D>
-__global__ void __launch_bounds__(NB_THREADS, 2) nbody_kernel(const NBParams P) {
+__global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(const NBParams P) {
     extern __shared__ __align__(128) float4 tiles[];
     double* acc = reinterpret_cast<double*>(reinterpret_cast<char*>(tiles) + NB_TILE_BYTES);
     __shared__ __align__(8) uint64_t bars[NB_STAGES];
@@ -290,8 +307,8 @@ static Plan make_plan(long long n_tgt, long long n0, long long n1) {
         const long long l1 = c1 ? (t1 + c1 - 1) / c1 : 0;
         const long long units = pl.n_tb * c;
         const long long waves = (units + slots - 1) / slots;
-        const double cost = (double)waves * (double)std::max(l0, l1) +
-                            0.03 * (double)c * (double)pl.n_tb / (double)slots;
+        // per-unit fixed cost ~ 0.25 tile (prologue, pipeline fill, partial-slot write)
+        const double cost = (double)waves * ((double)std::max(l0, l1) + 0.25);
         if (cost < best * 0.999) {
             best = cost;
             pl.nc0 = c0;
@@ -353,7 +370,7 @@ __global__ void pack_positions_kernel(const double* __restrict__ c, long long p,
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= p) return;
     const double* r = c + i * dims;
-    out[i] = make_float4((float)r[0], (float)r[1], dims == 3 ? (float)r[2] : 0.f, 1.f);
+    out[i] = pos_record(r[0], r[1], dims == 3 ? r[2] : 0.0);
 }
 
 __global__ void grid_sources_kernel(const double* __restrict__ rho, long long s0,

@@ -566,6 +566,86 @@ __device__ double systolic_batch(const double* __restrict__ s_in, double* __rest
 // violation is <= tol, the ring stops and sweeps j B .. k* are replayed (systolic_batch)
 // from the snapshot after sweep j B - 1 (j = k* / B), which the ring has not
 // overwritten yet because P >= ns + 4.  Bit-identical to the sequential polish.
+// State of one ring lane between steps.
+template <int D>
+struct RingLane {
+    Sample<D> slot[4];  // register window, roles rotate with the global step (mod 4)
+    double worst;
+    int t, j, k;        // local step in the current round, round, sweep index
+};
+
+// One global step of the ring.  R = st mod 4 fixes which window slot plays w0..w3
+// (w0 = slot[R], ..., w3 = slot[R+3]); the received sample overwrites slot[R] (the old
+// w0, handed on this step), so the window never moves between registers.
+template <int D, int R>
+__device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B, int W, int P,
+                                          int g, int lane, int warp, int max_sweeps, int kl,
+                                          double a, double b, int pin, double pv0,
+                                          double pv1, double pv2, double tol,
+                                          const double* __restrict__ s0, double* snap0,
+                                          double* snap1, double* res, double* xfer,
+                                          int* stop_sh) {
+    Sample<D>& w0 = L.slot[R & 3];
+    Sample<D>& w1 = L.slot[(R + 1) & 3];
+    Sample<D>& w2 = L.slot[(R + 2) & 3];
+    Sample<D>& w3 = L.slot[(R + 3) & 3];
+    const int t = L.t;
+    const bool on = t >= -2 && t <= ns + 1 && L.k < max_sweeps;
+    if (on) {
+        if (t == -2) L.worst = 0.0;
+        if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, L.worst);
+        if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, L.worst);
+        if (t >= 2) {
+            if (g == B - 1) {
+                double* sn = (L.j & 1) ? snap1 : snap0;
+#pragma unroll
+                for (int l = 0; l < D; ++l) sn[(t - 2) * D + l] = w0.v[l];
+            }
+            if (L.k == kl) {
+#pragma unroll
+                for (int l = 0; l < D; ++l) res[(t - 2) * D + l] = w0.v[l];
+            }
+        }
+        if (t == ns + 1 && L.worst <= tol) atomicMin(stop_sh, L.k);
+    }
+    // hand the finished sample w0 (= s[t-2]) to the next sweep; it is replaced in slot R
+    Sample<D> recv;
+#pragma unroll
+    for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, w0.v[l], 1);
+    if (lane == 31) {
+        double* x = xfer + ((warp * 2 + (st & 1)) * D);
+#pragma unroll
+        for (int l = 0; l < D; ++l) x[l] = w0.v[l];
+    }
+    if (on) {
+        const int m = t + 2;
+        if (m <= ns - 1) {
+            if (g == 0 && L.j == 0) {
+#pragma unroll
+                for (int l = 0; l < D; ++l) recv.v[l] = s0[m * D + l];
+            } else if (lane == 0) {
+                const int pw = warp == 0 ? W - 1 : warp - 1;
+                const double* x = xfer + ((pw * 2 + ((st - 1) & 1)) * D);
+#pragma unroll
+                for (int l = 0; l < D; ++l) recv.v[l] = x[l];
+            }
+            if (m == pin) {
+                recv.v[0] = pv0;
+                recv.v[1] = pv1;
+                if (D == 3) recv.v[D - 1] = pv2;
+            }
+            box_sample<D>(recv, L.worst);
+        }
+    }
+    w0 = recv;  // slot R now holds s[t+2] (the new w3 at the next step)
+    if (++L.t == P - 2) {
+        L.t = -2;
+        ++L.j;
+        L.k += B;
+    }
+    __syncthreads();
+}
+
 template <int D>
 __global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, double a,
                                                       double b, int pin, double pv0,
@@ -592,76 +672,28 @@ __global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, dou
     __syncthreads();
     const int kl = max_sweeps - 1;
     const int last_step = (kl / B) * P + lane_offset(kl % B) + ns + 3;
-    double worst = 0.0;
-    Sample<D> w0, w1, w2, w3;
+    RingLane<D> L;
 #pragma unroll
-    for (int l = 0; l < D; ++l) w0.v[l] = w1.v[l] = w2.v[l] = w3.v[l] = 0.0;
-    // incremental schedule: local step t of the current round, round j, sweep k
-    int t = -2 - off;
-    int j = 0;
-    int k = g;
-    for (int st = 0; st <= last_step; ++st) {
-        const bool on = t >= -2 && t <= ns + 1 && k < max_sweeps;
-        Sample<D> emit;
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int l = 0; l < D; ++l) emit.v[l] = 0.0;
-        if (on) {
-            if (t == -2) worst = 0.0;
-            if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, worst);
-            if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, worst);
-            emit = w0;
-            if (t >= 2) {
-                if (g == B - 1) {
-                    double* sn = (j & 1) ? snap1 : snap0;
-#pragma unroll
-                    for (int l = 0; l < D; ++l) sn[(t - 2) * D + l] = emit.v[l];
-                }
-                if (k == kl) {
-#pragma unroll
-                    for (int l = 0; l < D; ++l) res[(t - 2) * D + l] = emit.v[l];
-                }
-            }
-            if (t == ns + 1 && worst <= tol) atomicMin(&stop_sh, k);
-        }
-        Sample<D> recv;
-#pragma unroll
-        for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, emit.v[l], 1);
-        if (lane == 31) {
-            double* x = xfer + ((warp * 2 + (st & 1)) * D);
-#pragma unroll
-            for (int l = 0; l < D; ++l) x[l] = emit.v[l];
-        }
-        if (on) {
-            const int m = t + 2;
-            if (m <= ns - 1) {
-                if (g == 0 && j == 0) {
-#pragma unroll
-                    for (int l = 0; l < D; ++l) recv.v[l] = s0[m * D + l];
-                } else if (lane == 0) {
-                    const int pw = warp == 0 ? W - 1 : warp - 1;
-                    const double* x = xfer + ((pw * 2 + ((st - 1) & 1)) * D);
-#pragma unroll
-                    for (int l = 0; l < D; ++l) recv.v[l] = x[l];
-                }
-                if (m == pin) {
-#pragma unroll
-                    for (int l = 0; l < D; ++l) recv.v[l] = pv[l];
-                }
-                box_sample<D>(recv, worst);
-            }
-            w0 = w1;
-            w1 = w2;
-            w2 = w3;
-            w3 = recv;
-        }
-        if (++t == P - 2) {
-            t = -2;
-            ++j;
-            k += B;
-        }
-        __syncthreads();
-        if (stop_sh != 0x7fffffff) break;
+        for (int l = 0; l < D; ++l) L.slot[q].v[l] = 0.0;
+    L.worst = 0.0;
+    L.t = -2 - off;  // lane g starts its first sweep at global step off
+    L.j = 0;
+    L.k = g;
+#define SPK_RING_STEP(R)                                                                   \
+    {                                                                                      \
+        ring_step<D, R>(L, st + R, ns, B, W, P, g, lane, warp, max_sweeps, kl, a, b, pin,  \
+                        pv0, pv1, pv2, tol, s0, snap0, snap1, res, xfer, &stop_sh);       \
+        if (stop_sh != 0x7fffffff || st + R >= last_step) break;                           \
     }
+    for (int st = 0;; st += 4) {
+        SPK_RING_STEP(0)
+        SPK_RING_STEP(1)
+        SPK_RING_STEP(2)
+        SPK_RING_STEP(3)
+    }
+#undef SPK_RING_STEP
     const int kstar = stop_sh;
     int total = max_sweeps;
     if (kstar != 0x7fffffff) {
@@ -676,8 +708,7 @@ __global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, dou
     if (pos4) {
         for (int n = g; n < ns; n += B) {
             const double* r = res + n * D;
-            pos4[c * ns + n] =
-                make_float4((float)r[0], (float)r[1], D == 3 ? (float)r[2] : 0.f, 1.f);
+            pos4[c * ns + n] = pos_record(r[0], r[1], D == 3 ? r[2] : 0.0);
         }
     }
     if (g == 0 && sweeps_out) sweeps_out[c] = total;

@@ -44,6 +44,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Position record {x, y, z, |x|^2} consumed by the N-body kernels (fp32; the norm is
+// computed from the rounded coordinates with explicit roundings, identical in every TU).
+__device__ __forceinline__ float4 pos_record(double x, double y, double z) {
+    const float fx = (float)x, fy = (float)y, fz = (float)z;
+    return make_float4(fx, fy, fz, __fmaf_rn(fx, fx, __fmaf_rn(fy, fy, __fmul_rn(fz, fz))));
+}
+
 // ---- mbarrier + 1-D bulk TMA (cp.async.bulk) --------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
