@@ -30,16 +30,50 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-N_C, N_S, GRID_N, DIMS = 1024, 1024, 64, 3
+# Workloads (SURVEY 8 shapes).  The bench line is C2 (BASELINE configs[1], the config
+# the metric is quoted on for one GPU); the others are selectable with --config.
+WORKLOADS = {
+    "c2": dict(name="C2: 3D SPARKLING 1024 shots x 1024 samples, 129^3 density grid",
+               n_c=1024, n_s=1024, dims=3, grid_n=(64, 64, 64), pert=0.25,
+               fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208), dwell=2e-6),
+    "c4": dict(name="C4: full 3D SPARKLING 4096 shots x 2048 samples (8.4M), "
+                    "385x385x209 density grid (384x384x208 matrix)",
+               n_c=4096, n_s=2048, dims=3, grid_n=(192, 192, 104), pert=0.75,
+               fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208), dwell=2e-6),
+    "c1": dict(name="C1: 2D SPARKLING 64 shots x 512 samples, 257^2 density grid",
+               n_c=64, n_s=512, dims=2, grid_n=(128, 128), pert=0.25,
+               fov=0.192, matrix=64, dwell=2e-6),
+}
+W = dict(WORKLOADS["c2"])
 EPS_REP = 1e-3
-FLOPS_REP_3D, FLOPS_ATT_3D = 17, 19  # per pair
+
+
+def select_workload(key: str) -> None:
+    global N_C, N_S, DIMS, GRID_NS, GRID_N
+    W.clear()
+    W.update(WORKLOADS[key])
+    W["key"] = key
+    N_C, N_S, DIMS, GRID_NS = W["n_c"], W["n_s"], W["dims"], W["grid_n"]
+    GRID_N = max(GRID_NS)
+
+
+select_workload("c2")
+
+
+def density():
+    import paper_2108_02991_b200 as spk
+
+    params = spk.DensityParams(0.25, 2.0)
+    if len(set(GRID_NS)) == 1:
+        return spk.discretize(params, GRID_NS[0], DIMS)
+    return spk.discretize_anisotropic(params, GRID_NS, DIMS)
+FLOPS = {3: (17, 19), 2: (12, 14)}  # (repulsion, attraction) flops per pair
 METRIC = "pair-interactions/s"
 
 
 def workload_config():
-    return {"workload": "C2: 3D SPARKLING 1024 shots x 1024 samples, 129^3 density grid "
-                        "(exact attraction + exact repulsion + projection)",
-            "n_c": N_C, "n_s": N_S, "p": N_C * N_S, "grid": [2 * GRID_N + 1] * 3,
+    return {"workload": W["name"] + " (exact attraction + exact repulsion + projection)",
+            "n_c": N_C, "n_s": N_S, "p": N_C * N_S, "grid": [2 * n + 1 for n in GRID_NS],
             "grad_mode": "exact", "eps_rep": EPS_REP, "eps_att": 1.0 / (2 * GRID_N),
             "n_pit": 100, "hardware": "full3d.cfg limits (G 40 mT/m, S 180 T/m/s)",
             "l2": "flushed between steps (256 MiB memset outside the per-step events)"}
@@ -49,14 +83,13 @@ def hardware():
     import paper_2108_02991_b200 as spk
 
     return spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
-                            dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
-                            dims=3)
+                            dwell_dt=W["dwell"], fov=W["fov"], matrix=W["matrix"], dims=DIMS)
 
 
 def start_pattern():
     import paper_2108_02991_b200 as spk
 
-    return spk.perturb(spk.init_radial(N_C, N_S, DIMS), 0.25, 0)
+    return spk.perturb(spk.init_radial(N_C, N_S, DIMS), W["pert"], 0)
 
 
 def proj_config():
@@ -70,7 +103,7 @@ def proj_config():
 
 def pairs_per_step():
     p = N_C * N_S
-    g = (2 * GRID_N + 1) ** DIMS
+    g = int(np.prod([2 * n + 1 for n in GRID_NS]))
     return p, g, p * p, p * g
 
 
@@ -145,6 +178,16 @@ def fp32_peak_tflops(sm_mhz):
     return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
 
 
+def measured_fp32_peak():
+    """FP32 TFLOP/s measured by scripts/micro/fp32_peak.cu (profiles/fp32_peak.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "fp32_peak.json")) as fh:
+            d = json.load(fh)
+        return float(d["fp32_tflops"]), float(d["sm_mhz"])
+    except (OSError, ValueError, KeyError):
+        return None, None
+
+
 def committed_traffic():
     path = os.path.join(REPO, "profiles", "nbody_traffic.json")
     try:
@@ -173,7 +216,7 @@ def cpu_reference_sample(rows: int, threads: int = 0):
     import paper_2108_02991_b200 as spk
 
     pts = start_pattern().points().copy()
-    rho = spk.discretize(spk.DensityParams(0.25, 2.0), GRID_N, DIMS)
+    rho = density()
     p, g, rep_pairs, att_pairs = pairs_per_step()
     idx = np.linspace(0, p - 1, rows).astype(np.int64)
     t0 = time.perf_counter()
@@ -189,7 +232,7 @@ def cpu_reference_sample(rows: int, threads: int = 0):
     shots = start_pattern().coords[:n_sh]
     tau = 1.0 / spk.projection.stacked_operator_norm(N_S, N_S // 2)
     t0 = time.perf_counter()
-    orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, N_S // 2, np.zeros(3), 100,
+    orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, N_S // 2, np.zeros(DIMS), 100,
                     tau, 0.1 * cfg.feas_tol, nthreads=threads)
     t_proj = (time.perf_counter() - t0) * (N_C / n_sh)
     s_per_it = rep_pairs / (rows * p / t_rep) + att_pairs / (rows * g / t_att) + t_proj
@@ -230,8 +273,8 @@ def run_ours(args):
 
     hw = hardware()
     cfg = spk.OptimizerConfig(n_c=N_C, n_s=N_S, dims=DIMS, n_pit=100, grad_mode="exact",
-                              grid_n=GRID_N, seed=0, perturbation=0.25)
-    rho = spk.discretize(cfg.density, GRID_N, DIMS)
+                              grid_n=GRID_N, seed=0, perturbation=W["pert"])
+    rho = density()
     fld = spk.precompute_field(rho)
     pcfg = proj_config()
     ops = TimedOps()
@@ -287,15 +330,29 @@ def run_ours(args):
 
     # roofline of the dominant kernel (fused K1+K2 launch on this rank)
     local_t = run.local * N_S
-    flops = local_t * p * FLOPS_REP_3D + local_t * g * FLOPS_ATT_3D
+    f_rep, f_att = FLOPS[DIMS]
+    flops = local_t * p * f_rep + local_t * g * f_att
     achieved = flops / (nb_mean / 1e3) / 1e12
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = fp32_peak_tflops(sm_max)
+    peak, peak_mhz = measured_fp32_peak()
+    if peak is None:
+        peak, peak_mhz = fp32_peak_tflops(sm_max), sm_max
+        peak_source = (f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_max} MHz "
+                       f"(MEASURED_PEAKS.json clock)")
+    else:
+        peak_source = (f"measured FFMA2 throughput {peak:.2f} TFLOP/s at {peak_mhz:.0f} MHz "
+                       f"(scripts/micro/fp32_peak.cu, profiles/fp32_peak.json); "
+                       f"MEASURED_PEAKS.json has no FP32 entry")
     clocks = clk.summary()
 
     # end-to-end through the public drop-in API with host buffers
-    e2e = run_e2e(args, spk, fld, pcfg) if rank == 0 and world == 1 else None
+    if args.no_e2e:
+        e2e = None
+    elif world == 1:
+        e2e = run_e2e(args, spk, fld, pcfg) if rank == 0 else None
+    else:
+        e2e = run_e2e_sharded(args, run, step, world)
 
     if rank == 0:
         line = {
@@ -307,14 +364,17 @@ def run_ours(args):
             "config": workload_config() | {"parallelism": f"shots sharded over {world} GPU(s)"},
             "roofline": {"bound": "fp32+sfu", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
-                         "frac_at_measured_clock": (achieved / fp32_peak_tflops(clocks["sm_mhz"])
-                                                    if clocks.get("sm_mhz") else None),
+                         "frac_at_measured_clock": (
+                             achieved / (peak * clocks["sm_mhz"] / peak_mhz)
+                             if clocks.get("sm_mhz") else None),
                          "traffic": committed_traffic(),
                          "kernel": "nbody_kernel (fused K1+K2) + finalize",
-                         "flops_per_pair": {"repulsion": FLOPS_REP_3D, "attraction": FLOPS_ATT_3D},
+                         "flops_per_pair": {"repulsion": f_rep, "attraction": f_att},
                          "launch_ms": nb_mean,
-                         "peak_source": f"148 SM x 128 FP32 lanes x 2 x sm_max_mhz {sm_max} "
-                                        f"(MEASURED_PEAKS.json clock)"},
+                         "peak_source": peak_source,
+                         "pipe_bound_note": "the kernel issues 10 (rep) / 11 (att) FP32 "
+                                            "lane-ops per pair, so its FMA-pipe ceiling is "
+                                            "17/20 of this peak (see DESIGN.md)"},
             "clocks": clocks,
             "gpu_launches": launches,
         }
@@ -332,6 +392,41 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_e2e_sharded(args, run, step, world):
+    """N > 1: the sharded optimize iteration with this rank's shots copied H2D from pinned
+    host memory before, and the projected shots + scalars copied D2H after, every step
+    (device-timed per step, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    host_in = torch.empty(run.coords.shape, dtype=torch.float64, pin_memory=True)
+    host_in.copy_(run.coords)
+    host_out = torch.empty_like(host_in, pin_memory=True)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    torch.cuda.synchronize()
+    dist.barrier()
+    total = 0.0
+    for _ in range(steps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        run.coords.copy_(host_in, non_blocking=True)
+        step()
+        host_out.copy_(run.coords, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        total += s.elapsed_time(e)
+        host_in.copy_(host_out)
+    t = torch.tensor([total], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    p, g, rep_pairs, att_pairs = pairs_per_step()
+    nbytes = host_in.numel() * 8
+    return {"value": (rep_pairs + att_pairs) * steps / (float(t[0]) / 1e3), "unit": "pairs/s",
+            "s_per_iteration": float(t[0]) / 1e3 / steps, "steps": steps,
+            "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world + 48,
+            "api": "sharded optimize iteration (engine.ShardedRun) with per-step pinned "
+                   "H2D of every rank's shots and D2H of the projected shots"}
 
 
 def run_e2e(args, spk, fld, pcfg):
@@ -417,7 +512,10 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=2048)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
+    select_workload(args.config)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -61,8 +61,10 @@ class KernelField:
         self.density = density
         if grid_n is None:
             grid_n = density.grid_n if density is not None else (self._potential.shape[0] - 1) // 2
-        self.grid_n = int(grid_n)
-        self.kernel_eps = float(kernel_eps if kernel_eps is not None else 1.0 / (2.0 * grid_n))
+        # anisotropic densities carry one N per axis; eps defaults to half the finest cell
+        self.grid_n = grid_n if isinstance(grid_n, tuple) else int(grid_n)
+        n_max = max(grid_n) if isinstance(grid_n, tuple) else grid_n
+        self.kernel_eps = float(kernel_eps if kernel_eps is not None else 1.0 / (2.0 * n_max))
         self._dev = {}
 
     # -- grids ---------------------------------------------------------------------
@@ -72,7 +74,13 @@ class KernelField:
             return self._potential.ndim
         return self.density.dims
 
+    def _require_cubic(self) -> None:
+        if isinstance(self.grid_n, tuple):
+            raise ValueError("interpolated-field attraction needs a cubic (2N+1)^d grid; "
+                             "use grad_mode='exact' for anisotropic densities")
+
     def _evaluate_grids(self) -> None:
+        self._require_cubic()
         pot, force = self.device_grids()
         side = 2 * self.grid_n + 1
         shape = (side,) * self.dims
@@ -97,9 +105,8 @@ class KernelField:
             if self.density is None:
                 raise ValueError("exact attraction needs the density grid (precompute_field)")
             rho = _device.h2d(self.density.grid)
-            side = 2 * self.grid_n + 1
             out = torch.empty((rho.numel(), 4), dtype=torch.float32, device=rho.device)
-            sides = _native.i64_array([side] * self.dims)
+            sides = _native.i64_array(list(self.density.grid.shape))
             _native.call("spk_build_grid_sources", rho.data_ptr(), self.dims, sides,
                          out.data_ptr(), _device.stream())
             self._dev["src"] = out
@@ -142,7 +149,12 @@ def precompute_field(rho: TargetDensity, kernel_eps: float | None = None,
     """Kernel-density convolution grids (attraction.py:62-113); eps defaults to 1/(2N).
 
     Raises MemoryError with sizing guidance when the device workspace would exceed
-    ``mem_cap_bytes``, like the reference's FFT guard."""
+    ``mem_cap_bytes``, like the reference's FFT guard.  An AnisotropicDensity yields a
+    field for ``grad_mode="exact"`` only (eps defaults to half the finest cell)."""
+    if isinstance(rho.grid_n, tuple):
+        if kernel_eps is not None and kernel_eps <= 0:
+            raise ValueError("kernel_eps must be positive")
+        return KernelField(grid_n=rho.grid_n, kernel_eps=kernel_eps, density=rho)
     n = rho.grid_n
     dims = rho.dims
     if kernel_eps is None:
@@ -161,6 +173,7 @@ def field_eval_device(coords: torch.Tensor, field: KernelField, mode: str,
                       vals: torch.Tensor | None = None, grad: torch.Tensor | None = None):
     """Interpolated attraction at fp64 device coords (p, d): (vals, grad, n_clamped dev)."""
     dims = field.dims
+    field._require_cubic()
     p = coords.numel() // dims
     pot, force = field.device_grids()
     if vals is None:

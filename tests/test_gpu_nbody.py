@@ -164,3 +164,18 @@ def test_fused_equals_separate(spk):
                  *[b.data_ptr() for b in bufs], ws.data_ptr(), ws.numel(), _device.stream())
     for x, y in zip(bufs, (va, ga, vr, gr)):
         assert rel_l2(_device.d2h(x), _device.d2h(y)) <= 1e-6
+
+
+def test_exact_attraction_anisotropic_grid(spk):
+    """Non-cubic density grid (full3d's 384 x 384 x 208 matrix shape, scaled down):
+    K2 vs the oracle's anisotropic weighted sum."""
+    rng = np.random.default_rng(12)
+    rho = spk.discretize_anisotropic(spk.DensityParams(0.25, 2.0), (12, 12, 7), 3)
+    fld = spk.precompute_field(rho)
+    pts = rng.uniform(-1, 1, (2500, 3))
+    res = spk.eval_attraction(spk.SamplingPattern(pts[None]), fld, "exact")
+    cref, gref = orc.attraction_exact(pts, rho.grid, fld.kernel_eps)
+    assert abs(res.cost - cref) <= VAL_TOL * abs(cref)
+    assert rel_l2(res.grad, gref) <= GRAD_TOL
+    with pytest.raises(ValueError, match="cubic"):
+        spk.eval_attraction(spk.SamplingPattern(pts[None]), fld, "consistent")

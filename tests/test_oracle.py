@@ -116,3 +116,20 @@ def test_polish_bitwise_and_capped(proj):
         capped, n = orc.polish(proj["polish_in"][s], a, b, pin, np.zeros(3), 1e-7, 37)
         assert n == 37
         assert np.array_equal(capped, proj["polish_capped37"][s])
+
+
+def test_anisotropic_grid_sums_match_cubic_when_isotropic():
+    # The anisotropic oracle path reduces to the cubic one when all N_a agree.
+    rng = np.random.default_rng(3)
+    rho = rng.uniform(0, 1, (9, 9, 9))
+    rho /= rho.sum()
+    pts = rng.uniform(-1, 1, (20, 3))
+    v1, g1 = orc.grid_sums(pts, rho, 1e-3)
+    # an explicit O(G) restatement with node coordinates (i - N)/N
+    ax = (np.arange(9) - 4) / 4.0
+    X, Y, Z = np.meshgrid(ax, ax, ax, indexing="ij")
+    for t in range(3):
+        d = pts[t][:, None, None, None] - np.stack([X, Y, Z])
+        h = np.sqrt(1e-3 + (d * d).sum(0))
+        assert abs(v1[t] - (rho * h).sum()) <= 1e-12 * v1[t]
+        assert np.abs(g1[t] - (rho * d / h).reshape(3, -1).sum(1)).max() <= 1e-12
