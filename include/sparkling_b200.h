@@ -8,8 +8,8 @@
  * returns SPK_OK (0) or a nonzero SPK_ERR_* code; spk_last_error() then holds a
  * one-line message.  No C++ exception crosses this boundary.
  *
- * Positions used by the N-body kernels are float4 records {x, y, z, w}: for sample
- * positions w is ignored (z = 0 in 2D); for density-grid sources w is the weight rho.
+ * Sample positions used by the N-body kernels are float4 records {x, y, z, |x|^2} (z = 0
+ * in 2D); the density is passed as fp32 lattice weights with implicit node coordinates.
  * Trajectories are fp64 (n_shots, n_s, dims) row-major, shot-major, axis-innermost,
  * exactly the SamplingPattern.coords layout (reference src/core.py:141-186).
  *
@@ -40,8 +40,9 @@ const char* spk_last_error(void);
 
 /* ---------------------------------------------------------------- K1 / K2 N-body */
 
-/* Workspace for one spk_*_sums call with n_tgt targets and two source segments. */
-size_t spk_nbody_workspace_bytes(int64_t n_tgt, int64_t n_src0, int64_t n_src1);
+/* Workspace for one spk_*_sums call with n_tgt targets, n_cells lattice cells (segment 0)
+ * and n_pos positions (segment 1). */
+size_t spk_nbody_workspace_bytes(int64_t n_tgt, int64_t n_cells, int64_t n_pos);
 
 /* Repulsion raw sums.  Replaces _treecode.direct_sums (_treecode.py:506-534) and
  * direct_sums_subset (:474-503): for every target i,
@@ -54,30 +55,35 @@ int spk_direct_sums(const void* tgt, int64_t n_tgt, const void* src, int64_t n_s
                     int dims, float eps2, double* val, double* grad, void* ws,
                     size_t ws_bytes, spk_stream_t stream);
 
-/* Attraction raw sums over weighted grid sources (north-star attraction):
- *   val[i]  = sum_y w_y sqrt(|t_i - y|^2 + eps2),  grad[i] = sum_y w_y (t_i - y)/h.
+/* Attraction raw sums over the density lattice (north-star attraction):
+ *   val[i]  = sum_y w_y sqrt(|t_i - y|^2 + eps2),  grad[i] = sum_y w_y (t_i - y)/h,
+ * y over the side0 x side1 [x side2] node grid, node i on axis a at (i - N_a)/N_a with
+ * side_a = 2 N_a + 1 (density.py:58-67); grid_w: fp32 weights, row-major, zero-padded
+ * to a multiple of 4 (spk_build_grid_sources); side: host array of dims sides (<= 1023).
  * With the grid nodes themselves as targets this is precompute_field's potential and
  * force (attraction.py:62-113). */
-int spk_grid_sums(const void* tgt, int64_t n_tgt, const void* grid_src, int64_t n_cells,
+int spk_grid_sums(const void* tgt, int64_t n_tgt, const float* grid_w, const int64_t* side,
                   int dims, float eps2, double* val, double* grad, void* ws,
                   size_t ws_bytes, spk_stream_t stream);
 
 /* Both sums in ONE launch (the optimize() hot loop, optimizer.py:302-303): segment 0 =
- * weighted grid sources (attraction), segment 1 = unweighted positions (repulsion).
- * Either segment may be empty (n = 0, outputs untouched). */
-int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const void* grid_src,
-                   int64_t n_cells, float eps2_att, const void* pos_src, int64_t n_pos,
+ * the density lattice (attraction), segment 1 = positions (repulsion).  Either segment
+ * may be empty (grid_w = NULL or n_pos = 0). */
+int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const float* grid_w,
+                   const int64_t* side, float eps2_att, const void* pos_src, int64_t n_pos,
                    float eps2_rep, double* val_att, double* grad_att, double* val_rep,
                    double* grad_rep, void* ws, size_t ws_bytes, spk_stream_t stream);
 
-/* Pack fp64 (p, dims) coordinates into float4 {x, y, z|0, 1}. */
+/* Pack fp64 (p, dims) coordinates into position records float4 {x, y, z|0, |x|^2}. */
 int spk_pack_positions(const double* coords, int64_t p, int dims, void* pos4,
                        spk_stream_t stream);
 
-/* Grid sources {x, y, z|0, rho} for a (side0 x side1 [x side2]) node grid, node i on axis
- * a at (i - N_a)/N_a with side_a = 2 N_a + 1 (density.py:58-67).  rho: fp64 row-major. */
-int spk_build_grid_sources(const double* rho, int dims, const int64_t* side, void* out,
-                           spk_stream_t stream);
+/* Lattice sources from an fp64 density grid (rho row-major, `side` host array of dims odd
+ * sides): fp32 weights (caller allocates prod(side) rounded up to a multiple of 4
+ * floats) and, if `nodes` != NULL, the node position records float4 {x, y, z|0, |x|^2}
+ * (targets for precompute_field). */
+int spk_build_grid_sources(const double* rho, int dims, const int64_t* side, float* weights,
+                           void* nodes, spk_stream_t stream);
 
 /* Combine raw sums into the optimizer gradient and scalars (optimizer.py:302-321):
  *   grad[i] = grad_att[i] / p_att - grad_rep[i] / (p_rep * p_rep)

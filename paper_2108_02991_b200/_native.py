@@ -30,12 +30,12 @@ SIGNATURES = {
     "spk_nbody_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "spk_direct_sums": (c_int, [c_vp, c_i64, c_vp, c_i64, c_int, c_flt, c_vp, c_vp, c_vp,
                                 c_size, c_vp]),
-    "spk_grid_sums": (c_int, [c_vp, c_i64, c_vp, c_i64, c_int, c_flt, c_vp, c_vp, c_vp,
-                              c_size, c_vp]),
-    "spk_fused_sums": (c_int, [c_vp, c_i64, c_int, c_vp, c_i64, c_flt, c_vp, c_i64, c_flt,
-                               c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "spk_grid_sums": (c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(c_i64), c_int, c_flt, c_vp,
+                              c_vp, c_vp, c_size, c_vp]),
+    "spk_fused_sums": (c_int, [c_vp, c_i64, c_int, c_vp, ctypes.POINTER(c_i64), c_flt, c_vp,
+                               c_i64, c_flt, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "spk_pack_positions": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp]),
-    "spk_build_grid_sources": (c_int, [c_vp, c_int, ctypes.POINTER(c_i64), c_vp, c_vp]),
+    "spk_build_grid_sources": (c_int, [c_vp, c_int, ctypes.POINTER(c_i64), c_vp, c_vp, c_vp]),
     "spk_combine_workspace_bytes": (c_size, [c_i64]),
     "spk_combine_gradient": (c_int, [c_i64, c_int, c_vp, c_vp, c_dbl, c_vp, c_vp, c_dbl,
                                      c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),

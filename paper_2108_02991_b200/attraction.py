@@ -38,10 +38,11 @@ class AttractionResult(NamedTuple):
 
 
 def field_workspace_bytes(grid_n: int, dims: int) -> int:
-    """Device bytes needed to build the field: node sources (16 B), potential + force
-    (8 (1 + d) B) and the K2 partial-sum slots (<= 64 chunks x 32 B) per node."""
+    """Device bytes needed to build the field: lattice weights + node records (20 B),
+    potential + force (8 (1 + d) B) and the K2 partial-sum slots (<= 64 chunks x 32 B)
+    per node."""
     nodes = (2 * grid_n + 1) ** dims
-    return nodes * (16 + 8 * (1 + dims) + 64 * 32)
+    return nodes * (20 + 8 * (1 + dims) + 64 * 32)
 
 
 class KernelField:
@@ -99,18 +100,41 @@ class KernelField:
             self._evaluate_grids()
         return self._force
 
+    @property
+    def sides(self) -> tuple:
+        """Node-grid sides (2 N_a + 1 per axis)."""
+        if self.density is not None:
+            return tuple(self.density.grid.shape)
+        return tuple(self._potential.shape)
+
+    def _build_sources(self, with_nodes: bool) -> None:
+        if self.density is None:
+            raise ValueError("exact attraction needs the density grid (precompute_field)")
+        rho = _device.h2d(self.density.grid)
+        n = rho.numel()
+        w = torch.empty(((n + 3) // 4) * 4, dtype=torch.float32, device=rho.device)
+        nodes = None
+        if with_nodes:
+            nodes = torch.empty((n, 4), dtype=torch.float32, device=rho.device)
+        _native.call("spk_build_grid_sources", rho.data_ptr(), self.dims,
+                     _native.i64_array(self.sides), w.data_ptr(), _device.ptr(nodes),
+                     _device.stream())
+        self._dev["w"] = w
+        if with_nodes:
+            self._dev["nodes"] = nodes
+
     def device_sources(self) -> torch.Tensor:
-        """float4 {x, y, z, rho} records of every density node (the K2 sources)."""
-        if "src" not in self._dev:
-            if self.density is None:
-                raise ValueError("exact attraction needs the density grid (precompute_field)")
-            rho = _device.h2d(self.density.grid)
-            out = torch.empty((rho.numel(), 4), dtype=torch.float32, device=rho.device)
-            sides = _native.i64_array(list(self.density.grid.shape))
-            _native.call("spk_build_grid_sources", rho.data_ptr(), self.dims, sides,
-                         out.data_ptr(), _device.stream())
-            self._dev["src"] = out
-        return self._dev["src"]
+        """fp32 lattice weights (zero-padded to a multiple of 4) -- the K2 sources; node
+        coordinates are implicit in the kernel."""
+        if "w" not in self._dev:
+            self._build_sources(with_nodes=False)
+        return self._dev["w"]
+
+    def device_nodes(self) -> torch.Tensor:
+        """Node position records float4 {x, y, z, |x|^2} (targets for the field grids)."""
+        if "nodes" not in self._dev:
+            self._build_sources(with_nodes=True)
+        return self._dev["nodes"]
 
     def device_grids(self):
         """(potential [G] f64, force [d, G] f64) on the device."""
@@ -119,27 +143,32 @@ class KernelField:
                 self._dev["pot"] = _device.h2d(self._potential.reshape(-1))
                 self._dev["force"] = _device.h2d(self._force.reshape(self.dims, -1))
             else:
-                src = self.device_sources()
-                g = src.shape[0]
-                val = torch.empty(g, dtype=torch.float64, device=src.device)
-                grad = torch.empty((g, self.dims), dtype=torch.float64, device=src.device)
-                grid_sums_device(src, src, self.dims, self.kernel_eps ** 2, val, grad)
+                nodes = self.device_nodes()
+                g = nodes.shape[0]
+                val = torch.empty(g, dtype=torch.float64, device=nodes.device)
+                grad = torch.empty((g, self.dims), dtype=torch.float64, device=nodes.device)
+                grid_sums_device(nodes, self, self.kernel_eps ** 2, val, grad)
                 self._dev["pot"] = val
                 self._dev["force"] = grad.t().contiguous()
         return self._dev["pot"], self._dev["force"]
 
 
-def grid_sums_device(tgt4, src4, dims, eps2, val=None, grad=None):
-    """Raw K2 sums: val_i = sum_y w_y h, grad_i = sum_y w_y (t_i - y)/h (fp64 out)."""
-    n_t, n_c = tgt4.shape[0], src4.shape[0]
+def grid_sums_device(tgt4, field: "KernelField", eps2, val=None, grad=None):
+    """Raw K2 sums over the field's density lattice:
+    val_i = sum_y w_y h, grad_i = sum_y w_y (t_i - y)/h (fp64 out)."""
+    n_t = tgt4.shape[0]
+    dims = field.dims
+    w = field.device_sources()
+    sides = field.sides
+    n_c = int(np.prod(sides))
     if val is None:
         val = torch.empty(n_t, dtype=torch.float64, device=tgt4.device)
     if grad is None:
         grad = torch.empty((n_t, dims), dtype=torch.float64, device=tgt4.device)
     nbytes = _native.query("spk_nbody_workspace_bytes", n_t, n_c, 0)
     ws = _device.workspace(nbytes, "nbody")
-    _native.call("spk_grid_sums", tgt4.data_ptr(), n_t, src4.data_ptr(), n_c, dims,
-                 float(eps2), val.data_ptr(), grad.data_ptr(), ws.data_ptr(), ws.numel(),
+    _native.call("spk_grid_sums", tgt4.data_ptr(), n_t, w.data_ptr(), _native.i64_array(sides),
+                 dims, float(eps2), val.data_ptr(), grad.data_ptr(), ws.data_ptr(), ws.numel(),
                  _device.stream())
     return val, grad
 
@@ -212,9 +241,8 @@ def eval_attraction(k: SamplingPattern, field: KernelField,
     p = pts.shape[0]
     coords = _device.h2d(pts)
     if grad_mode == "exact":
-        src = field.device_sources()
         tgt = _device.pack_positions(coords)
-        val, grad = grid_sums_device(tgt, src, k.dims, field.kernel_eps ** 2)
+        val, grad = grid_sums_device(tgt, field, field.kernel_eps ** 2)
         vals_h = _device.d2h(val)
         n_clamped = _n_outside(pts)
     else:

@@ -55,16 +55,21 @@ constexpr int NB_TILE_BYTES = NB_STAGES * NB_TILE * 16;
 // fp64 per-target accumulators live in shared memory (per-thread slots) so that the
 // kernel fits 128 registers and two CTAs (16 warps) share an SM.
 constexpr int NB_ACC_BYTES = NB_TPT * 4 * NB_THREADS * 8;
-constexpr int NB_SMEM = NB_TILE_BYTES + NB_ACC_BYTES;
+constexpr int NB_AXES_BYTES = 3 * 1024 * 4;  // lattice node tables (NB_AXIS_MAX per axis)
+constexpr int NB_SMEM = NB_TILE_BYTES + NB_ACC_BYTES + NB_AXES_BYTES;
 constexpr int NB_MAX_CHUNKS = 64;
 
+// Source segment.  kind 0: positions, float4 {x, y, z, |x|^2} records (unweighted,
+// repulsion).  kind 1: the density lattice -- fp32 weights w[c] for the node grid
+// s0 x s1 (x s2), node coordinates implicit ((i - N_a)/N_a, density.py:58-67).
 struct SegDesc {
-    const float4* src;
-    long long n;      // source records
-    long long tiles;  // ceil(n / NB_TILE)
+    const void* src;
+    long long n;      // records (kind 0) or cells (kind 1)
+    long long tiles;  // ceil(n / tile size)
     int n_chunks;     // chunks this segment is split into (0 if empty)
-    int weighted;     // 1: multiply by w (grid density); 0: w ignored (positions)
+    int kind;
     float eps2;
+    int s0, s1, s2;   // lattice sides (kind 1); s2 = 1 in 2D
 };
 
 struct NBParams {
@@ -75,29 +80,34 @@ struct NBParams {
     double* part;  // [chunk][4][n_tgt]: value, gx, gy, gz
 };
 
+constexpr int NB_TILE_W = NB_TILE;  // lattice cells per stage (fp32 partials span <= 512 cells)
+constexpr int NB_AXIS_MAX = 1024;       // per-axis node table capacity (shared memory)
+
 __device__ __forceinline__ float rsqrt_sfu(float x) {
     float r;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
-// One shared-memory tile against this thread's NB_TPT targets.  W: weighted sources;
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+
+// Positions tile against this thread's NB_TPT targets (difference form).
 // G: guard r2 == 0 (eps2 == 0 => coincident points contribute value 0, gradient 0,
 // like the reference's `if h > 0` at _treecode.py:525).
-template <int D, bool W, bool G>
-__device__ __forceinline__ void tile_pairs(const float4* __restrict__ tile, int cnt,
-                                           const float2 (&X)[NB_PAIRS],
-                                           const float2 (&Y)[NB_PAIRS],
-                                           const float2 (&Z)[NB_PAIRS], float2 e2,
-                                           float2 (&av)[NB_PAIRS], float2 (&ax)[NB_PAIRS],
-                                           float2 (&ay)[NB_PAIRS],
-                                           float2 (&az)[NB_PAIRS]) {
+template <int D, bool G>
+__device__ __forceinline__ void tile_positions(const float4* __restrict__ tile, int cnt,
+                                               const float2 (&X)[NB_PAIRS],
+                                               const float2 (&Y)[NB_PAIRS],
+                                               const float2 (&Z)[NB_PAIRS], float2 e2,
+                                               float2 (&av)[NB_PAIRS], float2 (&ax)[NB_PAIRS],
+                                               float2 (&ay)[NB_PAIRS],
+                                               float2 (&az)[NB_PAIRS]) {
 #pragma unroll NB_UNROLL
     for (int j = 0; j < cnt; ++j) {
         const float4 s = tile[j];
-        const float2 nsx = make_float2(-s.x, -s.x);
-        const float2 nsy = make_float2(-s.y, -s.y);
-        const float2 nsz = make_float2(-s.z, -s.z);
+        const float2 nsx = bc(-s.x);
+        const float2 nsy = bc(-s.y);
+        const float2 nsz = bc(-s.z);
 #pragma unroll
         for (int k = 0; k < NB_PAIRS; ++k) {
             const float2 dx = __fadd2_rn(X[k], nsx);
@@ -116,8 +126,7 @@ __device__ __forceinline__ void tile_pairs(const float4* __restrict__ tile, int 
                 inv.x = r2.x > 0.0f ? inv.x : 0.0f;
                 inv.y = r2.y > 0.0f ? inv.y : 0.0f;
             }
-            if (W) inv = __fmul2_rn(inv, make_float2(s.w, s.w));
-            av[k] = __ffma2_rn(r2, inv, av[k]);  // sum w*h = sum r2 * (w/h)
+            av[k] = __ffma2_rn(r2, inv, av[k]);  // sum h = sum r2 / h
             ax[k] = __ffma2_rn(dx, inv, ax[k]);
             ay[k] = __ffma2_rn(dy, inv, ay[k]);
             if (D == 3) az[k] = __ffma2_rn(dz, inv, az[k]);
@@ -125,20 +134,105 @@ __device__ __forceinline__ void tile_pairs(const float4* __restrict__ tile, int 
     }
 }
 
-template <int D, bool W, bool G>
+// Lattice tile: cells [c0, c0 + cnt) of the density grid.  Cells are walked row by row
+// (a row = all nodes along the last axis with the other coordinates fixed), so along a
+// row only the last-axis difference dl changes: per target and row
+//     a = dx^2 (+ dy^2) + eps^2,  and per cell
+//     r2 = dl^2 + a,  winv = w / h,  v += r2 winv,  S += winv,  g_last += dl winv
+// then g_other += d_other * S at the end of the row.  6 FP32 lane-ops + 1 MUFU per pair
+// (the reference's algorithmic count stays 19 flops per pair).
+template <int D, bool G>
+__device__ __forceinline__ void tile_lattice(const float* __restrict__ tile, long long c0, int cnt,
+                                             const SegDesc& S, const float* __restrict__ axes,
+                                             const float2 (&X)[NB_PAIRS],
+                                             const float2 (&Y)[NB_PAIRS],
+                                             const float2 (&Z)[NB_PAIRS], float2 e2,
+                                             float2 (&av)[NB_PAIRS], float2 (&ax)[NB_PAIRS],
+                                             float2 (&ay)[NB_PAIRS],
+                                             float2 (&az)[NB_PAIRS]) {
+    const int R = D == 3 ? S.s2 : S.s1;  // row length
+    const float* AX = axes;
+    const float* AY = axes + S.s0;
+    const float* AL = D == 3 ? axes + S.s0 + S.s1 : AY;  // last-axis table
+    long long row = c0 / R;
+    int k = (int)(c0 - row * R);
+    int done = 0;
+    while (done < cnt) {
+        const int n_run = min(R - k, cnt - done);
+        // per-row constants
+        float2 d0[NB_PAIRS], d1[NB_PAIRS], A[NB_PAIRS], Sw[NB_PAIRS];
+        if (D == 3) {
+            const int i = (int)(row / S.s1), j = (int)(row - (long long)(row / S.s1) * S.s1);
+            const float2 nxi = bc(-AX[i]), nyj = bc(-AY[j]);
+#pragma unroll
+            for (int q = 0; q < NB_PAIRS; ++q) {
+                d0[q] = __fadd2_rn(X[q], nxi);
+                d1[q] = __fadd2_rn(Y[q], nyj);
+                A[q] = __ffma2_rn(d1[q], d1[q], __ffma2_rn(d0[q], d0[q], e2));
+                Sw[q] = bc(0.f);
+            }
+        } else {
+            const float2 nxi = bc(-AX[(int)row]);
+#pragma unroll
+            for (int q = 0; q < NB_PAIRS; ++q) {
+                d0[q] = __fadd2_rn(X[q], nxi);
+                A[q] = __ffma2_rn(d0[q], d0[q], e2);
+                Sw[q] = bc(0.f);
+            }
+        }
+        const float* wrow = tile + done;
+        const float* lrow = AL + k;
+#pragma unroll 4
+        for (int m = 0; m < n_run; ++m) {
+            const float w = wrow[m];
+            const float2 nl = bc(-lrow[m]);
+#pragma unroll
+            for (int q = 0; q < NB_PAIRS; ++q) {
+                const float2 dl = __fadd2_rn(D == 3 ? Z[q] : Y[q], nl);
+                const float2 r2 = __ffma2_rn(dl, dl, A[q]);
+                float2 inv;
+                inv.x = rsqrt_sfu(r2.x);
+                inv.y = rsqrt_sfu(r2.y);
+                if (G) {
+                    inv.x = r2.x > 0.0f ? inv.x : 0.0f;
+                    inv.y = r2.y > 0.0f ? inv.y : 0.0f;
+                }
+                const float2 winv = __fmul2_rn(inv, bc(w));
+                av[q] = __ffma2_rn(r2, winv, av[q]);
+                Sw[q] = __fadd2_rn(Sw[q], winv);
+                if (D == 3) az[q] = __ffma2_rn(dl, winv, az[q]);
+                else ay[q] = __ffma2_rn(dl, winv, ay[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NB_PAIRS; ++q) {
+            ax[q] = __ffma2_rn(d0[q], Sw[q], ax[q]);
+            if (D == 3) ay[q] = __ffma2_rn(d1[q], Sw[q], ay[q]);
+        }
+        done += n_run;
+        k = 0;
+        ++row;
+    }
+}
+
+template <int D, int KIND, bool G>
 __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, long long t_end,
-                                          float4* tiles, uint64_t* bars,
+                                          char* stages, uint64_t* bars, const float* axes,
                                           const float2 (&X)[NB_PAIRS],
                                           const float2 (&Y)[NB_PAIRS],
                                           const float2 (&Z)[NB_PAIRS], double* acc) {
     const int tid = threadIdx.x;
-    const float2 e2 = make_float2(S.eps2, S.eps2);
+    const float2 e2 = bc(S.eps2);
+    constexpr int TILE = KIND == 0 ? NB_TILE : NB_TILE_W;
+    constexpr int REC = KIND == 0 ? 16 : 4;
+    constexpr int STAGE_BYTES = NB_TILE * 16;
     auto issue = [&](long long t, int stage) {
-        const long long first = t * NB_TILE;
-        const long long cnt = min((long long)NB_TILE, S.n - first);
-        const uint32_t bytes = (uint32_t)(cnt * 16);
+        const long long first = t * TILE;
+        const long long cnt = min((long long)TILE, S.n - first);
+        const uint32_t bytes = (uint32_t)(((cnt * REC) + 15) & ~15LL);  // weights padded
         mbar_expect_tx(&bars[stage], bytes);
-        tma_load_1d(tiles + stage * NB_TILE, S.src + first, bytes, &bars[stage]);
+        tma_load_1d(stages + stage * STAGE_BYTES,
+                    static_cast<const char*>(S.src) + first * REC, bytes, &bars[stage]);
     };
     if (tid == 0) {
         for (int s = 0; s < NB_STAGES; ++s)
@@ -148,14 +242,19 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
         const long long i = t - t_begin;
         const int stage = (int)(i % NB_STAGES);
         const uint32_t parity = (uint32_t)((i / NB_STAGES) & 1);
-        const int cnt = (int)min((long long)NB_TILE, S.n - t * NB_TILE);
+        const int cnt = (int)min((long long)TILE, S.n - t * TILE);
         float2 av[NB_PAIRS], ax[NB_PAIRS], ay[NB_PAIRS], az[NB_PAIRS];
 #pragma unroll
         for (int k = 0; k < NB_PAIRS; ++k) {
-            av[k] = ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
+            av[k] = ax[k] = ay[k] = az[k] = bc(0.f);
         }
         mbar_wait(&bars[stage], parity);
-        tile_pairs<D, W, G>(tiles + stage * NB_TILE, cnt, X, Y, Z, e2, av, ax, ay, az);
+        if (KIND == 0)
+            tile_positions<D, G>(reinterpret_cast<const float4*>(stages + stage * STAGE_BYTES),
+                                 cnt, X, Y, Z, e2, av, ax, ay, az);
+        else
+            tile_lattice<D, G>(reinterpret_cast<const float*>(stages + stage * STAGE_BYTES),
+                               t * TILE, cnt, S, axes, X, Y, Z, e2, av, ax, ay, az);
 #define NB_ACC(k, c) acc[((k) * 4 + (c)) * NB_THREADS + tid]
 #pragma unroll
         for (int k = 0; k < NB_PAIRS; ++k) {
@@ -177,8 +276,9 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
 
 template <int D>
 __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(const NBParams P) {
-    extern __shared__ __align__(128) float4 tiles[];
-    double* acc = reinterpret_cast<double*>(reinterpret_cast<char*>(tiles) + NB_TILE_BYTES);
+    extern __shared__ __align__(128) char stages[];
+    double* acc = reinterpret_cast<double*>(stages + NB_TILE_BYTES);
+    float* axes = reinterpret_cast<float*>(stages + NB_TILE_BYTES + NB_ACC_BYTES);
     __shared__ __align__(8) uint64_t bars[NB_STAGES];
     const int tid = threadIdx.x;
     const long long unit = blockIdx.x;
@@ -204,7 +304,17 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(con
     }
 #pragma unroll
     for (int k = 0; k < NB_TPT * 4; ++k) acc[k * NB_THREADS + tid] = 0.0;
-
+    if (S.kind == 1) {
+        // node coordinate tables (i - N_a) / N_a, computed in fp64 then rounded
+        const int sides[3] = {S.s0, S.s1, S.s2};
+        int off = 0;
+        for (int a = 0; a < D; ++a) {
+            const int h = (sides[a] - 1) / 2;
+            for (int i = tid; i < sides[a]; i += NB_THREADS)
+                axes[off + i] = (float)((double)(i - h) / (double)h);
+            off += sides[a];
+        }
+    }
     if (tid == 0) {
         for (int s = 0; s < NB_STAGES; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
@@ -212,12 +322,12 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(con
     __syncthreads();
 
     const bool guard = !(S.eps2 >= FLT_MIN);
-    if (S.weighted) {
-        if (guard) run_chunk<D, true, true>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
-        else run_chunk<D, true, false>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
+    if (S.kind == 1) {
+        if (guard) run_chunk<D, 1, true>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        else run_chunk<D, 1, false>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
     } else {
-        if (guard) run_chunk<D, false, true>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
-        else run_chunk<D, false, false>(S, t_begin, t_end, tiles, bars, X, Y, Z, acc);
+        if (guard) run_chunk<D, 0, true>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        else run_chunk<D, 0, false>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
     }
 
     double* slot = P.part + (size_t)chunk * 4 * P.n_tgt;
@@ -280,21 +390,27 @@ static int nbody_slots() {
     return slots;
 }
 
-// Choose the chunk counts: minimise (waves x longest unit) + per-chunk reduction cost,
-// with the two segments split in proportion to their tile counts.
+// Relative cost of one tile: a position tile is NB_TILE pairs per target at ~10 FP32
+// lane-ops, a lattice tile NB_TILE_W pairs bounded by the SFU (16 / clk / SM).
+constexpr double NB_COST_POS_TILE = NB_TILE / 12.8;
+constexpr double NB_COST_LAT_TILE = NB_TILE_W / 16.0;
+
+// Choose the chunk counts: minimise (waves x longest unit) + per-unit overhead, with the
+// two segments split in proportion to their estimated cost.  seg0 is the lattice.
 static Plan make_plan(long long n_tgt, long long n0, long long n1) {
     Plan pl;
     if (n_tgt <= 0) return pl;
     pl.n_tb = (n_tgt + NB_TB - 1) / NB_TB;
-    const long long t0 = (n0 + NB_TILE - 1) / NB_TILE;
+    const long long t0 = (n0 + NB_TILE_W - 1) / NB_TILE_W;
     const long long t1 = (n1 + NB_TILE - 1) / NB_TILE;
+    const double w0 = t0 * NB_COST_LAT_TILE, w1 = t1 * NB_COST_POS_TILE;
     const long long slots = nbody_slots();
     double best = 1e300;
     const int cmin = (t0 > 0) + (t1 > 0);
     for (int c = std::max(cmin, 1); c <= NB_MAX_CHUNKS; ++c) {
         int c0 = 0, c1 = 0;
         if (t0 > 0 && t1 > 0) {
-            c0 = (int)std::llround((double)c * t0 / (double)(t0 + t1));
+            c0 = (int)std::llround((double)c * w0 / (w0 + w1));
             c0 = std::max(1, std::min(c - 1, c0));
             c1 = c - c0;
         } else if (t0 > 0) {
@@ -303,13 +419,13 @@ static Plan make_plan(long long n_tgt, long long n0, long long n1) {
             c1 = c;
         }
         if ((t0 > 0 && c0 > t0) || (t1 > 0 && c1 > t1)) break;
-        const long long l0 = c0 ? (t0 + c0 - 1) / c0 : 0;
-        const long long l1 = c1 ? (t1 + c1 - 1) / c1 : 0;
+        const double l0 = c0 ? (double)((t0 + c0 - 1) / c0) * NB_COST_LAT_TILE : 0.0;
+        const double l1 = c1 ? (double)((t1 + c1 - 1) / c1) * NB_COST_POS_TILE : 0.0;
         const long long units = pl.n_tb * c;
         const long long waves = (units + slots - 1) / slots;
-        // per-unit fixed cost ~ 0.25 tile (prologue, pipeline fill, partial-slot write)
-        const double cost = (double)waves * ((double)std::max(l0, l1) + 0.25);
-        if (cost < best * 0.999) {
+        // per-unit fixed cost ~ 0.25 position tile (prologue, pipeline fill, slot write)
+        const double cost = (double)waves * (std::max(l0, l1) + 0.25 * NB_COST_POS_TILE);
+        if (cost < best * 0.995) {
             best = cost;
             pl.nc0 = c0;
             pl.nc1 = c1;
@@ -319,12 +435,25 @@ static Plan make_plan(long long n_tgt, long long n0, long long n1) {
     return pl;
 }
 
-static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float4* s0,
-                       long long n0, float e0, int w0, const float4* s1, long long n1,
-                       float e1, int w1, double* val0, double* grad0, double* val1,
-                       double* grad1, void* ws, size_t ws_bytes, cudaStream_t stream) {
+// seg0 = lattice (weights w0 over `side`), seg1 = positions.
+static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float* w0,
+                       const int64_t* side, float e0, const float4* s1, long long n1, float e1,
+                       double* val0, double* grad0, double* val1, double* grad1, void* ws,
+                       size_t ws_bytes, cudaStream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
-    SPK_REQUIRE(n_tgt >= 0 && n0 >= 0 && n1 >= 0, SPK_ERR_ARG, "negative size");
+    long long n0 = 0;
+    int sd[3] = {1, 1, 1};
+    if (w0) {
+        SPK_REQUIRE(side != nullptr, SPK_ERR_ARG, "lattice sides missing");
+        n0 = 1;
+        for (int a = 0; a < dims; ++a) {
+            sd[a] = (int)side[a];
+            SPK_REQUIRE(side[a] >= 3 && (side[a] & 1) && side[a] <= NB_AXIS_MAX, SPK_ERR_ARG,
+                        "lattice sides must be odd, >= 3 and <= %d", NB_AXIS_MAX);
+            n0 *= side[a];
+        }
+    }
+    SPK_REQUIRE(n_tgt >= 0 && n1 >= 0, SPK_ERR_ARG, "negative size");
     if (n_tgt == 0 || (n0 == 0 && n1 == 0)) {
         // Empty sums: zero the outputs like a loop that never runs.
         if (n_tgt > 0) {
@@ -336,7 +465,7 @@ static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float
         return SPK_OK;
     }
     SPK_REQUIRE(tgt != nullptr, SPK_ERR_ARG, "null target pointer");
-    SPK_REQUIRE(((uintptr_t)s0 & 15) == 0 && ((uintptr_t)s1 & 15) == 0, SPK_ERR_ARG,
+    SPK_REQUIRE(((uintptr_t)w0 & 15) == 0 && ((uintptr_t)s1 & 15) == 0, SPK_ERR_ARG,
                 "source arrays must be 16-byte aligned");
     const Plan pl = make_plan(n_tgt, n0, n1);
     SPK_REQUIRE(ws != nullptr && ws_bytes >= pl.ws_bytes, SPK_ERR_WORKSPACE,
@@ -345,10 +474,12 @@ static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float
     P.tgt = tgt;
     P.n_tgt = n_tgt;
     P.n_tb = pl.n_tb;
-    P.seg[0] = SegDesc{s0, n0, (n0 + NB_TILE - 1) / NB_TILE, pl.nc0, w0, e0};
-    P.seg[1] = SegDesc{s1, n1, (n1 + NB_TILE - 1) / NB_TILE, pl.nc1, w1, e1};
+    P.seg[0] = SegDesc{w0, n0, (n0 + NB_TILE_W - 1) / NB_TILE_W, pl.nc0, 1, e0,
+                       sd[0], sd[1], dims == 3 ? sd[2] : 1};
+    P.seg[1] = SegDesc{s1, n1, (n1 + NB_TILE - 1) / NB_TILE, pl.nc1, 0, e1, 0, 0, 0};
     P.part = static_cast<double*>(ws);
     const long long grid = pl.n_tb * (pl.nc0 + pl.nc1);
+    nbody_slots();  // sets the shared-memory attribute once
     if (dims == 3)
         nbody_kernel<3><<<(unsigned)grid, NB_THREADS, NB_SMEM, stream>>>(P);
     else
@@ -373,20 +504,30 @@ __global__ void pack_positions_kernel(const double* __restrict__ c, long long p,
     out[i] = pos_record(r[0], r[1], dims == 3 ? r[2] : 0.0);
 }
 
+// Lattice weights (fp32, zero-padded to a multiple of 4) and, optionally, the node
+// position records {x, y, z, |x|^2} (targets for precompute_field).
 __global__ void grid_sources_kernel(const double* __restrict__ rho, long long s0,
                                     long long s1, long long s2, int dims,
-                                    float4* __restrict__ out) {
+                                    float* __restrict__ w, float4* __restrict__ nodes) {
     const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long n = s0 * s1 * s2;
-    if (c >= n) return;
-    const long long k = c % s2;
-    const long long j = (c / s2) % s1;
-    const long long i = c / (s1 * s2);
-    const long long h0 = (s0 - 1) / 2, h1 = (s1 - 1) / 2, h2 = (s2 - 1) / 2;
-    const double x = (double)(i - h0) / (double)h0;
-    const double y = (double)(j - h1) / (double)h1;
-    const double z = dims == 3 ? (double)(k - h2) / (double)h2 : 0.0;
-    out[c] = make_float4((float)x, (float)y, (float)z, (float)rho[c]);
+    const long long npad = (n + 3) & ~3LL;
+    if (c >= npad) return;
+    if (c >= n) {
+        w[c] = 0.f;
+        return;
+    }
+    w[c] = (float)rho[c];
+    if (nodes) {
+        const long long k = c % s2;
+        const long long j = (c / s2) % s1;
+        const long long i = c / (s1 * s2);
+        const long long h0 = (s0 - 1) / 2, h1 = (s1 - 1) / 2, h2 = (s2 - 1) / 2;
+        const double x = (double)(i - h0) / (double)h0;
+        const double y = (double)(j - h1) / (double)h1;
+        const double z = dims == 3 ? (double)(k - h2) / (double)h2 : 0.0;
+        nodes[c] = pos_record(x, y, z);
+    }
 }
 
 // ------------------------------------------------------------ gradient combination
@@ -479,26 +620,25 @@ size_t spk_nbody_workspace_bytes(int64_t n_tgt, int64_t n_src0, int64_t n_src1) 
 int spk_direct_sums(const void* tgt, int64_t n_tgt, const void* src, int64_t n_src, int dims,
                     float eps2, double* val, double* grad, void* ws, size_t ws_bytes,
                     spk_stream_t stream) {
-    return launch_sums((const float4*)tgt, n_tgt, dims, nullptr, 0, 0.f, 0,
-                       (const float4*)src, n_src, eps2, 0, nullptr, nullptr, val, grad, ws,
+    return launch_sums((const float4*)tgt, n_tgt, dims, nullptr, nullptr, 0.f,
+                       (const float4*)src, n_src, eps2, nullptr, nullptr, val, grad, ws,
                        ws_bytes, (cudaStream_t)stream);
 }
 
-int spk_grid_sums(const void* tgt, int64_t n_tgt, const void* grid_src, int64_t n_cells,
+int spk_grid_sums(const void* tgt, int64_t n_tgt, const float* grid_w, const int64_t* side,
                   int dims, float eps2, double* val, double* grad, void* ws, size_t ws_bytes,
                   spk_stream_t stream) {
-    return launch_sums((const float4*)tgt, n_tgt, dims, (const float4*)grid_src, n_cells,
-                       eps2, 1, nullptr, 0, 0.f, 0, val, grad, nullptr, nullptr, ws, ws_bytes,
-                       (cudaStream_t)stream);
+    return launch_sums((const float4*)tgt, n_tgt, dims, grid_w, side, eps2, nullptr, 0, 0.f,
+                       val, grad, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
-int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const void* grid_src,
-                   int64_t n_cells, float eps2_att, const void* pos_src, int64_t n_pos,
+int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const float* grid_w,
+                   const int64_t* side, float eps2_att, const void* pos_src, int64_t n_pos,
                    float eps2_rep, double* val_att, double* grad_att, double* val_rep,
                    double* grad_rep, void* ws, size_t ws_bytes, spk_stream_t stream) {
-    return launch_sums((const float4*)tgt, n_tgt, dims, (const float4*)grid_src, n_cells,
-                       eps2_att, 1, (const float4*)pos_src, n_pos, eps2_rep, 0, val_att,
-                       grad_att, val_rep, grad_rep, ws, ws_bytes, (cudaStream_t)stream);
+    return launch_sums((const float4*)tgt, n_tgt, dims, grid_w, side, eps2_att,
+                       (const float4*)pos_src, n_pos, eps2_rep, val_att, grad_att, val_rep,
+                       grad_rep, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int spk_pack_positions(const double* coords, int64_t p, int dims, void* pos4,
@@ -511,15 +651,15 @@ int spk_pack_positions(const double* coords, int64_t p, int dims, void* pos4,
     return SPK_OK;
 }
 
-int spk_build_grid_sources(const double* rho, int dims, const int64_t* side, void* out,
-                           spk_stream_t stream) {
+int spk_build_grid_sources(const double* rho, int dims, const int64_t* side, float* weights,
+                           void* nodes, spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
     const long long s0 = side[0], s1 = side[1], s2 = dims == 3 ? side[2] : 1;
     SPK_REQUIRE(s0 >= 3 && s1 >= 3 && s2 >= 1 && (s0 & 1) && (s1 & 1) && (s2 & 1),
                 SPK_ERR_ARG, "grid sides must be odd (2N+1) and >= 3");
-    const long long n = s0 * s1 * s2;
-    grid_sources_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        rho, s0, s1, s2, dims, (float4*)out);
+    const long long npad = (s0 * s1 * s2 + 3) & ~3LL;
+    grid_sources_kernel<<<(unsigned)((npad + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        rho, s0, s1, s2, dims, weights, (float4*)nodes);
     SPK_CHECK_LAUNCH("grid_sources");
     return SPK_OK;
 }

@@ -53,12 +53,14 @@ class CudaOps:
         if cfg.grad_mode == "exact":
             va = self.empty(n_t)
             ga = self.empty((n_t, d))
-            src = fld.device_sources()
-            n_cells = src.shape[0]
+            w = fld.device_sources()
+            sides = fld.sides
+            n_cells = int(np.prod(sides))
             nbytes = _native.query("spk_nbody_workspace_bytes", n_t, n_cells, src4.shape[0])
             ws = _device.workspace(nbytes, "nbody")
-            _native.call("spk_fused_sums", tgt4.data_ptr(), n_t, d, src.data_ptr(), n_cells,
-                         float(fld.kernel_eps ** 2), src4.data_ptr(), src4.shape[0],
+            _native.call("spk_fused_sums", tgt4.data_ptr(), n_t, d, w.data_ptr(),
+                         _native.i64_array(sides), float(fld.kernel_eps ** 2),
+                         src4.data_ptr(), src4.shape[0],
                          float(eps2_rep), va.data_ptr(), ga.data_ptr(), vr.data_ptr(),
                          gr.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
         else:

@@ -8,20 +8,23 @@
 
 int main() {
     const long long p = 1 << 20, g = 129LL * 129 * 129;
-    std::vector<float4> hp(p), hg(g);
+    std::vector<float4> hp(p);
+    std::vector<float> hg((g + 3) / 4 * 4, 0.f);
     srand(1);
     auto u = [] { return 2.f * rand() / (float)RAND_MAX - 1.f; };
-    for (auto& v : hp) v = make_float4(u(), u(), u(), 1.f);
-    for (long long c = 0; c < g; ++c) {
-        const long long i = c / (129 * 129), j = (c / 129) % 129, k = c % 129;
-        hg[c] = make_float4((i - 64) / 64.f, (j - 64) / 64.f, (k - 64) / 64.f, 1.f / g);
+    for (auto& v : hp) {
+        v = make_float4(u(), u(), u(), 0.f);
+        v.w = v.x * v.x + v.y * v.y + v.z * v.z;
     }
-    float4 *dp, *dg;
+    for (long long c = 0; c < g; ++c) hg[c] = 1.f / g;
+    const int64_t side[3] = {129, 129, 129};
+    float4* dp;
+    float* dg;
     double *va, *ga, *vr, *gr;
     cudaMalloc(&dp, p * 16);
-    cudaMalloc(&dg, g * 16);
+    cudaMalloc(&dg, hg.size() * 4);
     cudaMemcpy(dp, hp.data(), p * 16, cudaMemcpyHostToDevice);
-    cudaMemcpy(dg, hg.data(), g * 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(dg, hg.data(), hg.size() * 4, cudaMemcpyHostToDevice);
     cudaMalloc(&va, p * 8);
     cudaMalloc(&vr, p * 8);
     cudaMalloc(&ga, p * 24);
@@ -35,8 +38,8 @@ int main() {
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
         cudaEventRecord(s);
-        int rc = spk_fused_sums(dp, p, 3, dg, g, 1.f / (128.f * 128.f), dp, p, 1e-6f, va, ga, vr,
-                                gr, ws, wsb, nullptr);
+        int rc = spk_fused_sums(dp, p, 3, dg, side, 1.f / (128.f * 128.f), dp, p, 1e-6f, va, ga,
+                                vr, gr, ws, wsb, nullptr);
         cudaEventRecord(e);
         cudaEventSynchronize(e);
         if (rc) {

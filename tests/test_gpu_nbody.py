@@ -153,14 +153,15 @@ def test_fused_equals_separate(spk):
     fld = spk.precompute_field(rho)
     pts = rng.uniform(-1, 1, (7000, 3))
     p4 = _device.pack_positions(_device.h2d(pts))
-    src = fld.device_sources()
-    va, ga = grid_sums_device(p4, src, 3, fld.kernel_eps ** 2)
+    w = fld.device_sources()
+    va, ga = grid_sums_device(p4, fld, fld.kernel_eps ** 2)
     vr, gr = direct_sums_device(p4, p4, 3, 1e-6)
     bufs = [torch.empty_like(t) for t in (va, ga, vr, gr)]
-    nb = _native.query("spk_nbody_workspace_bytes", 7000, src.shape[0], 7000)
+    nb = _native.query("spk_nbody_workspace_bytes", 7000, 25 ** 3, 7000)
     ws = _device.workspace(nb, "nbody")
-    _native.call("spk_fused_sums", p4.data_ptr(), 7000, 3, src.data_ptr(), src.shape[0],
-                 float(fld.kernel_eps ** 2), p4.data_ptr(), 7000, 1e-6,
+    _native.call("spk_fused_sums", p4.data_ptr(), 7000, 3, w.data_ptr(),
+                 _native.i64_array(fld.sides), float(fld.kernel_eps ** 2), p4.data_ptr(), 7000,
+                 1e-6,
                  *[b.data_ptr() for b in bufs], ws.data_ptr(), ws.numel(), _device.stream())
     for x, y in zip(bufs, (va, ga, vr, gr)):
         assert rel_l2(_device.d2h(x), _device.d2h(y)) <= 1e-6
