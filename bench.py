@@ -188,6 +188,17 @@ def measured_fp32_peak():
         return None, None
 
 
+def sfu_pairs_per_s(mhz):
+    """Measured MUFU.RSQ throughput x 148 SMs (one rsqrt per pair)."""
+    per_clk = 15.87
+    try:
+        with open(os.path.join(REPO, "profiles", "fp32_peak.json")) as fh:
+            per_clk = float(json.load(fh)["mufu_rsq_per_clk_per_sm"])
+    except (OSError, ValueError, KeyError):
+        pass
+    return per_clk * 148 * mhz * 1e6
+
+
 def committed_traffic():
     path = os.path.join(REPO, "profiles", "nbody_traffic.json")
     try:
@@ -345,6 +356,11 @@ def run_ours(args):
                        f"(scripts/micro/fp32_peak.cu, profiles/fp32_peak.json); "
                        f"MEASURED_PEAKS.json has no FP32 entry")
     clocks = clk.summary()
+    # hardware-bound time of the launch: repulsion pairs at the FP32 roofline (f_rep flops
+    # per pair), attraction pairs at the measured SFU rate (the lattice kernel spends 6
+    # FP32 lane-ops + 1 MUFU per pair, so the SFU binds, profiles/fp32_peak.json)
+    sfu_rate = sfu_pairs_per_s(peak_mhz)
+    bound_ms = (local_t * p / (peak * 1e12 / f_rep) + local_t * g / sfu_rate) * 1e3
 
     # end-to-end through the public drop-in API with host buffers
     if args.no_e2e:
@@ -372,9 +388,14 @@ def run_ours(args):
                          "flops_per_pair": {"repulsion": f_rep, "attraction": f_att},
                          "launch_ms": nb_mean,
                          "peak_source": peak_source,
-                         "pipe_bound_note": "the kernel issues 10 (rep) / 11 (att) FP32 "
-                                            "lane-ops per pair, so its FMA-pipe ceiling is "
-                                            "17/20 of this peak (see DESIGN.md)"},
+                         "hw_bound_ms": bound_ms,
+                         "frac_of_hw_bound": bound_ms / nb_mean,
+                         "hw_bound_note": "repulsion pairs at the FP32 peak / 17 flops, "
+                                          "attraction pairs at the measured MUFU.RSQ rate "
+                                          f"({sfu_rate:.3g}/s): the lattice kernel does fewer "
+                                          "than the algorithmic 19 flops per pair, so "
+                                          "'frac' (algorithmic flops / FP32 peak) can "
+                                          "approach 1 while frac_of_hw_bound stays honest"},
             "clocks": clocks,
             "gpu_launches": launches,
         }

@@ -17,6 +17,7 @@
 //    exactly the reference's per-element operation sequence; a checkpoint + replay
 //    reproduces the reference's stopping sweep.
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "spk_common.cuh"
@@ -569,46 +570,57 @@ __device__ double systolic_batch(const double* __restrict__ s_in, double* __rest
 // State of one ring lane between steps.
 template <int D>
 struct RingLane {
-    Sample<D> slot[4];  // register window, roles rotate with the global step (mod 4)
+    Sample<D> slot[5];  // register window, roles rotate with the global step (mod 5)
     double worst;
     int t, j, k;        // local step in the current round, round, sweep index
 };
 
-// One global step of the ring.  R = st mod 4 fixes which window slot plays w0..w3
-// (w0 = slot[R], ..., w3 = slot[R+3]); the received sample overwrites slot[R] (the old
-// w0, handed on this step), so the window never moves between registers.
+// Ring lanes lag by 5 steps (+1 per warp boundary) because each step runs the speed pair
+// S(t) and the accel triple A(t-3) concurrently (they touch disjoint samples), which
+// halves the fp64 dependency chain per step compared with S(t) -> A(t-2).
+__device__ __forceinline__ int ring_offset(int g) { return 5 * g + (g >> 5); }
+
+// One global step of the ring.  R = st mod 5 fixes which window slot plays w0..w4
+// (w0 = s[t-3] = slot[R], ..., w4 = s[t+1] = slot[R+4]); the received sample s[t+2]
+// overwrites slot[R] (the old w0, handed on this step), so the window never moves
+// between registers.  Per sample the operation order is the reference's:
+// B(m) @ m-2, S(m-1) @ m-1, S(m) @ m, A(m-2) @ m+1, A(m-1) @ m+2, A(m) @ m+3.
 template <int D, int R>
-__device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B, int W, int P,
-                                          int g, int lane, int warp, int max_sweeps, int kl,
+__device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B, int P, int g,
+                                          int lane, int warp, int max_sweeps, int kl,
                                           double a, double b, int pin, double pv0,
                                           double pv1, double pv2, double tol,
                                           const double* __restrict__ s0, double* snap0,
                                           double* snap1, double* res, double* xfer,
-                                          int* stop_sh) {
-    Sample<D>& w0 = L.slot[R & 3];
-    Sample<D>& w1 = L.slot[(R + 1) & 3];
-    Sample<D>& w2 = L.slot[(R + 2) & 3];
-    Sample<D>& w3 = L.slot[(R + 3) & 3];
+                                          double* wrap, int* stop_sh) {
+    Sample<D>& w0 = L.slot[R % 5];
+    Sample<D>& w1 = L.slot[(R + 1) % 5];
+    Sample<D>& w2 = L.slot[(R + 2) % 5];
+    Sample<D>& w3 = L.slot[(R + 3) % 5];
+    Sample<D>& w4 = L.slot[(R + 4) % 5];
     const int t = L.t;
-    const bool on = t >= -2 && t <= ns + 1 && L.k < max_sweeps;
+    const bool on = t >= -2 && t <= ns + 2 && L.k < max_sweeps;
     if (on) {
         if (t == -2) L.worst = 0.0;
-        if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, L.worst);
-        if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, L.worst);
-        if (t >= 2) {
+        if (t >= 0 && t <= ns - 2) speed_pair<D>(w3, w4, t, a, pin, L.worst);
+        if (t >= 3 && t <= ns) accel_triple<D>(w0, w1, w2, t - 3, b, pin, L.worst);
+        if (t >= 3) {
             if (g == B - 1) {
                 double* sn = (L.j & 1) ? snap1 : snap0;
 #pragma unroll
-                for (int l = 0; l < D; ++l) sn[(t - 2) * D + l] = w0.v[l];
+                for (int l = 0; l < D; ++l) {
+                    sn[(t - 3) * D + l] = w0.v[l];
+                    wrap[(t - 3) * D + l] = w0.v[l];
+                }
             }
             if (L.k == kl) {
 #pragma unroll
-                for (int l = 0; l < D; ++l) res[(t - 2) * D + l] = w0.v[l];
+                for (int l = 0; l < D; ++l) res[(t - 3) * D + l] = w0.v[l];
             }
         }
-        if (t == ns + 1 && L.worst <= tol) atomicMin(stop_sh, L.k);
+        if (t == ns + 2 && L.worst <= tol) atomicMin(stop_sh, L.k);
     }
-    // hand the finished sample w0 (= s[t-2]) to the next sweep; it is replaced in slot R
+    // hand the finished sample w0 (= s[t-3]) to the next sweep; it is replaced in slot R
     Sample<D> recv;
 #pragma unroll
     for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, w0.v[l], 1);
@@ -620,12 +632,14 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
     if (on) {
         const int m = t + 2;
         if (m <= ns - 1) {
-            if (g == 0 && L.j == 0) {
+            if (g == 0) {
+                // first sweep of a round: the initial state (round 0) or the previous
+                // round's last sweep, handed over through the shared-memory wrap buffer
+                const double* src = L.j == 0 ? s0 : wrap;
 #pragma unroll
-                for (int l = 0; l < D; ++l) recv.v[l] = s0[m * D + l];
+                for (int l = 0; l < D; ++l) recv.v[l] = src[m * D + l];
             } else if (lane == 0) {
-                const int pw = warp == 0 ? W - 1 : warp - 1;
-                const double* x = xfer + ((pw * 2 + ((st - 1) & 1)) * D);
+                const double* x = xfer + (((warp - 1) * 2 + ((st - 1) & 1)) * D);
 #pragma unroll
                 for (int l = 0; l < D; ++l) recv.v[l] = x[l];
             }
@@ -637,7 +651,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
             box_sample<D>(recv, L.worst);
         }
     }
-    w0 = recv;  // slot R now holds s[t+2] (the new w3 at the next step)
+    w0 = recv;  // slot R now holds s[t+2] (w4 at the next step)
     if (++L.t == P - 2) {
         L.t = -2;
         ++L.j;
@@ -646,22 +660,30 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
     __syncthreads();
 }
 
-template <int D>
-__global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, double a,
+// Continuous ring: lane g runs sweeps g, g+B, g+2B, ...; sweep k starts at global step
+// (k / B) * P + ring_offset(k % B) with P = max(5 B + W, ns + 5).  The last lane writes
+// every round's output stream into a ping-pong snapshot (and the wrap buffer that feeds
+// lane 0 of the next round); when sweep k* is the first whose worst violation is
+// <= tol, the ring stops and sweeps j B .. k* are replayed (systolic_batch) from the
+// snapshot after sweep j B - 1 (j = k* / B), which the ring has not overwritten yet
+// because P >= ns + 5.  Bit-identical to the sequential polish.
+template <int D, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int ns, double a,
                                                       double b, int pin, double pv0,
                                                       double pv1, double pv2, double tol,
                                                       int max_sweeps, double* ws,
                                                       int32_t* sweeps_out, float4* pos4) {
-    extern __shared__ __align__(16) double xfer[];  // [W][2][D]
+    extern __shared__ __align__(16) double xfer[];  // [W][2][D], then wrap [ns][D]
     __shared__ int stop_sh;
     const long long c = blockIdx.x;
     const int B = blockDim.x;
     const int W = B >> 5;
-    const int P = 4 * B + W;
+    const int P = max(5 * B + W, ns + 5);
+    double* wrap = xfer + W * 2 * D;
     const int g = threadIdx.x;
     const int lane = g & 31;
     const int warp = g >> 5;
-    const int off = lane_offset(g);
+    const int off = ring_offset(g);
     const int nd = ns * D;
     const double pv[3] = {pv0, pv1, pv2};
     double* s0 = shots + c * (size_t)nd;
@@ -671,10 +693,10 @@ __global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, dou
     if (g == 0) stop_sh = 0x7fffffff;
     __syncthreads();
     const int kl = max_sweeps - 1;
-    const int last_step = (kl / B) * P + lane_offset(kl % B) + ns + 3;
+    const int last_step = (kl / B) * P + ring_offset(kl % B) + ns + 4;
     RingLane<D> L;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 5; ++q)
 #pragma unroll
         for (int l = 0; l < D; ++l) L.slot[q].v[l] = 0.0;
     L.worst = 0.0;
@@ -683,15 +705,16 @@ __global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, dou
     L.k = g;
 #define SPK_RING_STEP(R)                                                                   \
     {                                                                                      \
-        ring_step<D, R>(L, st + R, ns, B, W, P, g, lane, warp, max_sweeps, kl, a, b, pin,  \
-                        pv0, pv1, pv2, tol, s0, snap0, snap1, res, xfer, &stop_sh);       \
+        ring_step<D, R>(L, st + R, ns, B, P, g, lane, warp, max_sweeps, kl, a, b, pin,     \
+                        pv0, pv1, pv2, tol, s0, snap0, snap1, res, xfer, wrap, &stop_sh); \
         if (stop_sh != 0x7fffffff || st + R >= last_step) break;                           \
     }
-    for (int st = 0;; st += 4) {
+    for (int st = 0;; st += 5) {
         SPK_RING_STEP(0)
         SPK_RING_STEP(1)
         SPK_RING_STEP(2)
         SPK_RING_STEP(3)
+        SPK_RING_STEP(4)
     }
 #undef SPK_RING_STEP
     const int kstar = stop_sh;
@@ -714,10 +737,12 @@ __global__ void __launch_bounds__(1024) polish_kernel(double* shots, int ns, dou
     if (g == 0 && sweeps_out) sweeps_out[c] = total;
 }
 
+// Ring width: W warps; SPK_POLISH_WARPS overrides (fewer warps -> more shots resident
+// per SM, longer per-sweep latency).
 inline int polish_warps(int ns) {
-    // P = 129 W >= ns + 4
-    int w = (ns + 4 + 128) / 129;
-    return w < 1 ? 1 : w;
+    int w = (ns + 5 + 160) / 161;  // 5 B + W >= ns + 5: no idle lane in the ring
+    if (const char* e = getenv("SPK_POLISH_WARPS")) w = atoi(e);
+    return w < 1 ? 1 : (w > 32 ? 32 : w);
 }
 
 // ------------------------------------------------------------------ residuals
@@ -1004,17 +1029,39 @@ int spk_project_all(const double* in, const double* grad, double eta, double* ou
     // polish: systolic ring, one CTA of 32*pw lanes per shot; snapshots + result in the
     // (now free) FISTA workspace, warp hand-over slots in shared memory
     const int pw = polish_warps(n_s);
-    SPK_REQUIRE(pw <= 32, SPK_ERR_ARG, "N_s=%d too large for the polish ring (max 4124)", n_s);
-    const size_t psm = (size_t)pw * 2 * dims * sizeof(double);
+    const size_t psm = ((size_t)pw * 2 * dims + (size_t)n_s * dims) * sizeof(double);
+    SPK_REQUIRE(psm <= 220 * 1024, SPK_ERR_ARG, "N_s=%d too large for the polish ring", n_s);
+    cudaFuncSetAttribute(polish_kernel<3, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)psm);
+    cudaFuncSetAttribute(polish_kernel<2, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)psm);
+    cudaFuncSetAttribute(polish_kernel<3, 1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)psm);
+    cudaFuncSetAttribute(polish_kernel<2, 1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)psm);
     double* pws = static_cast<double*>(ws);
-    if (dims == 3)
-        polish_kernel<3><<<(unsigned)n_shots, 32 * pw, psm, stream>>>(
-            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-            (float4*)pos4);
-    else
-        polish_kernel<2><<<(unsigned)n_shots, 32 * pw, psm, stream>>>(
-            out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-            (float4*)pos4);
+    // <= 8 warps (N_s <= 1283): a register budget of 80 keeps the ring window in registers
+    // with 3 CTAs per SM; wider rings use the 1024-thread instantiation
+    const dim3 grid((unsigned)n_shots), block(32 * pw);
+    if (pw <= 8) {
+        if (dims == 3)
+            polish_kernel<3, 256, 3><<<grid, block, psm, stream>>>(
+                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
+                (float4*)pos4);
+        else
+            polish_kernel<2, 256, 3><<<grid, block, psm, stream>>>(
+                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
+                (float4*)pos4);
+    } else {
+        if (dims == 3)
+            polish_kernel<3, 1024, 1><<<grid, block, psm, stream>>>(
+                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
+                (float4*)pos4);
+        else
+            polish_kernel<2, 1024, 1><<<grid, block, psm, stream>>>(
+                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
+                (float4*)pos4);
+    }
     SPK_CHECK_LAUNCH("polish_kernel");
     return SPK_OK;
 }
