@@ -570,21 +570,22 @@ __device__ double systolic_batch(const double* __restrict__ s_in, double* __rest
 // State of one ring lane between steps.
 template <int D>
 struct RingLane {
-    Sample<D> slot[5];  // register window, roles rotate with the global step (mod 5)
+    Sample<D> slot[4];  // register window, roles rotate with the global step (mod 4)
     double worst;
     int t, j, k;        // local step in the current round, round, sweep index
 };
 
-// Ring lanes lag by 5 steps (+1 per warp boundary) because each step runs the speed pair
-// S(t) and the accel triple A(t-3) concurrently (they touch disjoint samples), which
-// halves the fp64 dependency chain per step compared with S(t) -> A(t-2).
-__device__ __forceinline__ int ring_offset(int g) { return 5 * g + (g >> 5); }
+// Ring lanes lag by 4 steps (+1 per warp boundary), the minimum for which the windows of
+// consecutive sweeps never overlap out of order.  (A variant running S(t) and A(t-3)
+// concurrently at lag 5 was measured slower: the per-step latency is dominated by
+// control flow, not by the S -> A fp64 chain.)
+__device__ __forceinline__ int ring_offset(int g) { return PL_LAG * g + (g >> 5); }
 
-// One global step of the ring.  R = st mod 5 fixes which window slot plays w0..w4
-// (w0 = s[t-3] = slot[R], ..., w4 = s[t+1] = slot[R+4]); the received sample s[t+2]
+// One global step of the ring.  R = st mod 4 fixes which window slot plays w0..w3
+// (w0 = s[t-2] = slot[R], ..., w3 = s[t+1] = slot[R+3]); the received sample s[t+2]
 // overwrites slot[R] (the old w0, handed on this step), so the window never moves
 // between registers.  Per sample the operation order is the reference's:
-// B(m) @ m-2, S(m-1) @ m-1, S(m) @ m, A(m-2) @ m+1, A(m-1) @ m+2, A(m) @ m+3.
+// B(m) @ m-2, S(m-1) @ m-1, S(m) @ m, A(m-2) @ m, A(m-1) @ m+1, A(m) @ m+2.
 template <int D, int R>
 __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B, int P, int g,
                                           int lane, int warp, int max_sweeps, int kl,
@@ -593,34 +594,33 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
                                           const double* __restrict__ s0, double* snap0,
                                           double* snap1, double* res, double* xfer,
                                           double* wrap, int* stop_sh) {
-    Sample<D>& w0 = L.slot[R % 5];
-    Sample<D>& w1 = L.slot[(R + 1) % 5];
-    Sample<D>& w2 = L.slot[(R + 2) % 5];
-    Sample<D>& w3 = L.slot[(R + 3) % 5];
-    Sample<D>& w4 = L.slot[(R + 4) % 5];
+    Sample<D>& w0 = L.slot[R & 3];
+    Sample<D>& w1 = L.slot[(R + 1) & 3];
+    Sample<D>& w2 = L.slot[(R + 2) & 3];
+    Sample<D>& w3 = L.slot[(R + 3) & 3];
     const int t = L.t;
-    const bool on = t >= -2 && t <= ns + 2 && L.k < max_sweeps;
+    const bool on = t >= -2 && t <= ns + 1 && L.k < max_sweeps;
     if (on) {
         if (t == -2) L.worst = 0.0;
-        if (t >= 0 && t <= ns - 2) speed_pair<D>(w3, w4, t, a, pin, L.worst);
-        if (t >= 3 && t <= ns) accel_triple<D>(w0, w1, w2, t - 3, b, pin, L.worst);
-        if (t >= 3) {
+        if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, L.worst);
+        if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, L.worst);
+        if (t >= 2) {
             if (g == B - 1) {
                 double* sn = (L.j & 1) ? snap1 : snap0;
 #pragma unroll
                 for (int l = 0; l < D; ++l) {
-                    sn[(t - 3) * D + l] = w0.v[l];
-                    wrap[(t - 3) * D + l] = w0.v[l];
+                    sn[(t - 2) * D + l] = w0.v[l];
+                    wrap[(t - 2) * D + l] = w0.v[l];
                 }
             }
             if (L.k == kl) {
 #pragma unroll
-                for (int l = 0; l < D; ++l) res[(t - 3) * D + l] = w0.v[l];
+                for (int l = 0; l < D; ++l) res[(t - 2) * D + l] = w0.v[l];
             }
         }
-        if (t == ns + 2 && L.worst <= tol) atomicMin(stop_sh, L.k);
+        if (t == ns + 1 && L.worst <= tol) atomicMin(stop_sh, L.k);
     }
-    // hand the finished sample w0 (= s[t-3]) to the next sweep; it is replaced in slot R
+    // hand the finished sample w0 (= s[t-2]) to the next sweep; it is replaced in slot R
     Sample<D> recv;
 #pragma unroll
     for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, w0.v[l], 1);
@@ -651,7 +651,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
             box_sample<D>(recv, L.worst);
         }
     }
-    w0 = recv;  // slot R now holds s[t+2] (w4 at the next step)
+    w0 = recv;  // slot R now holds s[t+2] (w3 at the next step)
     if (++L.t == P - 2) {
         L.t = -2;
         ++L.j;
@@ -661,12 +661,12 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
 }
 
 // Continuous ring: lane g runs sweeps g, g+B, g+2B, ...; sweep k starts at global step
-// (k / B) * P + ring_offset(k % B) with P = max(5 B + W, ns + 5).  The last lane writes
+// (k / B) * P + ring_offset(k % B) with P = max(4 B + W, ns + 4).  The last lane writes
 // every round's output stream into a ping-pong snapshot (and the wrap buffer that feeds
 // lane 0 of the next round); when sweep k* is the first whose worst violation is
 // <= tol, the ring stops and sweeps j B .. k* are replayed (systolic_batch) from the
 // snapshot after sweep j B - 1 (j = k* / B), which the ring has not overwritten yet
-// because P >= ns + 5.  Bit-identical to the sequential polish.
+// because P >= ns + 4.  Bit-identical to the sequential polish.
 template <int D, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int ns, double a,
                                                       double b, int pin, double pv0,
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     const long long c = blockIdx.x;
     const int B = blockDim.x;
     const int W = B >> 5;
-    const int P = max(5 * B + W, ns + 5);
+    const int P = max(4 * B + W, ns + 4);
     double* wrap = xfer + W * 2 * D;
     const int g = threadIdx.x;
     const int lane = g & 31;
@@ -693,10 +693,10 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     if (g == 0) stop_sh = 0x7fffffff;
     __syncthreads();
     const int kl = max_sweeps - 1;
-    const int last_step = (kl / B) * P + ring_offset(kl % B) + ns + 4;
+    const int last_step = (kl / B) * P + ring_offset(kl % B) + ns + 3;
     RingLane<D> L;
 #pragma unroll
-    for (int q = 0; q < 5; ++q)
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
         for (int l = 0; l < D; ++l) L.slot[q].v[l] = 0.0;
     L.worst = 0.0;
@@ -709,12 +709,11 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
                         pv0, pv1, pv2, tol, s0, snap0, snap1, res, xfer, wrap, &stop_sh); \
         if (stop_sh != 0x7fffffff || st + R >= last_step) break;                           \
     }
-    for (int st = 0;; st += 5) {
+    for (int st = 0;; st += 4) {
         SPK_RING_STEP(0)
         SPK_RING_STEP(1)
         SPK_RING_STEP(2)
         SPK_RING_STEP(3)
-        SPK_RING_STEP(4)
     }
 #undef SPK_RING_STEP
     const int kstar = stop_sh;
@@ -740,7 +739,7 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
 // Ring width: W warps; SPK_POLISH_WARPS overrides (fewer warps -> more shots resident
 // per SM, longer per-sweep latency).
 inline int polish_warps(int ns) {
-    int w = (ns + 5 + 160) / 161;  // 5 B + W >= ns + 5: no idle lane in the ring
+    int w = (ns + 4 + 128) / 129;  // 4 B + W >= ns + 4: no idle lane in the ring
     if (const char* e = getenv("SPK_POLISH_WARPS")) w = atoi(e);
     return w < 1 ? 1 : (w > 32 ? 32 : w);
 }
