@@ -180,3 +180,48 @@ def test_exact_attraction_anisotropic_grid(spk):
     assert rel_l2(res.grad, gref) <= GRAD_TOL
     with pytest.raises(ValueError, match="cubic"):
         spk.eval_attraction(spk.SamplingPattern(pts[None]), fld, "consistent")
+
+
+def _subset_sums(spk, pts, rows, fld):
+    """GPU K1 (rows vs all positions) and K2 (rows vs the lattice) for a row subset."""
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.attraction import grid_sums_device
+    from paper_2108_02991_b200.repulsion import direct_sums_device
+
+    t4 = _device.pack_positions(_device.h2d(pts[rows]))
+    s4 = _device.pack_positions(_device.h2d(pts))
+    vr, gr = direct_sums_device(t4, s4, pts.shape[1], 1e-6)
+    va, ga = grid_sums_device(t4, fld, fld.kernel_eps ** 2)
+    return [_device.d2h(x) for x in (vr, gr, va, ga)]
+
+
+def test_c2_scale_attraction_row_subset(spk):
+    """C2 (p = 2^20, 129^3 lattice): K2 on a 1024-row strided subset vs the fp64 oracle."""
+    from paper_2108_02991_b200 import optimizer as om
+
+    pts = om.perturb(om.init_radial(1024, 1024, 3), 0.25, 0).points().copy()
+    rho = spk.discretize(spk.DensityParams(0.25, 2.0), 64, 3)
+    fld = spk.precompute_field(rho)
+    rows = np.arange(0, pts.shape[0], pts.shape[0] // 1024, dtype=np.int64)
+    _, _, va, ga = _subset_sums(spk, pts, rows, fld)
+    vref, gref = orc.grid_sums(pts[rows], rho.grid, fld.kernel_eps ** 2)
+    assert rel_l2(va, vref) <= VAL_TOL
+    assert rel_l2(ga, gref) <= GRAD_TOL
+
+
+def test_c4_scale_row_subset(spk):
+    """C4 (4096 x 2048 = 8.4M samples, 385 x 385 x 209 lattice): K1 and K2 on a 512-row
+    strided subset of targets against all sources, vs the fp64 oracle."""
+    from paper_2108_02991_b200 import optimizer as om
+
+    pts = om.perturb(om.init_radial(4096, 2048, 3), 0.75, 0).points().copy()
+    rho = spk.discretize_anisotropic(spk.DensityParams(0.25, 2.0), (192, 192, 104), 3)
+    fld = spk.precompute_field(rho)
+    rows = np.arange(0, pts.shape[0], pts.shape[0] // 512, dtype=np.int64)
+    vr, gr, va, ga = _subset_sums(spk, pts, rows, fld)
+    vref, gref = orc.direct_sums_subset(pts, rows, 1e-6)
+    assert rel_l2(vr, vref) <= VAL_TOL
+    assert rel_l2(gr, gref) <= GRAD_TOL
+    aref, agref = orc.grid_sums(pts[rows], rho.grid, fld.kernel_eps ** 2)
+    assert rel_l2(va, aref) <= VAL_TOL
+    assert rel_l2(ga, agref) <= GRAD_TOL

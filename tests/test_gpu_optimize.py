@@ -136,3 +136,23 @@ def test_fixed_phase_monotone(spk):
                               repulsion=spk.RepulsionConfig(backend="direct"))
     res = spk.optimize(cfg, desk_hw(spk))
     assert np.max(np.diff(res.trace.costs())) <= 1e-8
+
+
+def test_multiresolution_3d_exact_full3d_limits(spk):
+    """C5-shaped schedule at reduced size: 3D, full3d hardware limits, 4 levels
+    (N_s = 32 -> 256), exact attraction; every level starts from the upsampled pattern
+    and the final pattern is feasible at the unscaled limits."""
+    hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                          dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
+                          dims=3)
+    cfg = spk.OptimizerConfig(n_c=64, n_s=256, dims=3, n_decim=3, n_git=3, n_pit=100,
+                              perturbation=0.75, seed=0, grad_mode="exact", grid_n=12)
+    res = spk.optimize(cfg, hw)
+    recs = res.trace.records
+    assert [r.samples_per_shot for r in recs] == [32] * 3 + [64] * 3 + [128] * 3 + [256] * 3
+    assert np.all(np.isfinite(res.trace.costs()))
+    lim = spk.normalized_limits(hw)
+    pin = spk.LinearConstraint(128, np.zeros(3))
+    pc = spk.ProjectionConfig(alpha=lim.alpha, beta=lim.beta, raster_dt=hw.raster_dt, pin=pin)
+    assert spk.feasibility_residuals(res.pattern, pc)["max"] <= pc.feas_tol
+    assert res.pattern.coords.shape == (64, 256, 3)
