@@ -74,6 +74,18 @@ int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const float* grid_w
                    float eps2_rep, double* val_att, double* grad_att, double* val_rep,
                    double* grad_rep, void* ws, size_t ws_bytes, spk_stream_t stream);
 
+/* Stack-of-SPARKLING batch (BASELINE config 3): n_groups independent problems of per_group
+ * targets each, targets contiguous by problem; problem q's repulsion sources are its own
+ * n_pos positions at pos_src + q * n_pos records; the density lattice is shared.  Same
+ * sums as spk_fused_sums per problem, one launch for the whole batch. */
+size_t spk_nbody_batched_workspace_bytes(int64_t n_groups, int64_t per_group, int64_t n_cells,
+                                         int64_t n_pos);
+int spk_fused_sums_batched(const void* tgt, int64_t n_groups, int64_t per_group, int dims,
+                           const float* grid_w, const int64_t* side, float eps2_att,
+                           const void* pos_src, int64_t n_pos, float eps2_rep,
+                           double* val_att, double* grad_att, double* val_rep,
+                           double* grad_rep, void* ws, size_t ws_bytes, spk_stream_t stream);
+
 /* Pack fp64 (p, dims) coordinates into position records float4 {x, y, z|0, |x|^2}. */
 int spk_pack_positions(const double* coords, int64_t p, int dims, void* pos4,
                        spk_stream_t stream);
@@ -99,6 +111,15 @@ int spk_combine_gradient(int64_t n_tgt, int dims, const double* val_att,
                          const double* prev_coords, const double* prev_grad, double* grad,
                          double* out, void* ws, size_t ws_bytes, spk_stream_t stream);
 
+/* Per-problem form of spk_combine_gradient for a batch: out[q * 6 + 0..5]. */
+size_t spk_combine_batched_workspace_bytes(int64_t n_groups, int64_t per_group);
+int spk_combine_gradient_batched(int64_t n_groups, int64_t per_group, int dims,
+                                 const double* val_att, const double* grad_att, double p_att,
+                                 const double* val_rep, const double* grad_rep, double p_rep,
+                                 const double* coords, const double* prev_coords,
+                                 const double* prev_grad, double* grad, double* out, void* ws,
+                                 size_t ws_bytes, spk_stream_t stream);
+
 /* ---------------------------------------------------------------- K3 projection */
 
 size_t spk_project_workspace_bytes(int64_t n_shots, int n_s, int dims, int with_trace);
@@ -108,15 +129,16 @@ size_t spk_project_workspace_bytes(int64_t n_shots, int n_s, int dims, int with_
  * the relaxed cyclic feasibility polish (_feasibility_polish, :287-373) to tol with at
  * most max_sweeps sweeps.  fp64, bit-identical to the reference.
  *   in:  shots (n_shots, n_s, dims) f64; if grad != NULL the projected point is
- *        in - eta * grad (the optimizer step, optimizer.py:326).
+ *        in - eta * grad (the optimizer step, optimizer.py:326); eta_per_shot (device,
+ *        nullable, n_shots f64) replaces eta per shot (batched independent problems).
  *   out: projected shots; pos4 (nullable) receives float4 positions of the result;
  *        sweeps (nullable) the polish sweep count per shot; trace (nullable,
  *        n_shots * n_pit f64) the dual objective per iteration (project_shot
  *        return_trace=True, :394-418); nonfinite (nullable, 1 int32) is set to 1 when
  *        the stepped input is not finite (SamplingPattern check, core.py:157).
  *   pin_idx < 0 means no pin; pin_val: host array of dims doubles. */
-int spk_project_all(const double* in, const double* grad, double eta, double* out,
-                    int64_t n_shots, int n_s, int dims, double a, double b, int pin_idx,
+int spk_project_all(const double* in, const double* grad, double eta,
+                    const double* eta_per_shot, double* out, int64_t n_shots, int n_s, int dims, double a, double b, int pin_idx,
                     const double* pin_val, int n_pit, double tau, int monotone, double tol,
                     int max_sweeps, void* pos4, int32_t* sweeps, double* trace,
                     int32_t* nonfinite, void* ws, size_t ws_bytes, spk_stream_t stream);
@@ -127,6 +149,12 @@ size_t spk_residuals_workspace_bytes(int64_t n_shots);
 int spk_feasibility_residuals(const double* coords, int64_t n_shots, int n_s, int dims,
                               double a, double b, int pin_idx, const double* pin_val,
                               double* out, void* ws, size_t ws_bytes, spk_stream_t stream);
+
+/* Per-problem residuals for a batch of n_groups x shots_per_group shots: out[q * 5 + ..]. */
+int spk_feasibility_residuals_batched(const double* coords, int64_t n_groups,
+                                      int64_t shots_per_group, int n_s, int dims, double a,
+                                      double b, int pin_idx, const double* pin_val, double* out,
+                                      void* ws, size_t ws_bytes, spk_stream_t stream);
 
 /* upsample_shots (optimizer.py:183-199): (n_shots, n_s, d) -> (n_shots, 2 n_s, d). */
 int spk_upsample_shots(const double* in, double* out, int64_t n_shots, int n_s, int dims,

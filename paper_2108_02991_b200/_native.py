@@ -34,13 +34,24 @@ SIGNATURES = {
                               c_vp, c_vp, c_size, c_vp]),
     "spk_fused_sums": (c_int, [c_vp, c_i64, c_int, c_vp, ctypes.POINTER(c_i64), c_flt, c_vp,
                                c_i64, c_flt, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "spk_nbody_batched_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),
+    "spk_fused_sums_batched": (c_int, [c_vp, c_i64, c_i64, c_int, c_vp, ctypes.POINTER(c_i64),
+                                       c_flt, c_vp, c_i64, c_flt, c_vp, c_vp, c_vp, c_vp,
+                                       c_vp, c_size, c_vp]),
+    "spk_combine_batched_workspace_bytes": (c_size, [c_i64, c_i64]),
+    "spk_combine_gradient_batched": (c_int, [c_i64, c_i64, c_int, c_vp, c_vp, c_dbl, c_vp,
+                                             c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                             c_size, c_vp]),
+    "spk_feasibility_residuals_batched": (c_int, [c_vp, c_i64, c_i64, c_int, c_int, c_dbl,
+                                                  c_dbl, c_int, ctypes.POINTER(c_dbl), c_vp,
+                                                  c_vp, c_size, c_vp]),
     "spk_pack_positions": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp]),
     "spk_build_grid_sources": (c_int, [c_vp, c_int, ctypes.POINTER(c_i64), c_vp, c_vp, c_vp]),
     "spk_combine_workspace_bytes": (c_size, [c_i64]),
     "spk_combine_gradient": (c_int, [c_i64, c_int, c_vp, c_vp, c_dbl, c_vp, c_vp, c_dbl,
                                      c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "spk_project_workspace_bytes": (c_size, [c_i64, c_int, c_int, c_int]),
-    "spk_project_all": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_i64, c_int, c_int, c_dbl, c_dbl,
+    "spk_project_all": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_vp, c_i64, c_int, c_int, c_dbl, c_dbl,
                                 c_int, ctypes.POINTER(c_dbl), c_int, c_dbl, c_int, c_dbl,
                                 c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "spk_residuals_workspace_bytes": (c_size, [c_i64]),
@@ -57,6 +68,8 @@ LAUNCHES = {
     "spk_direct_sums": 2, "spk_grid_sums": 2, "spk_fused_sums": 3, "spk_pack_positions": 1,
     "spk_build_grid_sources": 1, "spk_combine_gradient": 2, "spk_project_all": 2,
     "spk_feasibility_residuals": 2, "spk_upsample_shots": 1, "spk_field_eval": 1,
+    "spk_fused_sums_batched": 3, "spk_combine_gradient_batched": 2,
+    "spk_feasibility_residuals_batched": 2,
 }
 _launched = [0]
 

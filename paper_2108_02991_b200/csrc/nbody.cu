@@ -78,6 +78,12 @@ struct NBParams {
     long long n_tb;
     SegDesc seg[2];
     double* part;  // [chunk][4][n_tgt]: value, gx, gy, gz
+    // Independent problems batched in one launch (stack-of-SPARKLING, C3): targets are
+    // n_groups contiguous groups of per_group; group q's position sources start at
+    // record q * src_stride.  A single problem has n_groups = 1, src_stride = 0.
+    long long per_group;
+    long long tb_per_group;
+    long long src_stride;
 };
 
 constexpr int NB_TILE_W = NB_TILE;  // lattice cells per stage (fp32 partials span <= 512 cells)
@@ -290,12 +296,17 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(con
     const long long t_begin = lc * S.tiles / S.n_chunks;
     const long long t_end = (lc + 1) * S.tiles / S.n_chunks;
 
+    const long long grp = tb / P.tb_per_group;
+    const long long gfirst = grp * P.per_group;  // first target of this problem
+    const long long base = (tb - grp * P.tb_per_group) * NB_TB + tid;  // local index
+    SegDesc Sg = S;
+    if (S.kind == 0)
+        Sg.src = static_cast<const float4*>(S.src) + grp * P.src_stride;
     float2 X[NB_PAIRS], Y[NB_PAIRS], Z[NB_PAIRS];
-    const long long base = tb * NB_TB + tid;
 #pragma unroll
     for (int k = 0; k < NB_PAIRS; ++k) {
-        const long long i0 = min(base + (2 * k) * NB_THREADS, P.n_tgt - 1);
-        const long long i1 = min(base + (2 * k + 1) * NB_THREADS, P.n_tgt - 1);
+        const long long i0 = gfirst + min(base + (2 * k) * NB_THREADS, P.per_group - 1);
+        const long long i1 = gfirst + min(base + (2 * k + 1) * NB_THREADS, P.per_group - 1);
         const float4 a = P.tgt[i0];
         const float4 b = P.tgt[i1];
         X[k] = make_float2(a.x, b.x);
@@ -323,18 +334,19 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(con
 
     const bool guard = !(S.eps2 >= FLT_MIN);
     if (S.kind == 1) {
-        if (guard) run_chunk<D, 1, true>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
-        else run_chunk<D, 1, false>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        if (guard) run_chunk<D, 1, true>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        else run_chunk<D, 1, false>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
     } else {
-        if (guard) run_chunk<D, 0, true>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
-        else run_chunk<D, 0, false>(S, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        if (guard) run_chunk<D, 0, true>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        else run_chunk<D, 0, false>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
     }
 
     double* slot = P.part + (size_t)chunk * 4 * P.n_tgt;
 #pragma unroll
     for (int k = 0; k < NB_TPT; ++k) {
-        const long long i = base + k * NB_THREADS;
-        if (i < P.n_tgt) {
+        const long long li = base + k * NB_THREADS;
+        const long long i = gfirst + li;
+        if (li < P.per_group) {
             slot[i] = NB_ACC(k, 0);
             slot[P.n_tgt + i] = NB_ACC(k, 1);
             slot[2 * P.n_tgt + i] = NB_ACC(k, 2);
@@ -397,10 +409,11 @@ constexpr double NB_COST_LAT_TILE = NB_TILE_W / 16.0;
 
 // Choose the chunk counts: minimise (waves x longest unit) + per-unit overhead, with the
 // two segments split in proportion to their estimated cost.  seg0 is the lattice.
-static Plan make_plan(long long n_tgt, long long n0, long long n1) {
+static Plan make_plan(long long n_tgt, long long n0, long long n1, long long n_groups = 1) {
     Plan pl;
     if (n_tgt <= 0) return pl;
-    pl.n_tb = (n_tgt + NB_TB - 1) / NB_TB;
+    const long long per_group = n_tgt / n_groups;
+    pl.n_tb = n_groups * ((per_group + NB_TB - 1) / NB_TB);
     const long long t0 = (n0 + NB_TILE_W - 1) / NB_TILE_W;
     const long long t1 = (n1 + NB_TILE - 1) / NB_TILE;
     const double w0 = t0 * NB_COST_LAT_TILE, w1 = t1 * NB_COST_POS_TILE;
@@ -439,7 +452,9 @@ static Plan make_plan(long long n_tgt, long long n0, long long n1) {
 static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float* w0,
                        const int64_t* side, float e0, const float4* s1, long long n1, float e1,
                        double* val0, double* grad0, double* val1, double* grad1, void* ws,
-                       size_t ws_bytes, cudaStream_t stream) {
+                       size_t ws_bytes, cudaStream_t stream, long long n_groups = 1) {
+    SPK_REQUIRE(n_groups >= 1 && n_tgt % n_groups == 0, SPK_ERR_ARG,
+                "targets (%lld) must split evenly into %lld groups", n_tgt, n_groups);
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
     long long n0 = 0;
     int sd[3] = {1, 1, 1};
@@ -467,13 +482,16 @@ static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float
     SPK_REQUIRE(tgt != nullptr, SPK_ERR_ARG, "null target pointer");
     SPK_REQUIRE(((uintptr_t)w0 & 15) == 0 && ((uintptr_t)s1 & 15) == 0, SPK_ERR_ARG,
                 "source arrays must be 16-byte aligned");
-    const Plan pl = make_plan(n_tgt, n0, n1);
+    const Plan pl = make_plan(n_tgt, n0, n1, n_groups);
     SPK_REQUIRE(ws != nullptr && ws_bytes >= pl.ws_bytes, SPK_ERR_WORKSPACE,
                 "nbody workspace too small: need %zu bytes, got %zu", pl.ws_bytes, ws_bytes);
     NBParams P;
     P.tgt = tgt;
     P.n_tgt = n_tgt;
     P.n_tb = pl.n_tb;
+    P.per_group = n_tgt / n_groups;
+    P.tb_per_group = pl.n_tb / n_groups;
+    P.src_stride = n_groups > 1 ? n1 : 0;
     P.seg[0] = SegDesc{w0, n0, (n0 + NB_TILE_W - 1) / NB_TILE_W, pl.nc0, 1, e0,
                        sd[0], sd[1], dims == 3 ? sd[2] : 1};
     P.seg[1] = SegDesc{s1, n1, (n1 + NB_TILE - 1) / NB_TILE, pl.nc1, 0, e1, 0, 0, 0};
@@ -533,7 +551,8 @@ __global__ void grid_sources_kernel(const double* __restrict__ rho, long long s0
 // ------------------------------------------------------------ gradient combination
 constexpr int CB_THREADS = 256;
 
-__global__ void combine_kernel(long long n, int dims, const double* __restrict__ va,
+__global__ void combine_kernel(long long n, long long per_group, int dims,
+                               const double* __restrict__ va,
                                const double* __restrict__ ga, double pa,
                                const double* __restrict__ vr, const double* __restrict__ gr,
                                double pr, const double* __restrict__ coords,
@@ -541,9 +560,11 @@ __global__ void combine_kernel(long long n, int dims, const double* __restrict__
                                const double* __restrict__ prev_g, double* __restrict__ grad,
                                double* __restrict__ block_out) {
     __shared__ double red[5][CB_THREADS];
-    const long long i = blockIdx.x * (long long)CB_THREADS + threadIdx.x;
+    // blockIdx.y = group (problem); blocks never straddle two problems
+    const long long li = blockIdx.x * (long long)CB_THREADS + threadIdx.x;
+    const long long i = blockIdx.y * per_group + li;
     double s_va = 0, s_vr = 0, s_kg = 0, s_gg = 0, s_nf = 0;
-    if (i < n) {
+    if (li < per_group && i < n) {
         if (va) s_va = va[i];
         if (vr) s_vr = vr[i];
         const double prr = pr * pr;
@@ -573,15 +594,20 @@ __global__ void combine_kernel(long long n, int dims, const double* __restrict__
             for (int q = 0; q < 5; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x < 5) block_out[blockIdx.x * 5 + threadIdx.x] = red[threadIdx.x][0];
+    if (threadIdx.x < 5)
+        block_out[((long long)blockIdx.y * gridDim.x + blockIdx.x) * 5 + threadIdx.x] =
+            red[threadIdx.x][0];
 }
 
 __global__ void combine_final_kernel(const double* __restrict__ block_out, long long nb,
-                                     double* __restrict__ out) {
+                                     double* __restrict__ out_all) {
+    // one block per group: fixed-order sum of that group's nb block partials
     __shared__ double red[5][CB_THREADS];
+    const double* bo = block_out + (long long)blockIdx.x * nb * 5;
+    double* out = out_all + (long long)blockIdx.x * 6;
     double s[5] = {0, 0, 0, 0, 0};
     for (long long b = threadIdx.x; b < nb; b += CB_THREADS)
-        for (int q = 0; q < 5; ++q) s[q] += block_out[b * 5 + q];
+        for (int q = 0; q < 5; ++q) s[q] += bo[b * 5 + q];
     for (int q = 0; q < 5; ++q) red[q][threadIdx.x] = s[q];
     __syncthreads();
     for (int w = CB_THREADS / 2; w > 0; w >>= 1) {
@@ -615,6 +641,21 @@ const char* spk_last_error(void) { return g_err; }
 
 size_t spk_nbody_workspace_bytes(int64_t n_tgt, int64_t n_src0, int64_t n_src1) {
     return make_plan(n_tgt, n_src0, n_src1).ws_bytes + 256;
+}
+
+size_t spk_nbody_batched_workspace_bytes(int64_t n_groups, int64_t per_group, int64_t n_cells,
+                                         int64_t n_pos) {
+    return make_plan(n_groups * per_group, n_cells, n_pos, n_groups).ws_bytes + 256;
+}
+
+int spk_fused_sums_batched(const void* tgt, int64_t n_groups, int64_t per_group, int dims,
+                           const float* grid_w, const int64_t* side, float eps2_att,
+                           const void* pos_src, int64_t n_pos, float eps2_rep,
+                           double* val_att, double* grad_att, double* val_rep,
+                           double* grad_rep, void* ws, size_t ws_bytes, spk_stream_t stream) {
+    return launch_sums((const float4*)tgt, n_groups * per_group, dims, grid_w, side, eps2_att,
+                       (const float4*)pos_src, n_pos, eps2_rep, val_att, grad_att, val_rep,
+                       grad_rep, ws, ws_bytes, (cudaStream_t)stream, n_groups);
 }
 
 int spk_direct_sums(const void* tgt, int64_t n_tgt, const void* src, int64_t n_src, int dims,
@@ -679,11 +720,38 @@ int spk_combine_gradient(int64_t n_tgt, int dims, const double* val_att,
                 "combine workspace too small");
     const long long nb = (n_tgt + CB_THREADS - 1) / CB_THREADS;
     double* bo = static_cast<double*>(ws);
-    combine_kernel<<<(unsigned)nb, CB_THREADS, 0, (cudaStream_t)stream>>>(
-        n_tgt, dims, val_att, grad_att, p_att, val_rep, grad_rep, p_rep, coords, prev_coords,
-        prev_grad, grad, bo);
+    combine_kernel<<<dim3((unsigned)nb, 1), CB_THREADS, 0, (cudaStream_t)stream>>>(
+        n_tgt, n_tgt, dims, val_att, grad_att, p_att, val_rep, grad_rep, p_rep, coords,
+        prev_coords, prev_grad, grad, bo);
     combine_final_kernel<<<1, CB_THREADS, 0, (cudaStream_t)stream>>>(bo, nb, out);
     SPK_CHECK_LAUNCH("combine_gradient");
+    return SPK_OK;
+}
+
+size_t spk_combine_batched_workspace_bytes(int64_t n_groups, int64_t per_group) {
+    return (size_t)n_groups * ((per_group + CB_THREADS - 1) / CB_THREADS) * 5 * sizeof(double) +
+           256;
+}
+
+int spk_combine_gradient_batched(int64_t n_groups, int64_t per_group, int dims,
+                                 const double* val_att, const double* grad_att, double p_att,
+                                 const double* val_rep, const double* grad_rep, double p_rep,
+                                 const double* coords, const double* prev_coords,
+                                 const double* prev_grad, double* grad, double* out, void* ws,
+                                 size_t ws_bytes, spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    SPK_REQUIRE(n_groups >= 1 && per_group >= 1, SPK_ERR_ARG, "empty batch");
+    SPK_REQUIRE(ws_bytes >= spk_combine_batched_workspace_bytes(n_groups, per_group),
+                SPK_ERR_WORKSPACE, "combine workspace too small");
+    const long long nb = (per_group + CB_THREADS - 1) / CB_THREADS;
+    double* bo = static_cast<double*>(ws);
+    combine_kernel<<<dim3((unsigned)nb, (unsigned)n_groups), CB_THREADS, 0,
+                     (cudaStream_t)stream>>>(n_groups * per_group, per_group, dims, val_att,
+                                             grad_att, p_att, val_rep, grad_rep, p_rep, coords,
+                                             prev_coords, prev_grad, grad, bo);
+    combine_final_kernel<<<(unsigned)n_groups, CB_THREADS, 0, (cudaStream_t)stream>>>(bo, nb,
+                                                                                       out);
+    SPK_CHECK_LAUNCH("combine_gradient_batched");
     return SPK_OK;
 }
 

@@ -31,6 +31,7 @@ struct ProjArgs {
     const double* in;
     const double* grad;
     double eta;
+    const double* eta_shot;  // per-shot step (batched problems); overrides eta when set
     double* out;
     long long n_shots;
     int ns;
@@ -180,9 +181,10 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
     if (tid == 0) flag_sh[0] = 0;
     __syncthreads();
     int bad = 0;
+    const double eta = A.eta_shot ? A.eta_shot[c] : A.eta;
     for (int i = tid; i < nd; i += nt) {
         double kv = in[i];
-        if (gr) kv = kv - A.eta * gr[i];  // pattern.coords - eta * grad (optimizer.py:326)
+        if (gr) kv = kv - eta * gr[i];  // pattern.coords - eta * grad (optimizer.py:326)
         if (!isfinite(kv)) bad = 1;
         k[i] = kv;
         q0[i] = 0.0;
@@ -792,10 +794,13 @@ __global__ void residual_kernel(const double* __restrict__ co, int ns, int pin, 
     if (threadIdx.x < 4) per_shot[c * 4 + threadIdx.x] = red[threadIdx.x][0];
 }
 
-__global__ void residual_final_kernel(const double* __restrict__ per_shot, long long n_shots,
+__global__ void residual_final_kernel(const double* __restrict__ per_shot_all, long long n_shots,
                                       double a, double b, int has_pin,
-                                      double* __restrict__ out) {
+                                      double* __restrict__ out_all) {
+    // one block per group of n_shots shots (a single pattern: one block)
     __shared__ double red[4][RS_THREADS];
+    const double* per_shot = per_shot_all + (long long)blockIdx.x * n_shots * 4;
+    double* out = out_all + (long long)blockIdx.x * 5;
     double m[4] = {0.0, -INFINITY, -INFINITY, 0.0};
     for (long long c = threadIdx.x; c < n_shots; c += RS_THREADS)
         for (int q = 0; q < 4; ++q) m[q] = fmax(m[q], per_shot[c * 4 + q]);
@@ -976,7 +981,8 @@ size_t spk_project_workspace_bytes(int64_t n_shots, int n_s, int dims, int with_
     return (size_t)n_shots * proj_state_doubles(n_s, dims) * sizeof(double) + 256;
 }
 
-int spk_project_all(const double* in, const double* grad, double eta, double* out,
+int spk_project_all(const double* in, const double* grad, double eta,
+                    const double* eta_per_shot, double* out,
                     int64_t n_shots, int n_s, int dims, double a, double b, int pin_idx,
                     const double* pin_val, int n_pit, double tau, int monotone, double tol,
                     int max_sweeps, void* pos4, int32_t* sweeps, double* trace,
@@ -996,6 +1002,7 @@ int spk_project_all(const double* in, const double* grad, double eta, double* ou
     A.in = in;
     A.grad = grad;
     A.eta = eta;
+    A.eta_shot = eta_per_shot;
     A.out = out;
     A.n_shots = n_shots;
     A.ns = n_s;
@@ -1089,6 +1096,32 @@ int spk_feasibility_residuals(const double* coords, int64_t n_shots, int n_s, in
             coords, n_s, pin_idx, pv[0], pv[1], pv[2], per);
     residual_final_kernel<<<1, RS_THREADS, 0, stream>>>(per, n_shots, a, b, pin_idx >= 0, out);
     SPK_CHECK_LAUNCH("feasibility_residuals");
+    return SPK_OK;
+}
+
+int spk_feasibility_residuals_batched(const double* coords, int64_t n_groups,
+                                      int64_t shots_per_group, int n_s, int dims, double a,
+                                      double b, int pin_idx, const double* pin_val, double* out,
+                                      void* ws, size_t ws_bytes, spk_stream_t stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3");
+    SPK_REQUIRE(n_groups >= 1 && shots_per_group >= 1 && n_s >= 1, SPK_ERR_ARG, "empty batch");
+    const long long n_shots = n_groups * shots_per_group;
+    SPK_REQUIRE(ws_bytes >= spk_residuals_workspace_bytes(n_shots), SPK_ERR_WORKSPACE,
+                "residual workspace too small");
+    double pv[3] = {0, 0, 0};
+    if (pin_idx >= 0)
+        for (int l = 0; l < dims; ++l) pv[l] = pin_val[l];
+    double* per = static_cast<double*>(ws);
+    if (dims == 3)
+        residual_kernel<3><<<(unsigned)n_shots, RS_THREADS, 0, stream>>>(
+            coords, n_s, pin_idx, pv[0], pv[1], pv[2], per);
+    else
+        residual_kernel<2><<<(unsigned)n_shots, RS_THREADS, 0, stream>>>(
+            coords, n_s, pin_idx, pv[0], pv[1], pv[2], per);
+    residual_final_kernel<<<(unsigned)n_groups, RS_THREADS, 0, stream>>>(
+        per, shots_per_group, a, b, pin_idx >= 0, out);
+    SPK_CHECK_LAUNCH("feasibility_residuals_batched");
     return SPK_OK;
 }
 

@@ -1,4 +1,5 @@
-"""Constraint projection K3 on the B200 (fp64, one CTA per shot + warp wavefront polish).
+"""Constraint projection K3 on the B200 (fp64; one CTA per shot for FISTA, a systolic
+ring of sweeps per shot for the polish).
 
 Projects each shot onto {|s| <= 1, ||s[n+1]-s[n]|| <= alpha dt, ||s[n+2]-2s[n+1]+s[n]||
 <= beta dt^2, s[pin] = v} with the reference's algorithm
@@ -106,11 +107,12 @@ def _pin_arrays(cfg: ProjectionConfig, dims: int):
 def project_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad=None, eta=0.0,
                    out: torch.Tensor | None = None, pos4=None, sweeps=None, trace=None,
                    nonfinite=None, tau: float | None = None,
-                   max_sweeps: int = MAX_POLISH_SWEEPS) -> torch.Tensor:
+                   max_sweeps: int = MAX_POLISH_SWEEPS, eta_per_shot=None) -> torch.Tensor:
     """K3 on device buffers: out = P(coords - eta * grad) for every shot.
 
     ``coords``/``grad``/``out``: (n_shots, n_s, d) fp64 CUDA tensors.  ``pos4`` (optional)
-    receives the float4 positions of the result (the next N-body's sources)."""
+    receives the float4 positions of the result (the next N-body's sources);
+    ``eta_per_shot`` (optional device f64 [n_shots]) replaces ``eta`` shot by shot."""
     n_c, n_s, dims = coords.shape
     pin_idx, pin_val = _pin_arrays(cfg, dims)
     if pin_idx >= n_s:
@@ -125,8 +127,8 @@ def project_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad=None, et
     ws = _device.workspace(nbytes, "project")
     pv = _native.f64_array(list(pin_val) + [0.0] * (3 - dims))
     _native.call("spk_project_all", coords.data_ptr(), _device.ptr(grad), float(eta),
-                 out.data_ptr(), n_c, n_s, dims, cfg.speed_bound, cfg.accel_bound, pin_idx,
-                 pv, cfg.n_pit, float(tau), int(bool(cfg.monotone)), 0.1 * cfg.feas_tol,
+                 _device.ptr(eta_per_shot), out.data_ptr(), n_c, n_s, dims, cfg.speed_bound,
+                 cfg.accel_bound, pin_idx, pv, cfg.n_pit, float(tau), int(bool(cfg.monotone)), 0.1 * cfg.feas_tol,
                  int(max_sweeps), _device.ptr(pos4), _device.ptr(sweeps), _device.ptr(trace),
                  _device.ptr(nonfinite), ws.data_ptr(), ws.numel(), _device.stream())
     return out

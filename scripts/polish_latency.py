@@ -23,7 +23,7 @@ for n in NS:
     for r in range(2):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        _native.call("spk_project_all", shots.data_ptr(), None, 0.0, out.data_ptr(), n, 1024, 3,
+        _native.call("spk_project_all", shots.data_ptr(), None, 0.0, None, out.data_ptr(), n, 1024, 3,
                      cfg.speed_bound, cfg.accel_bound, 512, pv, 1, 0.048, 0, -1.0, sweeps,
                      None, None, None, None, ws.data_ptr(), ws.numel(), _device.stream())
         e.record()
