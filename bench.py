@@ -43,6 +43,10 @@ WORKLOADS = {
     "c1": dict(name="C1: 2D SPARKLING 64 shots x 512 samples, 257^2 density grid",
                n_c=64, n_s=512, dims=2, grid_n=(128, 128), pert=0.25,
                fov=0.192, matrix=64, dwell=2e-6),
+    "c3": dict(name="C3: stack-of-SPARKLING, 64 independent 2D problems of 64 shots x 512 "
+                    "samples, 257^2 density grid (one device batch)",
+               n_c=64, n_s=512, dims=2, grid_n=(128, 128), pert=0.25,
+               fov=0.192, matrix=64, dwell=2e-6, stack=64),
 }
 W = dict(WORKLOADS["c2"])
 EPS_REP = 1e-3
@@ -75,7 +79,9 @@ def workload_config():
     return {"workload": W["name"] + " (exact attraction + exact repulsion + projection)",
             "n_c": N_C, "n_s": N_S, "p": N_C * N_S, "grid": [2 * n + 1 for n in GRID_NS],
             "grad_mode": "exact", "eps_rep": EPS_REP, "eps_att": 1.0 / (2 * GRID_N),
-            "n_pit": 100, "hardware": "full3d.cfg limits (G 40 mT/m, S 180 T/m/s)",
+            "n_pit": 100,
+            "hardware": f"G 40 mT/m, S 180 T/m/s, raster 10 us, matrix {W['matrix']}, "
+                        f"fov {W['fov']} m",
             "l2": "flushed between steps (256 MiB memset outside the per-step events)"}
 
 
@@ -415,6 +421,95 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_stack(args):
+    """C3: one stacked optimize iteration of G independent problems per step (1 GPU)."""
+    import torch
+
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import _native, stack
+    from paper_2108_02991_b200.optimizer import _bb_step, default_eta0
+
+    torch.cuda.set_device(0)
+    G = W["stack"]
+    cfg = spk.OptimizerConfig(n_c=N_C, n_s=N_S, dims=DIMS, n_pit=100, grad_mode="exact",
+                              grid_n=GRID_N, seed=0, perturbation=W["pert"])
+    fld = spk.precompute_field(density())
+    pcfg = proj_config()
+    base = spk.init_radial(N_C, N_S, DIMS)
+    starts = np.stack([spk.perturb(base, W["pert"], q).coords for q in range(G)])
+    run = stack.StackedRun(starts, cfg, fld)
+    run.project(pcfg)
+    eta0 = default_eta0(run.p, EPS_REP)
+    st = {"etas": np.full(G, eta0), "it": 0, "have": False}
+    nb_events = []
+    orig_call = _native.call
+
+    def timed_call(name, *a):
+        if name == "spk_fused_sums_batched" and st.get("record"):
+            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            orig_call(name, *a)
+            e0.record()
+            nb_events.append((s0, e0))
+            return
+        orig_call(name, *a)
+
+    _native.call = timed_call
+
+    def step():
+        st["it"] += 1
+        att, rep, bad, dkdg, dgdg = run.evaluate()
+        if bad.any() or not np.isfinite(att - rep).all():
+            raise RuntimeError("non-finite during bench")
+        for q in range(G):
+            st["etas"][q] = _bb_step(st["it"], st["etas"][q], dkdg[q], dgdg[q], st["have"],
+                                     eta0, cfg.fixed_step_iters)
+        st["have"] = True
+        run.step_project(pcfg, st["etas"])
+        run.residual_max(pcfg)
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st["record"] = True
+    _native.reset_launch_count()
+    times = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            step()
+            e0.record()
+            times.append((s0, e0))
+        torch.cuda.synchronize()
+    _native.call = orig_call
+    total_ms = sum(a.elapsed_time(b) for a, b in times)
+    nb_ms = float(np.mean([a.elapsed_time(b) for a, b in nb_events]))
+    p, g, rep_pairs, att_pairs = pairs_per_step()
+    pairs = G * (rep_pairs + att_pairs)
+    f_rep, f_att = FLOPS[DIMS]
+    peak, peak_mhz = measured_fp32_peak() if measured_fp32_peak()[0] else (
+        fp32_peak_tflops(1965.0), 1965.0)
+    achieved = G * (rep_pairs * f_rep + att_pairs * f_att) / (nb_ms / 1e3) / 1e12
+    bound_ms = G * (rep_pairs / (peak * 1e12 / f_rep) + att_pairs / sfu_pairs_per_s(peak_mhz)) * 1e3
+    line = {
+        "metric": METRIC, "value": pairs * args.steps / (total_ms / 1e3), "unit": "pairs/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "s_per_iteration": total_ms / args.steps / 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
+        "config": workload_config() | {"stack": G, "parallelism": "one device batch"},
+        "roofline": {"bound": "fp32+sfu", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "launch_ms": nb_ms,
+                     "hw_bound_ms": bound_ms, "frac_of_hw_bound": bound_ms / nb_ms,
+                     "kernel": "nbody_kernel batched (spk_fused_sums_batched)"},
+        "clocks": clk.summary(), "gpu_launches": _native.launch_count(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_e2e_sharded(args, run, step, world):
     """N > 1: the sharded optimize iteration with this rank's shots copied H2D from pinned
     host memory before, and the projected shots + scalars copied D2H after, every step
@@ -539,6 +634,8 @@ def main():
     select_workload(args.config)
     if args.impl == "reference":
         run_reference(args)
+    elif W.get("stack"):
+        run_stack(args)
     else:
         run_ours(args)
 
