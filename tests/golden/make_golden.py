@@ -242,6 +242,18 @@ def host_fixtures():
     out["bb_dk"] = dk
     out["bb_dg"] = dg
     out["bb_eta"] = np.float64(om.step_size(25, 0.5, dk, dg, 0.01, 20))
+    # SPKT bytes written by the reference (format kept byte-identical)
+    import tempfile
+    from vdtraj import io as vio
+    pat = core.SamplingPattern(rng.uniform(-1, 1, (3, 7, 3)))
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "t.spkt")
+        vio.write_spkt(path, pat, (834.78, 834.78, 833.33), 1e-5)
+        out["spkt_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        vio.write_spkd(os.path.join(tmp, "d.spkd"), out["dens_2d_16"])
+        out["spkd_bytes"] = np.frombuffer(open(os.path.join(tmp, "d.spkd"), "rb").read(),
+                                          dtype=np.uint8)
+    out["spkt_coords"] = pat.coords
     np.savez_compressed(os.path.join(OUT, "host.npz"), **out)
 
 

@@ -156,3 +156,19 @@ def test_multiresolution_3d_exact_full3d_limits(spk):
     pc = spk.ProjectionConfig(alpha=lim.alpha, beta=lim.beta, raster_dt=hw.raster_dt, pin=pin)
     assert spk.feasibility_residuals(res.pattern, pc)["max"] <= pc.feas_tol
     assert res.pattern.coords.shape == (64, 256, 3)
+
+
+def test_step_api_equals_optimize(spk):
+    """start / step / finish (the `step` entry point) reproduces optimize() bitwise."""
+    cfg = spk.OptimizerConfig(n_c=4, n_s=32, dims=2, n_decim=1, n_git=3, perturbation=0.2,
+                              seed=7, grad_mode="exact")
+    hw = desk_hw(spk)
+    ref = spk.optimize(cfg, hw)
+    st = spk.start(cfg, hw)
+    recs = []
+    while (rec := spk.step(st)) is not None:
+        recs.append(rec)
+    res = spk.finish(st)
+    assert len(recs) == 6 and [r.level for r in recs] == [0, 0, 0, 1, 1, 1]
+    assert np.array_equal(res.pattern.coords, ref.pattern.coords)
+    assert np.array_equal(res.trace.costs(), ref.trace.costs())

@@ -129,3 +129,11 @@ def test_trace_csv(tmp_path):
     tr.write_csv(tmp_path / "t.csv")
     lines = (tmp_path / "t.csv").read_text().splitlines()
     assert lines[0].startswith("level,iteration") and len(lines) == 2
+
+
+def test_spkt_spkd_bytes_identical_to_reference(host, tmp_path):
+    pat = spk.SamplingPattern(host["spkt_coords"])
+    spk_io.write_spkt(tmp_path / "t.spkt", pat, (834.78, 834.78, 833.33), 1e-5)
+    assert (tmp_path / "t.spkt").read_bytes() == host["spkt_bytes"].tobytes()
+    spk_io.write_spkd(tmp_path / "d.spkd", host["dens_2d_16"])
+    assert (tmp_path / "d.spkd").read_bytes() == host["spkd_bytes"].tobytes()
