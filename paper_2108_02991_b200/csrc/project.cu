@@ -674,14 +674,18 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
                                                       double b, int pin, double pv0,
                                                       double pv1, double pv2, double tol,
                                                       int max_sweeps, double* ws,
-                                                      int32_t* sweeps_out, float4* pos4) {
+                                                      int32_t* sweeps_out, float4* pos4,
+                                                      int wrap_global) {
     extern __shared__ __align__(16) double xfer[];  // [W][2][D], then wrap [ns][D]
     __shared__ int stop_sh;
     const long long c = blockIdx.x;
     const int B = blockDim.x;
     const int W = B >> 5;
     const int P = max(4 * B + W, ns + 4);
-    double* wrap = xfer + W * 2 * D;
+    const int nd4 = ns * D;
+    // wrap buffer in shared memory, or (very long shots) in the per-shot workspace
+    double* wrap = wrap_global ? ws + blockIdx.x * (size_t)(4 * nd4) + 3 * nd4
+                               : xfer + W * 2 * D;
     const int g = threadIdx.x;
     const int lane = g & 31;
     const int warp = g >> 5;
@@ -689,7 +693,7 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     const int nd = ns * D;
     const double pv[3] = {pv0, pv1, pv2};
     double* s0 = shots + c * (size_t)nd;
-    double* snap0 = ws + c * (size_t)(3 * nd);
+    double* snap0 = ws + c * (size_t)(4 * nd);
     double* snap1 = snap0 + nd;
     double* res = snap1 + nd;
     if (g == 0) stop_sh = 0x7fffffff;
@@ -1035,8 +1039,9 @@ int spk_project_all(const double* in, const double* grad, double eta,
     // polish: systolic ring, one CTA of 32*pw lanes per shot; snapshots + result in the
     // (now free) FISTA workspace, warp hand-over slots in shared memory
     const int pw = polish_warps(n_s);
-    const size_t psm = ((size_t)pw * 2 * dims + (size_t)n_s * dims) * sizeof(double);
-    SPK_REQUIRE(psm <= 220 * 1024, SPK_ERR_ARG, "N_s=%d too large for the polish ring", n_s);
+    size_t psm = ((size_t)pw * 2 * dims + (size_t)n_s * dims) * sizeof(double);
+    const int wrap_global = psm > 200 * 1024;
+    if (wrap_global) psm = (size_t)pw * 2 * dims * sizeof(double);
     cudaFuncSetAttribute(polish_kernel<3, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)psm);
     cudaFuncSetAttribute(polish_kernel<2, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1053,20 +1058,20 @@ int spk_project_all(const double* in, const double* grad, double eta,
         if (dims == 3)
             polish_kernel<3, 256, 3><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4);
+                (float4*)pos4, wrap_global);
         else
             polish_kernel<2, 256, 3><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4);
+                (float4*)pos4, wrap_global);
     } else {
         if (dims == 3)
             polish_kernel<3, 1024, 1><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4);
+                (float4*)pos4, wrap_global);
         else
             polish_kernel<2, 1024, 1><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4);
+                (float4*)pos4, wrap_global);
     }
     SPK_CHECK_LAUNCH("polish_kernel");
     return SPK_OK;

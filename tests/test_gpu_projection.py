@@ -144,3 +144,21 @@ def test_upsample_device_bitwise(spk):
     h = golden("host")
     out = CudaOps().upsample(_device.h2d(h["ups_in"]))
     assert np.array_equal(_device.d2h(out), h["ups_out"])
+
+
+def test_very_long_shot_global_fallbacks(spk):
+    """N_s = 12000 (3D): FISTA state and the polish wrap buffer exceed shared memory and
+    fall back to the workspace; ring capped at 32 warps.  Still bit-identical."""
+    rng = np.random.default_rng(21)
+    ns = 12000
+    shots = np.cumsum(rng.normal(0, 3e-3, (2, ns, 3)), axis=1)
+    shots -= shots[:, ns // 2:ns // 2 + 1, :]
+    pin = spk.LinearConstraint(ns // 2, np.zeros(3))
+    cfg = spk.ProjectionConfig(alpha=2.0e-3, beta=3.0e-4, raster_dt=1.0, n_pit=30, pin=pin)
+    tau = 1.0 / spk.projection.stacked_operator_norm(ns, ns // 2)
+    for cap in (3, 200):
+        out, _, sw = run(spk, shots, cfg, tau, max_sweeps=cap)
+        ref, rsw = orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, ns // 2,
+                                   np.zeros(3), 30, tau, 0.1 * cfg.feas_tol, max_sweeps=cap)
+        assert np.array_equal(sw, rsw)
+        assert np.array_equal(out, ref), np.abs(out - ref).max()
