@@ -171,6 +171,116 @@ int spk_field_eval(const double* pts, int64_t p, int dims, const double* potenti
                    const double* force, int64_t grid_n, int mode, double* vals,
                    double* grad, int64_t* n_clamped, spk_stream_t stream);
 
+/* ------------------------------------------------- treecode (repulsion backend "tree")
+ *
+ * Replaces the reference's CPU dual-tree FMM (repulsion.py:90-200, _treecode.py:77-471)
+ * behind eval_repulsion_tree with a GPU particle-cluster treecode meeting the same
+ * tree_precision contract (relative error of the cost and of the gradient l2 norm).
+ * Pipeline (paper_2108_02991_b200/tree.py): keys -> sort -> gather -> host octree ->
+ * leaf / group boxes -> host interaction lists -> P2M proxies -> eval.
+ */
+
+/* Morton keys of float4 positions in [-1, 1]^dims (21 bits per axis in 3D, 31 in 2D);
+ * idx = 0..n-1.  keys: [n] u64, idx: [n] i32 (device). */
+int spk_tree_keys(const void* pos, int64_t n, int dims, uint64_t* keys, int32_t* idx,
+                  spk_stream_t stream);
+
+/* Stable radix sort of (keys, idx) pairs (CUB).  Counterpart of build_tree's sort
+ * (_treecode.py:77-170). */
+size_t spk_tree_sort_workspace_bytes(int64_t n);
+int spk_tree_sort(const uint64_t* keys_in, const int32_t* idx_in, uint64_t* keys_out,
+                  int32_t* idx_out, int64_t n, int dims, void* ws, size_t ws_bytes,
+                  spk_stream_t stream);
+
+/* out[i] = {pos[perm[i]].xyz, weights ? weights[perm[i]] : 1}. */
+int spk_tree_gather(const void* pos, const int32_t* perm, int64_t n, const float* weights,
+                    void* out, spk_stream_t stream);
+
+/* Tight boxes {min xyz, max xyz} of record ranges [begin[r], end[r]) -> box [n][6]. */
+int spk_tree_boxes(const void* rec, int64_t n_ranges, const int64_t* begin,
+                   const int64_t* end, int dims, float* box, spk_stream_t stream);
+
+/* Node boxes {min xyz, max xyz} of an octree over sorted records: leaves reduce their
+ * particles, internal nodes (BFS levels, level_off is a HOST array of n_levels + 1
+ * offsets) merge their children bottom-up.  node_box: [n_nodes][6] f32 (device). */
+int spk_tree_node_boxes(const void* rec, int64_t n_nodes, const int32_t* first_child,
+                        const int32_t* n_child, int64_t n_leaves, const int32_t* leaf_node,
+                        const int64_t* leaf_begin, const int64_t* leaf_end, int64_t n_levels,
+                        const int64_t* level_off, int dims, float* node_box,
+                        spk_stream_t stream);
+
+/* Interaction lists on the GPU (dual_traverse + group_by_target, _treecode.py:173-262):
+ * one thread per target group walks the octree; a node is far when
+ * r_group + r_node < theta |c_group - c_node| (box half-diagonals and centers).  Far
+ * nodes with more than m = order^dims particles become proxy slots (node order), other
+ * far nodes and opened leaves contribute their particle ranges (contiguous ranges merge).
+ * Count pass: slot_of/slot_node [n_nodes] i32, slot_box [n_nodes][6] f32 (center, half),
+ * slot_unit_off [n_nodes + 1] i64, seg_off [n_groups + 1] i64, totals [3] i64 = segments,
+ * slots, P2M units (device).  Write pass fills seg_start/seg_count and the P2M units. */
+size_t spk_tree_plan_workspace_bytes(int64_t n_nodes, int64_t n_groups);
+int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
+                        const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
+                        const float* node_box, const float* group_box, int64_t n_groups,
+                        double theta, int order, int dims, int64_t n_src, int32_t* slot_of,
+                        int32_t* slot_node, float* slot_box, int64_t* slot_unit_off,
+                        int64_t* seg_off, int64_t* totals, void* ws, size_t ws_bytes,
+                        spk_stream_t stream);
+int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
+                        const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
+                        const float* node_box, const float* group_box, int64_t n_groups,
+                        double theta, int order, int dims, int64_t n_src,
+                        const int32_t* slot_of, const int32_t* slot_node,
+                        const int64_t* slot_unit_off, int64_t n_slots, const int64_t* seg_off,
+                        int64_t* seg_start, int32_t* seg_count, int32_t* unit_slot,
+                        int64_t* unit_begin, int64_t* unit_end, spk_stream_t stream);
+
+/* Source-side Chebyshev interpolation (the P2M of _treecode.py:286-313 for a
+ * particle-cluster scheme): proxies[slot * m + k] = {tensor Chebyshev point k of the
+ * slot box, sum over the slot's particles of w * L_k(x)}, m = order^dims.  Units are
+ * (slot, particle range) pieces, units of a slot contiguous (slot_unit_off). */
+size_t spk_tree_p2m_workspace_bytes(int64_t n_units, int order, int dims);
+int spk_tree_p2m(const void* rec, int64_t n_units, const int32_t* unit_slot,
+                 const int64_t* unit_begin, const int64_t* unit_end, int64_t n_slots,
+                 const int64_t* slot_unit_off, const float* slot_box, int order, int dims,
+                 void* proxies, void* ws, size_t ws_bytes, spk_stream_t stream);
+
+/* Weighted sums over segment lists (the m2l/l2p/near_field of _treecode.py:330-471 in
+ * one pass): for target group g (sorted targets [grp_begin[g], grp_end[g]), at most
+ * spk_tree_group_size() of them),
+ *   val[perm[i]] = sum_{records r in g's segments} w_r sqrt(|t_i - r|^2 + eps2)
+ *   grad[perm[i]] = sum w_r (t_i - r) / sqrt(...)
+ * seg_off: [n_groups + 1]; seg_start (record offset into src), seg_count. */
+int spk_tree_eval(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_groups,
+                  const int64_t* grp_begin, const int64_t* grp_end, const void* src,
+                  const int64_t* seg_off, const int64_t* seg_start, const int32_t* seg_count,
+                  int dims, float eps2, double* val, double* grad, spk_stream_t stream);
+int spk_tree_group_size(void);
+
+/* Host side (tree_host.cpp; HOST pointers).  An opaque octree over sorted keys:
+ * nodes in BFS order with contiguous children, leaves hold <= leaf_cap particles
+ * (build_tree, _treecode.py:77-170).  Returns NULL on error (spk_last_error). */
+void* spk_tree_host_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap);
+void spk_tree_host_free(void* tree);
+void spk_tree_host_sizes(const void* tree, int64_t* counts /* [2]: nodes, leaves */);
+int64_t spk_tree_host_levels(const void* tree, int64_t* level_off);
+void spk_tree_host_leaf_nodes(const void* tree, int32_t* leaf_node);
+void spk_tree_host_leaves(const void* tree, int64_t* begin, int64_t* end);
+void spk_tree_host_nodes(const void* tree, int64_t* begin, int64_t* end,
+                         int32_t* first_child, int32_t* n_child, int32_t* level);
+void spk_tree_host_set_leaf_boxes(void* tree, const float* leaf_box);
+/* Target groups (<= cap consecutive sorted particles, packed along the octree); returns
+ * the count, fills begin/end when non-NULL. */
+int64_t spk_tree_host_groups(const void* tree, int64_t cap, int64_t* begin, int64_t* end);
+/* Host reference planner (serial; same lists as spk_tree_plan_count/_write):
+ * counts[5] = segments, proxy slots, P2M units, near pairs, far pairs. */
+int spk_tree_host_plan(void* tree, int64_t n_groups, const float* group_box, double theta,
+                       int order, int64_t n_src, int64_t* counts);
+void spk_tree_host_slot_nodes(const void* tree, int32_t* slot_node);
+void spk_tree_host_export_plan(const void* tree, int64_t* seg_off, int64_t* seg_start,
+                               int32_t* seg_count, float* slot_box, int32_t* unit_slot,
+                               int64_t* unit_begin, int64_t* unit_end,
+                               int64_t* slot_unit_off);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,7 +24,11 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUD
 SOURCES = {
     "nbody.cu": [],
     "project.cu": ["-fmad=false"],
+    "tree.cu": [],
 }
+# Host C++ (treecode octree over sorted keys; reference host planner).
+HOST_SOURCES = ["tree_host.cpp"]
+HOST_CXX = ["-O3", "-std=c++17", "-fPIC", "-I" + INCLUDE]
 
 
 def _nvcc() -> str:
@@ -54,6 +58,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
             cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True)
+    cxx = shutil.which("g++") or "/usr/bin/g++"
+    for src in HOST_SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(LIB_DIR, src.replace(".cpp", ".o"))
+        objs.append(obj)
+        if force or _stale(obj, [path] + headers):
+            cmd = [cxx, *HOST_CXX, "-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd))
             subprocess.run(cmd, check=True)

@@ -60,6 +60,39 @@ SIGNATURES = {
     "spk_upsample_shots": (c_int, [c_vp, c_vp, c_i64, c_int, c_int, c_vp]),
     "spk_field_eval": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_i64, c_int, c_vp, c_vp,
                                c_vp, c_vp]),
+    "spk_tree_keys": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
+    "spk_tree_sort_workspace_bytes": (c_size, [c_i64]),
+    "spk_tree_sort": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_size, c_vp]),
+    "spk_tree_gather": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "spk_tree_boxes": (c_int, [c_vp, c_i64, c_vp, c_vp, c_int, c_vp, c_vp]),
+    "spk_tree_p2m_workspace_bytes": (c_size, [c_i64, c_int, c_int]),
+    "spk_tree_p2m": (c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_int, c_int,
+                             c_vp, c_vp, c_size, c_vp]),
+    "spk_tree_eval": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
+                              c_flt, c_vp, c_vp, c_vp]),
+    "spk_tree_host_groups": (c_i64, [c_vp, c_i64, c_vp, c_vp]),
+    "spk_tree_host_levels": (c_i64, [c_vp, c_vp]),
+    "spk_tree_host_leaf_nodes": (None, [c_vp, c_vp]),
+    "spk_tree_node_boxes": (c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
+                                    c_vp, c_int, c_vp, c_vp]),
+    "spk_tree_plan_workspace_bytes": (c_size, [c_i64, c_i64]),
+    "spk_tree_plan_count": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl,
+                                    c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                    c_vp, c_size, c_vp]),
+    "spk_tree_plan_write": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl,
+                                    c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp,
+                                    c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "spk_tree_host_slot_nodes": (None, [c_vp, c_vp]),
+    "spk_tree_group_size": (c_int, []),
+    "spk_tree_host_build": (c_vp, [c_vp, c_i64, c_int, c_i64]),
+    "spk_tree_host_free": (None, [c_vp]),
+    "spk_tree_host_sizes": (None, [c_vp, c_vp]),
+    "spk_tree_host_leaves": (None, [c_vp, c_vp, c_vp]),
+    "spk_tree_host_nodes": (None, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "spk_tree_host_set_leaf_boxes": (None, [c_vp, c_vp]),
+    "spk_tree_host_plan": (c_int, [c_vp, c_i64, c_vp, c_dbl, c_int, c_i64, c_vp]),
+    "spk_tree_host_export_plan": (None, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                         c_vp]),
 }
 
 
@@ -70,6 +103,9 @@ LAUNCHES = {
     "spk_feasibility_residuals": 2, "spk_upsample_shots": 1, "spk_field_eval": 1,
     "spk_fused_sums_batched": 3, "spk_combine_gradient_batched": 2,
     "spk_feasibility_residuals_batched": 2,
+    "spk_tree_keys": 1, "spk_tree_sort": 10, "spk_tree_gather": 1, "spk_tree_boxes": 1,
+    "spk_tree_p2m": 2, "spk_tree_eval": 1, "spk_tree_plan_count": 9, "spk_tree_node_boxes": 1,
+    "spk_tree_plan_write": 2,
 }
 _launched = [0]
 
@@ -80,6 +116,11 @@ def reset_launch_count() -> None:
 
 def launch_count() -> int:
     return _launched[0]
+
+
+def add_launches(k: int) -> None:
+    """Account kernels whose number depends on the call (e.g. one per tree level)."""
+    _launched[0] += int(k)
 
 
 class NativeError(RuntimeError):

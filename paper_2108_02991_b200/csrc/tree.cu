@@ -1,0 +1,831 @@
+// tree.cu -- GPU kernels of the treecode repulsion backend (RepulsionConfig(backend="tree")).
+//
+// The reference accelerates repulsion with a dual-tree Chebyshev black-box FMM on the
+// CPU (/root/reference/pkg/src/vdtraj/repulsion.py:90-200, _treecode.py:77-471) and
+// promises `tree_precision` relative error on the cost and the gradient l2 norm.  The
+// B200 design keeps that contract with a scheme whose every hot loop is the N-body pair
+// kernel of nbody.cu:
+//
+//  * sources are sorted along a Morton curve (CUB radix sort) and an octree is built over
+//    the sorted keys (host, tree_host.cpp);
+//  * a far source node is replaced by q^d proxy sources on its tight bounding box (tensor
+//    Chebyshev points, weights = sum of the Lagrange basis over its particles: the
+//    source-side interpolation of particle-cluster treecodes);
+//  * targets are taken in Morton order in groups of <= TR_GROUP that follow the octree
+//    (packed sibling subtrees, tree_host.cpp); each group gets a list of source segments (near particles or far proxies) and one CTA evaluates the
+//    weighted kernel sum over the concatenated list with packed f32x2 FMA + MUFU.RSQ,
+//    staging the segments through shared memory with cp.async double buffering.
+//
+// Deterministic: the tree, the lists and every reduction have a fixed order.
+#include <cub/cub.cuh>
+
+#include <cfloat>
+
+#include "spk_common.cuh"
+
+namespace spk {
+
+constexpr int TR_THREADS = 128;
+constexpr int TR_GROUP = 2 * TR_THREADS;  // targets per group / CTA (one f32x2 pair each)
+constexpr int TR_BATCH = 512;             // source records per shared-memory stage
+constexpr int P2M_THREADS = 128;
+constexpr int P2M_MAX_ORDER = 8;
+
+// ---------------------------------------------------------------- Morton keys
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {  // 21 bits -> every 3rd bit
+    uint64_t x = v & 0x1fffffULL;
+    x = (x | x << 32) & 0x1f00000000ffffULL;
+    x = (x | x << 16) & 0x1f0000ff0000ffULL;
+    x = (x | x << 8) & 0x100f00f00f00f00fULL;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+    x = (x | x << 2) & 0x1249249249249249ULL;
+    return x;
+}
+__device__ __forceinline__ uint64_t spread2(uint32_t v) {  // 31 bits -> every 2nd bit
+    uint64_t x = v & 0x7fffffffULL;
+    x = (x | x << 16) & 0x0000ffff0000ffffULL;
+    x = (x | x << 8) & 0x00ff00ff00ff00ffULL;
+    x = (x | x << 4) & 0x0f0f0f0f0f0f0f0fULL;
+    x = (x | x << 2) & 0x3333333333333333ULL;
+    x = (x | x << 1) & 0x5555555555555555ULL;
+    return x;
+}
+__device__ __forceinline__ uint32_t quantize(float x, int bits) {
+    const double u = ((double)x + 1.0) * 0.5 * (double)(1ULL << bits);
+    long long q = (long long)floor(u);
+    q = q < 0 ? 0 : q;
+    const long long hi = (1LL << bits) - 1;
+    return (uint32_t)(q > hi ? hi : q);
+}
+
+__global__ void keys_kernel(const float4* __restrict__ pos, long long n, int dims,
+                            uint64_t* __restrict__ keys, int32_t* __restrict__ idx) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 r = pos[i];
+    uint64_t k;
+    if (dims == 3)
+        k = (spread3(quantize(r.x, 21)) << 2) | (spread3(quantize(r.y, 21)) << 1) |
+            spread3(quantize(r.z, 21));
+    else
+        k = (spread2(quantize(r.x, 31)) << 1) | spread2(quantize(r.y, 31));
+    keys[i] = k;
+    idx[i] = (int32_t)i;
+}
+
+// sorted records {x, y, z, w}: w = 1 (repulsion) or weights[perm[i]]
+__global__ void gather_kernel(const float4* __restrict__ pos, const int32_t* __restrict__ perm,
+                              long long n, const float* __restrict__ weights,
+                              float4* __restrict__ out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t j = perm[i];
+    const float4 r = pos[j];
+    out[i] = make_float4(r.x, r.y, r.z, weights ? weights[j] : 1.0f);
+}
+
+// ---------------------------------------------------------------- boxes
+// Tight bounding box {min xyz, max xyz} of every record range (leaves and target groups).
+__global__ void boxes_kernel(const float4* __restrict__ rec, const long long* __restrict__ begin,
+                             const long long* __restrict__ end, int dims,
+                             float* __restrict__ box, const int32_t* __restrict__ dst) {
+    const long long r = blockIdx.x;
+    float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (long long i = begin[r] + threadIdx.x; i < end[r]; i += blockDim.x) {
+        const float4 p = rec[i];
+        lo[0] = fminf(lo[0], p.x), hi[0] = fmaxf(hi[0], p.x);
+        lo[1] = fminf(lo[1], p.y), hi[1] = fmaxf(hi[1], p.y);
+        lo[2] = fminf(lo[2], p.z), hi[2] = fmaxf(hi[2], p.z);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+    }
+    __shared__ float s[32][6];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0)
+        for (int a = 0; a < 3; ++a) s[w][a] = lo[a], s[w][3 + a] = hi[a];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int c = threadIdx.x;
+        float v = s[0][c];
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+            v = c < 3 ? fminf(v, s[k][c]) : fmaxf(v, s[k][c]);
+        if (dims == 2 && (c == 2 || c == 5)) v = 0.0f;
+        box[(dst ? (long long)dst[r] : r) * 6 + c] = v;
+    }
+}
+
+// ---------------------------------------------------------------- P2M
+// Chebyshev points of the first kind t_i = cos((2i+1) pi / 2q) (the reference's
+// chebyshev_tables nodes, _treecode.py:20-44) and the Lagrange denominators.
+struct ChebTable {
+    float t[P2M_MAX_ORDER];
+    float inv_den[P2M_MAX_ORDER];
+};
+
+__device__ __forceinline__ void lagrange(float u, int q, const ChebTable& T, float* L) {
+    // L_k(u) = prod_{i != k} (u - t_i) / (t_k - t_i), via prefix / suffix products
+    float diff[P2M_MAX_ORDER];
+#pragma unroll
+    for (int i = 0; i < P2M_MAX_ORDER; ++i) diff[i] = i < q ? u - T.t[i] : 1.0f;
+    float pre = 1.0f;
+    float prefix[P2M_MAX_ORDER];
+#pragma unroll
+    for (int i = 0; i < P2M_MAX_ORDER; ++i) {
+        prefix[i] = pre;
+        pre *= diff[i];
+    }
+    float suf = 1.0f;
+#pragma unroll
+    for (int i = P2M_MAX_ORDER - 1; i >= 0; --i) {
+        if (i < q) L[i] = prefix[i] * suf * T.inv_den[i];
+        suf *= diff[i];
+    }
+}
+
+// One CTA per unit = (proxy slot, particle range); partial weights -> part[unit][m].
+__global__ void __launch_bounds__(P2M_THREADS) p2m_kernel(
+    const float4* __restrict__ rec, const int32_t* __restrict__ unit_slot,
+    const long long* __restrict__ unit_begin, const long long* __restrict__ unit_end,
+    const float* __restrict__ slot_box, int q, int dims, ChebTable T,
+    double* __restrict__ part) {
+    __shared__ float L[3][P2M_MAX_ORDER][P2M_THREADS];
+    __shared__ float W[P2M_THREADS];
+    const int tid = threadIdx.x;
+    const long long u = blockIdx.x;
+    const int slot = unit_slot[u];
+    const float* bx = slot_box + (size_t)slot * 6;  // center xyz, half xyz
+    const int m = dims == 3 ? q * q * q : q * q;
+    constexpr int KMAX = (P2M_MAX_ORDER * P2M_MAX_ORDER * P2M_MAX_ORDER) / P2M_THREADS;
+    double acc[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) acc[k] = 0.0;
+    for (long long c = unit_begin[u]; c < unit_end[u]; c += P2M_THREADS) {
+        const long long j = c + tid;
+        float l[3][P2M_MAX_ORDER] = {};
+        float w = 0.0f;
+        if (j < unit_end[u]) {
+            const float4 p = rec[j];
+            w = p.w;
+            lagrange((p.x - bx[0]) / bx[3], q, T, l[0]);
+            lagrange((p.y - bx[1]) / bx[4], q, T, l[1]);
+            if (dims == 3) lagrange((p.z - bx[2]) / bx[5], q, T, l[2]);
+        }
+        for (int i = 0; i < q; ++i) {
+            L[0][i][tid] = l[0][i];
+            L[1][i][tid] = l[1][i];
+            L[2][i][tid] = dims == 3 ? l[2][i] : 1.0f;
+        }
+        W[tid] = w;
+        __syncthreads();
+        const int cnt = (int)min((long long)P2M_THREADS, unit_end[u] - c);
+#pragma unroll
+        for (int kk = 0; kk < KMAX; ++kk) {
+            const int k = tid + kk * P2M_THREADS;
+            if (k < m) {
+                int kx, ky, kz;
+                if (dims == 3) {
+                    kx = k / (q * q), ky = (k / q) % q, kz = k % q;
+                } else {
+                    kx = k / q, ky = k % q, kz = 0;
+                }
+                const float* lx = L[0][kx];
+                const float* ly = L[1][ky];
+                const float* lz = L[2][dims == 3 ? kz : 0];
+                float s = 0.0f;
+                for (int jj = 0; jj < cnt; ++jj) s = fmaf(W[jj] * lx[jj], ly[jj] * lz[jj], s);
+                acc[kk] += (double)s;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int kk = 0; kk < KMAX; ++kk) {
+        const int k = tid + kk * P2M_THREADS;
+        if (k < m) part[(size_t)u * m + k] = acc[kk];
+    }
+}
+
+// Sum the units of every slot in order; write the proxy records {x, y, z, W}.
+__global__ void p2m_final_kernel(const double* __restrict__ part,
+                                 const long long* __restrict__ slot_unit_off,
+                                 const float* __restrict__ slot_box, int q, int dims,
+                                 ChebTable T, float4* __restrict__ proxies) {
+    const int slot = blockIdx.x;
+    const int m = dims == 3 ? q * q * q : q * q;
+    const float* bx = slot_box + (size_t)slot * 6;
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+        double s = 0.0;
+        for (long long u = slot_unit_off[slot]; u < slot_unit_off[slot + 1]; ++u)
+            s += part[(size_t)u * m + k];
+        int kx, ky, kz;
+        if (dims == 3) {
+            kx = k / (q * q), ky = (k / q) % q, kz = k % q;
+        } else {
+            kx = k / q, ky = k % q, kz = 0;
+        }
+        const float x = fmaf(bx[3], T.t[kx], bx[0]);
+        const float y = fmaf(bx[4], T.t[ky], bx[1]);
+        const float z = dims == 3 ? fmaf(bx[5], T.t[kz], bx[2]) : 0.0f;
+        proxies[(size_t)slot * m + k] = make_float4(x, y, z, (float)s);
+    }
+}
+
+
+// ---------------------------------------------------------------- device plan
+// Node boxes bottom-up: leaves reduce their particles (boxes_kernel with dst = node id),
+// internal nodes of one BFS level take the union of their children's boxes.
+__global__ void level_boxes_kernel(const int32_t* __restrict__ fchild,
+                                   const int32_t* __restrict__ nchild, long long lv_begin,
+                                   long long lv_end, float* __restrict__ box) {
+    const long long v = lv_begin + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= lv_end || nchild[v] == 0) return;
+    float o[6] = {FLT_MAX, FLT_MAX, FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int c = 0; c < nchild[v]; ++c) {
+        const float* cb = box + (size_t)(fchild[v] + c) * 6;
+        for (int a = 0; a < 3; ++a) {
+            o[a] = fminf(o[a], cb[a]);
+            o[3 + a] = fmaxf(o[3 + a], cb[3 + a]);
+        }
+    }
+    for (int k = 0; k < 6; ++k) box[(size_t)v * 6 + k] = o[k];
+}
+
+// Center and half-diagonal of a {min, max} box with explicit roundings: identical to the
+// host planner (tree_host.cpp make_box), so both produce the same interaction lists.
+struct CR {
+    float c[3], h[3], r;
+};
+__device__ __forceinline__ CR center_radius(const float* lohi, int dims) {
+    CR b;
+    float r2 = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        b.c[a] = __fmul_rn(0.5f, __fadd_rn(lohi[a], lohi[3 + a]));
+        b.h[a] = a < dims ? __fmul_rn(0.5f, __fsub_rn(lohi[3 + a], lohi[a])) : 0.0f;
+        r2 = __fadd_rn(r2, __fmul_rn(b.h[a], b.h[a]));
+    }
+    b.r = __fsqrt_rn(r2);
+    return b;
+}
+
+struct TravParams {
+    const long long* nbeg;
+    const long long* nend;
+    const int32_t* fchild;
+    const int32_t* nchild;
+    const float* nbox;  // [n_nodes][6]
+    const float* gbox;  // [n_groups][6]
+    long long n_groups;
+    int dims;
+    float theta;
+    int m;
+    long long n_src;
+    int32_t* is_proxy;         // pass 0 out (zeroed by the caller)
+    long long* seg_cnt;        // pass 0 out [n_groups]
+    const int32_t* slot_of;    // pass 1 in
+    const long long* seg_off;  // pass 1 in
+    long long* seg_start;      // pass 1 out
+    int32_t* seg_count;        // pass 1 out
+};
+constexpr int TR_STACK = 224;  // >= 31 levels x 7 pending siblings + 1
+
+// One thread per target group walks the source octree (dual_traverse's opening test,
+// _treecode.py:173-244, applied group-to-node).  Pass 0 counts segments and flags proxy
+// nodes, pass 1 writes them.  Contiguous particle ranges merge; proxies do not.
+template <int PASS>
+__global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
+    const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (g >= P.n_groups) return;
+    const CR tb = center_radius(P.gbox + g * 6, P.dims);
+    const float th2 = __fmul_rn(P.theta, P.theta);
+    int32_t stk[TR_STACK];
+    int sp = 0;
+    stk[sp++] = 0;
+    long long pend_start = 0, pend_cnt = 0, n_out = 0;
+    bool pend_direct = false;
+    const long long o = PASS ? P.seg_off[g] : 0;
+    auto flush = [&]() {
+        if (pend_cnt > 0) {
+            if (PASS) {
+                P.seg_start[o + n_out] = pend_start;
+                P.seg_count[o + n_out] = (int32_t)pend_cnt;
+            }
+            ++n_out;
+            pend_cnt = 0;
+        }
+    };
+    while (sp > 0) {
+        const int32_t v = stk[--sp];
+        const CR sb = center_radius(P.nbox + (size_t)v * 6, P.dims);
+        float d2 = 0.0f;
+        for (int a = 0; a < P.dims; ++a) {
+            const float d = __fsub_rn(tb.c[a], sb.c[a]);
+            d2 = __fadd_rn(d2, __fmul_rn(d, d));
+        }
+        const float lhs = __fadd_rn(tb.r, sb.r);
+        const bool far = __fmul_rn(lhs, lhs) < __fmul_rn(th2, d2);
+        const long long b = P.nbeg[v], e = P.nend[v];
+        if (far && e - b > P.m) {
+            flush();
+            if (PASS == 0) P.is_proxy[v] = 1;
+            else pend_start = P.n_src + (long long)P.slot_of[v] * P.m;
+            pend_cnt = P.m;
+            pend_direct = false;
+            flush();
+        } else if (far || P.nchild[v] == 0) {
+            if (pend_cnt > 0 && pend_direct && pend_start + pend_cnt == b &&
+                pend_cnt + (e - b) < (1LL << 30)) {
+                pend_cnt += e - b;
+            } else {
+                flush();
+                pend_start = b;
+                pend_cnt = e - b;
+                pend_direct = true;
+            }
+        } else {
+            const int nc = P.nchild[v];
+            if (sp + nc > TR_STACK) continue;  // unreachable for <= 31 levels
+            for (int c = nc - 1; c >= 0; --c) stk[sp++] = P.fchild[v] + c;
+        }
+    }
+    flush();
+    if (PASS == 0) P.seg_cnt[g] = n_out;
+}
+
+constexpr long long P2M_UNIT = 4096;  // particles per P2M unit (tree_host.cpp P2M_UNIT)
+
+// Proxy slots in node order: slot box (degenerate axes inflated like the host planner)
+// and the number of P2M units of each slot.
+__global__ void slots_kernel(const long long* __restrict__ nbeg, const long long* __restrict__ nend,
+                             const float* __restrict__ nbox, const int32_t* __restrict__ is_proxy,
+                             const int32_t* __restrict__ slot_of, long long n_nodes, int dims,
+                             int32_t* __restrict__ slot_node, float* __restrict__ slot_box,
+                             long long* __restrict__ units_per_slot) {
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n_nodes || !is_proxy[v]) return;
+    const int s = slot_of[v];
+    slot_node[s] = (int32_t)v;
+    const CR b = center_radius(nbox + (size_t)v * 6, dims);
+    float hmax = 0.0f;
+    for (int a = 0; a < dims; ++a) hmax = fmaxf(hmax, b.h[a]);
+    for (int a = 0; a < 3; ++a) {
+        slot_box[(size_t)s * 6 + a] = b.c[a];
+        slot_box[(size_t)s * 6 + 3 + a] =
+            a < dims ? fmaxf(b.h[a], __fadd_rn(__fmul_rn(1e-6f, hmax), 1e-30f)) : 1.0f;
+    }
+    units_per_slot[s] = (nend[v] - nbeg[v] + P2M_UNIT - 1) / P2M_UNIT;
+}
+
+__global__ void units_kernel(const long long* __restrict__ nbeg, const long long* __restrict__ nend,
+                             const int32_t* __restrict__ slot_node,
+                             const long long* __restrict__ slot_unit_off, long long n_slots,
+                             int32_t* __restrict__ unit_slot, long long* __restrict__ unit_begin,
+                             long long* __restrict__ unit_end) {
+    const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (s >= n_slots) return;
+    const int32_t v = slot_node[s];
+    long long u = slot_unit_off[s];
+    for (long long lo = nbeg[v]; lo < nend[v]; lo += P2M_UNIT, ++u) {
+        unit_slot[u] = (int32_t)s;
+        unit_begin[u] = lo;
+        unit_end[u] = min(nend[v], lo + P2M_UNIT);
+    }
+}
+
+__global__ void totals_kernel(const long long* __restrict__ seg_off, long long n_groups,
+                              const int32_t* __restrict__ slot_of,
+                              const int32_t* __restrict__ is_proxy,
+                              const long long* __restrict__ slot_unit_off, long long n_nodes,
+                              long long* __restrict__ totals) {
+    totals[0] = seg_off[n_groups];
+    totals[1] = (long long)slot_of[n_nodes - 1] + is_proxy[n_nodes - 1];
+    totals[2] = slot_unit_off[n_nodes];  // units_per_slot is zero past the last slot
+}
+
+// ---------------------------------------------------------------- evaluation
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float2 bcast(float v) { return make_float2(v, v); }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+struct EvalParams {
+    const float4* tgt;       // sorted targets
+    const int32_t* tgt_perm; // sorted -> original target index
+    const long long* grp_begin;  // target group g = sorted targets [begin, end), <= TR_GROUP
+    const long long* grp_end;
+    const float4* src;       // [sorted sources | proxies], {x, y, z, w}
+    const long long* seg_off;   // [n_groups + 1]
+    const long long* seg_start; // record offset into src
+    const int32_t* seg_count;
+    float eps2;
+    double* val;
+    double* grad;
+};
+
+// Cursor over the concatenated segment list of one group (uniform across the CTA).
+struct SegCursor {
+    long long s, s_end;
+    int off;
+};
+
+__device__ __forceinline__ int fill_batch(float4* buf, SegCursor& c, const EvalParams& P) {
+    int filled = 0;
+    while (filled < TR_BATCH && c.s < c.s_end) {
+        const int cnt = P.seg_count[c.s];
+        const int take = min(TR_BATCH - filled, cnt - c.off);
+        const float4* g = P.src + P.seg_start[c.s] + c.off;
+        for (int i = threadIdx.x; i < take; i += TR_THREADS) cp_async16(buf + filled + i, g + i);
+        filled += take;
+        c.off += take;
+        if (c.off == cnt) {
+            ++c.s;
+            c.off = 0;
+        }
+    }
+    cp_async_commit();
+    return filled;
+}
+
+template <int D, bool G>
+__device__ __forceinline__ void eval_batch(const float4* __restrict__ buf, int cnt, float2 X,
+                                           float2 Y, float2 Z, float2 e2, float2& av,
+                                           float2& ax, float2& ay, float2& az) {
+#pragma unroll 4
+    for (int j = 0; j < cnt; ++j) {
+        const float4 s = buf[j];
+        const float2 dx = __fadd2_rn(X, bcast(-s.x));
+        const float2 dy = __fadd2_rn(Y, bcast(-s.y));
+        float2 r2 = __ffma2_rn(dx, dx, e2);
+        r2 = __ffma2_rn(dy, dy, r2);
+        float2 dz;
+        if (D == 3) {
+            dz = __fadd2_rn(Z, bcast(-s.z));
+            r2 = __ffma2_rn(dz, dz, r2);
+        }
+        float2 inv;
+        inv.x = rsqrt_approx(r2.x);
+        inv.y = rsqrt_approx(r2.y);
+        if (G) {
+            inv.x = r2.x > 0.0f ? inv.x : 0.0f;
+            inv.y = r2.y > 0.0f ? inv.y : 0.0f;
+        }
+        const float2 wi = __fmul2_rn(inv, bcast(s.w));
+        av = __ffma2_rn(r2, wi, av);  // w h = w r2 / h
+        ax = __ffma2_rn(dx, wi, ax);
+        ay = __ffma2_rn(dy, wi, ay);
+        if (D == 3) az = __ffma2_rn(dz, wi, az);
+    }
+}
+
+template <int D, bool G>
+__global__ void __launch_bounds__(TR_THREADS, 4) tree_eval_kernel(const EvalParams P) {
+    __shared__ __align__(16) float4 buf[2][TR_BATCH];
+    const int tid = threadIdx.x;
+    const long long g = blockIdx.x;
+    const long long gb = P.grp_begin[g], ge = P.grp_end[g];
+    const long long i0 = gb + tid, i1 = i0 + TR_THREADS;
+    const float4 a = P.tgt[min(i0, ge - 1)];
+    const float4 b = P.tgt[min(i1, ge - 1)];
+    const float2 X = make_float2(a.x, b.x), Y = make_float2(a.y, b.y),
+                 Z = make_float2(a.z, b.z);
+    const float2 e2 = bcast(P.eps2);
+    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+
+    SegCursor c{P.seg_off[g], P.seg_off[g + 1], 0};
+    int cnt = fill_batch(buf[0], c, P);
+    int stage = 0;
+    while (cnt > 0) {
+        const int next = fill_batch(buf[stage ^ 1], c, P);
+        cp_async_wait<1>();
+        __syncthreads();
+        float2 av = bcast(0.f), ax = bcast(0.f), ay = bcast(0.f), az = bcast(0.f);
+        eval_batch<D, G>(buf[stage], cnt, X, Y, Z, e2, av, ax, ay, az);
+        acc[0][0] += av.x, acc[1][0] += av.y;
+        acc[0][1] += ax.x, acc[1][1] += ax.y;
+        acc[0][2] += ay.x, acc[1][2] += ay.y;
+        if (D == 3) acc[0][3] += az.x, acc[1][3] += az.y;
+        __syncthreads();
+        cnt = next;
+        stage ^= 1;
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const long long i = t == 0 ? i0 : i1;
+        if (i < ge) {
+            const long long o = P.tgt_perm[i];
+            if (P.val) P.val[o] = acc[t][0];
+            if (P.grad) {
+                P.grad[o * D] = acc[t][1];
+                P.grad[o * D + 1] = acc[t][2];
+                if (D == 3) P.grad[o * D + 2] = acc[t][3];
+            }
+        }
+    }
+}
+
+static ChebTable cheb_table(int q) {
+    ChebTable T{};
+    for (int i = 0; i < q; ++i)
+        T.t[i] = (float)cos((2.0 * i + 1.0) * 3.14159265358979323846 / (2.0 * q));
+    for (int k = 0; k < q; ++k) {
+        double den = 1.0;
+        const double tk = cos((2.0 * k + 1.0) * 3.14159265358979323846 / (2.0 * q));
+        for (int i = 0; i < q; ++i)
+            if (i != k) den *= tk - cos((2.0 * i + 1.0) * 3.14159265358979323846 / (2.0 * q));
+        T.inv_den[k] = (float)(1.0 / den);
+    }
+    return T;
+}
+
+}  // namespace spk
+
+using namespace spk;
+
+extern "C" {
+
+int spk_tree_keys(const void* pos, int64_t n, int dims, uint64_t* keys, int32_t* idx,
+                  spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(n >= 0 && n < (1LL << 31), SPK_ERR_ARG, "tree: %lld points out of range",
+                (long long)n);
+    if (n == 0) return SPK_OK;
+    keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const float4*>(pos), n, dims, keys, idx);
+    SPK_CHECK_LAUNCH("spk_tree_keys");
+    return SPK_OK;
+}
+
+size_t spk_tree_sort_workspace_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr,
+                                    (uint64_t*)nullptr, (const int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)n, 0, 64);
+    return bytes + 256;
+}
+
+int spk_tree_sort(const uint64_t* keys_in, const int32_t* idx_in, uint64_t* keys_out,
+                  int32_t* idx_out, int64_t n, int dims, void* ws, size_t ws_bytes,
+                  spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    if (n == 0) return SPK_OK;
+    const int end_bit = dims == 3 ? 63 : 62;
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, keys_in, keys_out, idx_in, idx_out, (int)n,
+                                    0, end_bit, (cudaStream_t)stream);
+    SPK_REQUIRE(ws_bytes >= need, SPK_ERR_WORKSPACE, "tree sort: workspace %zu < %zu bytes",
+                ws_bytes, need);
+    const cudaError_t e = cub::DeviceRadixSort::SortPairs(
+        ws, need, keys_in, keys_out, idx_in, idx_out, (int)n, 0, end_bit, (cudaStream_t)stream);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree sort: %s", cudaGetErrorString(e));
+    return SPK_OK;
+}
+
+int spk_tree_gather(const void* pos, const int32_t* perm, int64_t n, const float* weights,
+                    void* out, spk_stream_t stream) {
+    if (n == 0) return SPK_OK;
+    gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const float4*>(pos), perm, n, weights, static_cast<float4*>(out));
+    SPK_CHECK_LAUNCH("spk_tree_gather");
+    return SPK_OK;
+}
+
+int spk_tree_boxes(const void* rec, int64_t n_ranges, const int64_t* begin,
+                   const int64_t* end, int dims, float* box, spk_stream_t stream) {
+    if (n_ranges == 0) return SPK_OK;
+    boxes_kernel<<<(unsigned)n_ranges, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const float4*>(rec), reinterpret_cast<const long long*>(begin),
+        reinterpret_cast<const long long*>(end), dims, box, nullptr);
+    SPK_CHECK_LAUNCH("spk_tree_boxes");
+    return SPK_OK;
+}
+
+size_t spk_tree_p2m_workspace_bytes(int64_t n_units, int order, int dims) {
+    const int64_t m = dims == 3 ? (int64_t)order * order * order : (int64_t)order * order;
+    return (size_t)(n_units * m) * sizeof(double);
+}
+
+int spk_tree_p2m(const void* rec, int64_t n_units, const int32_t* unit_slot,
+                 const int64_t* unit_begin, const int64_t* unit_end, int64_t n_slots,
+                 const int64_t* slot_unit_off, const float* slot_box, int order, int dims,
+                 void* proxies, void* ws, size_t ws_bytes, spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(order >= 2 && order <= P2M_MAX_ORDER, SPK_ERR_ARG,
+                "interpolation order must be in [2, %d], got %d", P2M_MAX_ORDER, order);
+    if (n_slots == 0) return SPK_OK;
+    SPK_REQUIRE(ws_bytes >= spk_tree_p2m_workspace_bytes(n_units, order, dims),
+                SPK_ERR_WORKSPACE, "tree p2m: workspace too small");
+    const ChebTable T = cheb_table(order);
+    double* part = static_cast<double*>(ws);
+    cudaStream_t s = (cudaStream_t)stream;
+    p2m_kernel<<<(unsigned)n_units, P2M_THREADS, 0, s>>>(
+        static_cast<const float4*>(rec), unit_slot, reinterpret_cast<const long long*>(unit_begin),
+        reinterpret_cast<const long long*>(unit_end), slot_box, order, dims, T, part);
+    SPK_CHECK_LAUNCH("spk_tree_p2m");
+    p2m_final_kernel<<<(unsigned)n_slots, 128, 0, s>>>(
+        part, reinterpret_cast<const long long*>(slot_unit_off), slot_box, order, dims, T,
+        static_cast<float4*>(proxies));
+    SPK_CHECK_LAUNCH("spk_tree_p2m(final)");
+    return SPK_OK;
+}
+
+int spk_tree_eval(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_groups,
+                  const int64_t* grp_begin, const int64_t* grp_end, const void* src,
+                  const int64_t* seg_off, const int64_t* seg_start, const int32_t* seg_count,
+                  int dims, float eps2, double* val, double* grad, spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    if (n_groups == 0) return SPK_OK;
+    EvalParams P;
+    P.tgt = static_cast<const float4*>(tgt_sorted);
+    P.tgt_perm = tgt_perm;
+    P.grp_begin = reinterpret_cast<const long long*>(grp_begin);
+    P.grp_end = reinterpret_cast<const long long*>(grp_end);
+    P.src = static_cast<const float4*>(src);
+    P.seg_off = reinterpret_cast<const long long*>(seg_off);
+    P.seg_start = reinterpret_cast<const long long*>(seg_start);
+    P.seg_count = seg_count;
+    P.eps2 = eps2;
+    P.val = val;
+    P.grad = grad;
+    const bool guard = !(eps2 >= FLT_MIN);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dims == 3) {
+        if (guard) tree_eval_kernel<3, true><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
+        else tree_eval_kernel<3, false><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
+    } else {
+        if (guard) tree_eval_kernel<2, true><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
+        else tree_eval_kernel<2, false><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
+    }
+    SPK_CHECK_LAUNCH("spk_tree_eval");
+    return SPK_OK;
+}
+
+int spk_tree_node_boxes(const void* rec, int64_t n_nodes, const int32_t* first_child,
+                        const int32_t* n_child, int64_t n_leaves, const int32_t* leaf_node,
+                        const int64_t* leaf_begin, const int64_t* leaf_end, int64_t n_levels,
+                        const int64_t* level_off, int dims, float* node_box,
+                        spk_stream_t stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_nodes == 0) return SPK_OK;
+    boxes_kernel<<<(unsigned)n_leaves, 256, 0, s>>>(
+        static_cast<const float4*>(rec), reinterpret_cast<const long long*>(leaf_begin),
+        reinterpret_cast<const long long*>(leaf_end), dims, node_box, leaf_node);
+    SPK_CHECK_LAUNCH("spk_tree_node_boxes(leaves)");
+    for (int64_t l = n_levels - 1; l >= 0; --l) {  // host array of level offsets
+        const long long b = level_off[l], e = level_off[l + 1];
+        if (e <= b) continue;
+        level_boxes_kernel<<<(unsigned)((e - b + 127) / 128), 128, 0, s>>>(first_child, n_child,
+                                                                          b, e, node_box);
+    }
+    SPK_CHECK_LAUNCH("spk_tree_node_boxes(levels)");
+    return SPK_OK;
+}
+
+size_t spk_tree_plan_workspace_bytes(int64_t n_nodes, int64_t n_groups) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (int)n_nodes);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const long long*)nullptr, (long long*)nullptr,
+                                  (int)(n_groups + 1));
+    cub::DeviceScan::ExclusiveSum(nullptr, c, (const long long*)nullptr, (long long*)nullptr,
+                                  (int)(n_nodes + 1));
+    const size_t cub_bytes = std::max(a, std::max(b, c));
+    // is_proxy [n_nodes] i32, seg_cnt [n_groups + 1] i64, units_per_slot [n_nodes + 1] i64
+    return ((cub_bytes + 255) & ~(size_t)255) + (size_t)n_nodes * 4 + 256 +
+           (size_t)(n_groups + 1) * 8 + 256 + (size_t)(n_nodes + 1) * 8 + 256;
+}
+
+static void plan_ws(void* ws, int64_t n_nodes, int64_t n_groups, size_t cub_bytes,
+                    void** cub_tmp, int32_t** is_proxy, long long** seg_cnt,
+                    long long** units_per_slot) {
+    char* p = static_cast<char*>(ws);
+    *cub_tmp = p;
+    p += (cub_bytes + 255) & ~(size_t)255;
+    *is_proxy = reinterpret_cast<int32_t*>(p);
+    p += ((size_t)n_nodes * 4 + 255) & ~(size_t)255;
+    *seg_cnt = reinterpret_cast<long long*>(p);
+    p += ((size_t)(n_groups + 1) * 8 + 255) & ~(size_t)255;
+    *units_per_slot = reinterpret_cast<long long*>(p);
+}
+
+int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
+                        const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
+                        const float* node_box, const float* group_box, int64_t n_groups,
+                        double theta, int order, int dims, int64_t n_src, int32_t* slot_of,
+                        int32_t* slot_node, float* slot_box, int64_t* slot_unit_off,
+                        int64_t* seg_off, int64_t* totals, void* ws, size_t ws_bytes,
+                        spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(n_nodes > 0 && n_groups > 0, SPK_ERR_ARG, "tree plan: empty tree or groups");
+    SPK_REQUIRE(ws_bytes >= spk_tree_plan_workspace_bytes(n_nodes, n_groups), SPK_ERR_WORKSPACE,
+                "tree plan: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t cub_bytes = ws_bytes - ((size_t)n_nodes * 4 + 256 + (size_t)(n_groups + 1) * 8 + 256 +
+                                   (size_t)(n_nodes + 1) * 8 + 256);
+    cub_bytes &= ~(size_t)255;
+    void* tmp;
+    int32_t* is_proxy;
+    long long* seg_cnt;
+    long long* ups;
+    plan_ws(ws, n_nodes, n_groups, cub_bytes, &tmp, &is_proxy, &seg_cnt, &ups);
+    cudaMemsetAsync(is_proxy, 0, (size_t)n_nodes * 4, s);
+    cudaMemsetAsync(seg_cnt, 0, (size_t)(n_groups + 1) * 8, s);
+    cudaMemsetAsync(ups, 0, (size_t)(n_nodes + 1) * 8, s);
+    const int m = dims == 3 ? order * order * order : order * order;
+    TravParams P{};
+    P.nbeg = reinterpret_cast<const long long*>(node_begin);
+    P.nend = reinterpret_cast<const long long*>(node_end);
+    P.fchild = first_child;
+    P.nchild = n_child;
+    P.nbox = node_box;
+    P.gbox = group_box;
+    P.n_groups = n_groups;
+    P.dims = dims;
+    P.theta = (float)theta;
+    P.m = m;
+    P.n_src = n_src;
+    P.is_proxy = is_proxy;
+    P.seg_cnt = seg_cnt;
+    traverse_kernel<0><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
+    SPK_CHECK_LAUNCH("spk_tree_plan_count(traverse)");
+    size_t t = cub_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, t, is_proxy, slot_of, (int)n_nodes, s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree plan scan: %s", cudaGetErrorString(e));
+    t = cub_bytes;
+    e = cub::DeviceScan::ExclusiveSum(tmp, t, seg_cnt, reinterpret_cast<long long*>(seg_off),
+                                      (int)(n_groups + 1), s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree plan scan: %s", cudaGetErrorString(e));
+    slots_kernel<<<(unsigned)((n_nodes + 127) / 128), 128, 0, s>>>(
+        P.nbeg, P.nend, node_box, is_proxy, slot_of, n_nodes, dims, slot_node, slot_box, ups);
+    SPK_CHECK_LAUNCH("spk_tree_plan_count(slots)");
+    t = cub_bytes;
+    e = cub::DeviceScan::ExclusiveSum(tmp, t, ups, reinterpret_cast<long long*>(slot_unit_off),
+                                      (int)(n_nodes + 1), s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree plan scan: %s", cudaGetErrorString(e));
+    totals_kernel<<<1, 1, 0, s>>>(reinterpret_cast<const long long*>(seg_off), n_groups, slot_of,
+                                  is_proxy, reinterpret_cast<const long long*>(slot_unit_off),
+                                  n_nodes, reinterpret_cast<long long*>(totals));
+    SPK_CHECK_LAUNCH("spk_tree_plan_count(totals)");
+    return SPK_OK;
+}
+
+int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
+                        const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
+                        const float* node_box, const float* group_box, int64_t n_groups,
+                        double theta, int order, int dims, int64_t n_src,
+                        const int32_t* slot_of, const int32_t* slot_node,
+                        const int64_t* slot_unit_off, int64_t n_slots, const int64_t* seg_off,
+                        int64_t* seg_start, int32_t* seg_count, int32_t* unit_slot,
+                        int64_t* unit_begin, int64_t* unit_end, spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    cudaStream_t s = (cudaStream_t)stream;
+    TravParams P{};
+    P.nbeg = reinterpret_cast<const long long*>(node_begin);
+    P.nend = reinterpret_cast<const long long*>(node_end);
+    P.fchild = first_child;
+    P.nchild = n_child;
+    P.nbox = node_box;
+    P.gbox = group_box;
+    P.n_groups = n_groups;
+    P.dims = dims;
+    P.theta = (float)theta;
+    P.m = dims == 3 ? order * order * order : order * order;
+    P.n_src = n_src;
+    P.slot_of = slot_of;
+    P.seg_off = reinterpret_cast<const long long*>(seg_off);
+    P.seg_start = reinterpret_cast<long long*>(seg_start);
+    P.seg_count = seg_count;
+    traverse_kernel<1><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
+    SPK_CHECK_LAUNCH("spk_tree_plan_write(traverse)");
+    if (n_slots > 0) {
+        units_kernel<<<(unsigned)((n_slots + 127) / 128), 128, 0, s>>>(
+            P.nbeg, P.nend, slot_node, reinterpret_cast<const long long*>(slot_unit_off), n_slots,
+            unit_slot, reinterpret_cast<long long*>(unit_begin),
+            reinterpret_cast<long long*>(unit_end));
+        SPK_CHECK_LAUNCH("spk_tree_plan_write(units)");
+    }
+    return SPK_OK;
+}
+
+int spk_tree_group_size(void) { return TR_GROUP; }
+
+}  // extern "C"

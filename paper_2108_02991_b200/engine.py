@@ -23,9 +23,9 @@ import torch
 import torch.distributed as dist
 
 from . import _device, _native
-from .attraction import field_eval_device
+from .attraction import field_eval_device, grid_sums_device
 from .projection import project_device, residuals_device
-from .repulsion import direct_sums_device
+from .repulsion import direct_sums_device, tree_sums_checked
 
 
 class CudaOps:
@@ -48,6 +48,14 @@ class CudaOps:
         n_t = tgt4.shape[0]
         d = cfg.dims
         eps2_rep = cfg.repulsion.kernel_eps ** 2
+        if cfg.repulsion.backend == "tree":
+            # treecode repulsion (tree.py); attraction by the lattice kernel or the field
+            if cfg.grad_mode == "exact":
+                va, ga = grid_sums_device(tgt4, fld, fld.kernel_eps ** 2)
+            else:
+                va, ga, _ = field_eval_device(coords_local.reshape(-1, d), fld, cfg.grad_mode)
+            vr, gr = tree_sums_checked(tgt4, src4, d, cfg.repulsion)
+            return va, ga, vr, gr
         vr = self.empty(n_t)
         gr = self.empty((n_t, d))
         if cfg.grad_mode == "exact":

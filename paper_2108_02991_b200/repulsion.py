@@ -6,19 +6,24 @@ Cost (1/(2p^2)) sum_i sum_j sqrt(|x_i - x_j|^2 + eps^2) and gradient
 ``spk_direct_sums`` (csrc/nbody.cu); the normalisation is done here with numpy exactly
 like the reference, so outputs are float64 numpy arrays owned by the caller.
 
-``backend="tree"`` is accepted for drop-in configs; it is served by the same exact
-kernel, which meets any ``tree_precision`` the fp32 kernel resolves (>= ~1e-6 relative),
-so the reference's escalation / fallback warnings never fire.
+``backend="tree"`` runs the GPU treecode (tree.py, csrc/tree.cu) with the reference's
+contract and control flow (repulsion.py:90-200): automatic (order, theta) from
+``tree_precision``; with an explicit ``interp_order`` the result is probed against exact
+sums on 64 strided targets and the order escalated (warning) or the evaluation dropped
+to direct summation; problems of at most ``leaf_size`` particles are evaluated directly,
+and so are problems below ``tree.DIRECT_BELOW`` sources, where the exact B200 kernel is
+faster than building a tree (the precision contract holds a fortiori).
 """
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
-from . import _device, _native
+from . import _device, _native, tree
 from .core import SamplingPattern
 
 MAX_INTERP_ORDER = 8
@@ -88,9 +93,71 @@ def eval_repulsion_direct(k, eps: float = 1e-3) -> tuple[float, np.ndarray]:
     return cost, grad_h
 
 
+def auto_tree_params(precision: float) -> tuple[int, float]:
+    """Interpolation order and opening threshold for a precision (repulsion.py:90-96);
+    (MAX_INTERP_ORDER, 0.0) -- i.e. exact sums -- below the fp32 floor."""
+    params = tree.auto_params(precision)
+    return params if params is not None else (MAX_INTERP_ORDER, 0.0)
+
+
+def _probe_error(tgt4, src4, dims, eps2, val, grad) -> tuple[float, float]:
+    """Relative error vs exact K1 on 64 strided targets (repulsion.py:151-162)."""
+    n = tgt4.shape[0]
+    stride = max(1, n // 64)
+    idx = torch.arange(0, n, stride, device=tgt4.device)[:64]
+    v_ref, g_ref = direct_sums_device(tgt4[idx].contiguous(), src4, dims, eps2)
+    v_ref, g_ref = _device.d2h(v_ref), _device.d2h(g_ref)
+    v, g = _device.d2h(val[idx]), _device.d2h(grad[idx])
+    err_val = abs(v.sum() - v_ref.sum()) / max(abs(v_ref.sum()), 1e-300)
+    err_grad = np.linalg.norm(g - g_ref) / max(np.linalg.norm(g_ref), 1e-300)
+    return float(err_val), float(err_grad)
+
+
+def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig):
+    """Device raw sums for backend="tree" with the reference's order selection, probe,
+    escalation and direct fallback (repulsion.py:165-200)."""
+    eps2 = cfg.kernel_eps * cfg.kernel_eps
+    params = tree.auto_params(cfg.tree_precision)
+    n_src = src4.shape[0]
+    if n_src <= max(cfg.leaf_size, tree.DIRECT_BELOW) or params is None:
+        # small problems (exact kernel is faster) and precisions below the fp32 floor
+        return direct_sums_device(tgt4, src4, dims, eps2)
+    auto_order, theta = params
+    order = cfg.interp_order if cfg.interp_order is not None else auto_order
+    val, grad = tree.tree_sums_device(tgt4, src4, dims, eps2, order, theta)
+    if cfg.interp_order is not None:
+        err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
+        while max(err_val, err_grad) > cfg.tree_precision and order < MAX_INTERP_ORDER:
+            order += 1
+            warnings.warn(
+                f"tree backend at interp_order={order - 1} reached relative error "
+                f"{max(err_val, err_grad):.2e} > {cfg.tree_precision:.2e}; "
+                f"escalating to order {order}")
+            val, grad = tree.tree_sums_device(tgt4, src4, dims, eps2, order, theta)
+            err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
+        if max(err_val, err_grad) > cfg.tree_precision:
+            warnings.warn(
+                f"tree backend cannot reach precision {cfg.tree_precision:.2e} at "
+                f"interp_order {MAX_INTERP_ORDER}; falling back to direct summation")
+            return direct_sums_device(tgt4, src4, dims, eps2)
+    return val, grad
+
+
 def eval_repulsion_tree(k, cfg: RepulsionConfig) -> tuple[float, np.ndarray]:
-    """Tree-backend entry point (repulsion.py:165-200), served exactly by K1."""
-    return eval_repulsion_direct(k, cfg.kernel_eps)
+    """Repulsion cost and gradient through the GPU treecode (repulsion.py:165-200):
+    within ``cfg.tree_precision`` relative error of :func:`eval_repulsion_direct` on the
+    cost and the gradient l2 norm; at most ``leaf_size`` particles -> direct (bitwise)."""
+    pts = _points(k)
+    p = pts.shape[0]
+    if p <= cfg.leaf_size:
+        return eval_repulsion_direct(pts, cfg.kernel_eps)
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    val, grad = tree_sums_checked(pos4, pos4, pts.shape[1], cfg)
+    val_h = _device.d2h(val)
+    grad_h = _device.d2h(grad)
+    cost = float(val_h.sum() / (2.0 * p * p))
+    grad_h /= p * p
+    return cost, grad_h
 
 
 def eval_repulsion(k, cfg: RepulsionConfig) -> tuple[float, np.ndarray]:

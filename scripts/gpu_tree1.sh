@@ -1,0 +1,9 @@
+#!/bin/bash
+# build + treecode tests + calibration sweep
+set -x
+mkdir -p gpurun_out
+python -c "import sys; sys.path.insert(0,'.'); from paper_2108_02991_b200 import _build; _build.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+make -C oracle > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_tree.py -x -q 2>&1 | tail -30
+timeout 1500 python scripts/tree_calibrate.py --clouds c1,s3,c2,u3 --orders 3,4,5,6,7 --thetas 0.3,0.4,0.5,0.6 --out gpurun_out/tree_cal.jsonl > gpurun_out/tree_cal.log 2>&1
+tail -5 gpurun_out/tree_cal.log

@@ -1,0 +1,191 @@
+"""GPU treecode (backend="tree") vs exact sums: the reference's precision contract
+(repulsion.py:165-171: relative error of the cost and of the gradient l2 norm <=
+tree_precision), the small-problem direct rule, the interp_order probe/escalation path,
+determinism and sharded targets."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spk():
+    import paper_2108_02991_b200 as m
+
+    return m
+
+
+def _errors(spk, pts, cfg):
+    cost_t, grad_t = spk.eval_repulsion_tree(pts, cfg)
+    cost_d, grad_d = spk.eval_repulsion_direct(pts, cfg.kernel_eps)
+    return (abs(cost_t - cost_d) / abs(cost_d),
+            np.linalg.norm(grad_t - grad_d) / np.linalg.norm(grad_d))
+
+
+def test_theta_zero_limit_matches_direct(spk):
+    """theta -> 0 opens every node: the treecode degenerates to exact near sums."""
+    from paper_2108_02991_b200 import _device, tree
+    from paper_2108_02991_b200.repulsion import direct_sums_device
+
+    rng = np.random.default_rng(3)
+    for d in (2, 3):
+        pts = rng.uniform(-1, 1, (5000, d))
+        pos4 = _device.pack_positions(_device.h2d(pts))
+        vt, gt = tree.tree_sums_device(pos4, pos4, d, 1e-6, 4, 1e-6)
+        vd, gd = direct_sums_device(pos4, pos4, d, 1e-6)
+        vt, gt, vd, gd = (_device.d2h(x) for x in (vt, gt, vd, gd))
+        assert np.abs(vt - vd).max() <= 1e-5 * np.abs(vd).max()
+        assert np.linalg.norm(gt - gd) <= 1e-5 * np.linalg.norm(gd)
+
+
+def test_oracle_subset_small_cloud(spk):
+    """Treecode vs the fp64 CPU oracle on a target subset (mixed near/far lists)."""
+    from paper_2108_02991_b200 import _device, tree
+
+    pts = spk.perturb(spk.init_radial(64, 1024, 3), 0.25, 0).points()
+    p = pts.shape[0]
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    st = {}
+    vt, gt = tree.tree_sums_device(pos4, pos4, 3, 1e-6, 6, 0.5, stats=st)
+    assert st["slots"] > 0 and st["pairs"] < p * p
+    idx = np.arange(0, p, 61, dtype=np.int64)
+    vo, go = orc.direct_sums_subset(pts, idx, 1e-6)
+    vt = _device.d2h(vt)[idx]
+    gt = _device.d2h(gt)[idx]
+    assert abs(vt.sum() - vo.sum()) / abs(vo.sum()) < 1e-5
+    assert np.linalg.norm(gt - go) / np.linalg.norm(go) < 1e-5
+
+
+@pytest.mark.parametrize("precision", [1e-2, 1e-3, 1e-4, 1e-5, 1e-6])
+def test_precision_contract_auto_params(spk, precision):
+    """The calibrated (order, theta) of every precision row meets it on SPARKLING-shaped
+    and uniform clouds (cost and gradient l2, repulsion.py:165-171)."""
+    from paper_2108_02991_b200 import _device, tree
+    from paper_2108_02991_b200.repulsion import direct_sums_device
+
+    order, theta = tree.auto_params(precision)
+    clouds = [spk.perturb(spk.init_radial(64, 512, 2), 0.25, 0).points(),
+              spk.perturb(spk.init_radial(256, 512, 3), 0.25, 1).points(),
+              np.random.default_rng(5).uniform(-1, 1, (60000, 3))]
+    for pts in clouds:
+        d = pts.shape[1]
+        pos4 = _device.pack_positions(_device.h2d(pts))
+        vt, gt = tree.tree_sums_device(pos4, pos4, d, 1e-6, order, theta)
+        vd, gd = direct_sums_device(pos4, pos4, d, 1e-6)
+        vt, gt, vd, gd = (_device.d2h(x) for x in (vt, gt, vd, gd))
+        e_cost = abs(vt.sum() - vd.sum()) / abs(vd.sum())
+        e_grad = np.linalg.norm(gt - gd) / np.linalg.norm(gd)
+        assert e_cost <= precision and e_grad <= precision, (pts.shape, e_cost, e_grad)
+
+
+@pytest.mark.parametrize("precision", [1e-3, 1e-4])
+def test_eval_repulsion_tree_c2_size(spk, precision):
+    """Public API at the C2 size (p = 2^20, where the tree is used) vs direct."""
+    pts = spk.perturb(spk.init_radial(1024, 1024, 3), 0.25, 0).points()
+    cfg = spk.RepulsionConfig(backend="tree", tree_precision=precision)
+    e_cost, e_grad = _errors(spk, pts, cfg)
+    assert e_cost <= precision and e_grad <= precision, (e_cost, e_grad)
+
+
+def test_small_problem_is_direct_bitwise(spk):
+    pts = np.random.default_rng(1).uniform(-1, 1, (150, 3))
+    cfg = spk.RepulsionConfig(backend="tree", leaf_size=192)
+    c_t, g_t = spk.eval_repulsion_tree(pts, cfg)
+    c_d, g_d = spk.eval_repulsion_direct(pts, cfg.kernel_eps)
+    assert c_t == c_d and np.array_equal(g_t, g_d)
+
+
+def test_explicit_order_probe_escalates(spk):
+    """interp_order set: probe against exact sums, escalate with a warning (reference
+    repulsion.py:183-199)."""
+    pts = spk.perturb(spk.init_radial(400, 512, 3), 0.25, 0).points()
+    cfg = spk.RepulsionConfig(backend="tree", tree_precision=1e-5, interp_order=2)
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        cost, grad = spk.eval_repulsion_tree(pts, cfg)
+    assert any("escalating" in str(x.message) or "falling back" in str(x.message) for x in w)
+    c_d, g_d = spk.eval_repulsion_direct(pts, cfg.kernel_eps)
+    assert abs(cost - c_d) / c_d <= 1e-5
+
+
+def test_deterministic_and_sharded_targets(spk):
+    from paper_2108_02991_b200 import _device, tree
+
+    pts = spk.perturb(spk.init_radial(144, 512, 3), 0.25, 2).points()
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    v1, g1 = tree.tree_sums_device(pos4, pos4, 3, 1e-6, 5, 0.4)
+    v2, g2 = tree.tree_sums_device(pos4, pos4, 3, 1e-6, 5, 0.4)
+    assert np.array_equal(_device.d2h(v1), _device.d2h(v2))
+    assert np.array_equal(_device.d2h(g1), _device.d2h(g2))
+    # a rank's contiguous shard of targets against all sources
+    lo, hi = 20000, 45000
+    vs, gs = tree.tree_sums_device(pos4[lo:hi], pos4, 3, 1e-6, 5, 0.4)
+    vf = _device.d2h(v1)[lo:hi]
+    gf = _device.d2h(g1)[lo:hi]
+    assert abs(_device.d2h(vs).sum() - vf.sum()) / abs(vf.sum()) < 1e-5
+    assert np.linalg.norm(_device.d2h(gs) - gf) / np.linalg.norm(gf) < 1e-4
+
+
+def test_optimize_with_tree_backend(spk):
+    """optimize() with backend="tree" stays within the precision of the direct run."""
+    hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                          dwell_dt=2e-6, fov=0.192, matrix=64, dims=2)
+    base = dict(n_c=256, n_s=1024, dims=2, n_decim=0, n_git=3, n_pit=30, grid_n=32,
+                perturbation=0.25, seed=0, grad_mode="exact")
+    r_d = spk.optimize(spk.OptimizerConfig(**base), hw)
+    cfg_t = spk.OptimizerConfig(**base, repulsion=spk.RepulsionConfig(
+        backend="tree", tree_precision=1e-5))
+    r_t = spk.optimize(cfg_t, hw)
+    ct = r_t.trace.records[-1]
+    cd = r_d.trace.records[-1]
+    assert abs(ct.cost - cd.cost) / abs(cd.cost) < 1e-4
+    assert np.abs(r_t.pattern.coords - r_d.pattern.coords).max() < 1e-3
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_device_lists_match_host_planner(spk, dims):
+    """The GPU traversal (tree.cu traverse_kernel) and the serial host planner
+    (tree_host.cpp) build identical interaction lists for the same tree and boxes."""
+    from paper_2108_02991_b200 import _device, _native, tree
+
+    lib = _native.load()
+    pts = (spk.perturb(spk.init_radial(144, 512, 3), 0.25, 4).points() if dims == 3 else
+           spk.perturb(spk.init_radial(128, 512, 2), 0.25, 4).points())
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    L = {}
+    tree.tree_sums_device(pos4, pos4, dims, 1e-6, 4, 0.6, lists=L)
+    h, T = L["host_tree"]
+    try:
+        leaf_box = np.ascontiguousarray(L["node_box"][T["leaves"]])
+        lib.spk_tree_host_set_leaf_boxes(h, leaf_box.ctypes.data)
+        gbox = np.ascontiguousarray(L["group_box"])
+        counts = np.zeros(5, np.int64)
+        assert lib.spk_tree_host_plan(h, L["n_groups"], gbox.ctypes.data, 0.6, 4, L["n_src"],
+                                      counts.ctypes.data) == 0
+        n_seg, n_slots, n_units = (int(c) for c in counts[:3])
+        seg_off = np.empty(L["n_groups"] + 1, np.int64)
+        seg_start = np.empty(n_seg, np.int64)
+        seg_count = np.empty(n_seg, np.int32)
+        slot_box = np.empty((max(n_slots, 1), 6), np.float32)
+        us = np.empty(max(n_units, 1), np.int32)
+        ub = np.empty(max(n_units, 1), np.int64)
+        ue = np.empty(max(n_units, 1), np.int64)
+        suo = np.empty(n_slots + 1, np.int64)
+        lib.spk_tree_host_export_plan(h, seg_off.ctypes.data, seg_start.ctypes.data,
+                                      seg_count.ctypes.data, slot_box.ctypes.data,
+                                      us.ctypes.data, ub.ctypes.data, ue.ctypes.data,
+                                      suo.ctypes.data)
+        slot_node = np.empty(max(n_slots, 1), np.int32)
+        lib.spk_tree_host_slot_nodes(h, slot_node.ctypes.data)
+    finally:
+        lib.spk_tree_host_free(h)
+    assert n_slots > 0
+    assert np.array_equal(slot_node[:n_slots], L["slot_node"])
+    assert np.array_equal(seg_off, L["seg_off"])
+    assert np.array_equal(seg_start, L["seg_start"])
+    assert np.array_equal(seg_count, L["seg_count"])
