@@ -43,6 +43,18 @@ WORKLOADS = {
     "c1": dict(name="C1: 2D SPARKLING 64 shots x 512 samples, 257^2 density grid",
                n_c=64, n_s=512, dims=2, grid_n=(128, 128), pert=0.25,
                fov=0.192, matrix=64, dwell=2e-6),
+    "c4t": dict(name="C4 with treecodes: full 3D SPARKLING 4096 shots x 2048 samples (8.4M), "
+                     "385x385x209 density grid; repulsion backend=tree at tree_precision "
+                     "1e-3 (the reference's pkg/configs/full3d.cfg), attraction treecode "
+                     "at 1e-4 over the static lattice tree",
+                n_c=4096, n_s=2048, dims=3, grid_n=(192, 192, 104), pert=0.75,
+                fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208), dwell=2e-6, tree=True,
+                rep_prec=1e-3, att_prec=1e-4),
+    "c2t": dict(name="C2 with treecodes: 3D SPARKLING 1024 shots x 1024 samples, 129^3 "
+                     "density grid; repulsion tree 1e-3, attraction treecode 1e-4",
+                n_c=1024, n_s=1024, dims=3, grid_n=(64, 64, 64), pert=0.25,
+                fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208), dwell=2e-6, tree=True,
+                rep_prec=1e-3, att_prec=1e-4),
     "c3": dict(name="C3: stack-of-SPARKLING, 64 independent 2D problems of 64 shots x 512 "
                     "samples, 257^2 density grid (one device batch)",
                n_c=64, n_s=512, dims=2, grid_n=(128, 128), pert=0.25,
@@ -421,6 +433,101 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_tree(args):
+    """Treecode workloads (c2t, c4t): s/iteration of the full optimizer iteration with
+    RepulsionConfig(backend="tree") and the treecode attraction, through ShardedRun."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import _native, engine
+    from paper_2108_02991_b200.optimizer import _bb_step, default_eta0
+
+    hw = hardware()
+    cfg = spk.OptimizerConfig(n_c=N_C, n_s=N_S, dims=DIMS, n_pit=100, grad_mode="exact",
+                              grid_n=GRID_N, seed=0, perturbation=W["pert"],
+                              attraction_tree_precision=W["att_prec"],
+                              repulsion=spk.RepulsionConfig(backend="tree",
+                                                            tree_precision=W["rep_prec"]))
+    fld = spk.precompute_field(density())
+    pcfg = proj_config()
+    t0 = time.perf_counter()
+    fld.source_tree()
+    from paper_2108_02991_b200 import tree as _tree
+    fld.source_tree().static_proxies(_tree.auto_params(W["att_prec"])[0])
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    run = engine.ShardedRun(np.ascontiguousarray(start_pattern().coords), cfg, fld)
+    run.project(pcfg)
+    eta0 = default_eta0(run.p, EPS_REP)
+    state = {"eta": eta0, "it": 0, "have": False}
+
+    def step():
+        state["it"] += 1
+        att, rep, bad, dots = run.evaluate()
+        if bad or not np.isfinite(att - rep):
+            raise RuntimeError("non-finite during bench")
+        state["eta"] = _bb_step(state["it"], state["eta"], dots[0], dots[1], state["have"],
+                                eta0, cfg.fixed_step_iters)
+        state["have"] = True
+        run.step_project(pcfg, state["eta"])
+        run.residual_max(pcfg)
+        return att - rep
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    _native.reset_launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step()
+            e.record()
+            times.append((s, e))
+        torch.cuda.synchronize()
+    launches = _native.launch_count()
+    total_ms = sum(s.elapsed_time(e) for s, e in times)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t[0])
+    p, g, rep_pairs, att_pairs = pairs_per_step()
+    s_it = total_ms / args.steps / 1e3
+    if rank == 0:
+        line = {
+            "metric": "s/iteration", "value": s_it, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_it * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
+            "config": workload_config() | {
+                "parallelism": f"shots sharded over {world} GPU(s)",
+                "workload": W["name"], "repulsion": f"tree, tree_precision {W['rep_prec']}",
+                "attraction": f"treecode, precision {W['att_prec']}"},
+            "equivalent_direct_pairs_per_s": (rep_pairs + att_pairs) / s_it,
+            "setup_s": {"lattice_tree_and_proxies": t_setup},
+            "roofline": None,
+            "roofline_note": "treecode lists vary per iteration; the kernel roofline is "
+                             "reported on the exact C2 line",
+            "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_stack(args):
     """C3: one stacked optimize iteration of G independent problems per step (1 GPU)."""
     import torch
@@ -636,6 +743,8 @@ def main():
         run_reference(args)
     elif W.get("stack"):
         run_stack(args)
+    elif W.get("tree"):
+        run_tree(args)
     else:
         run_ours(args)
 

@@ -136,6 +136,16 @@ class KernelField:
             self._build_sources(with_nodes=True)
         return self._dev["nodes"]
 
+    def source_tree(self):
+        """The density lattice as a weighted tree.SourceTree (built once, cached)."""
+        if "tree" not in self._dev:
+            from . import tree
+
+            nodes = self.device_nodes()
+            w = self.device_sources()[:nodes.shape[0]]
+            self._dev["tree"] = tree.SourceTree(nodes, self.dims, weights=w)
+        return self._dev["tree"]
+
     def device_grids(self):
         """(potential [G] f64, force [d, G] f64) on the device."""
         if "pot" not in self._dev:
@@ -171,6 +181,25 @@ def grid_sums_device(tgt4, field: "KernelField", eps2, val=None, grad=None):
                  dims, float(eps2), val.data_ptr(), grad.data_ptr(), ws.data_ptr(), ws.numel(),
                  _device.stream())
     return val, grad
+
+
+def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg=None):
+    """Treecode approximation of :func:`grid_sums_device` (tree.py) within ``precision``
+    relative error of the cost and of the gradient l2 norm: the density lattice is a
+    static weighted source set, so its octree and the Chebyshev proxies of every node are
+    built once per field and reused every iteration; per call only the targets are
+    sorted and the interaction lists rebuilt.  ``tg``: precomputed tree.TargetGroups of
+    the same targets (shared with a treecode repulsion)."""
+    from . import tree
+
+    params = tree.auto_params(precision)
+    if params is None:
+        return grid_sums_device(tgt4, field, eps2)
+    order, theta = params
+    src = field.source_tree()
+    if tg is None:
+        tg = tree.TargetGroups(tgt4, field.dims)
+    return tree.tree_eval(tg, src, order, theta, eps2, static=True)
 
 
 def precompute_field(rho: TargetDensity, kernel_eps: float | None = None,

@@ -23,7 +23,7 @@ import torch
 import torch.distributed as dist
 
 from . import _device, _native
-from .attraction import field_eval_device, grid_sums_device
+from .attraction import field_eval_device, grid_sums_device, tree_grid_sums_device
 from .projection import project_device, residuals_device
 from .repulsion import direct_sums_device, tree_sums_checked
 
@@ -48,13 +48,22 @@ class CudaOps:
         n_t = tgt4.shape[0]
         d = cfg.dims
         eps2_rep = cfg.repulsion.kernel_eps ** 2
-        if cfg.repulsion.backend == "tree":
-            # treecode repulsion (tree.py); attraction by the lattice kernel or the field
-            if cfg.grad_mode == "exact":
+        att_tree = cfg.grad_mode == "exact" and cfg.attraction_tree_precision is not None
+        if cfg.repulsion.backend == "tree" or att_tree:
+            # treecode repulsion (tree.py) and/or treecode attraction; the targets'
+            # sort is shared when both run
+            tg = None
+            if cfg.repulsion.backend == "tree":
+                vr, gr, tg = tree_sums_checked(tgt4, src4, d, cfg.repulsion, return_groups=True)
+            else:
+                vr, gr = direct_sums_device(tgt4, src4, d, eps2_rep)
+            if att_tree:
+                va, ga = tree_grid_sums_device(tgt4, fld, fld.kernel_eps ** 2,
+                                               cfg.attraction_tree_precision, tg=tg)
+            elif cfg.grad_mode == "exact":
                 va, ga = grid_sums_device(tgt4, fld, fld.kernel_eps ** 2)
             else:
                 va, ga, _ = field_eval_device(coords_local.reshape(-1, d), fld, cfg.grad_mode)
-            vr, gr = tree_sums_checked(tgt4, src4, d, cfg.repulsion)
             return va, ga, vr, gr
         vr = self.empty(n_t)
         gr = self.empty((n_t, d))

@@ -113,18 +113,28 @@ def _probe_error(tgt4, src4, dims, eps2, val, grad) -> tuple[float, float]:
     return float(err_val), float(err_grad)
 
 
-def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig):
+def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
+                      return_groups: bool = False):
     """Device raw sums for backend="tree" with the reference's order selection, probe,
-    escalation and direct fallback (repulsion.py:165-200)."""
+    escalation and direct fallback (repulsion.py:165-200).  With ``return_groups`` also
+    returns the target groups (tree.TargetGroups, or None on the direct path) so that a
+    treecode attraction can reuse the targets' sort."""
     eps2 = cfg.kernel_eps * cfg.kernel_eps
     params = tree.auto_params(cfg.tree_precision)
     n_src = src4.shape[0]
+
+    def done(val, grad, tg=None):
+        return (val, grad, tg) if return_groups else (val, grad)
+
     if n_src <= max(cfg.leaf_size, tree.DIRECT_BELOW) or params is None:
         # small problems (exact kernel is faster) and precisions below the fp32 floor
-        return direct_sums_device(tgt4, src4, dims, eps2)
+        return done(*direct_sums_device(tgt4, src4, dims, eps2))
     auto_order, theta = params
     order = cfg.interp_order if cfg.interp_order is not None else auto_order
-    val, grad = tree.tree_sums_device(tgt4, src4, dims, eps2, order, theta)
+    same = tgt4.data_ptr() == src4.data_ptr() and tgt4.shape[0] == n_src
+    src = tree.SourceTree(src4, dims)
+    tg = tree.TargetGroups(tgt4, dims, same_as=src if same else None)
+    val, grad = tree.tree_eval(tg, src, order, theta, eps2)
     if cfg.interp_order is not None:
         err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         while max(err_val, err_grad) > cfg.tree_precision and order < MAX_INTERP_ORDER:
@@ -133,14 +143,14 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig):
                 f"tree backend at interp_order={order - 1} reached relative error "
                 f"{max(err_val, err_grad):.2e} > {cfg.tree_precision:.2e}; "
                 f"escalating to order {order}")
-            val, grad = tree.tree_sums_device(tgt4, src4, dims, eps2, order, theta)
+            val, grad = tree.tree_eval(tg, src, order, theta, eps2)
             err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         if max(err_val, err_grad) > cfg.tree_precision:
             warnings.warn(
                 f"tree backend cannot reach precision {cfg.tree_precision:.2e} at "
                 f"interp_order {MAX_INTERP_ORDER}; falling back to direct summation")
-            return direct_sums_device(tgt4, src4, dims, eps2)
-    return val, grad
+            return done(*direct_sums_device(tgt4, src4, dims, eps2), tg)
+    return done(val, grad, tg)
 
 
 def eval_repulsion_tree(k, cfg: RepulsionConfig) -> tuple[float, np.ndarray]:

@@ -108,84 +108,154 @@ def _node_tables(lib, tree):
     return dict(nb=nb, ne=ne, fc=fc, nc=nc, leaves=leaves, levels=lv)
 
 
-def tree_sums_device(tgt4: torch.Tensor, src4: torch.Tensor, dims: int, eps2: float,
-                     order: int, theta: float, *, leaf_cap: int = LEAF_CAP,
-                     stats: dict | None = None, lists: dict | None = None):
-    """Treecode approximation of ``direct_sums_device(tgt4, src4, ...)`` -> (val, grad)
-    fp64 on the device, in the targets' original order.
+class SourceTree:
+    """Sources sorted along the Morton curve, their octree and tight node boxes, resident
+    on the device.  ``weights`` (fp32 device, per source in input order) makes a weighted
+    source set (the density lattice); None means unit weights (repulsion).
 
-    ``stats`` (optional dict) receives the tree / list sizes; with ``stats["timing"] =
-    True`` also per-phase wall times (synchronising between phases).  ``lists``
-    (optional dict) receives the device interaction lists and the host planner's lists
-    for the same tree (tests)."""
-    import time
+    ``keep_host`` keeps the host octree handle (``self.host``) for the tests' cross-check
+    of the GPU planner; call :meth:`close` to free it."""
 
+    def __init__(self, src4: torch.Tensor, dims: int, leaf_cap: int = LEAF_CAP,
+                 weights: torch.Tensor | None = None, proxy_orders=(), keep_host=False):
+        lib = _native.load()
+        dev = src4.device
+        st = _device.stream()
+        self.dims, self.n = dims, src4.shape[0]
+        self.keys, self.perm = _sort(src4, dims)
+        tree = _host_tree(lib, self.keys, self.n, dims, leaf_cap)
+        try:
+            T = _node_tables(lib, tree)
+            self.groups_host = _groups(lib, tree, lib.spk_tree_group_size())
+        except BaseException:
+            lib.spk_tree_host_free(tree)
+            raise
+        if keep_host:
+            self.host = tree
+        else:
+            lib.spk_tree_host_free(tree)
+            self.host = None
+        self.tables = T
+        self.n_nodes, self.n_leaves = T["nb"].shape[0], T["leaves"].shape[0]
+        self.d_nb, self.d_ne, self.d_fc, self.d_nc, self.d_leaves = (
+            _to_dev(T[k], dev) for k in ("nb", "ne", "fc", "nc", "leaves"))
+        self.rec = torch.empty((self.n, 4), dtype=torch.float32, device=dev)
+        _native.call("spk_tree_gather", src4.data_ptr(), self.perm.data_ptr(), self.n,
+                     _device.ptr(weights), self.rec.data_ptr(), st)
+        self.node_box = torch.empty((self.n_nodes, 6), dtype=torch.float32, device=dev)
+        lb = self.d_nb[self.d_leaves.long()]
+        le = self.d_ne[self.d_leaves.long()]
+        lv = T["levels"]
+        _native.call("spk_tree_node_boxes", self.rec.data_ptr(), self.n_nodes,
+                     self.d_fc.data_ptr(), self.d_nc.data_ptr(), self.n_leaves,
+                     self.d_leaves.data_ptr(), lb.data_ptr(), le.data_ptr(), lv.shape[0] - 1,
+                     lv.ctypes.data, dims, self.node_box.data_ptr(), st)
+        _native.add_launches(int(np.count_nonzero(np.diff(lv))))
+        self._static = {}
+        for q in proxy_orders:
+            self.static_proxies(q)
+
+    def close(self):
+        if self.host:
+            _native.load().spk_tree_host_free(self.host)
+            self.host = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def static_proxies(self, order: int):
+        """Proxies of EVERY node holding more than order^d sources, computed once (for
+        source sets that do not move, e.g. the density lattice).  Returns (records
+        [n + slots * m] with the proxies after the sources, slot_of [n_nodes] i32)."""
+        hit = self._static.get(order)
+        if hit is not None:
+            return hit
+        dev = self.rec.device
+        st = _device.stream()
+        m = order ** self.dims
+        T = self.tables
+        cnt = T["ne"] - T["nb"]
+        eligible = cnt > m
+        slot_of = np.where(eligible, np.cumsum(eligible) - 1, -1).astype(np.int32)
+        nodes = np.nonzero(eligible)[0].astype(np.int32)
+        n_slots = nodes.shape[0]
+        rec = torch.empty((self.n + n_slots * m, 4), dtype=torch.float32, device=dev)
+        rec[:self.n].copy_(self.rec)
+        if n_slots:
+            units = (cnt[nodes] + 4095) // 4096
+            suo = np.concatenate([[0], np.cumsum(units)]).astype(np.int64)
+            n_units = int(suo[-1])
+            us = np.repeat(np.arange(n_slots, dtype=np.int32), units)
+            ub = T["nb"][nodes][us] + 4096 * (np.arange(n_units) - suo[us])
+            ue = np.minimum(ub + 4096, T["ne"][nodes][us])
+            # slot boxes (center, inflated half) from the device node boxes
+            nbox = self.node_box.cpu().numpy()[nodes]
+            c = 0.5 * (nbox[:, :3] + nbox[:, 3:])
+            h = 0.5 * (nbox[:, 3:] - nbox[:, :3])
+            hmax = h[:, :self.dims].max(axis=1, keepdims=True)
+            h = np.maximum(h, np.float32(1e-6) * hmax + np.float32(1e-30))
+            if self.dims == 2:
+                h[:, 2] = 1.0
+            sbox = np.ascontiguousarray(np.concatenate([c, h], axis=1), dtype=np.float32)
+            d_us, d_ub, d_ue, d_suo, d_sb = (_to_dev(a, dev) for a in (
+                us, ub.astype(np.int64), ue.astype(np.int64), suo, sbox))
+            ws = _device.workspace(_native.query("spk_tree_p2m_workspace_bytes", n_units,
+                                                 order, self.dims), "tree_p2m")
+            _native.call("spk_tree_p2m", rec.data_ptr(), n_units, d_us.data_ptr(),
+                         d_ub.data_ptr(), d_ue.data_ptr(), n_slots, d_suo.data_ptr(),
+                         d_sb.data_ptr(), order, self.dims, rec[self.n:].data_ptr(),
+                         ws.data_ptr(), ws.numel(), st)
+        hit = (rec, _to_dev(slot_of, dev))
+        self._static[order] = hit
+        return hit
+
+
+class TargetGroups:
+    """Targets sorted along the Morton curve and cut into groups of <= TR_GROUP that
+    follow their octree (sibling subtrees), with tight group boxes (device)."""
+
+    def __init__(self, tgt4: torch.Tensor, dims: int, same_as: SourceTree | None = None):
+        lib = _native.load()
+        dev = tgt4.device
+        st = _device.stream()
+        self.n = tgt4.shape[0]
+        group = lib.spk_tree_group_size()
+        if same_as is not None:
+            self.perm, self.rec = same_as.perm, same_as.rec
+            gb, ge = same_as.groups_host
+        else:
+            keys, self.perm = _sort(tgt4, dims)
+            self.rec = torch.empty((self.n, 4), dtype=torch.float32, device=dev)
+            _native.call("spk_tree_gather", tgt4.data_ptr(), self.perm.data_ptr(), self.n,
+                         None, self.rec.data_ptr(), st)
+            tree = _host_tree(lib, keys, self.n, dims, group)
+            try:
+                gb, ge = _groups(lib, tree, group)
+            finally:
+                lib.spk_tree_host_free(tree)
+        self.gb_host, self.ge_host = gb, ge
+        self.n_groups = gb.shape[0]
+        self.d_gb, self.d_ge = _to_dev(gb, dev), _to_dev(ge, dev)
+        self.box = torch.empty((self.n_groups, 6), dtype=torch.float32, device=dev)
+        _native.call("spk_tree_boxes", self.rec.data_ptr(), self.n_groups, self.d_gb.data_ptr(),
+                     self.d_ge.data_ptr(), dims, self.box.data_ptr(), st)
+
+
+def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2: float, *,
+              static: bool = False, stats: dict | None = None, lists: dict | None = None,
+              val: torch.Tensor | None = None, grad: torch.Tensor | None = None):
+    """Weighted treecode sums of the sources at the targets -> (val, grad) fp64, targets'
+    original order.  ``static`` uses the source tree's cached all-node proxies (no P2M in
+    the call); otherwise proxies are built for the nodes this traversal opens as far."""
     if not 2 <= order <= MAX_ORDER:
         raise ValueError(f"interp_order must be in [2, {MAX_ORDER}]")
-    lib = _native.load()
-    dev = src4.device
+    dev = src.rec.device
     st = _device.stream()
-    n_s, n_t = src4.shape[0], tgt4.shape[0]
-    same = tgt4.data_ptr() == src4.data_ptr() and n_t == n_s
-    m = order ** dims
-    group = lib.spk_tree_group_size()
-    timing = stats is not None and stats.get("timing", False)
-    marks = []
-
-    def mark(name):
-        if timing:
-            torch.cuda.synchronize()
-            marks.append((name, time.perf_counter()))
-
-    mark("start")
-    # 1. sort sources (and targets), host octree(s) over the sorted keys
-    skeys, sperm = _sort(src4, dims)
-    tree = _host_tree(lib, skeys, n_s, dims, leaf_cap)
-    ttree = None
-    try:
-        T = _node_tables(lib, tree)
-        if same:
-            gb, ge = _groups(lib, tree, group)
-        else:
-            tkeys, tperm = _sort(tgt4, dims)
-            ttree = _host_tree(lib, tkeys, n_t, dims, group)
-            gb, ge = _groups(lib, ttree, group)
-        if lists is not None:
-            lists["host_tree"] = (tree, T)
-            tree = None  # the caller frees it
-    finally:
-        if tree:
-            lib.spk_tree_host_free(tree)
-        if ttree:
-            lib.spk_tree_host_free(ttree)
-    mark("build")
-    n_nodes, n_leaves, n_groups = T["nb"].shape[0], T["leaves"].shape[0], gb.shape[0]
-    d_nb, d_ne, d_fc, d_nc, d_leaves, d_gb, d_ge = (_to_dev(a, dev) for a in (
-        T["nb"], T["ne"], T["fc"], T["nc"], T["leaves"], gb, ge))
-    d_lb = d_nb[d_leaves.long()]
-    d_le = d_ne[d_leaves.long()]
-    # 2. sorted records; proxies go after the n_s particles (at most one slot per node)
-    rec = torch.empty((n_s + n_nodes * m, 4), dtype=torch.float32, device=dev)
-    _native.call("spk_tree_gather", src4.data_ptr(), sperm.data_ptr(), n_s, None,
-                 rec.data_ptr(), st)
-    if same:
-        tperm, trec = sperm, rec
-    else:
-        trec = torch.empty((n_t, 4), dtype=torch.float32, device=dev)
-        _native.call("spk_tree_gather", tgt4.data_ptr(), tperm.data_ptr(), n_t, None,
-                     trec.data_ptr(), st)
-    # 3. node boxes (leaves reduce, levels merge) and target group boxes
-    node_box = torch.empty((n_nodes, 6), dtype=torch.float32, device=dev)
-    lv = T["levels"]
-    _native.call("spk_tree_node_boxes", rec.data_ptr(), n_nodes, d_fc.data_ptr(),
-                 d_nc.data_ptr(), n_leaves, d_leaves.data_ptr(), d_lb.data_ptr(),
-                 d_le.data_ptr(), lv.shape[0] - 1, lv.ctypes.data, dims, node_box.data_ptr(), st)
-    _native.add_launches(int(np.count_nonzero(np.diff(lv))))
-    group_box = torch.empty((n_groups, 6), dtype=torch.float32, device=dev)
-    _native.call("spk_tree_boxes", trec.data_ptr(), n_groups, d_gb.data_ptr(), d_ge.data_ptr(),
-                 dims, group_box.data_ptr(), st)
-    mark("boxes")
-    # 4. interaction lists on the device: count pass, sizes to the host, write pass
+    dims, n_s, m = src.dims, src.n, order ** src.dims
+    n_nodes, n_groups = src.n_nodes, tg.n_groups
     slot_of = torch.empty(n_nodes, dtype=torch.int32, device=dev)
     slot_node = torch.empty(n_nodes, dtype=torch.int32, device=dev)
     slot_box = torch.empty((n_nodes, 6), dtype=torch.float32, device=dev)
@@ -194,53 +264,100 @@ def tree_sums_device(tgt4: torch.Tensor, src4: torch.Tensor, dims: int, eps2: fl
     totals = torch.empty(3, dtype=torch.int64, device=dev)
     ws = _device.workspace(_native.query("spk_tree_plan_workspace_bytes", n_nodes, n_groups),
                            "tree_plan")
-    _native.call("spk_tree_plan_count", d_nb.data_ptr(), d_ne.data_ptr(), d_fc.data_ptr(),
-                 d_nc.data_ptr(), n_nodes, node_box.data_ptr(), group_box.data_ptr(), n_groups,
-                 float(theta), order, dims, n_s, slot_of.data_ptr(), slot_node.data_ptr(),
-                 slot_box.data_ptr(), slot_unit_off.data_ptr(), seg_off.data_ptr(),
-                 totals.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    _native.call("spk_tree_plan_count", src.d_nb.data_ptr(), src.d_ne.data_ptr(),
+                 src.d_fc.data_ptr(), src.d_nc.data_ptr(), n_nodes, src.node_box.data_ptr(),
+                 tg.box.data_ptr(), n_groups, float(theta), order, dims, n_s,
+                 slot_of.data_ptr(), slot_node.data_ptr(), slot_box.data_ptr(),
+                 slot_unit_off.data_ptr(), seg_off.data_ptr(), totals.data_ptr(),
+                 ws.data_ptr(), ws.numel(), st)
     n_seg, n_slots, n_units = (int(x) for x in totals.cpu().numpy())
+    if static:
+        rec, write_slot_of = src.static_proxies(order)
+        n_units_w = 0
+    else:
+        rec = torch.empty((n_s + n_slots * m, 4), dtype=torch.float32, device=dev)
+        rec[:n_s].copy_(src.rec)
+        write_slot_of = slot_of
+        n_units_w = n_units
     seg_start = torch.empty(max(n_seg, 1), dtype=torch.int64, device=dev)
     seg_count = torch.empty(max(n_seg, 1), dtype=torch.int32, device=dev)
-    unit_slot = torch.empty(max(n_units, 1), dtype=torch.int32, device=dev)
-    unit_begin = torch.empty(max(n_units, 1), dtype=torch.int64, device=dev)
-    unit_end = torch.empty(max(n_units, 1), dtype=torch.int64, device=dev)
-    _native.call("spk_tree_plan_write", d_nb.data_ptr(), d_ne.data_ptr(), d_fc.data_ptr(),
-                 d_nc.data_ptr(), n_nodes, node_box.data_ptr(), group_box.data_ptr(), n_groups,
-                 float(theta), order, dims, n_s, slot_of.data_ptr(), slot_node.data_ptr(),
-                 slot_unit_off.data_ptr(), n_slots, seg_off.data_ptr(), seg_start.data_ptr(),
+    unit_slot = torch.empty(max(n_units_w, 1), dtype=torch.int32, device=dev)
+    unit_begin = torch.empty(max(n_units_w, 1), dtype=torch.int64, device=dev)
+    unit_end = torch.empty(max(n_units_w, 1), dtype=torch.int64, device=dev)
+    _native.call("spk_tree_plan_write", src.d_nb.data_ptr(), src.d_ne.data_ptr(),
+                 src.d_fc.data_ptr(), src.d_nc.data_ptr(), n_nodes, src.node_box.data_ptr(),
+                 tg.box.data_ptr(), n_groups, float(theta), order, dims, n_s,
+                 write_slot_of.data_ptr(), slot_node.data_ptr(), slot_unit_off.data_ptr(),
+                 0 if static else n_slots, seg_off.data_ptr(), seg_start.data_ptr(),
                  seg_count.data_ptr(), unit_slot.data_ptr(), unit_begin.data_ptr(),
                  unit_end.data_ptr(), st)
-    mark("plan")
-    # 5. proxies (P2M) and the weighted sums
-    if n_slots:
+    if not static and n_slots:
         ws2 = _device.workspace(_native.query("spk_tree_p2m_workspace_bytes", n_units, order,
                                               dims), "tree_p2m")
         _native.call("spk_tree_p2m", rec.data_ptr(), n_units, unit_slot.data_ptr(),
                      unit_begin.data_ptr(), unit_end.data_ptr(), n_slots,
                      slot_unit_off.data_ptr(), slot_box.data_ptr(), order, dims,
                      rec[n_s:].data_ptr(), ws2.data_ptr(), ws2.numel(), st)
-    mark("p2m")
-    val = torch.empty(n_t, dtype=torch.float64, device=dev)
-    grad = torch.empty((n_t, dims), dtype=torch.float64, device=dev)
-    _native.call("spk_tree_eval", trec.data_ptr(), tperm.data_ptr(), n_groups, d_gb.data_ptr(),
-                 d_ge.data_ptr(), rec.data_ptr(), seg_off.data_ptr(), seg_start.data_ptr(),
-                 seg_count.data_ptr(), dims, float(eps2), val.data_ptr(), grad.data_ptr(), st)
-    mark("eval")
+    if val is None:
+        val = torch.empty(tg.n, dtype=torch.float64, device=dev)
+    if grad is None:
+        grad = torch.empty((tg.n, dims), dtype=torch.float64, device=dev)
+    _native.call("spk_tree_eval", tg.rec.data_ptr(), tg.perm.data_ptr(), n_groups,
+                 tg.d_gb.data_ptr(), tg.d_ge.data_ptr(), rec.data_ptr(), seg_off.data_ptr(),
+                 seg_start.data_ptr(), seg_count.data_ptr(), dims, float(eps2),
+                 val.data_ptr(), grad.data_ptr(), st)
     if stats is not None:
         so = seg_off.cpu().numpy()
         sc = seg_count[:n_seg].cpu().numpy().astype(np.int64)
-        per_group = np.add.reduceat(np.append(sc, 0), np.minimum(so[:-1], n_seg)) * (so[1:] > so[:-1])
-        stats.update(nodes=n_nodes, leaves=n_leaves, groups=n_groups, segments=n_seg,
+        per_group = np.add.reduceat(np.append(sc, 0), np.minimum(so[:-1], n_seg)) * \
+            (so[1:] > so[:-1])
+        stats.update(nodes=n_nodes, leaves=src.n_leaves, groups=n_groups, segments=n_seg,
                      slots=n_slots, units=n_units, interp_order=order, opening_theta=theta,
-                     pairs=int(np.dot(per_group, ge - gb)))
-        if timing:
-            stats["phases_ms"] = {marks[i][0]: 1e3 * (marks[i][1] - marks[i - 1][1])
-                                  for i in range(1, len(marks))}
+                     pairs=int(np.dot(per_group, tg.ge_host - tg.gb_host)))
     if lists is not None:
         lists.update(seg_off=seg_off.cpu().numpy(), seg_start=seg_start[:n_seg].cpu().numpy(),
                      seg_count=seg_count[:n_seg].cpu().numpy(),
                      slot_node=slot_node[:n_slots].cpu().numpy(),
-                     node_box=node_box.cpu().numpy(), group_box=group_box.cpu().numpy(),
+                     node_box=src.node_box.cpu().numpy(), group_box=tg.box.cpu().numpy(),
                      n_groups=n_groups, n_src=n_s)
+    return val, grad
+
+
+def tree_sums_device(tgt4: torch.Tensor, src4: torch.Tensor, dims: int, eps2: float,
+                     order: int, theta: float, *, leaf_cap: int = LEAF_CAP,
+                     stats: dict | None = None, lists: dict | None = None):
+    """Treecode approximation of ``direct_sums_device(tgt4, src4, ...)`` -> (val, grad)
+    fp64 on the device, in the targets' original order (unit-weight sources, proxies
+    built for this call).
+
+    ``stats`` (optional dict) receives the tree / list sizes; with ``stats["timing"] =
+    True`` also per-phase wall times (synchronising between phases).  ``lists``
+    (optional dict) receives the device interaction lists and, under "host_tree", the
+    host octree (handle, tables) for the tests' cross-check (caller frees the handle)."""
+    import time
+
+    if not 2 <= order <= MAX_ORDER:
+        raise ValueError(f"interp_order must be in [2, {MAX_ORDER}]")
+    timing = stats is not None and stats.get("timing", False)
+    marks = []
+
+    def mark(name):
+        if timing:
+            torch.cuda.synchronize()
+            marks.append((name, time.perf_counter()))
+
+    same = tgt4.data_ptr() == src4.data_ptr() and tgt4.shape[0] == src4.shape[0]
+    mark("start")
+    src = SourceTree(src4, dims, leaf_cap, keep_host=lists is not None)
+    mark("build")
+    tg = TargetGroups(tgt4, dims, same_as=src if same else None)
+    mark("boxes")
+    val, grad = tree_eval(tg, src, order, theta, eps2, stats=stats, lists=lists)
+    mark("eval")
+    if lists is not None:
+        lists["host_tree"] = (src.host, src.tables)
+        src.host = None  # ownership passes to the caller
+    if timing:
+        stats["phases_ms"] = {marks[i][0]: 1e3 * (marks[i][1] - marks[i - 1][1])
+                              for i in range(1, len(marks))}
     return val, grad

@@ -58,12 +58,18 @@ class PhaseOps(engine.CudaOps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=4)
+    ap.add_argument("--config", default="c2")
     args = ap.parse_args()
+    bench.select_workload(args.config)
+    W = bench.W
     torch.cuda.set_device(0)
-    hw = bench.hardware()
-    cfg = spk.OptimizerConfig(n_c=bench.N_C, n_s=bench.N_S, dims=3, grad_mode="exact",
-                              grid_n=bench.GRID_N, seed=0)
-    fld = spk.precompute_field(spk.discretize(cfg.density, bench.GRID_N, 3))
+    extra = {}
+    if W.get("tree"):
+        extra = dict(attraction_tree_precision=W["att_prec"],
+                     repulsion=spk.RepulsionConfig(backend="tree", tree_precision=W["rep_prec"]))
+    cfg = spk.OptimizerConfig(n_c=bench.N_C, n_s=bench.N_S, dims=bench.DIMS, grad_mode="exact",
+                              grid_n=bench.GRID_N, seed=0, perturbation=W["pert"], **extra)
+    fld = spk.precompute_field(bench.density())
     pcfg = bench.proj_config()
     ops = PhaseOps()
     run = engine.ShardedRun(np.ascontiguousarray(bench.start_pattern().coords), cfg, fld,

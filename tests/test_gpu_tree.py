@@ -189,3 +189,38 @@ def test_device_lists_match_host_planner(spk, dims):
     assert np.array_equal(seg_off, L["seg_off"])
     assert np.array_equal(seg_start, L["seg_start"])
     assert np.array_equal(seg_count, L["seg_count"])
+
+
+@pytest.mark.parametrize("precision", [1e-3, 1e-4, 1e-5])
+def test_attraction_tree_precision(spk, precision):
+    """Treecode attraction over the static lattice tree vs the exact K2 sums."""
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.attraction import grid_sums_device, tree_grid_sums_device
+
+    for n_c, n_s, d, n in ((128, 1024, 2, 128), (256, 512, 3, 24)):
+        pts = spk.perturb(spk.init_radial(n_c, n_s, d), 0.25, 0).points()
+        fld = spk.precompute_field(spk.discretize(spk.DensityParams(0.25, 2.0), n, d))
+        pos4 = _device.pack_positions(_device.h2d(pts))
+        eps2 = fld.kernel_eps ** 2
+        vt, gt = tree_grid_sums_device(pos4, fld, eps2, precision)
+        vd, gd = grid_sums_device(pos4, fld, eps2)
+        vt, gt, vd, gd = (_device.d2h(x) for x in (vt, gt, vd, gd))
+        e_cost = abs(vt.sum() - vd.sum()) / abs(vd.sum())
+        e_grad = np.linalg.norm(gt - gd) / np.linalg.norm(gd)
+        assert e_cost <= precision and e_grad <= precision, (d, e_cost, e_grad)
+
+
+def test_optimize_tree_attraction_and_repulsion(spk):
+    """optimize() with both N-body terms on the treecode stays close to the exact run."""
+    hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                          dwell_dt=2e-6, fov=0.192, matrix=64, dims=2)
+    base = dict(n_c=256, n_s=1024, dims=2, n_decim=0, n_git=3, n_pit=30, grid_n=64,
+                perturbation=0.25, seed=0, grad_mode="exact")
+    r_d = spk.optimize(spk.OptimizerConfig(**base), hw)
+    cfg_t = spk.OptimizerConfig(**base, attraction_tree_precision=1e-5,
+                                repulsion=spk.RepulsionConfig(backend="tree",
+                                                              tree_precision=1e-5))
+    r_t = spk.optimize(cfg_t, hw)
+    ct, cd = r_t.trace.records[-1], r_d.trace.records[-1]
+    assert abs(ct.cost - cd.cost) / abs(cd.cost) < 1e-4
+    assert np.abs(r_t.pattern.coords - r_d.pattern.coords).max() < 1e-3
