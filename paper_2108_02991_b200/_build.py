@@ -25,6 +25,7 @@ SOURCES = {
     "nbody.cu": [],
     "project.cu": ["-fmad=false"],
     "tree.cu": [],
+    "nudft.cu": [],
 }
 # Host C++ (treecode octree over sorted keys; reference host planner).
 HOST_SOURCES = ["tree_host.cpp"]

@@ -1,0 +1,412 @@
+// nudft.cu -- direct nonuniform DFT between trajectory samples and the image grid
+// (density compensation and the PSF of a pattern).
+//
+// Replaces the reference's numpy phase-table products (analysis.py:25-69):
+//   adjoint  out[r] = sum_i w_i exp(+i pi k_i . r)            (nudft_adjoint)
+//   forward  f_i    = sum_r img[r] exp(-i pi k_i . r)          (nudft_forward)
+// with r_a = 0..n_a-1 minus n_a/2 (integer voxel offsets) and k in [-1, 1]^d.
+//
+// Both are complex GEMM-shaped sums with generated operands.  The grid is split as
+// U x V (3D: U = (a, b), V = c; 2D: U = a, V = b):
+//   adjoint: out[u, v] = sum_i A_i[u] B_i[v],  A = e0 e1 (3D) or w e0 (2D),
+//            B = w e2 (3D) or e1 (2D); one CTA owns a 64 (u) x 32 (v) output tile and
+//            a slice of the samples, phase tables for 128 samples are generated in fp64
+//            by recurrence from one sincospi per row (exact start, fp64 steps) and stored
+//            as fp32 complex in shared memory; each thread accumulates 16 products per
+//            sample with packed FFMA, folding into fp64 every 128 samples.
+//   forward: one thread per sample; for every u the inner sum over v is a Horner
+//            polynomial in zeta = exp(-i pi k_v) (4 FFMA per voxel, image rows broadcast
+//            from shared memory), multiplied by conj(A_i[u]) kept by an fp32 recurrence
+//            re-seeded from fp64 at every 8-row stage and row wrap.
+// Deterministic: fixed sample slices per CTA and a fixed-order reduction of the slices.
+#include <algorithm>
+#include <cfloat>
+
+#include "spk_common.cuh"
+
+namespace spk {
+
+constexpr int NU_THREADS = 128;
+constexpr int NU_UT = 64;   // u per adjoint tile
+constexpr int NU_VT = 32;   // v per adjoint tile
+constexpr int NU_VPT = 16;  // v per thread
+constexpr int NU_CH = 128;  // samples per shared-memory chunk
+constexpr int NF_UT = 8;    // image rows (u) per forward stage
+constexpr int NF_VMAX = 1024;
+
+struct C2 {
+    float x, y;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// exp(i pi t) in fp64 (sincospi is exact in its argument reduction).
+__device__ __forceinline__ double2 cispi(double t) {
+    double s, c;
+    sincospi(t, &s, &c);
+    return make_double2(c, s);
+}
+
+struct AdjParams {
+    const double* pts;   // [p][dims]
+    const double* w;     // [p][2] complex weights (re, im)
+    long long p;
+    int dims;
+    int n0, n1, n2;      // grid (2D: n2 = 1)
+    long long U, V;      // U x V split of the grid
+    int slices;          // sample slices (split-K)
+    double* part;        // [slices][U][V][2]
+};
+
+// Generated operand tables for one chunk of samples.
+__global__ void __launch_bounds__(NU_THREADS) nudft_adjoint_kernel(const AdjParams P) {
+    extern __shared__ __align__(16) char sm[];
+    C2* At = reinterpret_cast<C2*>(sm);                 // [NU_CH][NU_UT]
+    C2* Bt = At + NU_CH * NU_UT;                        // [NU_CH][NU_VT]
+    const int tid = threadIdx.x;
+    const long long u0 = (long long)blockIdx.x * NU_UT;
+    const long long v0 = (long long)blockIdx.y * NU_VT;
+    const int slice = blockIdx.z;
+    const long long i_begin = P.p * slice / P.slices;
+    const long long i_end = P.p * (slice + 1) / P.slices;
+    const int u_loc = tid % NU_UT;
+    const int vg = tid / NU_UT;  // 0..1 -> v in [vg*16, vg*16+16)
+    double acc[NU_VPT][2];
+#pragma unroll
+    for (int k = 0; k < NU_VPT; ++k) acc[k][0] = acc[k][1] = 0.0;
+    const int h0 = P.n0 / 2, h1 = P.n1 / 2, h2 = P.n2 / 2;
+
+    for (long long c0 = i_begin; c0 < i_end; c0 += NU_CH) {
+        const int cnt = (int)min((long long)NU_CH, i_end - c0);
+        // ---- tables: thread j owns sample row j of the chunk
+        if (tid < NU_CH) {
+            const int j = tid;
+            const long long i = c0 + j;
+            if (j < cnt) {
+                const double k0 = P.pts[i * P.dims];
+                const double k1 = P.pts[i * P.dims + 1];
+                const double2 wi = make_double2(P.w[2 * i], P.w[2 * i + 1]);
+                if (P.dims == 3) {
+                    const double k2 = P.pts[i * P.dims + 2];
+                    // A[u] = e0[a] e1[b], u = a * n1 + b, over this tile's u range
+                    long long u = u0;
+                    int a = (int)(u / P.n1), b = (int)(u - (long long)a * P.n1);
+                    double2 e0 = cispi(k0 * (double)(a - h0));
+                    double2 e1 = cispi(k1 * (double)(b - h1));
+                    const double2 z1 = cispi(k1);
+                    for (int q = 0; q < NU_UT; ++q) {
+                        const double2 v = cmul(e0, e1);
+                        At[j * NU_UT + q] = C2{(float)v.x, (float)v.y};
+                        if (++b == P.n1) {
+                            b = 0;
+                            ++a;
+                            e0 = cispi(k0 * (double)(a - h0));
+                            e1 = cispi(k1 * (double)(b - h1));
+                        } else {
+                            e1 = cmul(e1, z1);
+                        }
+                    }
+                    // B[v] = w e2[c], v = c
+                    double2 e2 = cmul(wi, cispi(k2 * (double)(v0 - h2)));
+                    const double2 z2 = cispi(k2);
+                    for (int q = 0; q < NU_VT; ++q) {
+                        Bt[j * NU_VT + q] = C2{(float)e2.x, (float)e2.y};
+                        e2 = cmul(e2, z2);
+                    }
+                } else {
+                    double2 e0 = cmul(wi, cispi(k0 * (double)(u0 - h0)));
+                    const double2 z0 = cispi(k0);
+                    for (int q = 0; q < NU_UT; ++q) {
+                        At[j * NU_UT + q] = C2{(float)e0.x, (float)e0.y};
+                        e0 = cmul(e0, z0);
+                    }
+                    double2 e1 = cispi(k1 * (double)(v0 - h1));
+                    const double2 z1 = cispi(k1);
+                    for (int q = 0; q < NU_VT; ++q) {
+                        Bt[j * NU_VT + q] = C2{(float)e1.x, (float)e1.y};
+                        e1 = cmul(e1, z1);
+                    }
+                }
+            } else {
+                for (int q = 0; q < NU_UT; ++q) At[j * NU_UT + q] = C2{0.f, 0.f};
+                for (int q = 0; q < NU_VT; ++q) Bt[j * NU_VT + q] = C2{0.f, 0.f};
+            }
+        }
+        __syncthreads();
+        // ---- products: out[u, v] += A[u] B[v]
+        float2 re[NU_VPT / 2], im[NU_VPT / 2];  // packed over v pairs
+#pragma unroll
+        for (int k = 0; k < NU_VPT / 2; ++k) re[k] = im[k] = make_float2(0.f, 0.f);
+#pragma unroll 2
+        for (int j = 0; j < cnt; ++j) {
+            const C2 a = At[j * NU_UT + u_loc];
+            const float4* brow = reinterpret_cast<const float4*>(Bt + j * NU_VT + vg * NU_VPT);
+            const float2 ax = make_float2(a.x, a.x), ay = make_float2(a.y, a.y);
+            const float2 nay = make_float2(-a.y, -a.y);
+#pragma unroll
+            for (int k = 0; k < NU_VPT / 2; ++k) {
+                const float4 b = brow[k];  // (re, im) of v = 2k, 2k + 1
+                const float2 br = make_float2(b.x, b.z), bi = make_float2(b.y, b.w);
+                re[k] = __ffma2_rn(ax, br, re[k]);
+                re[k] = __ffma2_rn(nay, bi, re[k]);
+                im[k] = __ffma2_rn(ax, bi, im[k]);
+                im[k] = __ffma2_rn(ay, br, im[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NU_VPT / 2; ++k) {
+            acc[2 * k][0] += re[k].x;
+            acc[2 * k + 1][0] += re[k].y;
+            acc[2 * k][1] += im[k].x;
+            acc[2 * k + 1][1] += im[k].y;
+        }
+        __syncthreads();
+    }
+    const long long u = u0 + u_loc;
+    if (u >= P.U) return;
+    double* out = P.part + ((size_t)slice * P.U + u) * P.V * 2;
+#pragma unroll
+    for (int k = 0; k < NU_VPT; ++k) {
+        const long long v = v0 + vg * NU_VPT + k;
+        if (v < P.V) {
+            out[2 * v] = acc[k][0];
+            out[2 * v + 1] = acc[k][1];
+        }
+    }
+}
+
+__global__ void nudft_reduce_kernel(const double* __restrict__ part, int slices, long long n,
+                                    double* __restrict__ out) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    double s = 0.0;
+    for (int q = 0; q < slices; ++q) s += part[(size_t)q * n + e];
+    out[e] = s;
+}
+
+struct FwdParams {
+    const double* pts;  // [p][dims]
+    const double* img;  // [U][V][2]
+    long long p;
+    int dims;
+    int n0, n1, n2;
+    long long U, V;
+    int slices;         // u slices (split-K)
+    double* part;       // [slices][p][2]
+};
+
+__global__ void __launch_bounds__(NU_THREADS) nudft_forward_kernel(const FwdParams P) {
+    extern __shared__ __align__(16) char sm[];
+    float2* rows = reinterpret_cast<float2*>(sm);  // [NF_UT][V]
+    const int tid = threadIdx.x;
+    const long long i = (long long)blockIdx.x * NU_THREADS + tid;
+    const int slice = blockIdx.y;
+    const long long ub = P.U * slice / P.slices, ue = P.U * (slice + 1) / P.slices;
+    const bool live = i < P.p;
+    const long long ii = live ? i : P.p - 1;
+    const double k0 = P.pts[ii * P.dims];
+    const double k1 = P.pts[ii * P.dims + 1];
+    const double kv = P.dims == 3 ? P.pts[ii * P.dims + 2] : k1;
+    const int hv = (P.dims == 3 ? P.n2 : P.n1) / 2;
+    // zeta = exp(-i pi k_v); the Horner sum over v is sum_v img[u, v] zeta^v, then times
+    // zeta^(-hv) = exp(+i pi k_v hv)
+    const double2 zd = cispi(-kv);
+    const float zr = (float)zd.x, zi = (float)zd.y;
+    const double2 shift = cispi(kv * (double)hv);
+    // per-u step of conj(A): exp(-i pi k_b) along b (3D) or exp(-i pi k0) along a (2D)
+    const double2 wd = cispi(-(P.dims == 3 ? k1 : k0));
+    const float wr = (float)wd.x, wi = (float)wd.y;
+    double fr = 0.0, fi = 0.0;
+    for (long long s0 = ub; s0 < ue; s0 += NF_UT) {
+        const int nu = (int)min((long long)NF_UT, ue - s0);
+        __syncthreads();
+        for (long long e = tid; e < (long long)nu * P.V; e += NU_THREADS) {
+            const double* src = P.img + ((size_t)s0 * P.V + e) * 2;
+            rows[e] = make_float2((float)src[0], (float)src[1]);
+        }
+        __syncthreads();
+        float cr = 0.f, ci = 0.f;  // sum over this stage's rows of conj(A[u]) P_u
+        // conj(A[u]) = exp(-i pi (k0 (a - h0) [+ k1 (b - h1)])): exact fp64 seed at the
+        // stage start and at row wraps, fp32 steps by exp(-i pi k_b) in between
+        float ar = 0.f, ai = 0.f;
+        int a = 0, b = 0;
+        for (int q = 0; q < nu; ++q) {
+            const long long u = s0 + q;
+            bool seed = q == 0;
+            if (P.dims == 3) {
+                if (q == 0) {
+                    a = (int)(u / P.n1);
+                    b = (int)(u - (long long)a * P.n1);
+                } else if (++b == P.n1) {
+                    b = 0;
+                    ++a;
+                    seed = true;
+                }
+            }
+            if (seed) {
+                const double t = P.dims == 3
+                                     ? k0 * (double)(a - P.n0 / 2) + k1 * (double)(b - P.n1 / 2)
+                                     : k0 * (double)(u - P.n0 / 2);
+                const double2 ad = cispi(-t);
+                ar = (float)ad.x;
+                ai = (float)ad.y;
+            } else {
+                const float nr = fmaf(ar, wr, -ai * wi);
+                ai = fmaf(ar, wi, ai * wr);
+                ar = nr;
+            }
+            const float2* row = rows + (size_t)q * P.V;
+            float pr = 0.f, pi = 0.f;
+            for (long long v = P.V - 1; v >= 0; --v) {  // Horner: p = p zeta + img[v]
+                const float2 g = row[v];
+                const float nr = fmaf(pr, zr, fmaf(-pi, zi, g.x));
+                pi = fmaf(pr, zi, fmaf(pi, zr, g.y));
+                pr = nr;
+            }
+            cr = fmaf(ar, pr, fmaf(-ai, pi, cr));
+            ci = fmaf(ar, pi, fmaf(ai, pr, ci));
+        }
+        fr += (double)cr;
+        fi += (double)ci;
+    }
+    if (live) {
+        // times zeta^(-hv)
+        const double2 f = cmul(make_double2(fr, fi), shift);
+        double* out = P.part + ((size_t)slice * P.p + i) * 2;
+        out[0] = f.x;
+        out[1] = f.y;
+    }
+}
+
+// density_compensation update (analysis.py:90-96): w_i <- w_i / max(|back_i|, 1e-12)
+__global__ void dcf_update_kernel(double* __restrict__ w, const double* __restrict__ back,
+                                  long long p) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const double m = fmax(hypot(back[2 * i], back[2 * i + 1]), 1e-12);
+    w[2 * i] = w[2 * i] / m;
+    w[2 * i + 1] = w[2 * i + 1] / m;
+}
+
+// compute_psf magnitudes (analysis.py:126-131): |vol / sum(w)|
+__global__ void psf_magnitude_kernel(const double* __restrict__ vol, long long n, double total,
+                                     double* __restrict__ mag) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    mag[e] = hypot(vol[2 * e] / total, vol[2 * e + 1] / total);
+}
+
+}  // namespace spk
+
+using namespace spk;
+
+extern "C" {
+
+size_t spk_nudft_workspace_bytes(int64_t p, int dims, const int64_t* grid) {
+    const long long U = dims == 3 ? grid[0] * grid[1] : grid[0];
+    const long long V = dims == 3 ? grid[2] : grid[1];
+    // adjoint: up to 16 slices of U x V complex; forward: up to 16 slices of p complex
+    const size_t adj = (size_t)16 * U * V * 16;
+    const size_t fwd = (size_t)16 * p * 16;
+    return adj > fwd ? adj : fwd;
+}
+
+static int adj_slices(long long U, long long V, long long p) {
+    const long long tiles = ((U + NU_UT - 1) / NU_UT) * ((V + NU_VT - 1) / NU_VT);
+    const long long want = 2LL * num_sms() * 2;  // ~2 waves of 2 CTAs per SM
+    long long s = (want + tiles - 1) / tiles;
+    s = std::max(1LL, std::min(s, std::min(16LL, (p + NU_CH - 1) / NU_CH)));
+    return (int)s;
+}
+
+int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int dims,
+                      const int64_t* grid, double* out, void* ws, size_t ws_bytes,
+                      spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(p >= 1, SPK_ERR_ARG, "nudft: empty sample set");
+    AdjParams P{};
+    P.pts = pts;
+    P.w = weights;
+    P.p = p;
+    P.dims = dims;
+    P.n0 = (int)grid[0];
+    P.n1 = (int)grid[1];
+    P.n2 = dims == 3 ? (int)grid[2] : 1;
+    P.U = dims == 3 ? (long long)P.n0 * P.n1 : P.n0;
+    P.V = dims == 3 ? P.n2 : P.n1;
+    P.slices = adj_slices(P.U, P.V, p);
+    SPK_REQUIRE(ws_bytes >= (size_t)P.slices * P.U * P.V * 16, SPK_ERR_WORKSPACE,
+                "nudft adjoint: workspace too small");
+    P.part = static_cast<double*>(ws);
+    const size_t smem = (size_t)NU_CH * (NU_UT + NU_VT) * sizeof(C2);
+    cudaFuncSetAttribute(nudft_adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    dim3 grid3((unsigned)((P.U + NU_UT - 1) / NU_UT), (unsigned)((P.V + NU_VT - 1) / NU_VT),
+               (unsigned)P.slices);
+    cudaStream_t s = (cudaStream_t)stream;
+    nudft_adjoint_kernel<<<grid3, NU_THREADS, smem, s>>>(P);
+    SPK_CHECK_LAUNCH("spk_nudft_adjoint");
+    const long long n = P.U * P.V * 2;
+    nudft_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P.part, P.slices, n, out);
+    SPK_CHECK_LAUNCH("spk_nudft_adjoint(reduce)");
+    return SPK_OK;
+}
+
+int spk_nudft_forward(const double* pts, const double* image, int64_t p, int dims,
+                      const int64_t* grid, double* out, void* ws, size_t ws_bytes,
+                      spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(p >= 1, SPK_ERR_ARG, "nudft: empty sample set");
+    FwdParams P{};
+    P.pts = pts;
+    P.img = image;
+    P.p = p;
+    P.dims = dims;
+    P.n0 = (int)grid[0];
+    P.n1 = (int)grid[1];
+    P.n2 = dims == 3 ? (int)grid[2] : 1;
+    P.U = dims == 3 ? (long long)P.n0 * P.n1 : P.n0;
+    P.V = dims == 3 ? P.n2 : P.n1;
+    SPK_REQUIRE(P.V <= NF_VMAX, SPK_ERR_ARG, "nudft forward: last grid axis %lld > %d",
+                P.V, NF_VMAX);
+    const long long blocks = (p + NU_THREADS - 1) / NU_THREADS;
+    const long long want = 4LL * num_sms();
+    long long sl = std::max(1LL, std::min(16LL, (want + blocks - 1) / blocks));
+    sl = std::min(sl, P.U);
+    P.slices = (int)sl;
+    SPK_REQUIRE(ws_bytes >= (size_t)P.slices * p * 16, SPK_ERR_WORKSPACE,
+                "nudft forward: workspace too small");
+    P.part = static_cast<double*>(ws);
+    const size_t smem = (size_t)NF_UT * P.V * sizeof(float2);
+    cudaFuncSetAttribute(nudft_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(smem, (size_t)1));
+    dim3 grid2((unsigned)blocks, (unsigned)P.slices);
+    cudaStream_t s = (cudaStream_t)stream;
+    nudft_forward_kernel<<<grid2, NU_THREADS, smem, s>>>(P);
+    SPK_CHECK_LAUNCH("spk_nudft_forward");
+    const long long n = p * 2;
+    nudft_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P.part, P.slices, n, out);
+    SPK_CHECK_LAUNCH("spk_nudft_forward(reduce)");
+    return SPK_OK;
+}
+
+int spk_dcf_update(double* weights, const double* back, int64_t p, spk_stream_t stream) {
+    if (p == 0) return SPK_OK;
+    dcf_update_kernel<<<(unsigned)((p + 255) / 256), 256, 0, (cudaStream_t)stream>>>(weights,
+                                                                                   back, p);
+    SPK_CHECK_LAUNCH("spk_dcf_update");
+    return SPK_OK;
+}
+
+int spk_psf_magnitude(const double* vol, int64_t n, double total, double* mag,
+                      spk_stream_t stream) {
+    if (n == 0) return SPK_OK;
+    psf_magnitude_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        vol, n, total, mag);
+    SPK_CHECK_LAUNCH("spk_psf_magnitude");
+    return SPK_OK;
+}
+
+}  // extern "C"

@@ -474,6 +474,20 @@ __device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sampl
     nrm = sqrt(nrm);
     if (!(nrm > b)) return;
     if (nrm - b > worst) worst = nrm - b;
+    if (pin != n && pin != n + 1 && pin != n + 2) {
+        // unpinned triple: c = (1, -2, 1), denom = 6 exactly; step * 1 and step * -2 are
+        // exact, so this is the general branch below with the constants folded
+        const double step = omega * (nrm - b) / (6.0 * nrm);
+        const double step1 = step * -2.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            const double w = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
+            x0.v[l] -= step * w;
+            x1.v[l] -= step1 * w;
+            x2.v[l] -= step * w;
+        }
+        return;
+    }
     double c0 = 1.0, c1 = -2.0, c2 = 1.0;
     if (pin == n) c0 = 0.0;
     else if (pin == n + 1) c1 = 0.0;

@@ -286,12 +286,78 @@ def optimize_fixture():
     np.savez_compressed(os.path.join(OUT, "optimize.npz"), **out)
 
 
+def analysis_fixtures():
+    """NUDFT adjoint / forward, density compensation, PSF + metrics, dwell resampling and
+    density compliance (analysis.py, core.py:286-311)."""
+    from vdtraj import analysis as an
+
+    rng = np.random.default_rng(424242)
+    out = {}
+    # raw NUDFT
+    for name, (p, grid) in {"a2": (200, (16, 13)), "a3": (150, (8, 7, 10))}.items():
+        pts = rng.uniform(-1, 1, (p, len(grid)))
+        w = rng.normal(size=p) + 1j * rng.normal(size=p)
+        img = rng.normal(size=grid) + 1j * rng.normal(size=grid)
+        out[f"{name}_pts"] = pts
+        out[f"{name}_grid"] = np.array(grid)
+        out[f"{name}_w"] = w
+        out[f"{name}_adj"] = an.nudft_adjoint(pts, w, grid)
+        out[f"{name}_img"] = img
+        out[f"{name}_fwd"] = an.nudft_forward(pts, img)
+    # density compensation and PSF on SPARKLING-like patterns
+    hw2 = core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                            dwell_dt=2e-6, fov=0.192, matrix=32, dims=2)
+    k2 = om.perturb(om.init_radial(8, 32, 2), 0.25, 0)
+    k3 = om.perturb(om.init_radial(4, 16, 3), 0.25, 0)
+    out["dcf2_coords"] = k2.coords
+    out["dcf2"] = an.density_compensation(k2, (16, 16), iters=3)
+    out["dcf3_coords"] = k3.coords
+    out["dcf3"] = an.density_compensation(k3, (8, 8, 8), iters=2)
+    psf2 = an.compute_psf(k2, (32, 32), weights=out["dcf2"])
+    out["psf2"] = psf2.values
+    out["psf2_peak"] = np.array(psf2.peak_index)
+    psf2h = an.compute_psf(k2, (24, 24), hw=hw2)
+    out["psf2h"] = psf2h.values
+    psf3 = an.compute_psf(k3, (12, 12, 12))
+    out["psf3"] = psf3.values
+    for name, psf in (("psf2", psf2), ("psf2h", psf2h), ("psf3", psf3)):
+        m = an.psf_metrics(psf)
+        out[f"{name}_metrics"] = np.array(list(m.fwhm) + [m.psl_db, m.pnl_db,
+                                                          float(m.fwhm_bounded)])
+    # a smooth synthetic PSF (Gaussian) for the FWHM interpolation
+    ax = np.arange(33) - 16
+    g = np.exp(-0.5 * (ax[:, None] ** 2 + ax[None, :] ** 2) / 2.0 ** 2)
+    gv = an.PsfVolume(values=g, peak_index=(16, 16), peak_value=1.0)
+    mg = an.psf_metrics(gv)
+    out["gauss"] = g
+    out["gauss_metrics"] = np.array(list(mg.fwhm) + [mg.psl_db, mg.pnl_db,
+                                                      float(mg.fwhm_bounded)])
+    # dwell resampling (ratio 5) and density compliance
+    out["dwell_in"] = k2.coords
+    out["dwell_out"] = core.resample_to_dwell(k2, hw2).coords
+    rho = density.discretize(density.DensityParams(0.25, 2.0), 16, 2)
+    l1, hs, hr = an.density_compliance(k2, rho, bins=8)
+    out["compl_l1"] = np.float64(l1)
+    out["compl_hs"] = hs
+    out["compl_hr"] = hr
+    np.savez_compressed(os.path.join(OUT, "analysis.npz"), **out)
+
+
 if __name__ == "__main__":
-    repulsion_fixtures()
-    attraction_fixtures()
-    projection_fixtures()
-    host_fixtures()
-    optimize_fixture()
+    which = sys.argv[1:] or ["repulsion", "attraction", "projection", "host", "optimize",
+                             "analysis"]
+    if "repulsion" in which:
+        repulsion_fixtures()
+    if "attraction" in which:
+        attraction_fixtures()
+    if "projection" in which:
+        projection_fixtures()
+    if "host" in which:
+        host_fixtures()
+    if "optimize" in which:
+        optimize_fixture()
+    if "analysis" in which:
+        analysis_fixtures()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
