@@ -30,13 +30,29 @@ constexpr int NU_THREADS = 128;
 constexpr int NU_UT = 64;   // u per adjoint tile
 constexpr int NU_VT = 32;   // v per adjoint tile
 constexpr int NU_VPT = 16;  // v per thread
-constexpr int NU_CH = 128;  // samples per shared-memory chunk
+#ifndef NU_CH_CFG
+#define NU_CH_CFG 64
+#endif
+constexpr int NU_CH = NU_CH_CFG;  // samples per shared-memory chunk (48 KB of tables)
 constexpr int NF_UT = 8;    // image rows (u) per forward stage
 constexpr int NF_VMAX = 1024;
 
 struct C2 {
     float x, y;
 };
+// Table row strides (complex elements), padded so that the row-per-thread generation
+// does not put a whole warp on one shared-memory bank; B rows stay 16-byte aligned for
+// the float4 reads of the product loop.
+constexpr int NU_AS = NU_UT + 1;
+constexpr int NU_BS = NU_VT + 2;
+
+// B rows are stored as (re_2k, re_2k+1, im_2k, im_2k+1) quadruples so that one float4
+// load yields the packed real and imaginary pairs the FFMA2s consume.
+__device__ __forceinline__ void put_b(C2* row, int q, double2 v) {
+    float* f = reinterpret_cast<float*>(row) + (q >> 1) * 4 + (q & 1);
+    f[0] = (float)v.x;
+    f[2] = (float)v.y;
+}
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -61,10 +77,10 @@ struct AdjParams {
 };
 
 // Generated operand tables for one chunk of samples.
-__global__ void __launch_bounds__(NU_THREADS) nudft_adjoint_kernel(const AdjParams P) {
+__global__ void __launch_bounds__(NU_THREADS, 4) nudft_adjoint_kernel(const AdjParams P) {
     extern __shared__ __align__(16) char sm[];
-    C2* At = reinterpret_cast<C2*>(sm);                 // [NU_CH][NU_UT]
-    C2* Bt = At + NU_CH * NU_UT;                        // [NU_CH][NU_VT]
+    C2* At = reinterpret_cast<C2*>(sm);                  // [NU_CH][NU_AS]
+    C2* Bt = At + ((NU_CH * NU_AS + 1) & ~1);            // [NU_CH][NU_BS], 16-B aligned
     const int tid = threadIdx.x;
     const long long u0 = (long long)blockIdx.x * NU_UT;
     const long long v0 = (long long)blockIdx.y * NU_VT;
@@ -80,25 +96,31 @@ __global__ void __launch_bounds__(NU_THREADS) nudft_adjoint_kernel(const AdjPara
 
     for (long long c0 = i_begin; c0 < i_end; c0 += NU_CH) {
         const int cnt = (int)min((long long)NU_CH, i_end - c0);
-        // ---- tables: thread j owns sample row j of the chunk
-        if (tid < NU_CH) {
-            const int j = tid;
+        // ---- tables: work item r < NU_CH builds A row r, r >= NU_CH builds B row r - NU_CH
+        for (int r = tid; r < 2 * NU_CH; r += NU_THREADS) {
+            const bool rowA = r < NU_CH;
+            const int j = rowA ? r : r - NU_CH;
             const long long i = c0 + j;
-            if (j < cnt) {
-                const double k0 = P.pts[i * P.dims];
-                const double k1 = P.pts[i * P.dims + 1];
-                const double2 wi = make_double2(P.w[2 * i], P.w[2 * i + 1]);
-                if (P.dims == 3) {
-                    const double k2 = P.pts[i * P.dims + 2];
+            if (j >= cnt) {
+                if (rowA)
+                    for (int q = 0; q < NU_UT; ++q) At[j * NU_AS + q] = C2{0.f, 0.f};
+                else
+                    for (int q = 0; q < NU_VT; ++q) Bt[j * NU_BS + q] = C2{0.f, 0.f};  // any layout
+                continue;
+            }
+            const double k0 = P.pts[i * P.dims];
+            const double k1 = P.pts[i * P.dims + 1];
+            const double2 wi = make_double2(P.w[2 * i], P.w[2 * i + 1]);
+            if (P.dims == 3) {
+                if (rowA) {
                     // A[u] = e0[a] e1[b], u = a * n1 + b, over this tile's u range
-                    long long u = u0;
-                    int a = (int)(u / P.n1), b = (int)(u - (long long)a * P.n1);
+                    int a = (int)(u0 / P.n1), b = (int)(u0 - (long long)a * P.n1);
                     double2 e0 = cispi(k0 * (double)(a - h0));
                     double2 e1 = cispi(k1 * (double)(b - h1));
                     const double2 z1 = cispi(k1);
                     for (int q = 0; q < NU_UT; ++q) {
                         const double2 v = cmul(e0, e1);
-                        At[j * NU_UT + q] = C2{(float)v.x, (float)v.y};
+                        At[j * NU_AS + q] = C2{(float)v.x, (float)v.y};
                         if (++b == P.n1) {
                             b = 0;
                             ++a;
@@ -108,30 +130,30 @@ __global__ void __launch_bounds__(NU_THREADS) nudft_adjoint_kernel(const AdjPara
                             e1 = cmul(e1, z1);
                         }
                     }
+                } else {
                     // B[v] = w e2[c], v = c
+                    const double k2 = P.pts[i * P.dims + 2];
                     double2 e2 = cmul(wi, cispi(k2 * (double)(v0 - h2)));
                     const double2 z2 = cispi(k2);
                     for (int q = 0; q < NU_VT; ++q) {
-                        Bt[j * NU_VT + q] = C2{(float)e2.x, (float)e2.y};
+                        put_b(Bt + j * NU_BS, q, e2);
                         e2 = cmul(e2, z2);
                     }
-                } else {
-                    double2 e0 = cmul(wi, cispi(k0 * (double)(u0 - h0)));
-                    const double2 z0 = cispi(k0);
-                    for (int q = 0; q < NU_UT; ++q) {
-                        At[j * NU_UT + q] = C2{(float)e0.x, (float)e0.y};
-                        e0 = cmul(e0, z0);
-                    }
-                    double2 e1 = cispi(k1 * (double)(v0 - h1));
-                    const double2 z1 = cispi(k1);
-                    for (int q = 0; q < NU_VT; ++q) {
-                        Bt[j * NU_VT + q] = C2{(float)e1.x, (float)e1.y};
-                        e1 = cmul(e1, z1);
-                    }
+                }
+            } else if (rowA) {
+                double2 e0 = cmul(wi, cispi(k0 * (double)(u0 - h0)));
+                const double2 z0 = cispi(k0);
+                for (int q = 0; q < NU_UT; ++q) {
+                    At[j * NU_AS + q] = C2{(float)e0.x, (float)e0.y};
+                    e0 = cmul(e0, z0);
                 }
             } else {
-                for (int q = 0; q < NU_UT; ++q) At[j * NU_UT + q] = C2{0.f, 0.f};
-                for (int q = 0; q < NU_VT; ++q) Bt[j * NU_VT + q] = C2{0.f, 0.f};
+                double2 e1 = cispi(k1 * (double)(v0 - h1));
+                const double2 z1 = cispi(k1);
+                for (int q = 0; q < NU_VT; ++q) {
+                    put_b(Bt + j * NU_BS, q, e1);
+                    e1 = cmul(e1, z1);
+                }
             }
         }
         __syncthreads();
@@ -141,14 +163,14 @@ __global__ void __launch_bounds__(NU_THREADS) nudft_adjoint_kernel(const AdjPara
         for (int k = 0; k < NU_VPT / 2; ++k) re[k] = im[k] = make_float2(0.f, 0.f);
 #pragma unroll 2
         for (int j = 0; j < cnt; ++j) {
-            const C2 a = At[j * NU_UT + u_loc];
-            const float4* brow = reinterpret_cast<const float4*>(Bt + j * NU_VT + vg * NU_VPT);
+            const C2 a = At[j * NU_AS + u_loc];
+            const float4* brow = reinterpret_cast<const float4*>(Bt + j * NU_BS + vg * NU_VPT);
             const float2 ax = make_float2(a.x, a.x), ay = make_float2(a.y, a.y);
             const float2 nay = make_float2(-a.y, -a.y);
 #pragma unroll
             for (int k = 0; k < NU_VPT / 2; ++k) {
-                const float4 b = brow[k];  // (re, im) of v = 2k, 2k + 1
-                const float2 br = make_float2(b.x, b.z), bi = make_float2(b.y, b.w);
+                const float4 b = brow[k];  // (re, re, im, im) of v = 2k, 2k + 1
+                const float2 br = make_float2(b.x, b.y), bi = make_float2(b.z, b.w);
                 re[k] = __ffma2_rn(ax, br, re[k]);
                 re[k] = __ffma2_rn(nay, bi, re[k]);
                 im[k] = __ffma2_rn(ax, bi, im[k]);
@@ -340,7 +362,7 @@ int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int d
     SPK_REQUIRE(ws_bytes >= (size_t)P.slices * P.U * P.V * 16, SPK_ERR_WORKSPACE,
                 "nudft adjoint: workspace too small");
     P.part = static_cast<double*>(ws);
-    const size_t smem = (size_t)NU_CH * (NU_UT + NU_VT) * sizeof(C2);
+    const size_t smem = ((size_t)((NU_CH * NU_AS + 1) & ~1) + (size_t)NU_CH * NU_BS) * sizeof(C2);
     cudaFuncSetAttribute(nudft_adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     dim3 grid3((unsigned)((P.U + NU_UT - 1) / NU_UT), (unsigned)((P.V + NU_VT - 1) / NU_VT),
