@@ -340,6 +340,19 @@ def analysis_fixtures():
     out["compl_l1"] = np.float64(l1)
     out["compl_hs"] = hs
     out["compl_hr"] = hr
+    # waveform export of a projected (feasible) and of a raw pattern
+    hw3 = core.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                            dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
+                            dims=3)
+    for name, kk in (("wf3", k3), ("wf2", k2)):
+        hw = hw3 if kk.dims == 3 else hw2
+        g, sl, rep = core.kspace_to_waveforms(kk, hw)
+        out[f"{name}_in"] = kk.coords
+        out[f"{name}_g"] = g
+        out[f"{name}_s"] = sl
+        out[f"{name}_rep"] = np.array([rep.max_grad, rep.max_slew, rep.grad_saturation_fraction,
+                                       rep.slew_saturation_fraction, float(rep.feasible)])
+        out[f"{name}_back"] = core.integrate_waveforms(kk.coords[:, 0, :], g, hw)
     np.savez_compressed(os.path.join(OUT, "analysis.npz"), **out)
 
 

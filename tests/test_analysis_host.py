@@ -76,3 +76,21 @@ def test_budget_guard_and_validation():
     psf = an.PsfVolume(values=np.zeros((4, 4)), peak_index=(0, 0), peak_value=0.0)
     with pytest.raises(ValueError, match="peak"):
         spk.psf_metrics(psf)
+
+
+def test_waveform_export_bitwise():
+    g = golden("analysis")
+    hw3 = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                           dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
+                           dims=3)
+    hw2 = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                           dwell_dt=2e-6, fov=0.192, matrix=32, dims=2)
+    for name, hw in (("wf3", hw3), ("wf2", hw2)):
+        k = spk.SamplingPattern(g[f"{name}_in"])
+        gr, sl, rep = spk.kspace_to_waveforms(k, hw)
+        assert np.array_equal(gr, g[f"{name}_g"]) and np.array_equal(sl, g[f"{name}_s"])
+        got = np.array([rep.max_grad, rep.max_slew, rep.grad_saturation_fraction,
+                        rep.slew_saturation_fraction, float(rep.feasible)])
+        assert np.array_equal(got, g[f"{name}_rep"])
+        back = spk.integrate_waveforms(k.coords[:, 0, :], gr, hw)
+        assert np.array_equal(back, g[f"{name}_back"])
