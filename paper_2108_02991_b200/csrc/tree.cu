@@ -12,9 +12,10 @@
 //    Chebyshev points, weights = sum of the Lagrange basis over its particles: the
 //    source-side interpolation of particle-cluster treecodes);
 //  * targets are taken in Morton order in groups of <= TR_GROUP that follow the octree
-//    (packed sibling subtrees, tree_host.cpp); each group gets a list of source segments (near particles or far proxies) and one CTA evaluates the
-//    weighted kernel sum over the concatenated list with packed f32x2 FMA + MUFU.RSQ,
-//    staging the segments through shared memory with cp.async double buffering.
+//    (packed sibling subtrees, tree_host.cpp); each group gets a list of source segments
+//    (near particles or far proxies) and one warp evaluates the weighted kernel sum over
+//    the concatenated list with packed f32x2 FMA + MUFU.RSQ, staging the segments
+//    through shared memory with cp.async double buffering.
 //
 // Deterministic: the tree, the lists and every reduction have a fixed order.
 #include <cub/cub.cuh>
@@ -25,9 +26,10 @@
 
 namespace spk {
 
-constexpr int TR_THREADS = 128;
-constexpr int TR_GROUP = 2 * TR_THREADS;  // targets per group / CTA (one f32x2 pair each)
-constexpr int TR_BATCH = 512;             // source records per shared-memory stage
+constexpr int TR_THREADS = 128;            // 4 warps per CTA, one target group per warp
+constexpr int TR_WARPS = TR_THREADS / 32;
+constexpr int TR_GROUP = 64;               // targets per group (32 lanes x one f32x2 pair)
+constexpr int TR_BATCH = 256;              // source records per warp and stage
 constexpr int P2M_THREADS = 128;
 constexpr int P2M_MAX_ORDER = 8;
 
@@ -441,19 +443,36 @@ struct EvalParams {
     double* grad;
 };
 
-// Cursor over the concatenated segment list of one group (uniform across the CTA).
+// Cursor over the concatenated segment list of one group (uniform across the warp).  The
+// segment descriptors are fetched 32 at a time (lane i holds descriptor base + i) so the
+// staging loop does not wait on one dependent global load per segment.
 struct SegCursor {
     long long s, s_end;
     int off;
+    long long base;  // first descriptor held in the lane window
+    long long w_start;
+    int w_cnt;
 };
 
-__device__ __forceinline__ int fill_batch(float4* buf, SegCursor& c, const EvalParams& P) {
+__device__ __forceinline__ void load_window(SegCursor& c, const EvalParams& P, int lane) {
+    c.base = c.s;
+    const long long d = c.s + lane;
+    c.w_start = d < c.s_end ? P.seg_start[d] : 0;
+    c.w_cnt = d < c.s_end ? P.seg_count[d] : 0;
+}
+
+// The warp stages the next TR_BATCH records of its concatenated segment list.
+__device__ __forceinline__ int fill_batch(float4* buf, SegCursor& c, const EvalParams& P,
+                                          int lane) {
     int filled = 0;
     while (filled < TR_BATCH && c.s < c.s_end) {
-        const int cnt = P.seg_count[c.s];
+        if (c.s - c.base >= 32) load_window(c, P, lane);
+        const int k = (int)(c.s - c.base);
+        const int cnt = __shfl_sync(0xffffffffu, c.w_cnt, k);
+        const long long start = __shfl_sync(0xffffffffu, c.w_start, k);
         const int take = min(TR_BATCH - filled, cnt - c.off);
-        const float4* g = P.src + P.seg_start[c.s] + c.off;
-        for (int i = threadIdx.x; i < take; i += TR_THREADS) cp_async16(buf + filled + i, g + i);
+        const float4* g = P.src + start + c.off;
+        for (int i = lane; i < take; i += 32) cp_async16(buf + filled + i, g + i);
         filled += take;
         c.off += take;
         if (c.off == cnt) {
@@ -496,13 +515,18 @@ __device__ __forceinline__ void eval_batch(const float4* __restrict__ buf, int c
     }
 }
 
+// One warp per target group (<= 64 targets, two per lane as one f32x2 pair): small
+// groups keep the near field small (near pairs per target grow with the group's
+// volume), and the warp walks its own segment list, double-buffered with cp.async.
 template <int D, bool G>
-__global__ void __launch_bounds__(TR_THREADS, 4) tree_eval_kernel(const EvalParams P) {
-    __shared__ __align__(16) float4 buf[2][TR_BATCH];
-    const int tid = threadIdx.x;
-    const long long g = blockIdx.x;
+__global__ void __launch_bounds__(TR_THREADS, 4) tree_eval_kernel(const EvalParams P,
+                                                                  long long n_groups) {
+    __shared__ __align__(16) float4 buf[TR_WARPS][2][TR_BATCH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long g = (long long)blockIdx.x * TR_WARPS + warp;
+    if (g >= n_groups) return;
     const long long gb = P.grp_begin[g], ge = P.grp_end[g];
-    const long long i0 = gb + tid, i1 = i0 + TR_THREADS;
+    const long long i0 = gb + lane, i1 = i0 + 32;
     const float4 a = P.tgt[min(i0, ge - 1)];
     const float4 b = P.tgt[min(i1, ge - 1)];
     const float2 X = make_float2(a.x, b.x), Y = make_float2(a.y, b.y),
@@ -510,20 +534,21 @@ __global__ void __launch_bounds__(TR_THREADS, 4) tree_eval_kernel(const EvalPara
     const float2 e2 = bcast(P.eps2);
     double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
 
-    SegCursor c{P.seg_off[g], P.seg_off[g + 1], 0};
-    int cnt = fill_batch(buf[0], c, P);
+    SegCursor c{P.seg_off[g], P.seg_off[g + 1], 0, 0, 0, 0};
+    load_window(c, P, lane);
+    int cnt = fill_batch(buf[warp][0], c, P, lane);
     int stage = 0;
     while (cnt > 0) {
-        const int next = fill_batch(buf[stage ^ 1], c, P);
+        const int next = fill_batch(buf[warp][stage ^ 1], c, P, lane);
         cp_async_wait<1>();
-        __syncthreads();
+        __syncwarp();
         float2 av = bcast(0.f), ax = bcast(0.f), ay = bcast(0.f), az = bcast(0.f);
-        eval_batch<D, G>(buf[stage], cnt, X, Y, Z, e2, av, ax, ay, az);
+        eval_batch<D, G>(buf[warp][stage], cnt, X, Y, Z, e2, av, ax, ay, az);
         acc[0][0] += av.x, acc[1][0] += av.y;
         acc[0][1] += ax.x, acc[1][1] += ax.y;
         acc[0][2] += ay.x, acc[1][2] += ay.y;
         if (D == 3) acc[0][3] += az.x, acc[1][3] += az.y;
-        __syncthreads();
+        __syncwarp();
         cnt = next;
         stage ^= 1;
     }
@@ -668,12 +693,13 @@ int spk_tree_eval(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_gro
     P.grad = grad;
     const bool guard = !(eps2 >= FLT_MIN);
     cudaStream_t s = (cudaStream_t)stream;
+    const unsigned blocks = (unsigned)((n_groups + TR_WARPS - 1) / TR_WARPS);
     if (dims == 3) {
-        if (guard) tree_eval_kernel<3, true><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
-        else tree_eval_kernel<3, false><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
+        if (guard) tree_eval_kernel<3, true><<<blocks, TR_THREADS, 0, s>>>(P, n_groups);
+        else tree_eval_kernel<3, false><<<blocks, TR_THREADS, 0, s>>>(P, n_groups);
     } else {
-        if (guard) tree_eval_kernel<2, true><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
-        else tree_eval_kernel<2, false><<<(unsigned)n_groups, TR_THREADS, 0, s>>>(P);
+        if (guard) tree_eval_kernel<2, true><<<blocks, TR_THREADS, 0, s>>>(P, n_groups);
+        else tree_eval_kernel<2, false><<<blocks, TR_THREADS, 0, s>>>(P, n_groups);
     }
     SPK_CHECK_LAUNCH("spk_tree_eval");
     return SPK_OK;

@@ -8,13 +8,14 @@ out for the B200 (csrc/tree.cu, csrc/tree_host.cpp):
 
   1. GPU: Morton keys of the float4 positions, CUB radix sort, gather sorted records.
   2. host: octree over the sorted keys (BFS, contiguous children, <= LEAF_CAP per leaf)
-     and target groups (<= TR_GROUP consecutive targets forming sibling subtrees).
+     and target groups (<= 64 consecutive targets forming sibling subtrees).
   3. GPU: tight node boxes (leaves reduce, levels merge bottom-up) and group boxes.
   4. GPU: one thread per target group walks the octree -> segments of near particles and
      of far-node proxies (q^d tensor Chebyshev points on the node's box); count pass,
      one 24-byte read-back of the totals, write pass.
-  5. GPU: P2M proxy weights; one CTA per target group sums the weighted kernel over its
-     segments (packed f32x2 FMA + MUFU.RSQ, fp64 accumulation per 512-record batch).
+  5. GPU: P2M proxy weights; one warp per target group (<= 64 targets) sums the weighted
+     kernel over its segments (packed f32x2 FMA + MUFU.RSQ, fp64 accumulation per
+     256-record batch).
 
 The (order, theta) table was calibrated on the B200 against the exact K1 kernel on the
 SPARKLING distributions (profiles/r01_tree_calibration.jsonl): every row meets its
@@ -30,13 +31,14 @@ from . import _device, _native
 
 # (precision floor, interpolation order, opening threshold) -- same role as the
 # reference's _AUTO_PARAMS (repulsion.py:24-30), calibrated for this scheme on the B200
-# (profiles/r01_tree_calibration.jsonl: worst gradient error over the C1, C2, 3D-radial
-# and uniform clouds is at least 1.9x below the floor).  Below 1e-6 the fp32 pair
-# arithmetic itself (~3e-7 vs fp64) is the limit: such precisions run the exact kernel.
+# (profiles/r01_tree_calibration.jsonl, r01_tree_att_calibration.jsonl): the worst
+# gradient error over the C1, C2, C4, 3D-radial and uniform clouds, repulsion and lattice
+# attraction, is at least 2.5x below the floor.  Below 1e-6 the fp32 pair arithmetic
+# itself (~3e-7 vs fp64) is the limit: such precisions run the exact kernels.
 AUTO_PARAMS = (
     (1e-2, 3, 0.8),
-    (1e-3, 4, 0.8),
-    (1e-4, 5, 0.8),
+    (1e-3, 4, 0.7),
+    (1e-4, 5, 0.7),
     (1e-5, 6, 0.7),
     (1e-6, 6, 0.5),
 )
@@ -252,10 +254,21 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
     the call); otherwise proxies are built for the nodes this traversal opens as far."""
     if not 2 <= order <= MAX_ORDER:
         raise ValueError(f"interp_order must be in [2, {MAX_ORDER}]")
+    import time
+
     dev = src.rec.device
     st = _device.stream()
     dims, n_s, m = src.dims, src.n, order ** src.dims
     n_nodes, n_groups = src.n_nodes, tg.n_groups
+    timing = stats is not None and stats.get("timing", False)
+    marks = []
+
+    def mark(name):
+        if timing:
+            torch.cuda.synchronize()
+            marks.append((name, time.perf_counter()))
+
+    mark("start")
     slot_of = torch.empty(n_nodes, dtype=torch.int32, device=dev)
     slot_node = torch.empty(n_nodes, dtype=torch.int32, device=dev)
     slot_box = torch.empty((n_nodes, 6), dtype=torch.float32, device=dev)
@@ -271,6 +284,7 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  slot_unit_off.data_ptr(), seg_off.data_ptr(), totals.data_ptr(),
                  ws.data_ptr(), ws.numel(), st)
     n_seg, n_slots, n_units = (int(x) for x in totals.cpu().numpy())
+    mark("plan_count")
     if static:
         rec, write_slot_of = src.static_proxies(order)
         n_units_w = 0
@@ -291,6 +305,7 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  0 if static else n_slots, seg_off.data_ptr(), seg_start.data_ptr(),
                  seg_count.data_ptr(), unit_slot.data_ptr(), unit_begin.data_ptr(),
                  unit_end.data_ptr(), st)
+    mark("plan_write")
     if not static and n_slots:
         ws2 = _device.workspace(_native.query("spk_tree_p2m_workspace_bytes", n_units, order,
                                               dims), "tree_p2m")
@@ -298,6 +313,7 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                      unit_begin.data_ptr(), unit_end.data_ptr(), n_slots,
                      slot_unit_off.data_ptr(), slot_box.data_ptr(), order, dims,
                      rec[n_s:].data_ptr(), ws2.data_ptr(), ws2.numel(), st)
+    mark("p2m")
     if val is None:
         val = torch.empty(tg.n, dtype=torch.float64, device=dev)
     if grad is None:
@@ -306,6 +322,10 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  tg.d_gb.data_ptr(), tg.d_ge.data_ptr(), rec.data_ptr(), seg_off.data_ptr(),
                  seg_start.data_ptr(), seg_count.data_ptr(), dims, float(eps2),
                  val.data_ptr(), grad.data_ptr(), st)
+    mark("eval")
+    if timing:
+        stats["eval_phases_ms"] = {marks[i][0]: 1e3 * (marks[i][1] - marks[i - 1][1])
+                                   for i in range(1, len(marks))}
     if stats is not None:
         so = seg_off.cpu().numpy()
         sc = seg_count[:n_seg].cpu().numpy().astype(np.int64)
