@@ -13,7 +13,40 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2108_02991_b200 as spk  # noqa: E402
+from paper_2108_02991_b200 import engine  # noqa: E402
 from paper_2108_02991_b200 import optimizer as om  # noqa: E402
+
+
+class PhaseOps(engine.CudaOps):
+    """CUDA-event timing of the N-body sums and the projection, per level (by N_s)."""
+
+    def __init__(self):
+        super().__init__()
+        self.ev = {}
+
+    def _t(self, key, fn, *a, **k):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn(*a, **k)
+        e.record()
+        self.ev.setdefault(key, []).append((s, e))
+        return out
+
+    def sums(self, tgt4, *a, **k):
+        return self._t(("nbody", a[1].shape[1] if a[1].dim() == 3 else 0), super().sums,
+                       tgt4, *a, **k)
+
+    def project(self, coords, *a, **k):
+        return self._t(("project", coords.shape[1]), super().project, coords, *a, **k)
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for (name, n_s), v in sorted(self.ev.items()):
+            ms = [s.elapsed_time(e) for s, e in v]
+            out.setdefault(str(n_s), {})[name] = {"calls": len(ms), "mean_ms": float(np.mean(ms)),
+                                                  "total_s": float(np.sum(ms)) / 1e3}
+        return out
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n-git", type=int, default=100)
@@ -32,7 +65,8 @@ cfg = spk.OptimizerConfig(n_c=a.n_c, n_s=a.n_s, dims=3, n_decim=6, n_git=a.n_git
 rho = spk.discretize_anisotropic(spk.DensityParams(0.25, 2.0), (192, 192, 104), 3)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-state = om.start(cfg, hw, rho)
+ops = PhaseOps()
+state = om.start(cfg, hw, rho, ops=ops)
 torch.cuda.synchronize()
 t_start = time.perf_counter() - t0
 while om.step(state) is not None:
@@ -58,4 +92,4 @@ if a.trace:
 print(json.dumps(dict(workload="full3d schedule: %d x %d, n_decim 6, n_git %d" %
                       (a.n_c, a.n_s, a.n_git), total_wall_s=t_total, setup_s=t_start,
                       iterations=len(recs), levels=levels, final_feasibility=feas,
-                      final_cost=recs[-1].cost)))
+                      final_cost=recs[-1].cost, phases_by_samples_per_shot=ops.summary())))
