@@ -200,6 +200,27 @@ int spk_tree_gather(const void* pos, const int32_t* perm, int64_t n, const float
 int spk_tree_boxes(const void* rec, int64_t n_ranges, const int64_t* begin,
                    const int64_t* end, int dims, float* box, spk_stream_t stream);
 
+/* Octree over sorted keys on the GPU, level by level (build_tree, _treecode.py:77-170):
+ * BFS node order, children contiguous in child-digit order, a node splits when it holds
+ * more than leaf_cap particles and is above the finest level -- the same tree as
+ * spk_tree_host_build.  Device outputs node_begin/node_end [capacity] i64, first_child /
+ * n_child [capacity] i32 (first_child -1 for leaves), leaf_node [capacity] i32; HOST
+ * outputs level_off [64] (level l = nodes [off[l], off[l+1])) and counts [3] = nodes,
+ * leaves, levels.  Returns SPK_ERR_WORKSPACE when node_capacity is too small (retry). */
+size_t spk_tree_build_workspace_bytes(int64_t n, int64_t node_capacity);
+int spk_tree_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
+                   int64_t node_capacity, int64_t* node_begin, int64_t* node_end,
+                   int32_t* first_child, int32_t* n_child, int32_t* leaf_node,
+                   int64_t* level_off, int64_t* counts, void* ws, size_t ws_bytes,
+                   spk_stream_t stream);
+/* Target groups of <= cap particles following the octree (spk_tree_host_groups),
+ * sorted by first particle: grp_begin/grp_end [group_capacity] i64 (device), n_groups
+ * HOST.  Workspace: spk_tree_build_workspace_bytes(0, max(n_nodes, group_capacity)). */
+int spk_tree_groups(const int64_t* node_begin, const int64_t* node_end,
+                    const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
+                    int64_t cap, int64_t group_capacity, int64_t* grp_begin, int64_t* grp_end,
+                    int64_t* n_groups, void* ws, size_t ws_bytes, spk_stream_t stream);
+
 /* Node boxes {min xyz, max xyz} of an octree over sorted records: leaves reduce their
  * particles, internal nodes (BFS levels, level_off is a HOST array of n_levels + 1
  * offsets) merge their children bottom-up.  node_box: [n_nodes][6] f32 (device). */

@@ -20,6 +20,7 @@
 // Deterministic: the tree, the lists and every reduction have a fixed order.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "spk_common.cuh"
@@ -237,6 +238,137 @@ __global__ void p2m_final_kernel(const double* __restrict__ part,
     }
 }
 
+
+// ---------------------------------------------------------------- device octree build
+// Level-synchronous construction over the sorted Morton keys, identical to the host
+// builder (tree_host.cpp spk_tree_host_build): BFS node order, children contiguous and in
+// child-digit order, a node splits when it holds more than leaf_cap particles and is above
+// the finest level.  One thread per node of the current level finds its children by
+// binary search; a scan of the child counts places the next level.
+__device__ __forceinline__ long long lower_bound_u64(const uint64_t* __restrict__ keys,
+                                                     long long lo, long long hi, uint64_t v) {
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (keys[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void split_kernel(const uint64_t* __restrict__ keys, const long long* __restrict__ nbeg,
+                             const long long* __restrict__ nend, long long lv_b, long long lv_e,
+                             int level, int dims, int bits, long long cap,
+                             int32_t* __restrict__ nchild, long long* __restrict__ child) {
+    const long long v = lv_b + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= lv_e) return;
+    const long long b = nbeg[v], e = nend[v];
+    const long long w = v - lv_b;
+    if (e - b <= cap || level >= bits) {
+        nchild[w] = 0;
+        return;
+    }
+    const int nc = 1 << dims;
+    const int shift = dims * (bits - level - 1);
+    const uint64_t prefix = keys[b] >> (shift + dims);
+    long long lo = b;
+    int cnt = 0;
+    for (int c = 0; c < nc; ++c) {
+        long long hi = e;
+        if (c + 1 < nc) hi = lower_bound_u64(keys, lo, e, ((prefix << dims) | (uint64_t)(c + 1)) << shift);
+        if (hi > lo) {
+            child[w * 16 + 2 * cnt] = lo;
+            child[w * 16 + 2 * cnt + 1] = hi;
+            ++cnt;
+        }
+        lo = hi;
+    }
+    nchild[w] = cnt;
+}
+
+__global__ void link_kernel(const int32_t* __restrict__ nchild, const int32_t* __restrict__ off,
+                            const long long* __restrict__ child, long long lv_b, long long lv_e,
+                            long long* __restrict__ nbeg, long long* __restrict__ nend,
+                            int32_t* __restrict__ first_child, int32_t* __restrict__ n_child) {
+    const long long v = lv_b + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= lv_e) return;
+    const long long w = v - lv_b;
+    const int nc = nchild[w];
+    n_child[v] = nc;
+    first_child[v] = nc ? (int32_t)(lv_e + off[w]) : -1;
+    for (int k = 0; k < nc; ++k) {
+        const long long u = lv_e + off[w] + k;
+        nbeg[u] = child[w * 16 + 2 * k];
+        nend[u] = child[w * 16 + 2 * k + 1];
+    }
+}
+
+__global__ void root_kernel(long long n, long long* nbeg, long long* nend) {
+    nbeg[0] = 0;
+    nend[0] = n;
+}
+
+__global__ void leaf_flag_kernel(const int32_t* __restrict__ n_child, long long n_nodes,
+                                 int32_t* __restrict__ flag) {
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v < n_nodes) flag[v] = n_child[v] == 0;
+}
+
+__global__ void leaf_write_kernel(const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
+                                  long long n_nodes, int32_t* __restrict__ leaf_node) {
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v < n_nodes && flag[v]) leaf_node[pos[v]] = (int32_t)v;
+}
+
+// Target groups (tree_host.cpp spk_tree_host_groups): under every node holding more than
+// `cap` particles, maximal runs of consecutive children with <= cap particles are packed
+// greedily into groups of <= cap; oversized leaves are cut into chunks; a root with
+// <= cap particles is one group.  Pass 0 counts per node, pass 1 writes; the groups are
+// then sorted by their first particle.
+template <int PASS>
+__global__ void groups_kernel(const long long* __restrict__ nbeg, const long long* __restrict__ nend,
+                              const int32_t* __restrict__ first_child,
+                              const int32_t* __restrict__ n_child, long long n_nodes,
+                              long long cap, long long* __restrict__ cnt_out,
+                              const long long* __restrict__ off, long long* __restrict__ gb,
+                              long long* __restrict__ ge) {
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n_nodes) return;
+    const long long b = nbeg[v], e = nend[v];
+    long long k = 0;
+    const long long o = PASS ? off[v] : 0;
+    auto emit = [&](long long x, long long y) {
+        if (PASS) {
+            gb[o + k] = x;
+            ge[o + k] = y;
+        }
+        ++k;
+    };
+    if (e - b <= cap) {
+        if (v == 0) emit(b, e);
+    } else if (n_child[v] == 0) {
+        for (long long x = b; x < e; x += cap) emit(x, min(e, x + cap));
+    } else {
+        long long cb = -1, ce = -1;
+        for (int c = 0; c < n_child[v]; ++c) {
+            const long long u = first_child[v] + c;
+            const long long ub = nbeg[u], ue = nend[u];
+            if (ue - ub > cap) {
+                if (cb >= 0) emit(cb, ce);
+                cb = -1;
+                continue;
+            }
+            if (cb >= 0 && ue - cb <= cap) {
+                ce = ue;
+            } else {
+                if (cb >= 0) emit(cb, ce);
+                cb = ub;
+                ce = ue;
+            }
+        }
+        if (cb >= 0) emit(cb, ce);
+    }
+    if (!PASS) cnt_out[v] = k;
+}
 
 // ---------------------------------------------------------------- device plan
 // Node boxes bottom-up: leaves reduce their particles (boxes_kernel with dst = node id),
@@ -849,6 +981,153 @@ int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
             reinterpret_cast<long long*>(unit_end));
         SPK_CHECK_LAUNCH("spk_tree_plan_write(units)");
     }
+    return SPK_OK;
+}
+
+size_t spk_tree_build_workspace_bytes(int64_t n, int64_t node_capacity) {
+    const long long m = node_capacity + 1;
+    size_t a = 0, b = 0, c = 0, d = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (const int32_t*)nullptr, (int32_t*)nullptr, (int)m);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const long long*)nullptr, (long long*)nullptr,
+                                  (int)m);
+    cub::DeviceRadixSort::SortPairs(nullptr, c, (const long long*)nullptr, (long long*)nullptr,
+                                    (const long long*)nullptr, (long long*)nullptr, (int)m);
+    d = std::max(std::max(a, b), c);
+    // nchild i32 + off i32 (m each), child ranges (16 i64 per node), group counts/offsets
+    // (2 x m i64), group sort buffers (4 x m i64)
+    return ((d + 255) & ~(size_t)255) + (size_t)m * (4 + 4 + 128 + 16 + 32) + 4096;
+}
+
+namespace {
+struct BuildWs {
+    void* cub;
+    size_t cub_bytes;
+    int32_t* nchild;
+    int32_t* off;
+    long long* child;
+    long long* gcnt;
+    long long* goff;
+    long long* sort_k;
+    long long* sort_v;
+};
+BuildWs build_ws(void* ws, size_t ws_bytes, long long m) {
+    BuildWs w;
+    const size_t fixed = (size_t)m * (4 + 4 + 128 + 16 + 32) + 4096;
+    w.cub_bytes = (ws_bytes - fixed) & ~(size_t)255;
+    char* p = static_cast<char*>(ws);
+    w.cub = p;
+    p += w.cub_bytes;
+    auto take = [&](size_t bytes) {
+        char* q = p;
+        p += (bytes + 255) & ~(size_t)255;
+        return q;
+    };
+    w.nchild = reinterpret_cast<int32_t*>(take((size_t)m * 4));
+    w.off = reinterpret_cast<int32_t*>(take((size_t)m * 4));
+    w.child = reinterpret_cast<long long*>(take((size_t)m * 128));
+    w.gcnt = reinterpret_cast<long long*>(take((size_t)m * 8));
+    w.goff = reinterpret_cast<long long*>(take((size_t)m * 8));
+    w.sort_k = reinterpret_cast<long long*>(take((size_t)m * 16));
+    w.sort_v = reinterpret_cast<long long*>(take((size_t)m * 16));
+    return w;
+}
+}  // namespace
+
+int spk_tree_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
+                   int64_t node_capacity, int64_t* node_begin, int64_t* node_end,
+                   int32_t* first_child, int32_t* n_child, int32_t* leaf_node,
+                   int64_t* level_off, int64_t* counts, void* ws, size_t ws_bytes,
+                   spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(n >= 1 && leaf_cap >= 1, SPK_ERR_ARG, "tree build: n=%lld leaf_cap=%lld",
+                (long long)n, (long long)leaf_cap);
+    SPK_REQUIRE(ws_bytes >= spk_tree_build_workspace_bytes(n, node_capacity), SPK_ERR_WORKSPACE,
+                "tree build: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int bits = dims == 3 ? 21 : 31;
+    BuildWs w = build_ws(ws, ws_bytes, node_capacity + 1);
+    long long* nb = reinterpret_cast<long long*>(node_begin);
+    long long* ne = reinterpret_cast<long long*>(node_end);
+    root_kernel<<<1, 1, 0, s>>>(n, nb, ne);
+    long long lv_b = 0, lv_e = 1;
+    int level = 0;
+    level_off[0] = 0;
+    int32_t total_h = 0;
+    while (lv_e > lv_b) {
+        const long long m = lv_e - lv_b;
+        SPK_REQUIRE(lv_e + 8 * m <= node_capacity, SPK_ERR_WORKSPACE,
+                    "tree build: node capacity %lld exceeded", (long long)node_capacity);
+        SPK_REQUIRE(level < 63, SPK_ERR_ARG, "tree build: too many levels");
+        const unsigned blocks = (unsigned)((m + 127) / 128);
+        split_kernel<<<blocks, 128, 0, s>>>(keys, nb, ne, lv_b, lv_e, level, dims, bits,
+                                            (long long)leaf_cap, w.nchild, w.child);
+        cudaMemsetAsync(w.nchild + m, 0, 4, s);
+        size_t t = w.cub_bytes;
+        cudaError_t e = cub::DeviceScan::ExclusiveSum(w.cub, t, w.nchild, w.off, (int)(m + 1), s);
+        SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree build scan: %s", cudaGetErrorString(e));
+        link_kernel<<<blocks, 128, 0, s>>>(w.nchild, w.off, w.child, lv_b, lv_e, nb, ne,
+                                           first_child, n_child);
+        e = cudaMemcpyAsync(&total_h, w.off + m, 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree build: %s", cudaGetErrorString(e));
+        level_off[++level] = lv_e;
+        lv_b = lv_e;
+        lv_e += total_h;
+    }
+    SPK_CHECK_LAUNCH("spk_tree_build(levels)");
+    const long long n_nodes = lv_e;
+    // leaves in BFS order
+    const unsigned nb_blocks = (unsigned)((n_nodes + 255) / 256);
+    leaf_flag_kernel<<<nb_blocks, 256, 0, s>>>(n_child, n_nodes, w.nchild);
+    cudaMemsetAsync(w.nchild + n_nodes, 0, 4, s);
+    size_t t = w.cub_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(w.cub, t, w.nchild, w.off, (int)(n_nodes + 1), s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree build scan: %s", cudaGetErrorString(e));
+    leaf_write_kernel<<<nb_blocks, 256, 0, s>>>(w.nchild, w.off, n_nodes, leaf_node);
+    SPK_CHECK_LAUNCH("spk_tree_build(leaves)");
+    e = cudaMemcpyAsync(&total_h, w.off + n_nodes, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree build: %s", cudaGetErrorString(e));
+    counts[0] = n_nodes;
+    counts[1] = total_h;
+    counts[2] = level;  // level_off has level + 1 entries
+    return SPK_OK;
+}
+
+int spk_tree_groups(const int64_t* node_begin, const int64_t* node_end,
+                    const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
+                    int64_t cap, int64_t group_capacity, int64_t* grp_begin, int64_t* grp_end,
+                    int64_t* n_groups, void* ws, size_t ws_bytes, spk_stream_t stream) {
+    SPK_REQUIRE(cap >= 1, SPK_ERR_ARG, "tree groups: cap must be >= 1");
+    SPK_REQUIRE(ws_bytes >= spk_tree_build_workspace_bytes(0, std::max(n_nodes, group_capacity)),
+                SPK_ERR_WORKSPACE, "tree groups: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    BuildWs w = build_ws(ws, ws_bytes, std::max(n_nodes, group_capacity) + 1);
+    const long long* nb = reinterpret_cast<const long long*>(node_begin);
+    const long long* ne = reinterpret_cast<const long long*>(node_end);
+    const unsigned blocks = (unsigned)((n_nodes + 127) / 128);
+    groups_kernel<0><<<blocks, 128, 0, s>>>(nb, ne, first_child, n_child, n_nodes, cap, w.gcnt,
+                                            nullptr, nullptr, nullptr);
+    cudaMemsetAsync(w.gcnt + n_nodes, 0, 8, s);
+    size_t t = w.cub_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(w.cub, t, w.gcnt, w.goff, (int)(n_nodes + 1), s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree groups scan: %s", cudaGetErrorString(e));
+    long long total = 0;
+    e = cudaMemcpyAsync(&total, w.goff + n_nodes, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree groups: %s", cudaGetErrorString(e));
+    *n_groups = total;
+    SPK_REQUIRE(total <= group_capacity, SPK_ERR_WORKSPACE,
+                "tree groups: %lld groups exceed capacity %lld", total, (long long)group_capacity);
+    groups_kernel<1><<<blocks, 128, 0, s>>>(nb, ne, first_child, n_child, n_nodes, cap, nullptr,
+                                            w.goff, w.sort_k, w.sort_v);
+    SPK_CHECK_LAUNCH("spk_tree_groups");
+    t = w.cub_bytes;
+    e = cub::DeviceRadixSort::SortPairs(w.cub, t, w.sort_k,
+                                        reinterpret_cast<long long*>(grp_begin), w.sort_v,
+                                        reinterpret_cast<long long*>(grp_end), (int)total, 0, 40,
+                                        s);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree groups sort: %s", cudaGetErrorString(e));
     return SPK_OK;
 }
 

@@ -7,8 +7,10 @@ direct summation.  This module keeps the contract with a particle-cluster treeco
 out for the B200 (csrc/tree.cu, csrc/tree_host.cpp):
 
   1. GPU: Morton keys of the float4 positions, CUB radix sort, gather sorted records.
-  2. host: octree over the sorted keys (BFS, contiguous children, <= LEAF_CAP per leaf)
-     and target groups (<= 64 consecutive targets forming sibling subtrees).
+  2. GPU: octree over the sorted keys, level by level (BFS, contiguous children,
+     <= LEAF_CAP per leaf), and target groups (<= 64 consecutive targets forming sibling
+     subtrees); the serial host builder (tree_host.cpp) is the reference it is tested
+     against.
   3. GPU: tight node boxes (leaves reduce, levels merge bottom-up) and group boxes.
   4. GPU: one thread per target group walks the octree -> segments of near particles and
      of far-node proxies (q^d tensor Chebyshev points on the node's box); count pass,
@@ -110,6 +112,58 @@ def _node_tables(lib, tree):
     return dict(nb=nb, ne=ne, fc=fc, nc=nc, leaves=leaves, levels=lv)
 
 
+class _DeviceOctree:
+    """Octree over sorted keys built on the GPU (spk_tree_build): node tables on the
+    device, BFS level offsets on the host.  Same nodes as the host builder."""
+
+    def __init__(self, keys: torch.Tensor, n: int, dims: int, leaf_cap: int):
+        dev = keys.device
+        st = _device.stream()
+        cap = 16 * n // max(leaf_cap, 1) + 1024
+        while True:
+            self.nb = torch.empty(cap, dtype=torch.int64, device=dev)
+            self.ne = torch.empty(cap, dtype=torch.int64, device=dev)
+            self.fc = torch.empty(cap, dtype=torch.int32, device=dev)
+            self.nc = torch.empty(cap, dtype=torch.int32, device=dev)
+            self.leaves = torch.empty(cap, dtype=torch.int32, device=dev)
+            self.levels = np.zeros(64, dtype=np.int64)
+            counts = np.zeros(3, dtype=np.int64)
+            ws = _device.workspace(_native.query("spk_tree_build_workspace_bytes", n, cap),
+                                   "tree_build")
+            try:
+                _native.call("spk_tree_build", keys.data_ptr(), n, dims, leaf_cap, cap,
+                             self.nb.data_ptr(), self.ne.data_ptr(), self.fc.data_ptr(),
+                             self.nc.data_ptr(), self.leaves.data_ptr(), self.levels.ctypes.data,
+                             counts.ctypes.data, ws.data_ptr(), ws.numel(), st)
+                break
+            except _native.NativeError as exc:
+                if "capacity" not in str(exc):
+                    raise
+                cap *= 2
+        self.n_nodes, self.n_leaves, n_lv = (int(c) for c in counts)
+        self.levels = self.levels[:n_lv + 1].copy()
+        _native.add_launches(3 * n_lv + 3)
+        self.nb, self.ne = self.nb[:self.n_nodes], self.ne[:self.n_nodes]
+        self.fc, self.nc = self.fc[:self.n_nodes], self.nc[:self.n_nodes]
+        self.leaves = self.leaves[:self.n_leaves]
+
+    def groups(self, cap: int):
+        """Target groups (spk_tree_groups) -> device (begin, end) sorted by begin."""
+        dev = self.nb.device
+        gcap = max(self.n_nodes * 8, int(self.ne[:1].item() // cap) * 4 + 1024)
+        gb = torch.empty(gcap, dtype=torch.int64, device=dev)
+        ge = torch.empty(gcap, dtype=torch.int64, device=dev)
+        n_groups = np.zeros(1, dtype=np.int64)
+        ws = _device.workspace(_native.query("spk_tree_build_workspace_bytes", 0,
+                                             max(self.n_nodes, gcap)), "tree_groups")
+        _native.call("spk_tree_groups", self.nb.data_ptr(), self.ne.data_ptr(),
+                     self.fc.data_ptr(), self.nc.data_ptr(), self.n_nodes, cap, gcap,
+                     gb.data_ptr(), ge.data_ptr(), n_groups.ctypes.data, ws.data_ptr(),
+                     ws.numel(), _device.stream())
+        k = int(n_groups[0])
+        return gb[:k], ge[:k]
+
+
 class SourceTree:
     """Sources sorted along the Morton curve, their octree and tight node boxes, resident
     on the device.  ``weights`` (fp32 device, per source in input order) makes a weighted
@@ -125,29 +179,24 @@ class SourceTree:
         st = _device.stream()
         self.dims, self.n = dims, src4.shape[0]
         self.keys, self.perm = _sort(src4, dims)
-        tree = _host_tree(lib, self.keys, self.n, dims, leaf_cap)
-        try:
-            T = _node_tables(lib, tree)
-            self.groups_host = _groups(lib, tree, lib.spk_tree_group_size())
-        except BaseException:
-            lib.spk_tree_host_free(tree)
-            raise
-        if keep_host:
-            self.host = tree
-        else:
-            lib.spk_tree_host_free(tree)
-            self.host = None
-        self.tables = T
-        self.n_nodes, self.n_leaves = T["nb"].shape[0], T["leaves"].shape[0]
+        octree = _DeviceOctree(self.keys, self.n, dims, leaf_cap)
+        self.octree = octree
+        self.host = None
+        if keep_host:  # the serial host builder, for the tests' cross-checks
+            self.host = _host_tree(lib, self.keys, self.n, dims, leaf_cap)
+            self.tables = _node_tables(lib, self.host)
+        self.n_nodes, self.n_leaves = octree.n_nodes, octree.n_leaves
         self.d_nb, self.d_ne, self.d_fc, self.d_nc, self.d_leaves = (
-            _to_dev(T[k], dev) for k in ("nb", "ne", "fc", "nc", "leaves"))
+            octree.nb, octree.ne, octree.fc, octree.nc, octree.leaves)
+        self.levels = octree.levels
+        self._groups = None
         self.rec = torch.empty((self.n, 4), dtype=torch.float32, device=dev)
         _native.call("spk_tree_gather", src4.data_ptr(), self.perm.data_ptr(), self.n,
                      _device.ptr(weights), self.rec.data_ptr(), st)
         self.node_box = torch.empty((self.n_nodes, 6), dtype=torch.float32, device=dev)
         lb = self.d_nb[self.d_leaves.long()]
         le = self.d_ne[self.d_leaves.long()]
-        lv = T["levels"]
+        lv = self.levels
         _native.call("spk_tree_node_boxes", self.rec.data_ptr(), self.n_nodes,
                      self.d_fc.data_ptr(), self.d_nc.data_ptr(), self.n_leaves,
                      self.d_leaves.data_ptr(), lb.data_ptr(), le.data_ptr(), lv.shape[0] - 1,
@@ -156,6 +205,12 @@ class SourceTree:
         self._static = {}
         for q in proxy_orders:
             self.static_proxies(q)
+
+    def groups(self):
+        """Target groups of these particles used as targets (device begin, end)."""
+        if self._groups is None:
+            self._groups = self.octree.groups(_native.load().spk_tree_group_size())
+        return self._groups
 
     def close(self):
         if self.host:
@@ -178,7 +233,7 @@ class SourceTree:
         dev = self.rec.device
         st = _device.stream()
         m = order ** self.dims
-        T = self.tables
+        T = {"nb": self.d_nb.cpu().numpy(), "ne": self.d_ne.cpu().numpy()}
         cnt = T["ne"] - T["nb"]
         eligible = cnt > m
         slot_of = np.where(eligible, np.cumsum(eligible) - 1, -1).astype(np.int32)
@@ -227,20 +282,14 @@ class TargetGroups:
         group = lib.spk_tree_group_size()
         if same_as is not None:
             self.perm, self.rec = same_as.perm, same_as.rec
-            gb, ge = same_as.groups_host
+            self.d_gb, self.d_ge = same_as.groups()
         else:
             keys, self.perm = _sort(tgt4, dims)
             self.rec = torch.empty((self.n, 4), dtype=torch.float32, device=dev)
             _native.call("spk_tree_gather", tgt4.data_ptr(), self.perm.data_ptr(), self.n,
                          None, self.rec.data_ptr(), st)
-            tree = _host_tree(lib, keys, self.n, dims, group)
-            try:
-                gb, ge = _groups(lib, tree, group)
-            finally:
-                lib.spk_tree_host_free(tree)
-        self.gb_host, self.ge_host = gb, ge
-        self.n_groups = gb.shape[0]
-        self.d_gb, self.d_ge = _to_dev(gb, dev), _to_dev(ge, dev)
+            self.d_gb, self.d_ge = _DeviceOctree(keys, self.n, dims, group).groups(group)
+        self.n_groups = self.d_gb.shape[0]
         self.box = torch.empty((self.n_groups, 6), dtype=torch.float32, device=dev)
         _native.call("spk_tree_boxes", self.rec.data_ptr(), self.n_groups, self.d_gb.data_ptr(),
                      self.d_ge.data_ptr(), dims, self.box.data_ptr(), st)
@@ -331,9 +380,10 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
         sc = seg_count[:n_seg].cpu().numpy().astype(np.int64)
         per_group = np.add.reduceat(np.append(sc, 0), np.minimum(so[:-1], n_seg)) * \
             (so[1:] > so[:-1])
+        sizes = (tg.d_ge - tg.d_gb).cpu().numpy()
         stats.update(nodes=n_nodes, leaves=src.n_leaves, groups=n_groups, segments=n_seg,
                      slots=n_slots, units=n_units, interp_order=order, opening_theta=theta,
-                     pairs=int(np.dot(per_group, tg.ge_host - tg.gb_host)))
+                     pairs=int(np.dot(per_group, sizes)))
     if lists is not None:
         lists.update(seg_off=seg_off.cpu().numpy(), seg_start=seg_start[:n_seg].cpu().numpy(),
                      seg_count=seg_count[:n_seg].cpu().numpy(),

@@ -224,3 +224,34 @@ def test_optimize_tree_attraction_and_repulsion(spk):
     ct, cd = r_t.trace.records[-1], r_d.trace.records[-1]
     assert abs(ct.cost - cd.cost) / abs(cd.cost) < 1e-4
     assert np.abs(r_t.pattern.coords - r_d.pattern.coords).max() < 1e-3
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_device_octree_matches_host_builder(spk, dims):
+    """spk_tree_build / spk_tree_groups (GPU) == spk_tree_host_build / _groups (host)."""
+    from paper_2108_02991_b200 import _device, _native, tree
+
+    lib = _native.load()
+    rng = np.random.default_rng(17 + dims)
+    pts = np.concatenate([rng.uniform(-1, 1, (30000, dims)),
+                          rng.normal(0, 0.02, (30000, dims)).clip(-1, 1)])
+    pts[:500] = pts[500]  # duplicate keys -> leaves at the finest level
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    keys, _ = tree._sort(pos4, dims)
+    for cap in (64, 256):
+        dt = tree._DeviceOctree(keys, pts.shape[0], dims, cap)
+        h = tree._host_tree(lib, keys, pts.shape[0], dims, cap)
+        try:
+            T = tree._node_tables(lib, h)
+            gb_h, ge_h = tree._groups(lib, h, 64)
+        finally:
+            lib.spk_tree_host_free(h)
+        assert np.array_equal(dt.nb.cpu().numpy(), T["nb"])
+        assert np.array_equal(dt.ne.cpu().numpy(), T["ne"])
+        assert np.array_equal(dt.nc.cpu().numpy(), T["nc"])
+        fc = dt.fc.cpu().numpy()
+        assert np.array_equal(fc[T["nc"] > 0], T["fc"][T["nc"] > 0])
+        assert np.array_equal(dt.leaves.cpu().numpy(), T["leaves"])
+        assert np.array_equal(dt.levels, T["levels"])
+        gb, ge = dt.groups(64)
+        assert np.array_equal(gb.cpu().numpy(), gb_h) and np.array_equal(ge.cpu().numpy(), ge_h)
