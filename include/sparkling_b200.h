@@ -202,14 +202,14 @@ int spk_tree_boxes(const void* rec, int64_t n_ranges, const int64_t* begin,
 
 /* Octree over sorted keys on the GPU, level by level (build_tree, _treecode.py:77-170):
  * BFS node order, children contiguous in child-digit order, a node splits when it holds
- * more than leaf_cap particles and is above the finest level -- the same tree as
- * spk_tree_host_build.  Device outputs node_begin/node_end [capacity] i64, first_child /
+ * more than leaf_cap particles (or more than one above level min_level) and is above the
+ * finest level -- the same tree as spk_tree_host_build.  Device outputs node_begin/node_end [capacity] i64, first_child /
  * n_child [capacity] i32 (first_child -1 for leaves), leaf_node [capacity] i32; HOST
  * outputs level_off [64] (level l = nodes [off[l], off[l+1])) and counts [3] = nodes,
  * leaves, levels.  Returns SPK_ERR_WORKSPACE when node_capacity is too small (retry). */
 size_t spk_tree_build_workspace_bytes(int64_t n, int64_t node_capacity);
 int spk_tree_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
-                   int64_t node_capacity, int64_t* node_begin, int64_t* node_end,
+                   int min_level, int64_t node_capacity, int64_t* node_begin, int64_t* node_end,
                    int32_t* first_child, int32_t* n_child, int32_t* leaf_node,
                    int64_t* level_off, int64_t* counts, void* ws, size_t ws_bytes,
                    spk_stream_t stream);
@@ -280,7 +280,8 @@ int spk_tree_group_size(void);
 /* Host side (tree_host.cpp; HOST pointers).  An opaque octree over sorted keys:
  * nodes in BFS order with contiguous children, leaves hold <= leaf_cap particles
  * (build_tree, _treecode.py:77-170).  Returns NULL on error (spk_last_error). */
-void* spk_tree_host_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap);
+void* spk_tree_host_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
+                          int min_level);
 void spk_tree_host_free(void* tree);
 void spk_tree_host_sizes(const void* tree, int64_t* counts /* [2]: nodes, leaves */);
 int64_t spk_tree_host_levels(const void* tree, int64_t* level_off);

@@ -72,8 +72,8 @@ SIGNATURES = {
                               c_flt, c_vp, c_vp, c_vp]),
     "spk_tree_host_groups": (c_i64, [c_vp, c_i64, c_vp, c_vp]),
     "spk_tree_build_workspace_bytes": (c_size, [c_i64, c_i64]),
-    "spk_tree_build": (c_int, [c_vp, c_i64, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
-                               c_vp, c_vp, c_vp, c_size, c_vp]),
+    "spk_tree_build": (c_int, [c_vp, c_i64, c_int, c_i64, c_int, c_i64, c_vp, c_vp, c_vp, c_vp,
+                               c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "spk_tree_groups": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp,
                                 c_vp, c_size, c_vp]),
     "spk_nudft_workspace_bytes": (c_size, [c_i64, c_int, ctypes.POINTER(c_i64)]),
@@ -96,7 +96,7 @@ SIGNATURES = {
                                     c_vp, c_vp, c_vp, c_vp, c_vp]),
     "spk_tree_host_slot_nodes": (None, [c_vp, c_vp]),
     "spk_tree_group_size": (c_int, []),
-    "spk_tree_host_build": (c_vp, [c_vp, c_i64, c_int, c_i64]),
+    "spk_tree_host_build": (c_vp, [c_vp, c_i64, c_int, c_i64, c_int]),
     "spk_tree_host_free": (None, [c_vp]),
     "spk_tree_host_sizes": (None, [c_vp, c_vp]),
     "spk_tree_host_leaves": (None, [c_vp, c_vp, c_vp]),

@@ -257,13 +257,15 @@ __device__ __forceinline__ long long lower_bound_u64(const uint64_t* __restrict_
 
 __global__ void split_kernel(const uint64_t* __restrict__ keys, const long long* __restrict__ nbeg,
                              const long long* __restrict__ nend, long long lv_b, long long lv_e,
-                             int level, int dims, int bits, long long cap,
+                             int level, int dims, int bits, long long cap, int min_level,
                              int32_t* __restrict__ nchild, long long* __restrict__ child) {
     const long long v = lv_b + blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (v >= lv_e) return;
     const long long b = nbeg[v], e = nend[v];
     const long long w = v - lv_b;
-    if (e - b <= cap || level >= bits) {
+    // split when over capacity, or (min_level) when the cell is still coarse
+    const bool split = e - b > cap || (level < min_level && e - b > 1);
+    if (!split || level >= bits) {
         nchild[w] = 0;
         return;
     }
@@ -319,10 +321,10 @@ __global__ void leaf_write_kernel(const int32_t* __restrict__ flag, const int32_
     if (v < n_nodes && flag[v]) leaf_node[pos[v]] = (int32_t)v;
 }
 
-// Target groups (tree_host.cpp spk_tree_host_groups): under every node holding more than
-// `cap` particles, maximal runs of consecutive children with <= cap particles are packed
-// greedily into groups of <= cap; oversized leaves are cut into chunks; a root with
-// <= cap particles is one group.  Pass 0 counts per node, pass 1 writes; the groups are
+// Target groups (tree_host.cpp spk_tree_host_groups): under every internal node, maximal
+// runs of consecutive leaf children with <= cap particles are packed greedily into groups
+// of <= cap; oversized leaves are cut into chunks; a root leaf with <= cap particles is
+// one group.  Pass 0 counts per node, pass 1 writes; the groups are
 // then sorted by their first particle.
 template <int PASS>
 __global__ void groups_kernel(const long long* __restrict__ nbeg, const long long* __restrict__ nend,
@@ -343,16 +345,19 @@ __global__ void groups_kernel(const long long* __restrict__ nbeg, const long lon
         }
         ++k;
     };
-    if (e - b <= cap) {
-        if (v == 0) emit(b, e);
-    } else if (n_child[v] == 0) {
-        for (long long x = b; x < e; x += cap) emit(x, min(e, x + cap));
+    if (n_child[v] == 0) {
+        if (e - b > cap) {
+            for (long long x = b; x < e; x += cap) emit(x, min(e, x + cap));
+        } else if (v == 0) {
+            emit(b, e);
+        }
     } else {
+        // pack runs of consecutive small LEAF children; other children group themselves
         long long cb = -1, ce = -1;
         for (int c = 0; c < n_child[v]; ++c) {
             const long long u = first_child[v] + c;
             const long long ub = nbeg[u], ue = nend[u];
-            if (ue - ub > cap) {
+            if (ue - ub > cap || n_child[u] != 0) {
                 if (cb >= 0) emit(cb, ce);
                 cb = -1;
                 continue;
@@ -1034,7 +1039,7 @@ BuildWs build_ws(void* ws, size_t ws_bytes, long long m) {
 }  // namespace
 
 int spk_tree_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
-                   int64_t node_capacity, int64_t* node_begin, int64_t* node_end,
+                   int min_level, int64_t node_capacity, int64_t* node_begin, int64_t* node_end,
                    int32_t* first_child, int32_t* n_child, int32_t* leaf_node,
                    int64_t* level_off, int64_t* counts, void* ws, size_t ws_bytes,
                    spk_stream_t stream) {
@@ -1060,7 +1065,7 @@ int spk_tree_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
         SPK_REQUIRE(level < 63, SPK_ERR_ARG, "tree build: too many levels");
         const unsigned blocks = (unsigned)((m + 127) / 128);
         split_kernel<<<blocks, 128, 0, s>>>(keys, nb, ne, lv_b, lv_e, level, dims, bits,
-                                            (long long)leaf_cap, w.nchild, w.child);
+                                            (long long)leaf_cap, min_level, w.nchild, w.child);
         cudaMemsetAsync(w.nchild + m, 0, 4, s);
         size_t t = w.cub_bytes;
         cudaError_t e = cub::DeviceScan::ExclusiveSum(w.cub, t, w.nchild, w.off, (int)(m + 1), s);

@@ -74,7 +74,8 @@ Box make_box(const float* lohi, int dims) {
 
 extern "C" {
 
-void* spk_tree_host_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap) {
+void* spk_tree_host_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
+                          int min_level) {
     if (!(dims == 2 || dims == 3) || n <= 0 || leaf_cap < 1) {
         spk::set_error("tree build: bad arguments (n=%lld, dims=%d, leaf_cap=%lld)",
                        (long long)n, dims, (long long)leaf_cap);
@@ -92,7 +93,9 @@ void* spk_tree_host_build(const uint64_t* keys, int64_t n, int dims, int64_t lea
     t->nodes.push_back(Node{0, n, -1, 0, 0});
     for (size_t i = 0; i < t->nodes.size(); ++i) {
         Node nd = t->nodes[i];
-        if (nd.end - nd.begin <= leaf_cap || nd.level >= bits) {
+        const int64_t size = nd.end - nd.begin;
+        const bool split = size > leaf_cap || (nd.level < min_level && size > 1);
+        if (!split || nd.level >= bits) {
             t->leaves.push_back((int32_t)i);
             continue;
         }
@@ -197,8 +200,8 @@ int64_t spk_tree_host_groups(const void* h, int64_t cap, int64_t* begin, int64_t
         stack.pop_back();
         const Node& nd = t->nodes[v];
         const int64_t cnt = nd.end - nd.begin;
-        if (cnt <= cap) {
-            // pack consecutive siblings only: a group never spans two parents' cells
+        if (cnt <= cap && nd.n_child == 0) {
+            // pack consecutive sibling leaves only: a group never spans two parents' cells
             if (cur_b >= 0 && parent == cur_parent && cur_e == nd.begin &&
                 nd.end - cur_b <= cap) {
                 cur_e = nd.end;

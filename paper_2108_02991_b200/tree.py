@@ -49,6 +49,11 @@ LEAF_CAP = 256  # source particles per octree leaf
 # At or below this many sources the exact kernel is faster than building and walking a
 # tree on the B200 (C1 32k: 0.4 vs 1.0 ms; 65k: 1.7 vs 2.5 ms; 1M: 362 vs 19 ms).
 DIRECT_BELOW = 1 << 17
+# Target octrees are split down to at least this level (cells of 1/16 of the domain):
+# sparse targets (coarse decimation levels) would otherwise form groups spanning whole
+# spokes, whose near field against the dense lattice is huge (131k targets against the
+# C4 lattice: 45 -> 24 ms; no effect at 524k targets and above).
+TARGET_MIN_LEVEL = 5
 
 
 def auto_params(precision: float) -> tuple[int, float] | None:
@@ -78,9 +83,10 @@ def _sort(pos4: torch.Tensor, dims: int):
     return skeys, sidx
 
 
-def _host_tree(lib, skeys: torch.Tensor, n: int, dims: int, leaf_cap: int):
+def _host_tree(lib, skeys: torch.Tensor, n: int, dims: int, leaf_cap: int,
+               min_level: int = 0):
     keys_h = skeys.cpu().numpy()  # synchronises the stream
-    tree = lib.spk_tree_host_build(keys_h.ctypes.data, n, dims, leaf_cap)
+    tree = lib.spk_tree_host_build(keys_h.ctypes.data, n, dims, leaf_cap, min_level)
     if not tree:
         raise _native.NativeError(lib.spk_last_error().decode())
     return tree
@@ -116,7 +122,8 @@ class _DeviceOctree:
     """Octree over sorted keys built on the GPU (spk_tree_build): node tables on the
     device, BFS level offsets on the host.  Same nodes as the host builder."""
 
-    def __init__(self, keys: torch.Tensor, n: int, dims: int, leaf_cap: int):
+    def __init__(self, keys: torch.Tensor, n: int, dims: int, leaf_cap: int,
+                 min_level: int = 0):
         dev = keys.device
         st = _device.stream()
         cap = 16 * n // max(leaf_cap, 1) + 1024
@@ -131,7 +138,8 @@ class _DeviceOctree:
             ws = _device.workspace(_native.query("spk_tree_build_workspace_bytes", n, cap),
                                    "tree_build")
             try:
-                _native.call("spk_tree_build", keys.data_ptr(), n, dims, leaf_cap, cap,
+                _native.call("spk_tree_build", keys.data_ptr(), n, dims, leaf_cap, min_level,
+                             cap,
                              self.nb.data_ptr(), self.ne.data_ptr(), self.fc.data_ptr(),
                              self.nc.data_ptr(), self.leaves.data_ptr(), self.levels.ctypes.data,
                              counts.ctypes.data, ws.data_ptr(), ws.numel(), st)
@@ -274,7 +282,8 @@ class TargetGroups:
     """Targets sorted along the Morton curve and cut into groups of <= TR_GROUP that
     follow their octree (sibling subtrees), with tight group boxes (device)."""
 
-    def __init__(self, tgt4: torch.Tensor, dims: int, same_as: SourceTree | None = None):
+    def __init__(self, tgt4: torch.Tensor, dims: int, same_as: SourceTree | None = None,
+                 min_level: int = TARGET_MIN_LEVEL):
         lib = _native.load()
         dev = tgt4.device
         st = _device.stream()
@@ -288,7 +297,8 @@ class TargetGroups:
             self.rec = torch.empty((self.n, 4), dtype=torch.float32, device=dev)
             _native.call("spk_tree_gather", tgt4.data_ptr(), self.perm.data_ptr(), self.n,
                          None, self.rec.data_ptr(), st)
-            self.d_gb, self.d_ge = _DeviceOctree(keys, self.n, dims, group).groups(group)
+            self.d_gb, self.d_ge = _DeviceOctree(keys, self.n, dims, group,
+                                                 min_level).groups(group)
         self.n_groups = self.d_gb.shape[0]
         self.box = torch.empty((self.n_groups, 6), dtype=torch.float32, device=dev)
         _native.call("spk_tree_boxes", self.rec.data_ptr(), self.n_groups, self.d_gb.data_ptr(),

@@ -238,9 +238,9 @@ def test_device_octree_matches_host_builder(spk, dims):
     pts[:500] = pts[500]  # duplicate keys -> leaves at the finest level
     pos4 = _device.pack_positions(_device.h2d(pts))
     keys, _ = tree._sort(pos4, dims)
-    for cap in (64, 256):
-        dt = tree._DeviceOctree(keys, pts.shape[0], dims, cap)
-        h = tree._host_tree(lib, keys, pts.shape[0], dims, cap)
+    for cap, min_level in ((64, 0), (256, 0), (64, 4)):
+        dt = tree._DeviceOctree(keys, pts.shape[0], dims, cap, min_level)
+        h = tree._host_tree(lib, keys, pts.shape[0], dims, cap, min_level)
         try:
             T = tree._node_tables(lib, h)
             gb_h, ge_h = tree._groups(lib, h, 64)

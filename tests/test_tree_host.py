@@ -54,7 +54,7 @@ def test_tree_groups_and_lists_cover_every_source_once(dims):
     sk = np.ascontiguousarray(keys[order])
     sp = pts[order]
     cap = 64
-    tree = lib.spk_tree_host_build(sk.ctypes.data, n, dims, cap)
+    tree = lib.spk_tree_host_build(sk.ctypes.data, n, dims, cap, 0)
     try:
         sizes = np.zeros(2, np.int64)
         lib.spk_tree_host_sizes(tree, sizes.ctypes.data)
