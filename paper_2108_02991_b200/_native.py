@@ -117,7 +117,7 @@ LAUNCHES = {
     "spk_feasibility_residuals_batched": 2,
     "spk_tree_keys": 1, "spk_tree_sort": 10, "spk_tree_gather": 1, "spk_tree_boxes": 1,
     "spk_tree_p2m": 2, "spk_tree_eval": 1, "spk_tree_plan_count": 9, "spk_tree_node_boxes": 1,
-    "spk_tree_groups": 6,
+    "spk_tree_groups": 11,
     "spk_tree_plan_write": 2, "spk_nudft_adjoint": 2, "spk_nudft_forward": 2,
     "spk_dcf_update": 1, "spk_psf_magnitude": 1,
 }

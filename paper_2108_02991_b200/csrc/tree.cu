@@ -622,34 +622,49 @@ __device__ __forceinline__ int fill_batch(float4* buf, SegCursor& c, const EvalP
 }
 
 template <int D, bool G>
+__device__ __forceinline__ void pair_step(const float4 s, float2 X, float2 Y, float2 Z, float2 e2,
+                                          float2& av, float2& ax, float2& ay, float2& az) {
+    const float2 dx = __fadd2_rn(X, bcast(-s.x));
+    const float2 dy = __fadd2_rn(Y, bcast(-s.y));
+    float2 r2 = __ffma2_rn(dx, dx, e2);
+    r2 = __ffma2_rn(dy, dy, r2);
+    float2 dz;
+    if (D == 3) {
+        dz = __fadd2_rn(Z, bcast(-s.z));
+        r2 = __ffma2_rn(dz, dz, r2);
+    }
+    float2 inv;
+    inv.x = rsqrt_approx(r2.x);
+    inv.y = rsqrt_approx(r2.y);
+    if (G) {
+        inv.x = r2.x > 0.0f ? inv.x : 0.0f;
+        inv.y = r2.y > 0.0f ? inv.y : 0.0f;
+    }
+    const float2 wi = __fmul2_rn(inv, bcast(s.w));
+    av = __ffma2_rn(r2, wi, av);  // w h = w r2 / h
+    ax = __ffma2_rn(dx, wi, ax);
+    ay = __ffma2_rn(dy, wi, ay);
+    if (D == 3) az = __ffma2_rn(dz, wi, az);
+}
+
+// Two accumulator sets (even / odd records) so that consecutive sources do not serialise
+// on the accumulator FFMA2 latency at the low occupancy of this kernel.
+template <int D, bool G>
 __device__ __forceinline__ void eval_batch(const float4* __restrict__ buf, int cnt, float2 X,
                                            float2 Y, float2 Z, float2 e2, float2& av,
                                            float2& ax, float2& ay, float2& az) {
-#pragma unroll 4
-    for (int j = 0; j < cnt; ++j) {
-        const float4 s = buf[j];
-        const float2 dx = __fadd2_rn(X, bcast(-s.x));
-        const float2 dy = __fadd2_rn(Y, bcast(-s.y));
-        float2 r2 = __ffma2_rn(dx, dx, e2);
-        r2 = __ffma2_rn(dy, dy, r2);
-        float2 dz;
-        if (D == 3) {
-            dz = __fadd2_rn(Z, bcast(-s.z));
-            r2 = __ffma2_rn(dz, dz, r2);
-        }
-        float2 inv;
-        inv.x = rsqrt_approx(r2.x);
-        inv.y = rsqrt_approx(r2.y);
-        if (G) {
-            inv.x = r2.x > 0.0f ? inv.x : 0.0f;
-            inv.y = r2.y > 0.0f ? inv.y : 0.0f;
-        }
-        const float2 wi = __fmul2_rn(inv, bcast(s.w));
-        av = __ffma2_rn(r2, wi, av);  // w h = w r2 / h
-        ax = __ffma2_rn(dx, wi, ax);
-        ay = __ffma2_rn(dy, wi, ay);
-        if (D == 3) az = __ffma2_rn(dz, wi, az);
+    float2 bv = bcast(0.f), bx = bcast(0.f), by = bcast(0.f), bz = bcast(0.f);
+    int j = 0;
+#pragma unroll 2
+    for (; j + 1 < cnt; j += 2) {
+        pair_step<D, G>(buf[j], X, Y, Z, e2, av, ax, ay, az);
+        pair_step<D, G>(buf[j + 1], X, Y, Z, e2, bv, bx, by, bz);
     }
+    if (j < cnt) pair_step<D, G>(buf[j], X, Y, Z, e2, av, ax, ay, az);
+    av = __fadd2_rn(av, bv);
+    ax = __fadd2_rn(ax, bx);
+    ay = __fadd2_rn(ay, by);
+    if (D == 3) az = __fadd2_rn(az, bz);
 }
 
 // One warp per target group (<= 64 targets, two per lane as one f32x2 pair): small

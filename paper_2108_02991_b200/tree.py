@@ -150,7 +150,7 @@ class _DeviceOctree:
                 cap *= 2
         self.n_nodes, self.n_leaves, n_lv = (int(c) for c in counts)
         self.levels = self.levels[:n_lv + 1].copy()
-        _native.add_launches(3 * n_lv + 3)
+        _native.add_launches(4 * n_lv + 5)  # per level: split, scan (2), link; + leaves
         self.nb, self.ne = self.nb[:self.n_nodes], self.ne[:self.n_nodes]
         self.fc, self.nc = self.fc[:self.n_nodes], self.nc[:self.n_nodes]
         self.leaves = self.leaves[:self.n_leaves]
