@@ -24,7 +24,7 @@
 
 namespace spk {
 
-constexpr int PJ_THREADS = 256;
+constexpr int PJ_THREADS = 512;  // FISTA CTA size: 16 warps hide the state loads
 constexpr int PJ_SMEM_LIMIT = 200 * 1024;
 
 struct ProjArgs {
@@ -45,7 +45,7 @@ struct ProjArgs {
     int32_t* nonfinite;
     double* ws;         // per-shot state, stride = ws_stride doubles
     long long ws_stride;
-    int smem_arrays;    // 1: s/y1/y2 in shared memory
+    int smem_arrays;    // 1: s/y1/y2 in shared memory, 2: s/y1/y2/y0
 };
 
 // Workspace layout per shot (units of ns*D doubles): k, q0, q1, q2, y0, z0, z1, z2, s_obj,
@@ -142,6 +142,56 @@ __device__ __forceinline__ void block_sum2(double& x, double& y, double* red) {
     y = red[65];
 }
 
+// Dual prox of sample n (projection.py:186-213): z0 = tau (y0/tau + s - clamp(...)),
+// z1 / z2 = tau * ball-projection residuals of the first / second differences.  Used by
+// the prox pass, recomputed bit-identically by the update pass and the serial restart
+// fallback instead of storing z (three state arrays of HBM traffic per iteration).
+template <int D>
+__device__ __forceinline__ void prox_sample(int n, int ns, const double* __restrict__ s,
+                                            const double* __restrict__ y0,
+                                            const double* __restrict__ y1,
+                                            const double* __restrict__ y2, double a, double b,
+                                            double tau, double inv_tau, double (&z0)[D],
+                                            double (&z1)[D], double (&z2)[D]) {
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        const int e = n * D + l;
+        const double z = y0[e] * inv_tau + s[e];
+        const double pz = clamp_unit(z);
+        z0[l] = tau * (z - pz);
+    }
+    if (n <= ns - 2) {
+        double zv[D];
+        double nrm = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            const int e = n * D + l;
+            const double z = y1[e] * inv_tau + (s[e + D] - s[e]);
+            zv[l] = z;
+            nrm += z * z;
+        }
+        nrm = sqrt(nrm);
+        const double scale = (nrm <= a) ? 0.0 : 1.0 - a / nrm;
+#pragma unroll
+        for (int l = 0; l < D; ++l) z1[l] = tau * zv[l] * scale;
+    }
+    if (n <= ns - 3) {
+        double zv[D];
+        double nrm = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            const int e = n * D + l;
+            const double z = y2[e] * inv_tau + (s[e + 2 * D] - 2.0 * s[e + D] + s[e]);
+            zv[l] = z;
+            nrm += z * z;
+        }
+        nrm = sqrt(nrm);
+        const double scale = (nrm <= b) ? 0.0 : 1.0 - b / nrm;
+#pragma unroll
+        for (int l = 0; l < D; ++l) z2[l] = tau * zv[l] * scale;
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
     extern __shared__ __align__(16) double smem[];
@@ -157,7 +207,7 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
     double* q0 = W + 1 * (size_t)nd;
     double* q1 = W + 2 * (size_t)nd;
     double* q2 = W + 3 * (size_t)nd;
-    double* y0 = W + 4 * (size_t)nd;
+    double* y0 = W + 4 * (size_t)nd;  // (shared memory when smem_arrays == 2)
     double* z0 = W + 5 * (size_t)nd;
     double* z1 = W + 6 * (size_t)nd;
     double* z2 = W + 7 * (size_t)nd;
@@ -167,6 +217,7 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
         s = smem;
         y1 = smem + nd;
         y2 = smem + 2 * nd;
+        if (A.smem_arrays == 2) y0 = smem + 3 * nd;
     } else {
         s = W + 9 * (size_t)nd;
         y1 = W + 10 * (size_t)nd;
@@ -211,62 +262,37 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
                 for (int l = 0; l < D; ++l) s[n * D + l] = pv[l];
         }
         __syncthreads();
-        // ---- dual prox -> z, restart terms
+        // ---- dual prox -> z, restart terms (z stored only when the monotone objective
+        // needs it; otherwise it is recomputed by the update pass)
         double gd = 0.0, ga = 0.0;
+        const bool keep_z = A.monotone;
         for (int n = tid; n < ns; n += nt) {
+            double zz0[D], zz1[D], zz2[D];
+            prox_sample<D>(n, ns, s, y0, y1, y2, a, b, tau, inv_tau, zz0, zz1, zz2);
 #pragma unroll
             for (int l = 0; l < D; ++l) {
                 const int e = n * D + l;
-                const double yv = y0[e];
-                const double z = yv * inv_tau + s[e];
-                const double pz = clamp_unit(z);
-                const double zz = tau * (z - pz);
-                z0[e] = zz;
-                const double term = (yv - zz) * (zz - q0[e]);
+                if (keep_z) z0[e] = zz0[l];
+                const double term = (y0[e] - zz0[l]) * (zz0[l] - q0[e]);
                 gd += term;
                 ga += fabs(term);
             }
             if (n <= ns - 2) {
-                double zv[D];
-                double nrm = 0.0;
 #pragma unroll
                 for (int l = 0; l < D; ++l) {
                     const int e = n * D + l;
-                    const double z = y1[e] * inv_tau + (s[e + D] - s[e]);
-                    zv[l] = z;
-                    nrm += z * z;
-                }
-                nrm = sqrt(nrm);
-                const double scale = (nrm <= a) ? 0.0 : 1.0 - a / nrm;
-#pragma unroll
-                for (int l = 0; l < D; ++l) {
-                    const int e = n * D + l;
-                    const double zz = tau * zv[l] * scale;
-                    z1[e] = zz;
-                    const double term = (y1[e] - zz) * (zz - q1[e]);
+                    if (keep_z) z1[e] = zz1[l];
+                    const double term = (y1[e] - zz1[l]) * (zz1[l] - q1[e]);
                     gd += term;
                     ga += fabs(term);
                 }
             }
             if (n <= ns - 3) {
-                double zv[D];
-                double nrm = 0.0;
 #pragma unroll
                 for (int l = 0; l < D; ++l) {
                     const int e = n * D + l;
-                    const double z =
-                        y2[e] * inv_tau + (s[e + 2 * D] - 2.0 * s[e + D] + s[e]);
-                    zv[l] = z;
-                    nrm += z * z;
-                }
-                nrm = sqrt(nrm);
-                const double scale = (nrm <= b) ? 0.0 : 1.0 - b / nrm;
-#pragma unroll
-                for (int l = 0; l < D; ++l) {
-                    const int e = n * D + l;
-                    const double zz = tau * zv[l] * scale;
-                    z2[e] = zz;
-                    const double term = (y2[e] - zz) * (zz - q2[e]);
+                    if (keep_z) z2[e] = zz2[l];
+                    const double term = (y2[e] - zz2[l]) * (zz2[l] - q2[e]);
                     gd += term;
                     ga += fabs(term);
                 }
@@ -280,9 +306,24 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
             // Sign not certified: reproduce the reference's sequential sum exactly.
             if (tid == 0) {
                 double g = 0.0;
-                for (int i = 0; i < nd; ++i) g += (y0[i] - z0[i]) * (z0[i] - q0[i]);
-                for (int i = 0; i < n1; ++i) g += (y1[i] - z1[i]) * (z1[i] - q1[i]);
-                for (int i = 0; i < n2; ++i) g += (y2[i] - z2[i]) * (z2[i] - q2[i]);
+                if (keep_z) {
+                    for (int i = 0; i < nd; ++i) g += (y0[i] - z0[i]) * (z0[i] - q0[i]);
+                    for (int i = 0; i < n1; ++i) g += (y1[i] - z1[i]) * (z1[i] - q1[i]);
+                    for (int i = 0; i < n2; ++i) g += (y2[i] - z2[i]) * (z2[i] - q2[i]);
+                } else {  // same terms, same order, z recomputed
+                    double zz0[D], zz1[D], zz2[D];
+                    for (int pass = 0; pass < 3; ++pass)
+                        for (int n = 0; n < ns - pass; ++n) {
+                            prox_sample<D>(n, ns, s, y0, y1, y2, a, b, tau, inv_tau, zz0, zz1,
+                                           zz2);
+                            for (int l = 0; l < D; ++l) {
+                                const int e = n * D + l;
+                                if (pass == 0) g += (y0[e] - zz0[l]) * (zz0[l] - q0[e]);
+                                else if (pass == 1) g += (y1[e] - zz1[l]) * (zz1[l] - q1[e]);
+                                else g += (y2[e] - zz2[l]) * (zz2[l] - q2[e]);
+                            }
+                        }
+                }
                 flag_sh[1] = g > 0.0;
             }
             __syncthreads();
@@ -336,21 +377,20 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
         } else {
             const double mom = (t - 1.0) / t_next;
             for (int n = tid; n < ns; n += nt) {
+                double zz0[D], zz1[D], zz2[D];
+                prox_sample<D>(n, ns, s, y0, y1, y2, a, b, tau, inv_tau, zz0, zz1, zz2);
 #pragma unroll
                 for (int l = 0; l < D; ++l) {
                     const int e = n * D + l;
-                    double zz = z0[e];
-                    y0[e] = zz + mom * (zz - q0[e]);
-                    q0[e] = zz;
+                    y0[e] = zz0[l] + mom * (zz0[l] - q0[e]);
+                    q0[e] = zz0[l];
                     if (n <= ns - 2) {
-                        zz = z1[e];
-                        y1[e] = zz + mom * (zz - q1[e]);
-                        q1[e] = zz;
+                        y1[e] = zz1[l] + mom * (zz1[l] - q1[e]);
+                        q1[e] = zz1[l];
                     }
                     if (n <= ns - 3) {
-                        zz = z2[e];
-                        y2[e] = zz + mom * (zz - q2[e]);
-                        q2[e] = zz;
+                        y2[e] = zz2[l] + mom * (zz2[l] - q2[e]);
+                        q2[e] = zz2[l];
                     }
                 }
             }
@@ -1036,8 +1076,9 @@ int spk_project_all(const double* in, const double* grad, double eta,
     A.ws = static_cast<double*>(ws);
     A.ws_stride = (long long)proj_state_doubles(n_s, dims);
     const size_t smem3 = (size_t)3 * n_s * dims * sizeof(double);
-    A.smem_arrays = smem3 <= (size_t)PJ_SMEM_LIMIT;
-    const size_t dyn = A.smem_arrays ? smem3 : 0;
+    const size_t smem4 = (size_t)4 * n_s * dims * sizeof(double);
+    A.smem_arrays = smem4 <= (size_t)PJ_SMEM_LIMIT ? 2 : smem3 <= (size_t)PJ_SMEM_LIMIT ? 1 : 0;
+    const size_t dyn = A.smem_arrays == 2 ? smem4 : A.smem_arrays == 1 ? smem3 : 0;
     int nt = PJ_THREADS;
     if (n_s < PJ_THREADS) nt = ((n_s + 31) / 32) * 32;
     if (dims == 3) {
