@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
-            cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]
+            cmd = [nvcc, *ARCH, *COMMON, *extra, *os.environ.get("SPK_NVCC_EXTRA", "").split(),
+                   "-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd))
             subprocess.run(cmd, check=True)

@@ -446,16 +446,15 @@ struct Sample {
 
 template <int D>
 __device__ __forceinline__ void box_sample(Sample<D>& s, double& worst) {
+    // branch-free: the excess is 0 when inside [-1, 1] and worst >= 0, so the selects
+    // reproduce the reference's `if v > 1 / elif v < -1` updates exactly
 #pragma unroll
     for (int l = 0; l < D; ++l) {
         const double v = s.v[l];
-        if (v > 1.0) {
-            if (v - 1.0 > worst) worst = v - 1.0;
-            s.v[l] = 1.0;
-        } else if (v < -1.0) {
-            if (-1.0 - v > worst) worst = -1.0 - v;
-            s.v[l] = -1.0;
-        }
+        const bool hi = v > 1.0, lo = v < -1.0;
+        const double ex = hi ? v - 1.0 : (lo ? -1.0 - v : 0.0);
+        worst = ex > worst ? ex : worst;
+        s.v[l] = hi ? 1.0 : (lo ? -1.0 : v);
     }
 }
 
@@ -464,11 +463,12 @@ template <int D>
 __device__ __forceinline__ void speed_pair(Sample<D>& x0, Sample<D>& x1, int n, double a,
                                            int pin, double& worst) {
     const double omega = 1.8;
+    double df[D];  // x1 - x0, reused by the update (the samples do not change in between)
     double nrm = 0.0;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double df = x1.v[l] - x0.v[l];
-        nrm += df * df;
+        df[l] = x1.v[l] - x0.v[l];
+        nrm += df[l] * df[l];
     }
     nrm = sqrt(nrm);
     if (!(nrm > a)) return;
@@ -478,25 +478,18 @@ __device__ __forceinline__ void speed_pair(Sample<D>& x0, Sample<D>& x1, int n, 
         const double shrink = omega * (nrm - a) / nrm;
         if (n == pin) {
 #pragma unroll
-            for (int l = 0; l < D; ++l) {
-                const double df = x1.v[l] - x0.v[l];
-                x1.v[l] -= 1.0 * shrink * df;
-            }
+            for (int l = 0; l < D; ++l) x1.v[l] -= 1.0 * shrink * df[l];
         } else {
 #pragma unroll
-            for (int l = 0; l < D; ++l) {
-                const double df = x1.v[l] - x0.v[l];
-                x0.v[l] -= -1.0 * shrink * df;
-            }
+            for (int l = 0; l < D; ++l) x0.v[l] -= -1.0 * shrink * df[l];
         }
         return;
     }
     const double shrink = omega * 0.5 * (nrm - a) / nrm;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double df = x1.v[l] - x0.v[l];
-        x0.v[l] += shrink * df;
-        x1.v[l] -= shrink * df;
+        x0.v[l] += shrink * df[l];
+        x1.v[l] -= shrink * df[l];
     }
 }
 
@@ -505,11 +498,12 @@ template <int D>
 __device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sample<D>& x2, int n,
                                              double b, int pin, double& worst) {
     const double omega = 1.8;
+    double w[D];  // second differences, reused by the update
     double nrm = 0.0;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double w = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
-        nrm += w * w;
+        w[l] = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
+        nrm += w[l] * w[l];
     }
     nrm = sqrt(nrm);
     if (!(nrm > b)) return;
@@ -521,10 +515,9 @@ __device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sampl
         const double step1 = step * -2.0;
 #pragma unroll
         for (int l = 0; l < D; ++l) {
-            const double w = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
-            x0.v[l] -= step * w;
-            x1.v[l] -= step1 * w;
-            x2.v[l] -= step * w;
+            x0.v[l] -= step * w[l];
+            x1.v[l] -= step1 * w[l];
+            x2.v[l] -= step * w[l];
         }
         return;
     }
@@ -537,10 +530,9 @@ __device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sampl
         const double step = omega * (nrm - b) / (denom * nrm);
 #pragma unroll
         for (int l = 0; l < D; ++l) {
-            const double w = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
-            x0.v[l] -= step * c0 * w;
-            x1.v[l] -= step * c1 * w;
-            x2.v[l] -= step * c2 * w;
+            x0.v[l] -= step * c0 * w[l];
+            x1.v[l] -= step * c1 * w[l];
+            x2.v[l] -= step * c2 * w[l];
         }
     }
 }
@@ -629,7 +621,25 @@ struct RingLane {
     Sample<D> slot[4];  // register window, roles rotate with the global step (mod 4)
     double worst;
     int t, j, k;        // local step in the current round, round, sweep index
+#ifdef SPK_POLISH_PROF
+    unsigned long long prof[7];
+    unsigned long long tp;
+#endif
 };
+
+#ifdef SPK_POLISH_PROF
+// Per-phase cycle sums of one observed lane (block 0, thread 40): speed, accel,
+// hand-over, box, barrier, steps.  Diagnostic build only (scripts/polish_profile.sh).
+__device__ unsigned long long spk_polish_prof[3][7];
+#define SPK_PROF_MARK(L, i)                                                              \
+    {                                                                                    \
+        const unsigned long long now__ = clock64();                                      \
+        (L).prof[i] += now__ - (L).tp;                                                   \
+        (L).tp = now__;                                                                  \
+    }
+#else
+#define SPK_PROF_MARK(L, i)
+#endif
 
 // Ring lanes lag by 4 steps (+1 per warp boundary), the minimum for which the windows of
 // consecutive sweeps never overlap out of order.  (A variant running S(t) and A(t-3)
@@ -658,8 +668,15 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
     const bool on = t >= -2 && t <= ns + 1 && L.k < max_sweeps;
     if (on) {
         if (t == -2) L.worst = 0.0;
+#ifndef SPK_EXP_NOSPEED
         if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, L.worst);
+#endif
+        SPK_PROF_MARK(L, 0)
+#ifndef SPK_EXP_NOACCEL
         if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, L.worst);
+#endif
+        SPK_PROF_MARK(L, 1)
+#ifndef SPK_EXP_NOSNAP
         if (t >= 2) {
             if (g == B - 1) {
                 double* sn = (L.j & 1) ? snap1 : snap0;
@@ -674,37 +691,46 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
                 for (int l = 0; l < D; ++l) res[(t - 2) * D + l] = w0.v[l];
             }
         }
+#endif
         if (t == ns + 1 && L.worst <= tol) atomicMin(stop_sh, L.k);
     }
     // hand the finished sample w0 (= s[t-2]) to the next sweep; it is replaced in slot R
     Sample<D> recv;
 #pragma unroll
     for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, w0.v[l], 1);
+#ifndef SPK_EXP_NOXFER
     if (lane == 31) {
         double* x = xfer + ((warp * 2 + (st & 1)) * D);
 #pragma unroll
         for (int l = 0; l < D; ++l) x[l] = w0.v[l];
     }
+#endif
     if (on) {
         const int m = t + 2;
         if (m <= ns - 1) {
             if (g == 0) {
-                // first sweep of a round: the initial state (round 0) or the previous
-                // round's last sweep, handed over through the shared-memory wrap buffer
-                const double* src = L.j == 0 ? s0 : wrap;
+                // first sweep of a round: the previous round's last sweep (the initial
+                // state for round 0, staged at kernel start), through the wrap buffer
 #pragma unroll
-                for (int l = 0; l < D; ++l) recv.v[l] = src[m * D + l];
-            } else if (lane == 0) {
+                for (int l = 0; l < D; ++l) recv.v[l] = wrap[m * D + l];
+            }
+#ifndef SPK_EXP_NOXFER
+            else if (lane == 0) {
                 const double* x = xfer + (((warp - 1) * 2 + ((st - 1) & 1)) * D);
 #pragma unroll
                 for (int l = 0; l < D; ++l) recv.v[l] = x[l];
             }
+#endif
             if (m == pin) {
                 recv.v[0] = pv0;
                 recv.v[1] = pv1;
                 if (D == 3) recv.v[D - 1] = pv2;
             }
+            SPK_PROF_MARK(L, 2)
+#ifndef SPK_EXP_NOBOX
             box_sample<D>(recv, L.worst);
+#endif
+            SPK_PROF_MARK(L, 3)
         }
     }
     w0 = recv;  // slot R now holds s[t+2] (w3 at the next step)
@@ -713,7 +739,14 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
         ++L.j;
         L.k += B;
     }
+    SPK_PROF_MARK(L, 4)
+#ifndef SPK_EXP_NOSYNC
     __syncthreads();
+#endif
+#ifdef SPK_POLISH_PROF
+    SPK_PROF_MARK(L, 5)
+    L.prof[6] += 1;
+#endif
 }
 
 // Continuous ring: lane g runs sweeps g, g+B, g+2B, ...; sweep k starts at global step
@@ -751,6 +784,10 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     double* snap1 = snap0 + nd;
     double* res = snap1 + nd;
     if (g == 0) stop_sh = 0x7fffffff;
+    // stage the initial state in the wrap buffer: lane 0 then reads round 0 from it like
+    // every later round (no global-load latency on the ring's critical path).  Lane B-1
+    // overwrites position q only 4 + ring_offset(B-1) steps after lane 0 has read it.
+    for (int i = g; i < nd; i += B) wrap[i] = s0[i];
     __syncthreads();
     const int kl = max_sweeps - 1;
     const int last_step = (kl / B) * P + ring_offset(kl % B) + ns + 3;
@@ -761,6 +798,10 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
         for (int l = 0; l < D; ++l) L.slot[q].v[l] = 0.0;
     L.worst = 0.0;
     L.t = -2 - off;  // lane g starts its first sweep at global step off
+#ifdef SPK_POLISH_PROF
+    for (int q = 0; q < 7; ++q) L.prof[q] = 0;
+    L.tp = clock64();
+#endif
     L.j = 0;
     L.k = g;
 #define SPK_RING_STEP(R)                                                                   \
@@ -776,6 +817,13 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
         SPK_RING_STEP(3)
     }
 #undef SPK_RING_STEP
+#ifdef SPK_POLISH_PROF
+    if (blockIdx.x == 0) {
+        const int slot = g == 5 ? 0 : g == 40 ? 1 : g == B - 9 ? 2 : -1;
+        if (slot >= 0)
+            for (int q = 0; q < 7; ++q) spk_polish_prof[slot][q] = L.prof[q];
+    }
+#endif
     const int kstar = stop_sh;
     int total = max_sweeps;
     if (kstar != 0x7fffffff) {
@@ -1033,6 +1081,15 @@ static size_t proj_state_doubles(int n_s, int dims) {
 }
 
 extern "C" {
+
+#ifdef SPK_POLISH_PROF
+int spk_polish_prof_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, spk_polish_prof, sizeof(unsigned long long) * 21) ==
+                   cudaSuccess
+               ? 0
+               : 4;
+}
+#endif
 
 size_t spk_project_workspace_bytes(int64_t n_shots, int n_s, int dims, int with_trace) {
     (void)with_trace;
