@@ -658,8 +658,8 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
                                           double a, double b, int pin, double pv0,
                                           double pv1, double pv2, double tol,
                                           const double* __restrict__ s0, double* snap0,
-                                          double* snap1, double* res, double* xfer,
-                                          double* wrap, int* stop_sh) {
+                                          double* res, double* xfer, double* wrap0,
+                                          int wstride, int* stop_sh) {
     Sample<D>& w0 = L.slot[R & 3];
     Sample<D>& w1 = L.slot[(R + 1) & 3];
     Sample<D>& w2 = L.slot[(R + 2) & 3];
@@ -679,11 +679,15 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
 #ifndef SPK_EXP_NOSNAP
         if (t >= 2) {
             if (g == B - 1) {
-                double* sn = (L.j & 1) ? snap1 : snap0;
+                // round j's output stream: wrap buffer j & 1 (both the same buffer when
+                // single-buffered, which then needs the global ping-pong snapshots)
+                double* wb = wrap0 + (L.j & 1) * wstride;
 #pragma unroll
-                for (int l = 0; l < D; ++l) {
-                    sn[(t - 2) * D + l] = w0.v[l];
-                    wrap[(t - 2) * D + l] = w0.v[l];
+                for (int l = 0; l < D; ++l) wb[(t - 2) * D + l] = w0.v[l];
+                if (wstride == 0) {  // single wrap buffer: ping-pong snapshots in global
+                    double* sn = snap0 + (L.j & 1) * (ns * D);
+#pragma unroll
+                    for (int l = 0; l < D; ++l) sn[(t - 2) * D + l] = w0.v[l];
                 }
             }
             if (L.k == kl) {
@@ -711,8 +715,9 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
             if (g == 0) {
                 // first sweep of a round: the previous round's last sweep (the initial
                 // state for round 0, staged at kernel start), through the wrap buffer
+                const double* rb = wrap0 + ((L.j + 1) & 1) * wstride;  // round j - 1's stream
 #pragma unroll
-                for (int l = 0; l < D; ++l) recv.v[l] = wrap[m * D + l];
+                for (int l = 0; l < D; ++l) recv.v[l] = rb[m * D + l];
             }
 #ifndef SPK_EXP_NOXFER
             else if (lane == 0) {
@@ -762,17 +767,22 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
                                                       double pv1, double pv2, double tol,
                                                       int max_sweeps, double* ws,
                                                       int32_t* sweeps_out, float4* pos4,
-                                                      int wrap_global) {
-    extern __shared__ __align__(16) double xfer[];  // [W][2][D], then wrap [ns][D]
+                                                      int wrap_mode) {
+    // wrap_mode 2: two wrap buffers in shared memory (round parity), which double as the
+    // replay snapshot -- no global snapshot stores on the ring's critical path;
+    // 1: one shared wrap buffer + global ping-pong snapshots; 0: wrap in the workspace.
+    extern __shared__ __align__(16) double xfer[];  // [W][2][D], then wrap [1|2][ns][D]
     __shared__ int stop_sh;
     const long long c = blockIdx.x;
     const int B = blockDim.x;
     const int W = B >> 5;
     const int P = max(4 * B + W, ns + 4);
     const int nd4 = ns * D;
-    // wrap buffer in shared memory, or (very long shots) in the per-shot workspace
-    double* wrap = wrap_global ? ws + blockIdx.x * (size_t)(4 * nd4) + 3 * nd4
-                               : xfer + W * 2 * D;
+    // wrap buffer(s) in shared memory, or (very long shots) in the per-shot workspace
+    double* wrap0 = wrap_mode == 0 ? ws + blockIdx.x * (size_t)(4 * nd4) + 3 * nd4
+                                   : xfer + W * 2 * D;
+    const int wstride = wrap_mode == 2 ? nd4 : 0;
+    double* wrap1 = wrap0 + wstride;
     const int g = threadIdx.x;
     const int lane = g & 31;
     const int warp = g >> 5;
@@ -787,7 +797,7 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     // stage the initial state in the wrap buffer: lane 0 then reads round 0 from it like
     // every later round (no global-load latency on the ring's critical path).  Lane B-1
     // overwrites position q only 4 + ring_offset(B-1) steps after lane 0 has read it.
-    for (int i = g; i < nd; i += B) wrap[i] = s0[i];
+    for (int i = g; i < nd; i += B) wrap1[i] = s0[i];  // round 0 reads buffer (0 - 1) & 1
     __syncthreads();
     const int kl = max_sweeps - 1;
     const int last_step = (kl / B) * P + ring_offset(kl % B) + ns + 3;
@@ -807,7 +817,8 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
 #define SPK_RING_STEP(R)                                                                   \
     {                                                                                      \
         ring_step<D, R>(L, st + R, ns, B, P, g, lane, warp, max_sweeps, kl, a, b, pin,     \
-                        pv0, pv1, pv2, tol, s0, snap0, snap1, res, xfer, wrap, &stop_sh); \
+                        pv0, pv1, pv2, tol, s0, snap0, res, xfer, wrap0, wstride,          \
+                        &stop_sh);                                                         \
         if (stop_sh != 0x7fffffff || st + R >= last_step) break;                           \
     }
     for (int st = 0;; st += 4) {
@@ -828,7 +839,9 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     int total = max_sweeps;
     if (kstar != 0x7fffffff) {
         const int jj = kstar / B;
-        const double* src = jj == 0 ? s0 : ((jj - 1) & 1 ? snap1 : snap0);
+        const double* src = jj == 0    ? s0
+                            : wstride ? ((jj - 1) & 1 ? wrap1 : wrap0)
+                                     : ((jj - 1) & 1 ? snap1 : snap0);
         __syncthreads();
         systolic_batch<D>(src, res, xfer, ns, a, b, pin, pv, kstar - jj * B + 1);
         total = kstar + 1;
@@ -1151,9 +1164,10 @@ int spk_project_all(const double* in, const double* grad, double eta,
     // polish: systolic ring, one CTA of 32*pw lanes per shot; snapshots + result in the
     // (now free) FISTA workspace, warp hand-over slots in shared memory
     const int pw = polish_warps(n_s);
-    size_t psm = ((size_t)pw * 2 * dims + (size_t)n_s * dims) * sizeof(double);
-    const int wrap_global = psm > 200 * 1024;
-    if (wrap_global) psm = (size_t)pw * 2 * dims * sizeof(double);
+    const size_t xb = (size_t)pw * 2 * dims * sizeof(double);
+    const size_t wb = (size_t)n_s * dims * sizeof(double);
+    const int wrap_mode = xb + 2 * wb <= 200 * 1024 ? 2 : xb + wb <= 200 * 1024 ? 1 : 0;
+    const size_t psm = xb + (wrap_mode == 2 ? 2 * wb : wrap_mode == 1 ? wb : 0);
     cudaFuncSetAttribute(polish_kernel<3, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)psm);
     cudaFuncSetAttribute(polish_kernel<2, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1170,20 +1184,20 @@ int spk_project_all(const double* in, const double* grad, double eta,
         if (dims == 3)
             polish_kernel<3, 256, 3><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_global);
+                (float4*)pos4, wrap_mode);
         else
             polish_kernel<2, 256, 3><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_global);
+                (float4*)pos4, wrap_mode);
     } else {
         if (dims == 3)
             polish_kernel<3, 1024, 1><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_global);
+                (float4*)pos4, wrap_mode);
         else
             polish_kernel<2, 1024, 1><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_global);
+                (float4*)pos4, wrap_mode);
     }
     SPK_CHECK_LAUNCH("polish_kernel");
     return SPK_OK;
