@@ -287,10 +287,19 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(con
     float* axes = reinterpret_cast<float*>(stages + NB_TILE_BYTES + NB_ACC_BYTES);
     __shared__ __align__(8) uint64_t bars[NB_STAGES];
     const int tid = threadIdx.x;
-    const long long unit = blockIdx.x;
-    const long long tb = unit % P.n_tb;
-    const int chunk = (int)(unit / P.n_tb);
-    const bool first = chunk < P.seg[0].n_chunks;
+    // Interleave the lattice (SFU-bound) and position (FMA-bound) units in launch order,
+    // in proportion to their counts (Bresenham), so that the CTAs resident on an SM mix
+    // both kinds and the two pipes overlap instead of running one phase after the other.
+    // Unit k of a segment is (tb = k % n_tb, chunk k / n_tb): slots and the fixed-order
+    // finalize are unchanged.
+    const long long u = blockIdx.x;
+    const long long U0 = P.n_tb * P.seg[0].n_chunks;
+    const long long U = U0 + P.n_tb * P.seg[1].n_chunks;
+    const long long i0 = u * U0 / U;
+    const bool first = (u + 1) * U0 / U > i0;
+    const long long k = first ? i0 : u - i0;
+    const long long tb = k % P.n_tb;
+    const int chunk = (int)(k / P.n_tb) + (first ? 0 : P.seg[0].n_chunks);
     const SegDesc S = first ? P.seg[0] : P.seg[1];
     const long long lc = first ? chunk : chunk - P.seg[0].n_chunks;
     const long long t_begin = lc * S.tiles / S.n_chunks;
