@@ -446,15 +446,15 @@ struct Sample {
 
 template <int D>
 __device__ __forceinline__ void box_sample(Sample<D>& s, double& worst) {
-    // branch-free: the excess is 0 when inside [-1, 1] and worst >= 0, so the selects
-    // reproduce the reference's `if v > 1 / elif v < -1` updates exactly
+    // branch-free and short: the excess |v| - 1 equals the reference's v - 1 / -1 - v
+    // bit for bit, and fmax leaves worst (>= 0) unchanged when |v| <= 1 or v is NaN;
+    // only |v| > 1 replaces v, by +-1 with v's sign (NaN and +-0 pass through)
 #pragma unroll
     for (int l = 0; l < D; ++l) {
         const double v = s.v[l];
-        const bool hi = v > 1.0, lo = v < -1.0;
-        const double ex = hi ? v - 1.0 : (lo ? -1.0 - v : 0.0);
-        worst = ex > worst ? ex : worst;
-        s.v[l] = hi ? 1.0 : (lo ? -1.0 : v);
+        const double av = fabs(v);
+        worst = fmax(worst, av - 1.0);
+        s.v[l] = av > 1.0 ? copysign(1.0, v) : v;
     }
 }
 
