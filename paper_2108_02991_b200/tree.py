@@ -391,9 +391,13 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
         per_group = np.add.reduceat(np.append(sc, 0), np.minimum(so[:-1], n_seg)) * \
             (so[1:] > so[:-1])
         sizes = (tg.d_ge - tg.d_gb).cpu().numpy()
+        ss = seg_start[:n_seg].cpu().numpy()
+        near = np.add.reduceat(np.append(np.where(ss < n_s, sc, 0), 0),
+                               np.minimum(so[:-1], n_seg)) * (so[1:] > so[:-1])
         stats.update(nodes=n_nodes, leaves=src.n_leaves, groups=n_groups, segments=n_seg,
                      slots=n_slots, units=n_units, interp_order=order, opening_theta=theta,
-                     pairs=int(np.dot(per_group, sizes)))
+                     pairs=int(np.dot(per_group, sizes)),
+                     near_pairs=int(np.dot(near, sizes)))
     if lists is not None:
         lists.update(seg_off=seg_off.cpu().numpy(), seg_start=seg_start[:n_seg].cpu().numpy(),
                      seg_count=seg_count[:n_seg].cpu().numpy(),

@@ -68,6 +68,7 @@ def main():
                        t_tree_s=best, t_exact_s=t_exact, speedup=t_exact / best,
                        t_lattice_tree_build_s=t_build, t_static_proxies_s=t_prox,
                        pairs_per_target=st["pairs"] / pts.shape[0],
+                       near_fraction=st["near_pairs"] / max(st["pairs"], 1),
                        **{k: v for k, v in st.items() if k not in ("interp_order", "opening_theta")})
             print(json.dumps(rec), flush=True)
             lines.append(rec)

@@ -83,7 +83,8 @@ def main():
                 rec = dict(cloud=cname, p=p, dims=d,
                            err_cost=e_cost, err_grad=e_grad, t_tree_s=t_tree,
                            t_direct_s=t_direct, speedup=t_direct / t_tree,
-                           leaf=a.leaf, pairs_per_target=st["pairs"] / p, **st)
+                           leaf=a.leaf, pairs_per_target=st["pairs"] / p,
+                           near_fraction=st["near_pairs"] / max(st["pairs"], 1), **st)
                 print(json.dumps(rec), flush=True)
                 lines.append(rec)
     if a.out:
