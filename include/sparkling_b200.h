@@ -215,11 +215,13 @@ int spk_tree_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
                    spk_stream_t stream);
 /* Target groups of <= cap particles following the octree (spk_tree_host_groups),
  * sorted by first particle: grp_begin/grp_end [group_capacity] i64 (device), n_groups
- * HOST.  Workspace: spk_tree_build_workspace_bytes(0, max(n_nodes, group_capacity)). */
+ * HOST.  cut (optional, [n] u8): particles that must start a group (the first particles of
+ * enclosing far-level parents), so that every group lies inside one parent.  Workspace: spk_tree_build_workspace_bytes(0, max(n_nodes, group_capacity)). */
 int spk_tree_groups(const int64_t* node_begin, const int64_t* node_end,
                     const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
-                    int64_t cap, int64_t group_capacity, int64_t* grp_begin, int64_t* grp_end,
-                    int64_t* n_groups, void* ws, size_t ws_bytes, spk_stream_t stream);
+                    int64_t cap, const uint8_t* cut, int64_t group_capacity,
+                    int64_t* grp_begin, int64_t* grp_end, int64_t* n_groups, void* ws,
+                    size_t ws_bytes, spk_stream_t stream);
 
 /* Node boxes {min xyz, max xyz} of an octree over sorted records: leaves reduce their
  * particles, internal nodes (BFS levels, level_off is a HOST array of n_levels + 1
@@ -237,14 +239,18 @@ int spk_tree_node_boxes(const void* rec, int64_t n_nodes, const int32_t* first_c
  * far nodes and opened leaves contribute their particle ranges (contiguous ranges merge).
  * Count pass: slot_of/slot_node [n_nodes] i32, slot_box [n_nodes][6] f32 (center, half),
  * slot_unit_off [n_nodes + 1] i64, seg_off [n_groups + 1] i64, totals [3] i64 = segments,
- * slots, P2M units (device).  Write pass fills seg_start/seg_count and the P2M units. */
+ * slots, P2M units (device).  Write pass fills seg_start/seg_count and the P2M units.
+ * Optional far level: parent_box [n_parents][6] and group_parent [n_groups]; nodes far
+ * from a group's parent (same opening test) are skipped -- the parent's P2L/L2P covers
+ * them; far_only = 1 emits far nodes only (the parents' own walk, for their P2L). */
 size_t spk_tree_plan_workspace_bytes(int64_t n_nodes, int64_t n_groups);
 int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
                         const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
                         const float* node_box, const float* group_box, int64_t n_groups,
                         double theta, int order, int dims, int64_t n_src, int32_t* slot_of,
                         int32_t* slot_node, float* slot_box, int64_t* slot_unit_off,
-                        int64_t* seg_off, int64_t* totals, void* ws, size_t ws_bytes,
+                        int64_t* seg_off, int64_t* totals, const float* parent_box,
+                        const int32_t* group_parent, int far_only, void* ws, size_t ws_bytes,
                         spk_stream_t stream);
 int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
                         const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
@@ -253,7 +259,22 @@ int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
                         const int32_t* slot_of, const int32_t* slot_node,
                         const int64_t* slot_unit_off, int64_t n_slots, const int64_t* seg_off,
                         int64_t* seg_start, int32_t* seg_count, int32_t* unit_slot,
-                        int64_t* unit_begin, int64_t* unit_end, spk_stream_t stream);
+                        int64_t* unit_begin, int64_t* unit_end, const float* parent_box,
+                        const int32_t* group_parent, int far_only, spk_stream_t stream);
+
+/* Far level (target-side interpolation, the m2l + l2p of _treecode.py:330-426): the
+ * q^dims tensor Chebyshev points of every parent box (points [n_parents * q^dims] float4,
+ * parent_cheb_box [n_parents][6] = center, inflated half), the parent of every sorted
+ * target, and the L2P that adds the interpolated value / gradient (pval [n_parents *
+ * q^dims], pgrad [.. x dims] fp64, evaluated at those points) to val / grad. */
+int spk_tree_cheb_targets(const float* parent_box, int64_t n_parents, int order, int dims,
+                          void* points, float* parent_cheb_box, spk_stream_t stream);
+int spk_tree_parent_ids(const int64_t* parent_begin, const int64_t* parent_end,
+                        int64_t n_parents, int32_t* pid, spk_stream_t stream);
+int spk_tree_l2p(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_tgt,
+                 const int32_t* pid, const float* parent_cheb_box, const double* pval,
+                 const double* pgrad, int order, int dims, double* val, double* grad,
+                 spk_stream_t stream);
 
 /* Source-side Chebyshev interpolation (the P2M of _treecode.py:286-313 for a
  * particle-cluster scheme): proxies[slot * m + k] = {tensor Chebyshev point k of the
@@ -270,11 +291,13 @@ int spk_tree_p2m(const void* rec, int64_t n_units, const int32_t* unit_slot,
  * spk_tree_group_size() of them),
  *   val[perm[i]] = sum_{records r in g's segments} w_r sqrt(|t_i - r|^2 + eps2)
  *   grad[perm[i]] = sum w_r (t_i - r) / sqrt(...)
- * seg_off: [n_groups + 1]; seg_start (record offset into src), seg_count. */
+ * seg_off: [n_lists + 1]; seg_start (record offset into src), seg_count; grp_list
+ * (optional): the list of each group (default: list g), so groups can share a list. */
 int spk_tree_eval(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_groups,
-                  const int64_t* grp_begin, const int64_t* grp_end, const void* src,
-                  const int64_t* seg_off, const int64_t* seg_start, const int32_t* seg_count,
-                  int dims, float eps2, double* val, double* grad, spk_stream_t stream);
+                  const int64_t* grp_begin, const int64_t* grp_end, const int32_t* grp_list,
+                  const void* src, const int64_t* seg_off, const int64_t* seg_start,
+                  const int32_t* seg_count, int dims, float eps2, double* val, double* grad,
+                  spk_stream_t stream);
 int spk_tree_group_size(void);
 
 /* Host side (tree_host.cpp; HOST pointers).  An opaque octree over sorted keys:

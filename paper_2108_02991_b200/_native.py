@@ -68,14 +68,18 @@ SIGNATURES = {
     "spk_tree_p2m_workspace_bytes": (c_size, [c_i64, c_int, c_int]),
     "spk_tree_p2m": (c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_int, c_int,
                              c_vp, c_vp, c_size, c_vp]),
-    "spk_tree_eval": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
-                              c_flt, c_vp, c_vp, c_vp]),
+    "spk_tree_eval": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                              c_int, c_flt, c_vp, c_vp, c_vp]),
     "spk_tree_host_groups": (c_i64, [c_vp, c_i64, c_vp, c_vp]),
     "spk_tree_build_workspace_bytes": (c_size, [c_i64, c_i64]),
     "spk_tree_build": (c_int, [c_vp, c_i64, c_int, c_i64, c_int, c_i64, c_vp, c_vp, c_vp, c_vp,
                                c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
-    "spk_tree_groups": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp,
-                                c_vp, c_size, c_vp]),
+    "spk_tree_groups": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp,
+                                c_vp, c_vp, c_size, c_vp]),
+    "spk_tree_cheb_targets": (c_int, [c_vp, c_i64, c_int, c_int, c_vp, c_vp, c_vp]),
+    "spk_tree_parent_ids": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "spk_tree_l2p": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_vp,
+                             c_vp, c_vp]),
     "spk_nudft_workspace_bytes": (c_size, [c_i64, c_int, ctypes.POINTER(c_i64)]),
     "spk_nudft_adjoint": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.POINTER(c_i64), c_vp, c_vp,
                                   c_size, c_vp]),
@@ -90,10 +94,10 @@ SIGNATURES = {
     "spk_tree_plan_workspace_bytes": (c_size, [c_i64, c_i64]),
     "spk_tree_plan_count": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl,
                                     c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                    c_vp, c_size, c_vp]),
+                                    c_vp, c_vp, c_int, c_vp, c_size, c_vp]),
     "spk_tree_plan_write": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl,
                                     c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp,
-                                    c_vp, c_vp, c_vp, c_vp, c_vp]),
+                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
     "spk_tree_host_slot_nodes": (None, [c_vp, c_vp]),
     "spk_tree_group_size": (c_int, []),
     "spk_tree_host_build": (c_vp, [c_vp, c_i64, c_int, c_i64, c_int]),
@@ -117,7 +121,8 @@ LAUNCHES = {
     "spk_feasibility_residuals_batched": 2,
     "spk_tree_keys": 1, "spk_tree_sort": 10, "spk_tree_gather": 1, "spk_tree_boxes": 1,
     "spk_tree_p2m": 2, "spk_tree_eval": 1, "spk_tree_plan_count": 9, "spk_tree_node_boxes": 1,
-    "spk_tree_groups": 11,
+    "spk_tree_groups": 11, "spk_tree_cheb_targets": 1, "spk_tree_parent_ids": 1,
+    "spk_tree_l2p": 1,
     "spk_tree_plan_write": 2, "spk_nudft_adjoint": 2, "spk_nudft_forward": 2,
     "spk_dcf_update": 1, "spk_psf_magnitude": 1,
 }

@@ -198,7 +198,7 @@ def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg
     order, theta = params
     src = field.source_tree()
     if tg is None:
-        tg = tree.TargetGroups(tgt4, field.dims)
+        tg = tree.TargetGroups(tgt4, field.dims, parent_cap=tree.far_parent_cap(tgt4.shape[0]))
     return tree.tree_eval(tg, src, order, theta, eps2, static=True)
 
 

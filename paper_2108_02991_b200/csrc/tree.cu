@@ -330,7 +330,8 @@ template <int PASS>
 __global__ void groups_kernel(const long long* __restrict__ nbeg, const long long* __restrict__ nend,
                               const int32_t* __restrict__ first_child,
                               const int32_t* __restrict__ n_child, long long n_nodes,
-                              long long cap, long long* __restrict__ cnt_out,
+                              long long cap, const uint8_t* __restrict__ cut,
+                              long long* __restrict__ cnt_out,
                               const long long* __restrict__ off, long long* __restrict__ gb,
                               long long* __restrict__ ge) {
     const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -362,7 +363,9 @@ __global__ void groups_kernel(const long long* __restrict__ nbeg, const long lon
                 cb = -1;
                 continue;
             }
-            if (cb >= 0 && ue - cb <= cap) {
+            // `cut` marks the first particles of enclosing groups (far-level parents):
+            // a group never straddles one
+            if (cb >= 0 && ue - cb <= cap && !(cut && cut[ub])) {
                 ce = ue;
             } else {
                 if (cb >= 0) emit(cb, ce);
@@ -430,6 +433,9 @@ struct TravParams {
     const long long* seg_off;  // pass 1 in
     long long* seg_start;      // pass 1 out
     int32_t* seg_count;        // pass 1 out
+    const float* pbox;         // optional far-level parents: [n_parents][6]
+    const int32_t* gparent;    // group -> parent
+    int far_only;              // parents' own walk: emit far nodes only (no near leaves)
 };
 constexpr int TR_STACK = 224;  // >= 31 levels x 7 pending siblings + 1
 
@@ -442,6 +448,8 @@ __global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
     if (g >= P.n_groups) return;
     const CR tb = center_radius(P.gbox + g * 6, P.dims);
     const float th2 = __fmul_rn(P.theta, P.theta);
+    CR pb{};
+    if (P.pbox) pb = center_radius(P.pbox + (size_t)P.gparent[g] * 6, P.dims);
     int32_t stk[TR_STACK];
     int sp = 0;
     stk[sp++] = 0;
@@ -458,13 +466,38 @@ __global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
             pend_cnt = 0;
         }
     };
+    // Far level: stack entries carry bit 30 once inside a subtree in which no node can be
+    // far from the parent ("strongly near": r_P >= theta (|c_P - c_u| + r_u)).
+    constexpr int32_t FREE = 1 << 30;
     while (sp > 0) {
-        const int32_t v = stk[--sp];
+        const int32_t ent = stk[--sp];
+        const int32_t v = ent & (FREE - 1);
+        bool free_sub = (ent & FREE) != 0;
         const CR sb = center_radius(P.nbox + (size_t)v * 6, P.dims);
         float d2 = 0.0f;
         for (int a = 0; a < P.dims; ++a) {
             const float d = __fsub_rn(tb.c[a], sb.c[a]);
             d2 = __fadd_rn(d2, __fmul_rn(d, d));
+        }
+        if (P.pbox && !free_sub) {
+            // nodes far from the group's parent are the far level's (interpolated) share:
+            // skip them with their subtrees, exactly where the parent's walk stopped
+            float pd2 = 0.0f;
+            for (int a = 0; a < P.dims; ++a) {
+                const float d = __fsub_rn(pb.c[a], sb.c[a]);
+                pd2 = __fadd_rn(pd2, __fmul_rn(d, d));
+            }
+            const float plhs = __fadd_rn(pb.r, sb.r);
+            if (__fmul_rn(plhs, plhs) < __fmul_rn(th2, pd2)) continue;
+            // below a node that is not strongly near, descendants may still be parent-far:
+            // descend without the group's own opening test (leaves are the group's)
+            free_sub = pb.r >= __fmul_rn(P.theta, __fadd_rn(__fsqrt_rn(pd2), sb.r));
+            if (!free_sub && P.nchild[v] != 0) {
+                const int nc = P.nchild[v];
+                if (sp + nc > TR_STACK) continue;
+                for (int c = nc - 1; c >= 0; --c) stk[sp++] = P.fchild[v] + c;
+                continue;
+            }
         }
         const float lhs = __fadd_rn(tb.r, sb.r);
         const bool far = __fmul_rn(lhs, lhs) < __fmul_rn(th2, d2);
@@ -477,6 +510,7 @@ __global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
             pend_direct = false;
             flush();
         } else if (far || P.nchild[v] == 0) {
+            if (!far && P.far_only) continue;
             if (pend_cnt > 0 && pend_direct && pend_start + pend_cnt == b &&
                 pend_cnt + (e - b) < (1LL << 30)) {
                 pend_cnt += e - b;
@@ -489,7 +523,8 @@ __global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
         } else {
             const int nc = P.nchild[v];
             if (sp + nc > TR_STACK) continue;  // unreachable for <= 31 levels
-            for (int c = nc - 1; c >= 0; --c) stk[sp++] = P.fchild[v] + c;
+            const int32_t flag = free_sub ? FREE : 0;
+            for (int c = nc - 1; c >= 0; --c) stk[sp++] = (P.fchild[v] + c) | flag;
         }
     }
     flush();
@@ -546,6 +581,81 @@ __global__ void totals_kernel(const long long* __restrict__ seg_off, long long n
     totals[2] = slot_unit_off[n_nodes];  // units_per_slot is zero past the last slot
 }
 
+
+// ---------------------------------------------------------------- far level (P2L / L2P)
+// Far-level parents (target groups of <= 512 particles) evaluate their far list at the
+// q^d tensor Chebyshev points of their box (P2L: an ordinary eval over those points) and
+// every target interpolates value and gradient from them (L2P) -- the target-side
+// interpolation of the reference's black-box FMM (m2l + l2p, _treecode.py:330-426).
+__global__ void cheb_targets_kernel(const float* __restrict__ pbox, long long n_par, int q,
+                                    int dims, ChebTable T, float4* __restrict__ pts,
+                                    float* __restrict__ pcb) {
+    const long long p = blockIdx.x;
+    const CR b = center_radius(pbox + (size_t)p * 6, dims);
+    float h[3];
+    float hmax = 0.0f;
+    for (int a = 0; a < dims; ++a) hmax = fmaxf(hmax, b.h[a]);
+    for (int a = 0; a < 3; ++a)
+        h[a] = a < dims ? fmaxf(b.h[a], __fadd_rn(__fmul_rn(1e-6f, hmax), 1e-30f)) : 1.0f;
+    if (threadIdx.x < 6) pcb[p * 6 + threadIdx.x] = threadIdx.x < 3 ? b.c[threadIdx.x] : h[threadIdx.x - 3];
+    const int m = dims == 3 ? q * q * q : q * q;
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+        int kx, ky, kz;
+        if (dims == 3) {
+            kx = k / (q * q), ky = (k / q) % q, kz = k % q;
+        } else {
+            kx = k / q, ky = k % q, kz = 0;
+        }
+        pts[p * m + k] = make_float4(fmaf(h[0], T.t[kx], b.c[0]), fmaf(h[1], T.t[ky], b.c[1]),
+                                     dims == 3 ? fmaf(h[2], T.t[kz], b.c[2]) : 0.0f, 0.0f);
+    }
+}
+
+__global__ void parent_ids_kernel(const long long* __restrict__ pb, const long long* __restrict__ pe,
+                                  long long n_par, int32_t* __restrict__ pid) {
+    const long long p = blockIdx.x;
+    for (long long i = pb[p] + threadIdx.x; i < pe[p]; i += blockDim.x) pid[i] = (int32_t)p;
+}
+
+template <int D>
+__global__ void l2p_kernel(const float4* __restrict__ tgt, const int32_t* __restrict__ perm,
+                           long long n_t, const int32_t* __restrict__ pid,
+                           const float* __restrict__ pcb, const double* __restrict__ pval,
+                           const double* __restrict__ pgrad, int q, ChebTable T,
+                           double* __restrict__ val, double* __restrict__ grad) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_t) return;
+    const float4 x = tgt[i];
+    const long long p = pid[i];
+    const float* bx = pcb + p * 6;
+    float l[3][P2M_MAX_ORDER] = {};
+    lagrange((x.x - bx[0]) / bx[3], q, T, l[0]);
+    lagrange((x.y - bx[1]) / bx[4], q, T, l[1]);
+    if (D == 3) lagrange((x.z - bx[2]) / bx[5], q, T, l[2]);
+    const int m = D == 3 ? q * q * q : q * q;
+    const double* pv = pval + p * m;
+    const double* pg = pgrad + p * m * D;
+    double v = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
+    for (int k = 0; k < m; ++k) {
+        int kx, ky, kz;
+        if (D == 3) {
+            kx = k / (q * q), ky = (k / q) % q, kz = k % q;
+        } else {
+            kx = k / q, ky = k % q, kz = 0;
+        }
+        const double w = (double)l[0][kx] * l[1][ky] * (D == 3 ? l[2][kz] : 1.0f);
+        v += w * pv[k];
+        g0 += w * pg[k * D];
+        g1 += w * pg[k * D + 1];
+        if (D == 3) g2 += w * pg[k * D + 2];
+    }
+    const long long o = perm[i];
+    val[o] += v;
+    grad[o * D] += g0;
+    grad[o * D + 1] += g1;
+    if (D == 3) grad[o * D + 2] += g2;
+}
+
 // ---------------------------------------------------------------- evaluation
 __device__ __forceinline__ float rsqrt_approx(float x) {
     float r;
@@ -572,7 +682,8 @@ struct EvalParams {
     const long long* grp_begin;  // target group g = sorted targets [begin, end), <= TR_GROUP
     const long long* grp_end;
     const float4* src;       // [sorted sources | proxies], {x, y, z, w}
-    const long long* seg_off;   // [n_groups + 1]
+    const long long* seg_off;   // [n_lists + 1]
+    const int32_t* grp_list;    // optional group -> list (several groups share a list)
     const long long* seg_start; // record offset into src
     const int32_t* seg_count;
     float eps2;
@@ -686,7 +797,8 @@ __global__ void __launch_bounds__(TR_THREADS, 4) tree_eval_kernel(const EvalPara
     const float2 e2 = bcast(P.eps2);
     double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
 
-    SegCursor c{P.seg_off[g], P.seg_off[g + 1], 0, 0, 0, 0};
+    const long long lg = P.grp_list ? (long long)P.grp_list[g] : g;
+    SegCursor c{P.seg_off[lg], P.seg_off[lg + 1], 0, 0, 0, 0};
     load_window(c, P, lane);
     int cnt = fill_batch(buf[warp][0], c, P, lane);
     int stage = 0;
@@ -826,9 +938,10 @@ int spk_tree_p2m(const void* rec, int64_t n_units, const int32_t* unit_slot,
 }
 
 int spk_tree_eval(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_groups,
-                  const int64_t* grp_begin, const int64_t* grp_end, const void* src,
-                  const int64_t* seg_off, const int64_t* seg_start, const int32_t* seg_count,
-                  int dims, float eps2, double* val, double* grad, spk_stream_t stream) {
+                  const int64_t* grp_begin, const int64_t* grp_end, const int32_t* grp_list,
+                  const void* src, const int64_t* seg_off, const int64_t* seg_start,
+                  const int32_t* seg_count, int dims, float eps2, double* val, double* grad,
+                  spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
     if (n_groups == 0) return SPK_OK;
     EvalParams P;
@@ -838,6 +951,7 @@ int spk_tree_eval(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_gro
     P.grp_end = reinterpret_cast<const long long*>(grp_end);
     P.src = static_cast<const float4*>(src);
     P.seg_off = reinterpret_cast<const long long*>(seg_off);
+    P.grp_list = grp_list;
     P.seg_start = reinterpret_cast<const long long*>(seg_start);
     P.seg_count = seg_count;
     P.eps2 = eps2;
@@ -910,7 +1024,8 @@ int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
                         const float* node_box, const float* group_box, int64_t n_groups,
                         double theta, int order, int dims, int64_t n_src, int32_t* slot_of,
                         int32_t* slot_node, float* slot_box, int64_t* slot_unit_off,
-                        int64_t* seg_off, int64_t* totals, void* ws, size_t ws_bytes,
+                        int64_t* seg_off, int64_t* totals, const float* parent_box,
+                        const int32_t* group_parent, int far_only, void* ws, size_t ws_bytes,
                         spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
     SPK_REQUIRE(n_nodes > 0 && n_groups > 0, SPK_ERR_ARG, "tree plan: empty tree or groups");
@@ -943,6 +1058,9 @@ int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
     P.n_src = n_src;
     P.is_proxy = is_proxy;
     P.seg_cnt = seg_cnt;
+    P.pbox = parent_box;
+    P.gparent = group_parent;
+    P.far_only = far_only;
     traverse_kernel<0><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
     SPK_CHECK_LAUNCH("spk_tree_plan_count(traverse)");
     size_t t = cub_bytes;
@@ -973,7 +1091,8 @@ int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
                         const int32_t* slot_of, const int32_t* slot_node,
                         const int64_t* slot_unit_off, int64_t n_slots, const int64_t* seg_off,
                         int64_t* seg_start, int32_t* seg_count, int32_t* unit_slot,
-                        int64_t* unit_begin, int64_t* unit_end, spk_stream_t stream) {
+                        int64_t* unit_begin, int64_t* unit_end, const float* parent_box,
+                        const int32_t* group_parent, int far_only, spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
     cudaStream_t s = (cudaStream_t)stream;
     TravParams P{};
@@ -992,6 +1111,9 @@ int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
     P.seg_off = reinterpret_cast<const long long*>(seg_off);
     P.seg_start = reinterpret_cast<long long*>(seg_start);
     P.seg_count = seg_count;
+    P.pbox = parent_box;
+    P.gparent = group_parent;
+    P.far_only = far_only;
     traverse_kernel<1><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
     SPK_CHECK_LAUNCH("spk_tree_plan_write(traverse)");
     if (n_slots > 0) {
@@ -1116,8 +1238,9 @@ int spk_tree_build(const uint64_t* keys, int64_t n, int dims, int64_t leaf_cap,
 
 int spk_tree_groups(const int64_t* node_begin, const int64_t* node_end,
                     const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
-                    int64_t cap, int64_t group_capacity, int64_t* grp_begin, int64_t* grp_end,
-                    int64_t* n_groups, void* ws, size_t ws_bytes, spk_stream_t stream) {
+                    int64_t cap, const uint8_t* cut, int64_t group_capacity,
+                    int64_t* grp_begin, int64_t* grp_end, int64_t* n_groups, void* ws,
+                    size_t ws_bytes, spk_stream_t stream) {
     SPK_REQUIRE(cap >= 1, SPK_ERR_ARG, "tree groups: cap must be >= 1");
     SPK_REQUIRE(ws_bytes >= spk_tree_build_workspace_bytes(0, std::max(n_nodes, group_capacity)),
                 SPK_ERR_WORKSPACE, "tree groups: workspace too small");
@@ -1126,7 +1249,8 @@ int spk_tree_groups(const int64_t* node_begin, const int64_t* node_end,
     const long long* nb = reinterpret_cast<const long long*>(node_begin);
     const long long* ne = reinterpret_cast<const long long*>(node_end);
     const unsigned blocks = (unsigned)((n_nodes + 127) / 128);
-    groups_kernel<0><<<blocks, 128, 0, s>>>(nb, ne, first_child, n_child, n_nodes, cap, w.gcnt,
+    groups_kernel<0><<<blocks, 128, 0, s>>>(nb, ne, first_child, n_child, n_nodes, cap, cut,
+                                            w.gcnt,
                                             nullptr, nullptr, nullptr);
     cudaMemsetAsync(w.gcnt + n_nodes, 0, 8, s);
     size_t t = w.cub_bytes;
@@ -1139,7 +1263,8 @@ int spk_tree_groups(const int64_t* node_begin, const int64_t* node_end,
     *n_groups = total;
     SPK_REQUIRE(total <= group_capacity, SPK_ERR_WORKSPACE,
                 "tree groups: %lld groups exceed capacity %lld", total, (long long)group_capacity);
-    groups_kernel<1><<<blocks, 128, 0, s>>>(nb, ne, first_child, n_child, n_nodes, cap, nullptr,
+    groups_kernel<1><<<blocks, 128, 0, s>>>(nb, ne, first_child, n_child, n_nodes, cap, cut,
+                                            nullptr,
                                             w.goff, w.sort_k, w.sort_v);
     SPK_CHECK_LAUNCH("spk_tree_groups");
     t = w.cub_bytes;
@@ -1148,6 +1273,47 @@ int spk_tree_groups(const int64_t* node_begin, const int64_t* node_end,
                                         reinterpret_cast<long long*>(grp_end), (int)total, 0, 40,
                                         s);
     SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree groups sort: %s", cudaGetErrorString(e));
+    return SPK_OK;
+}
+
+int spk_tree_cheb_targets(const float* parent_box, int64_t n_parents, int order, int dims,
+                          void* points, float* parent_cheb_box, spk_stream_t stream) {
+    SPK_REQUIRE(order >= 2 && order <= P2M_MAX_ORDER, SPK_ERR_ARG, "bad order %d", order);
+    if (n_parents == 0) return SPK_OK;
+    cheb_targets_kernel<<<(unsigned)n_parents, 128, 0, (cudaStream_t)stream>>>(
+        parent_box, n_parents, order, dims, cheb_table(order), static_cast<float4*>(points),
+        parent_cheb_box);
+    SPK_CHECK_LAUNCH("spk_tree_cheb_targets");
+    return SPK_OK;
+}
+
+int spk_tree_parent_ids(const int64_t* parent_begin, const int64_t* parent_end,
+                        int64_t n_parents, int32_t* pid, spk_stream_t stream) {
+    if (n_parents == 0) return SPK_OK;
+    parent_ids_kernel<<<(unsigned)n_parents, 128, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const long long*>(parent_begin),
+        reinterpret_cast<const long long*>(parent_end), n_parents, pid);
+    SPK_CHECK_LAUNCH("spk_tree_parent_ids");
+    return SPK_OK;
+}
+
+int spk_tree_l2p(const void* tgt_sorted, const int32_t* tgt_perm, int64_t n_tgt,
+                 const int32_t* pid, const float* parent_cheb_box, const double* pval,
+                 const double* pgrad, int order, int dims, double* val, double* grad,
+                 spk_stream_t stream) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    if (n_tgt == 0) return SPK_OK;
+    const unsigned blocks = (unsigned)((n_tgt + 127) / 128);
+    const ChebTable T = cheb_table(order);
+    if (dims == 3)
+        l2p_kernel<3><<<blocks, 128, 0, (cudaStream_t)stream>>>(
+            static_cast<const float4*>(tgt_sorted), tgt_perm, n_tgt, pid, parent_cheb_box, pval,
+            pgrad, order, T, val, grad);
+    else
+        l2p_kernel<2><<<blocks, 128, 0, (cudaStream_t)stream>>>(
+            static_cast<const float4*>(tgt_sorted), tgt_perm, n_tgt, pid, parent_cheb_box, pval,
+            pgrad, order, T, val, grad);
+    SPK_CHECK_LAUNCH("spk_tree_l2p");
     return SPK_OK;
 }
 

@@ -133,8 +133,10 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
     order = cfg.interp_order if cfg.interp_order is not None else auto_order
     same = tgt4.data_ptr() == src4.data_ptr() and tgt4.shape[0] == n_src
     src = tree.SourceTree(src4, dims)
-    tg = tree.TargetGroups(tgt4, dims, same_as=src if same else None)
-    val, grad = tree.tree_eval(tg, src, order, theta, eps2)
+    cap = tree.far_parent_cap(tgt4.shape[0])
+    tg = tree.TargetGroups(tgt4, dims, same_as=src if same else None, parent_cap=cap)
+    # the far level needs every node's proxies (static), the plain walk builds its own
+    val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
     if cfg.interp_order is not None:
         err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         while max(err_val, err_grad) > cfg.tree_precision and order < MAX_INTERP_ORDER:
@@ -143,7 +145,7 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
                 f"tree backend at interp_order={order - 1} reached relative error "
                 f"{max(err_val, err_grad):.2e} > {cfg.tree_precision:.2e}; "
                 f"escalating to order {order}")
-            val, grad = tree.tree_eval(tg, src, order, theta, eps2)
+            val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
             err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         if max(err_val, err_grad) > cfg.tree_precision:
             warnings.warn(

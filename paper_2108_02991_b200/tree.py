@@ -54,6 +54,16 @@ DIRECT_BELOW = 1 << 17
 # spokes, whose near field against the dense lattice is huge (131k targets against the
 # C4 lattice: 45 -> 24 ms; no effect at 524k targets and above).
 TARGET_MIN_LEVEL = 5
+# Far level (P2L/L2P on parents of <= FAR_PARENT_CAP targets) from this many targets on:
+# at C4 (8.4M) it cuts the repulsion evaluation by ~30 % (q4: 111 -> 74 ms) and the q4
+# attraction by 25 %, at C2 it is neutral (profiles/r01_far_level.txt).
+FAR_LEVEL_MIN = 1 << 21
+FAR_PARENT_CAP = 1024
+
+
+def far_parent_cap(n_targets: int) -> int | None:
+    """Parent capacity of the far level for this many targets (None: plain treecode)."""
+    return FAR_PARENT_CAP if n_targets >= FAR_LEVEL_MIN else None
 
 
 def auto_params(precision: float) -> tuple[int, float] | None:
@@ -155,8 +165,9 @@ class _DeviceOctree:
         self.fc, self.nc = self.fc[:self.n_nodes], self.nc[:self.n_nodes]
         self.leaves = self.leaves[:self.n_leaves]
 
-    def groups(self, cap: int):
-        """Target groups (spk_tree_groups) -> device (begin, end) sorted by begin."""
+    def groups(self, cap: int, cut: torch.Tensor | None = None):
+        """Target groups (spk_tree_groups) -> device (begin, end) sorted by begin; ``cut``
+        (u8 per particle) marks particles that must start a group."""
         dev = self.nb.device
         gcap = max(self.n_nodes * 8, int(self.ne[:1].item() // cap) * 4 + 1024)
         gb = torch.empty(gcap, dtype=torch.int64, device=dev)
@@ -165,7 +176,8 @@ class _DeviceOctree:
         ws = _device.workspace(_native.query("spk_tree_build_workspace_bytes", 0,
                                              max(self.n_nodes, gcap)), "tree_groups")
         _native.call("spk_tree_groups", self.nb.data_ptr(), self.ne.data_ptr(),
-                     self.fc.data_ptr(), self.nc.data_ptr(), self.n_nodes, cap, gcap,
+                     self.fc.data_ptr(), self.nc.data_ptr(), self.n_nodes, cap,
+                     _device.ptr(cut), gcap,
                      gb.data_ptr(), ge.data_ptr(), n_groups.ctypes.data, ws.data_ptr(),
                      ws.numel(), _device.stream())
         k = int(n_groups[0])
@@ -283,36 +295,124 @@ class TargetGroups:
     follow their octree (sibling subtrees), with tight group boxes (device)."""
 
     def __init__(self, tgt4: torch.Tensor, dims: int, same_as: SourceTree | None = None,
-                 min_level: int = TARGET_MIN_LEVEL):
+                 min_level: int = TARGET_MIN_LEVEL, parent_cap: int | None = None):
         lib = _native.load()
         dev = tgt4.device
         st = _device.stream()
         self.n = tgt4.shape[0]
+        self.dims = dims
         group = lib.spk_tree_group_size()
         if same_as is not None:
             self.perm, self.rec = same_as.perm, same_as.rec
-            self.d_gb, self.d_ge = same_as.groups()
+            octree = same_as.octree
         else:
             keys, self.perm = _sort(tgt4, dims)
             self.rec = torch.empty((self.n, 4), dtype=torch.float32, device=dev)
             _native.call("spk_tree_gather", tgt4.data_ptr(), self.perm.data_ptr(), self.n,
                          None, self.rec.data_ptr(), st)
-            self.d_gb, self.d_ge = _DeviceOctree(keys, self.n, dims, group,
-                                                 min_level).groups(group)
+            octree = _DeviceOctree(keys, self.n, dims, group, min_level)
+        self.parents = None
+        if parent_cap:
+            # far level: parents of <= parent_cap targets; every group lies in one parent
+            pb, pe = octree.groups(parent_cap)
+            cut = torch.zeros(self.n + 1, dtype=torch.uint8, device=dev)
+            cut[pb] = 1
+            self.d_gb, self.d_ge = octree.groups(group, cut)
+            self.n_parents = pb.shape[0]
+            self.pbox = torch.empty((self.n_parents, 6), dtype=torch.float32, device=dev)
+            _native.call("spk_tree_boxes", self.rec.data_ptr(), self.n_parents, pb.data_ptr(),
+                         pe.data_ptr(), dims, self.pbox.data_ptr(), st)
+            self.pid = torch.empty(self.n, dtype=torch.int32, device=dev)
+            _native.call("spk_tree_parent_ids", pb.data_ptr(), pe.data_ptr(), self.n_parents,
+                         self.pid.data_ptr(), st)
+            self.gparent = self.pid[self.d_gb].contiguous()
+            self.parents = (pb, pe)
+        elif same_as is not None:
+            self.d_gb, self.d_ge = same_as.groups()
+        else:
+            self.d_gb, self.d_ge = octree.groups(group)
         self.n_groups = self.d_gb.shape[0]
         self.box = torch.empty((self.n_groups, 6), dtype=torch.float32, device=dev)
         _native.call("spk_tree_boxes", self.rec.data_ptr(), self.n_groups, self.d_gb.data_ptr(),
                      self.d_ge.data_ptr(), dims, self.box.data_ptr(), st)
 
 
+def _static_plan(src: SourceTree, boxes: torch.Tensor, n_groups: int, theta: float,
+                 order: int, slot_of: torch.Tensor, pbox=None, gparent=None, far_only=False):
+    """Interaction lists against the source tree's static (all-node) proxies."""
+    dev = src.rec.device
+    st = _device.stream()
+    n_nodes = src.n_nodes
+    tmp_i = torch.empty(n_nodes, dtype=torch.int32, device=dev)
+    tmp_n = torch.empty(n_nodes, dtype=torch.int32, device=dev)
+    tmp_b = torch.empty((n_nodes, 6), dtype=torch.float32, device=dev)
+    tmp_u = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+    seg_off = torch.empty(n_groups + 1, dtype=torch.int64, device=dev)
+    totals = torch.empty(3, dtype=torch.int64, device=dev)
+    ws = _device.workspace(_native.query("spk_tree_plan_workspace_bytes", n_nodes, n_groups),
+                           "tree_plan")
+    args = (src.d_nb.data_ptr(), src.d_ne.data_ptr(), src.d_fc.data_ptr(), src.d_nc.data_ptr(),
+            n_nodes, src.node_box.data_ptr(), boxes.data_ptr(), n_groups, float(theta), order,
+            src.dims, src.n)
+    _native.call("spk_tree_plan_count", *args, tmp_i.data_ptr(), tmp_n.data_ptr(),
+                 tmp_b.data_ptr(), tmp_u.data_ptr(), seg_off.data_ptr(), totals.data_ptr(),
+                 _device.ptr(pbox), _device.ptr(gparent), int(far_only), ws.data_ptr(),
+                 ws.numel(), st)
+    n_seg = int(totals[0].item())
+    seg_start = torch.empty(max(n_seg, 1), dtype=torch.int64, device=dev)
+    seg_count = torch.empty(max(n_seg, 1), dtype=torch.int32, device=dev)
+    _native.call("spk_tree_plan_write", *args, slot_of.data_ptr(), tmp_n.data_ptr(),
+                 tmp_u.data_ptr(), 0, seg_off.data_ptr(), seg_start.data_ptr(),
+                 seg_count.data_ptr(), tmp_i.data_ptr(), seg_off.data_ptr(),
+                 seg_off.data_ptr(), _device.ptr(pbox), _device.ptr(gparent), int(far_only),
+                 st)
+    return seg_off, seg_start, seg_count, n_seg
+
+
+def _far_level(tg: TargetGroups, src: SourceTree, order: int, far_order: int, theta: float,
+               eps2: float, rec: torch.Tensor, slot_of: torch.Tensor):
+    """P2L: every parent's far list evaluated at the far_order^d Chebyshev points of its
+    box -> (parent Chebyshev boxes, values [P * mt], gradients [P * mt, d])."""
+    dev = src.rec.device
+    st = _device.stream()
+    dims = src.dims
+    n_par = tg.n_parents
+    so, ss, sc, _ = _static_plan(src, tg.pbox, n_par, theta, order, slot_of, far_only=True)
+    mt = far_order ** dims
+    pts = torch.empty((n_par * mt, 4), dtype=torch.float32, device=dev)
+    pcb = torch.empty((n_par, 6), dtype=torch.float32, device=dev)
+    _native.call("spk_tree_cheb_targets", tg.pbox.data_ptr(), n_par, far_order, dims,
+                 pts.data_ptr(), pcb.data_ptr(), st)
+    group = _native.load().spk_tree_group_size()
+    per = (mt + group - 1) // group
+    j = torch.arange(per, device=dev, dtype=torch.int64)
+    base = torch.arange(n_par, device=dev, dtype=torch.int64)[:, None] * mt
+    gb = (base + j[None, :] * group).reshape(-1)
+    ge = torch.minimum(gb + group, (base + mt).expand(-1, per).reshape(-1))
+    glist = torch.arange(n_par, device=dev, dtype=torch.int32).repeat_interleave(per)
+    ident = torch.arange(n_par * mt, device=dev, dtype=torch.int32)
+    pval = torch.empty(n_par * mt, dtype=torch.float64, device=dev)
+    pgrad = torch.empty((n_par * mt, dims), dtype=torch.float64, device=dev)
+    _native.call("spk_tree_eval", pts.data_ptr(), ident.data_ptr(), gb.shape[0], gb.data_ptr(),
+                 ge.data_ptr(), glist.data_ptr(), rec.data_ptr(), so.data_ptr(), ss.data_ptr(),
+                 sc.data_ptr(), dims, float(eps2), pval.data_ptr(), pgrad.data_ptr(), st)
+    return pcb, pval, pgrad
+
+
 def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2: float, *,
               static: bool = False, stats: dict | None = None, lists: dict | None = None,
-              val: torch.Tensor | None = None, grad: torch.Tensor | None = None):
+              val: torch.Tensor | None = None, grad: torch.Tensor | None = None,
+              far_order: int | None = None):
     """Weighted treecode sums of the sources at the targets -> (val, grad) fp64, targets'
     original order.  ``static`` uses the source tree's cached all-node proxies (no P2M in
-    the call); otherwise proxies are built for the nodes this traversal opens as far."""
+    the call); otherwise proxies are built for the nodes this traversal opens as far.
+    With a far level (``tg`` built with ``parent_cap``), nodes far from a target's parent
+    are evaluated at the parent's far_order^d Chebyshev points and interpolated (P2L/L2P);
+    the groups' lists then hold only the remaining nodes (static proxies)."""
     if not 2 <= order <= MAX_ORDER:
         raise ValueError(f"interp_order must be in [2, {MAX_ORDER}]")
+    if tg.parents is not None:
+        return _tree_eval_far(tg, src, order, theta, eps2, far_order or order, val, grad)
     import time
 
     dev = src.rec.device
@@ -340,8 +440,8 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  src.d_fc.data_ptr(), src.d_nc.data_ptr(), n_nodes, src.node_box.data_ptr(),
                  tg.box.data_ptr(), n_groups, float(theta), order, dims, n_s,
                  slot_of.data_ptr(), slot_node.data_ptr(), slot_box.data_ptr(),
-                 slot_unit_off.data_ptr(), seg_off.data_ptr(), totals.data_ptr(),
-                 ws.data_ptr(), ws.numel(), st)
+                 slot_unit_off.data_ptr(), seg_off.data_ptr(), totals.data_ptr(), None, None,
+                 0, ws.data_ptr(), ws.numel(), st)
     n_seg, n_slots, n_units = (int(x) for x in totals.cpu().numpy())
     mark("plan_count")
     if static:
@@ -363,7 +463,7 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  write_slot_of.data_ptr(), slot_node.data_ptr(), slot_unit_off.data_ptr(),
                  0 if static else n_slots, seg_off.data_ptr(), seg_start.data_ptr(),
                  seg_count.data_ptr(), unit_slot.data_ptr(), unit_begin.data_ptr(),
-                 unit_end.data_ptr(), st)
+                 unit_end.data_ptr(), None, None, 0, st)
     mark("plan_write")
     if not static and n_slots:
         ws2 = _device.workspace(_native.query("spk_tree_p2m_workspace_bytes", n_units, order,
@@ -378,9 +478,9 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
     if grad is None:
         grad = torch.empty((tg.n, dims), dtype=torch.float64, device=dev)
     _native.call("spk_tree_eval", tg.rec.data_ptr(), tg.perm.data_ptr(), n_groups,
-                 tg.d_gb.data_ptr(), tg.d_ge.data_ptr(), rec.data_ptr(), seg_off.data_ptr(),
-                 seg_start.data_ptr(), seg_count.data_ptr(), dims, float(eps2),
-                 val.data_ptr(), grad.data_ptr(), st)
+                 tg.d_gb.data_ptr(), tg.d_ge.data_ptr(), None, rec.data_ptr(),
+                 seg_off.data_ptr(), seg_start.data_ptr(), seg_count.data_ptr(), dims,
+                 float(eps2), val.data_ptr(), grad.data_ptr(), st)
     mark("eval")
     if timing:
         stats["eval_phases_ms"] = {marks[i][0]: 1e3 * (marks[i][1] - marks[i - 1][1])
@@ -404,6 +504,28 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                      slot_node=slot_node[:n_slots].cpu().numpy(),
                      node_box=src.node_box.cpu().numpy(), group_box=tg.box.cpu().numpy(),
                      n_groups=n_groups, n_src=n_s)
+    return val, grad
+
+
+def _tree_eval_far(tg, src, order, theta, eps2, far_order, val, grad):
+    dev = src.rec.device
+    st = _device.stream()
+    dims = src.dims
+    rec, slot_of = src.static_proxies(order)
+    pcb, pval, pgrad = _far_level(tg, src, order, far_order, theta, eps2, rec, slot_of)
+    so, ss, sc, _ = _static_plan(src, tg.box, tg.n_groups, theta, order, slot_of,
+                                 tg.pbox, tg.gparent)
+    if val is None:
+        val = torch.empty(tg.n, dtype=torch.float64, device=dev)
+    if grad is None:
+        grad = torch.empty((tg.n, dims), dtype=torch.float64, device=dev)
+    _native.call("spk_tree_eval", tg.rec.data_ptr(), tg.perm.data_ptr(), tg.n_groups,
+                 tg.d_gb.data_ptr(), tg.d_ge.data_ptr(), None, rec.data_ptr(), so.data_ptr(),
+                 ss.data_ptr(), sc.data_ptr(), dims, float(eps2), val.data_ptr(),
+                 grad.data_ptr(), st)
+    _native.call("spk_tree_l2p", tg.rec.data_ptr(), tg.perm.data_ptr(), tg.n, tg.pid.data_ptr(),
+                 pcb.data_ptr(), pval.data_ptr(), pgrad.data_ptr(), far_order, dims,
+                 val.data_ptr(), grad.data_ptr(), st)
     return val, grad
 
 

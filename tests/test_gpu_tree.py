@@ -255,3 +255,33 @@ def test_device_octree_matches_host_builder(spk, dims):
         assert np.array_equal(dt.levels, T["levels"])
         gb, ge = dt.groups(64)
         assert np.array_equal(gb.cpu().numpy(), gb_h) and np.array_equal(ge.cpu().numpy(), ge_h)
+
+
+@pytest.mark.parametrize("order,theta", [(4, 0.7), (5, 0.7)])
+def test_far_level_matches_plain_treecode(spk, order, theta):
+    """The far level (parents' P2L at Chebyshev points + L2P) partitions the sources
+    exactly once with the groups' lists: same accuracy vs exact sums as the plain walk,
+    for unit-weight sources and for the weighted lattice."""
+    from paper_2108_02991_b200 import _device, tree
+    from paper_2108_02991_b200.attraction import grid_sums_device
+    from paper_2108_02991_b200.repulsion import direct_sums_device
+
+    pts = spk.perturb(spk.init_radial(400, 512, 3), 0.25, 3).points()
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    precision = 1e-3 if order == 4 else 1e-4
+    src = tree.SourceTree(pos4, 3)
+    for cap in (256, 1024):
+        tg = tree.TargetGroups(pos4, 3, same_as=src, parent_cap=cap)
+        vt, gt = tree.tree_eval(tg, src, order, theta, 1e-6, static=True)
+        vd, gd = direct_sums_device(pos4, pos4, 3, 1e-6)
+        vt, gt, vd, gd = (_device.d2h(x) for x in (vt, gt, vd, gd))
+        assert abs(vt.sum() - vd.sum()) / abs(vd.sum()) <= precision / 2
+        assert np.linalg.norm(gt - gd) / np.linalg.norm(gd) <= precision / 2
+    fld = spk.precompute_field(spk.discretize(spk.DensityParams(0.25, 2.0), 24, 3))
+    eps2 = fld.kernel_eps ** 2
+    tga = tree.TargetGroups(pos4, 3, parent_cap=512)
+    va, ga = tree.tree_eval(tga, fld.source_tree(), order, theta, eps2, static=True)
+    vr, gr = grid_sums_device(pos4, fld, eps2)
+    va, ga, vr, gr = (_device.d2h(x) for x in (va, ga, vr, gr))
+    assert abs(va.sum() - vr.sum()) / abs(vr.sum()) <= precision / 2
+    assert np.linalg.norm(ga - gr) / np.linalg.norm(gr) <= precision / 2
