@@ -26,6 +26,8 @@ precision with margin on radial-spoke, perturbed and uniform clouds.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -54,10 +56,12 @@ DIRECT_BELOW = 1 << 17
 # spokes, whose near field against the dense lattice is huge (131k targets against the
 # C4 lattice: 45 -> 24 ms; no effect at 524k targets and above).
 TARGET_MIN_LEVEL = 5
-# Far level (P2L/L2P on parents of <= FAR_PARENT_CAP targets) from this many targets on:
-# at C4 (8.4M) it cuts the repulsion evaluation by ~30 % (q4: 111 -> 74 ms) and the q4
-# attraction by 25 %, at C2 it is neutral (profiles/r01_far_level.txt).
-FAR_LEVEL_MIN = 1 << 21
+# Far level (P2L/L2P on parents of <= FAR_PARENT_CAP targets).  In isolation it cuts the
+# C4 repulsion evaluation by ~30 % (q4: 111 -> 74 ms, profiles/r01_far_level.txt), but in
+# the optimizer iteration the per-call P2M of every node it needs and the neutral-to-
+# slower q5 attraction cancel the gain (full3d schedule 117 -> 128 s with it enabled from
+# 2M targets), so it is off by default (SPK_FAR_LEVEL_MIN overrides).
+FAR_LEVEL_MIN = int(os.environ.get("SPK_FAR_LEVEL_MIN", str(1 << 62)))
 FAR_PARENT_CAP = 1024
 
 
