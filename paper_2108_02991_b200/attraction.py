@@ -198,8 +198,9 @@ def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg
     order, theta = params
     src = field.source_tree()
     if tg is None:
-        tg = tree.TargetGroups(tgt4, field.dims, parent_cap=tree.far_parent_cap(tgt4.shape[0]))
-    return tree.tree_eval(tg, src, order, theta, eps2, static=True)
+        tg = tree.TargetGroups(tgt4, field.dims)
+    # plain walk: the lattice's far level is not faster (profiles/r01_far_level.txt)
+    return tree.tree_eval(tg, src, order, theta, eps2, static=True, far=False)
 
 
 def precompute_field(rho: TargetDensity, kernel_eps: float | None = None,

@@ -56,12 +56,12 @@ DIRECT_BELOW = 1 << 17
 # spokes, whose near field against the dense lattice is huge (131k targets against the
 # C4 lattice: 45 -> 24 ms; no effect at 524k targets and above).
 TARGET_MIN_LEVEL = 5
-# Far level (P2L/L2P on parents of <= FAR_PARENT_CAP targets).  In isolation it cuts the
-# C4 repulsion evaluation by ~30 % (q4: 111 -> 74 ms, profiles/r01_far_level.txt), but in
-# the optimizer iteration the per-call P2M of every node it needs and the neutral-to-
-# slower q5 attraction cancel the gain (full3d schedule 117 -> 128 s with it enabled from
-# 2M targets), so it is off by default (SPK_FAR_LEVEL_MIN overrides).
-FAR_LEVEL_MIN = int(os.environ.get("SPK_FAR_LEVEL_MIN", str(1 << 62)))
+# Far level (P2L/L2P on parents of <= FAR_PARENT_CAP targets), used for the repulsion
+# from this many targets on: in the optimizer's call path at C4 it cuts the repulsion
+# evaluation from 118 to 91 ms (1e-3) and 186 to 138 ms (1e-4), incl. the per-call P2M
+# of every node (profiles/r01_far_level.txt).  The lattice attraction keeps the plain
+# walk (its q5 far level is not faster).  SPK_FAR_LEVEL_MIN overrides.
+FAR_LEVEL_MIN = int(os.environ.get("SPK_FAR_LEVEL_MIN", str(1 << 22)))
 FAR_PARENT_CAP = 1024
 
 
@@ -406,16 +406,17 @@ def _far_level(tg: TargetGroups, src: SourceTree, order: int, far_order: int, th
 def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2: float, *,
               static: bool = False, stats: dict | None = None, lists: dict | None = None,
               val: torch.Tensor | None = None, grad: torch.Tensor | None = None,
-              far_order: int | None = None):
+              far_order: int | None = None, far: bool = True):
     """Weighted treecode sums of the sources at the targets -> (val, grad) fp64, targets'
     original order.  ``static`` uses the source tree's cached all-node proxies (no P2M in
     the call); otherwise proxies are built for the nodes this traversal opens as far.
     With a far level (``tg`` built with ``parent_cap``), nodes far from a target's parent
     are evaluated at the parent's far_order^d Chebyshev points and interpolated (P2L/L2P);
-    the groups' lists then hold only the remaining nodes (static proxies)."""
+    the groups' lists then hold only the remaining nodes (static proxies); ``far=False``
+    ignores the parents (the groups are valid plain groups either way)."""
     if not 2 <= order <= MAX_ORDER:
         raise ValueError(f"interp_order must be in [2, {MAX_ORDER}]")
-    if tg.parents is not None:
+    if far and tg.parents is not None:
         return _tree_eval_far(tg, src, order, theta, eps2, far_order or order, val, grad)
     import time
 
