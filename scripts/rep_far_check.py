@@ -11,7 +11,8 @@ import paper_2108_02991_b200 as spk  # noqa: E402
 from paper_2108_02991_b200 import _device  # noqa: E402
 from paper_2108_02991_b200.repulsion import tree_sums_checked  # noqa: E402
 
-pts = spk.perturb(spk.init_radial(4096, 2048, 3), 0.75, 0).points()
+n_s = int(os.environ.get("NS", "2048"))
+pts = spk.perturb(spk.init_radial(4096, n_s, 3), 0.75, 0).points()
 pos4 = _device.pack_positions(_device.h2d(np.ascontiguousarray(pts)))
 cfg = spk.RepulsionConfig(backend="tree", tree_precision=float(sys.argv[1]) if len(sys.argv) > 1 else 1e-3)
 best = 1e30
@@ -21,4 +22,4 @@ for _ in range(4):
     tree_sums_checked(pos4, pos4, 3, cfg)
     torch.cuda.synchronize()
     best = min(best, time.perf_counter() - t0)
-print(f"far_min={os.environ.get('SPK_FAR_LEVEL_MIN', 'default')} precision={cfg.tree_precision}: {best*1e3:.1f} ms", flush=True)
+print(f"p={pts.shape[0]} far_min={os.environ.get('SPK_FAR_LEVEL_MIN', 'default')} precision={cfg.tree_precision}: {best*1e3:.1f} ms", flush=True)

@@ -162,3 +162,28 @@ def test_very_long_shot_global_fallbacks(spk):
                                    np.zeros(3), 30, tau, 0.1 * cfg.feas_tol, max_sweeps=cap)
         assert np.array_equal(sw, rsw)
         assert np.array_equal(out, ref), np.abs(out - ref).max()
+
+
+@pytest.mark.parametrize("d,ns,pin,mono,cap", [
+    (3, 1500, 700, False, 3000),   # 12-warp ring (<1024,1> instantiation)
+    (2, 2100, -1, False, 2000),    # 17 warps, unpinned 2D
+    (3, 5000, 2500, False, 300),   # single shared wrap buffer + global snapshots
+    (2, 700, 350, True, 5000),     # monotone FISTA + 6-warp ring
+    (3, 3, 1, False, 50),          # smallest pinned shot
+])
+def test_ring_configurations_vs_oracle(spk, d, ns, pin, mono, cap):
+    """Bit-identity across the ring's instantiations and wrap-buffer modes (sweep caps
+    bound the oracle's run time; the cap path and the stop/replay path are both hit)."""
+    rng = np.random.default_rng(ns + d)
+    shots = np.cumsum(rng.normal(0, 6e-3, (2, ns, d)), axis=1)
+    shots = np.clip(shots - shots.mean(axis=1, keepdims=True), -1.05, 1.05)
+    pv = np.zeros(d)
+    pc = None if pin < 0 else spk.LinearConstraint(pin, pv)
+    cfg = spk.ProjectionConfig(alpha=4e-3, beta=8e-4, raster_dt=1.0, n_pit=40, pin=pc,
+                               monotone=mono)
+    tau = 1.0 / spk.projection.stacked_operator_norm(ns, pin)
+    out, _, sw = run(spk, shots, cfg, tau, max_sweeps=cap)
+    ref, rsw = orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, pin, pv, 40, tau,
+                               0.1 * cfg.feas_tol, monotone=mono, max_sweeps=cap)
+    assert np.array_equal(sw, rsw), (sw, rsw)
+    assert np.array_equal(out, ref), np.abs(out - ref).max()
