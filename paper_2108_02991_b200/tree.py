@@ -27,6 +27,7 @@ precision with margin on radial-spoke, perturbed and uniform clouds.
 from __future__ import annotations
 
 import os
+import time
 
 import numpy as np
 import torch
@@ -418,8 +419,6 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
         raise ValueError(f"interp_order must be in [2, {MAX_ORDER}]")
     if far and tg.parents is not None:
         return _tree_eval_far(tg, src, order, theta, eps2, far_order or order, val, grad)
-    import time
-
     dev = src.rec.device
     st = _device.stream()
     dims, n_s, m = src.dims, src.n, order ** src.dims
@@ -545,8 +544,6 @@ def tree_sums_device(tgt4: torch.Tensor, src4: torch.Tensor, dims: int, eps2: fl
     True`` also per-phase wall times (synchronising between phases).  ``lists``
     (optional dict) receives the device interaction lists and, under "host_tree", the
     host octree (handle, tables) for the tests' cross-check (caller frees the handle)."""
-    import time
-
     if not 2 <= order <= MAX_ORDER:
         raise ValueError(f"interp_order must be in [2, {MAX_ORDER}]")
     timing = stats is not None and stats.get("timing", False)
