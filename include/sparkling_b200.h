@@ -331,16 +331,19 @@ void spk_tree_host_export_plan(const void* tree, int64_t* seg_off, int64_t* seg_
  * Replaces analysis.py:25-69 (per-axis phase tables + matrix products).  Points k are
  * fp64 [p][dims] in [-1, 1]; grid is a HOST array of dims sizes; voxel offsets are
  * r_a = 0..n_a-1 minus n_a/2.  Complex arrays are interleaved fp64 (re, im), grid arrays
- * row-major (C order).  fp32 products with fp64 phase generation and accumulation.
+ * row-major (C order).  mode SPK_NUDFT_FP64: fp64 tables and products (the reference's
+ * numerics; density compensation needs them, see nudft.cu); SPK_NUDFT_MIXED: fp32
+ * products with fp64 phase generation and accumulation (opt-in, ~2x faster).
  */
+enum { SPK_NUDFT_FP64 = 0, SPK_NUDFT_MIXED = 1 };
 size_t spk_nudft_workspace_bytes(int64_t p, int dims, const int64_t* grid);
 /* out[r] = sum_i w_i exp(+i pi k_i . r)  (nudft_adjoint, analysis.py:41-55) */
 int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int dims,
-                      const int64_t* grid, double* out, void* ws, size_t ws_bytes,
+                      const int64_t* grid, int mode, double* out, void* ws, size_t ws_bytes,
                       spk_stream_t stream);
 /* out[i] = sum_r image[r] exp(-i pi k_i . r)  (nudft_forward, analysis.py:58-69) */
 int spk_nudft_forward(const double* pts, const double* image, int64_t p, int dims,
-                      const int64_t* grid, double* out, void* ws, size_t ws_bytes,
+                      const int64_t* grid, int mode, double* out, void* ws, size_t ws_bytes,
                       spk_stream_t stream);
 /* w_i <- w_i / max(|back_i|, 1e-12)  (density_compensation, analysis.py:90-96) */
 int spk_dcf_update(double* weights, const double* back, int64_t p, spk_stream_t stream);

@@ -81,10 +81,10 @@ SIGNATURES = {
     "spk_tree_l2p": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_vp,
                              c_vp, c_vp]),
     "spk_nudft_workspace_bytes": (c_size, [c_i64, c_int, ctypes.POINTER(c_i64)]),
-    "spk_nudft_adjoint": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.POINTER(c_i64), c_vp, c_vp,
-                                  c_size, c_vp]),
-    "spk_nudft_forward": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.POINTER(c_i64), c_vp, c_vp,
-                                  c_size, c_vp]),
+    "spk_nudft_adjoint": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.POINTER(c_i64), c_int, c_vp,
+                                  c_vp, c_size, c_vp]),
+    "spk_nudft_forward": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.POINTER(c_i64), c_int, c_vp,
+                                  c_vp, c_size, c_vp]),
     "spk_dcf_update": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "spk_psf_magnitude": (c_int, [c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "spk_tree_host_levels": (c_i64, [c_vp, c_vp]),

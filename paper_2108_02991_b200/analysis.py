@@ -2,9 +2,11 @@
 
 Mirrors /root/reference/pkg/src/vdtraj/analysis.py (same names, arguments, budget guard
 and exceptions).  The nonuniform DFTs -- the only O(p x voxels) work -- run in our
-kernels (csrc/nudft.cu: generated-operand complex products, fp32 math with fp64 phases
-and accumulation; rel. error ~1e-6 of the reference's complex128 result); the metrics
-are O(voxels) host code on the returned magnitudes.
+kernels (csrc/nudft.cu: generated-operand complex products).  ``precision="fp64"`` (the
+default) computes in fp64 like the reference's complex128 numpy; ``"mixed"`` uses fp32
+products with fp64 phases and accumulation (~1e-6 relative, about twice as fast) -- not
+suitable for density_compensation, whose fixed-point iteration amplifies that noise by
+~1e6.  The metrics are O(voxels) host code on the returned magnitudes.
 """
 
 from __future__ import annotations
@@ -19,6 +21,7 @@ from .core import HardwareSpec, SamplingPattern, resample_to_dwell
 from .density import TargetDensity
 
 DB_CAP = 300.0
+PRECISIONS = {"fp64": 0, "mixed": 1}  # SPK_NUDFT_FP64 / SPK_NUDFT_MIXED
 # p * grid-voxel budget of the direct DFT before allow_slow is required (analysis.py:18-19)
 DFT_BUDGET = 1 << 31
 
@@ -53,26 +56,36 @@ def _to_complex(t: torch.Tensor, shape) -> np.ndarray:
     return np.ascontiguousarray(_device.d2h(t)).view(np.complex128).reshape(shape)
 
 
-def nudft_adjoint_device(pts: torch.Tensor, w: torch.Tensor, grid_shape) -> torch.Tensor:
+def _mode(precision: str) -> int:
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {tuple(PRECISIONS)}, got {precision!r}")
+    return PRECISIONS[precision]
+
+
+def nudft_adjoint_device(pts: torch.Tensor, w: torch.Tensor, grid_shape,
+                         precision: str = "fp64") -> torch.Tensor:
     """Device adjoint NUDFT: pts [p, d] f64, w [p, 2] f64 (complex) -> [prod(grid), 2]."""
+    mode = _mode(precision)
     p, dims = pts.shape
     shape = _grid(grid_shape, dims)
     g = _native.i64_array(shape)
     out = torch.empty((int(np.prod(shape)), 2), dtype=torch.float64, device=pts.device)
     ws = _device.workspace(_native.query("spk_nudft_workspace_bytes", p, dims, g), "nudft")
-    _native.call("spk_nudft_adjoint", pts.data_ptr(), w.data_ptr(), p, dims, g,
+    _native.call("spk_nudft_adjoint", pts.data_ptr(), w.data_ptr(), p, dims, g, mode,
                  out.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
     return out
 
 
-def nudft_forward_device(pts: torch.Tensor, img: torch.Tensor, grid_shape) -> torch.Tensor:
+def nudft_forward_device(pts: torch.Tensor, img: torch.Tensor, grid_shape,
+                         precision: str = "fp64") -> torch.Tensor:
     """Device forward NUDFT: img [prod(grid), 2] f64 (complex) -> [p, 2]."""
+    mode = _mode(precision)
     p, dims = pts.shape
     shape = _grid(grid_shape, dims)
     g = _native.i64_array(shape)
     out = torch.empty((p, 2), dtype=torch.float64, device=pts.device)
     ws = _device.workspace(_native.query("spk_nudft_workspace_bytes", p, dims, g), "nudft")
-    _native.call("spk_nudft_forward", pts.data_ptr(), img.data_ptr(), p, dims, g,
+    _native.call("spk_nudft_forward", pts.data_ptr(), img.data_ptr(), p, dims, g, mode,
                  out.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
     return out
 
@@ -85,18 +98,19 @@ def _points(points) -> np.ndarray:
 
 
 def nudft_adjoint(points: np.ndarray, weights: np.ndarray, grid_shape,
-                  allow_slow: bool = False) -> np.ndarray:
+                  allow_slow: bool = False, precision: str = "fp64") -> np.ndarray:
     """Grid weighted samples onto the image grid (analysis.py:41-55):
     out[r] = sum_i w_i exp(i pi k_i . r), r_a = 0..n_a-1 minus n_a // 2."""
     pts = _points(points)
     p, dims = pts.shape
     _check_budget(p, grid_shape, allow_slow)
     shape = _grid(grid_shape, dims)
-    out = nudft_adjoint_device(_device.h2d(pts), _complex_dev(weights, p), shape)
+    out = nudft_adjoint_device(_device.h2d(pts), _complex_dev(weights, p), shape, precision)
     return _to_complex(out, shape)
 
 
-def nudft_forward(points: np.ndarray, image: np.ndarray, allow_slow: bool = False) -> np.ndarray:
+def nudft_forward(points: np.ndarray, image: np.ndarray, allow_slow: bool = False,
+                  precision: str = "fp64") -> np.ndarray:
     """Sample an image-grid function at the trajectory points (analysis.py:58-69):
     f_i = sum_r image[r] exp(-i pi k_i . r)."""
     pts = _points(points)
@@ -105,16 +119,17 @@ def nudft_forward(points: np.ndarray, image: np.ndarray, allow_slow: bool = Fals
     _check_budget(p, image.shape, allow_slow)
     shape = _grid(image.shape, dims)
     out = nudft_forward_device(_device.h2d(pts), _complex_dev(image, int(np.prod(shape))),
-                               shape)
+                               shape, precision)
     return _to_complex(out, (p,))
 
 
 def density_compensation(k: SamplingPattern, grid_shape, iters: int = 10,
-                         allow_slow: bool = False) -> np.ndarray:
+                         allow_slow: bool = False, precision: str = "fp64") -> np.ndarray:
     """Iterative density-compensation weights (analysis.py:72-96): start from ones, then
     w <- w / max(|forward(adjoint(w))|, 1e-12), ``iters`` times; device-resident."""
     if iters < 1:
         raise ValueError("iters must be >= 1")
+    _mode(precision)
     pts = k.points()
     if pts.shape[0] == 0:
         raise ValueError("empty sampling pattern")
@@ -125,8 +140,8 @@ def density_compensation(k: SamplingPattern, grid_shape, iters: int = 10,
     w = torch.zeros((p, 2), dtype=torch.float64, device=d_pts.device)
     w[:, 0] = 1.0
     for _ in range(iters):
-        gridded = nudft_adjoint_device(d_pts, w, shape)
-        back = nudft_forward_device(d_pts, gridded, shape)
+        gridded = nudft_adjoint_device(d_pts, w, shape, precision)
+        back = nudft_forward_device(d_pts, gridded, shape, precision)
         _native.call("spk_dcf_update", w.data_ptr(), back.data_ptr(), p, _device.stream())
     return np.ascontiguousarray(_device.d2h(w[:, 0]))
 
@@ -145,7 +160,8 @@ class PsfVolume:
 
 
 def compute_psf(k: SamplingPattern, grid_shape, weights: np.ndarray | None = None,
-                hw: HardwareSpec | None = None, allow_slow: bool = False) -> PsfVolume:
+                hw: HardwareSpec | None = None, allow_slow: bool = False,
+                precision: str = "fp64") -> PsfVolume:
     """Density-compensated adjoint response to unit measurements (analysis.py:112-137);
     with ``hw`` the pattern is first resampled to the ADC dwell grid."""
     if hw is not None:
@@ -160,7 +176,7 @@ def compute_psf(k: SamplingPattern, grid_shape, weights: np.ndarray | None = Non
     _check_budget(p, grid_shape, allow_slow)
     shape = _grid(grid_shape, dims)
     vol = nudft_adjoint_device(_device.h2d(np.ascontiguousarray(pts)),
-                               _complex_dev(weights, p), shape)
+                               _complex_dev(weights, p), shape, precision)
     total = np.sum(weights)
     mag = torch.empty(vol.shape[0], dtype=torch.float64, device=vol.device)
     if np.iscomplexobj(total):

@@ -20,6 +20,7 @@
 //            re-seeded from fp64 at every 8-row stage and row wrap.
 // Deterministic: fixed sample slices per CTA and a fixed-order reduction of the slices.
 #include <algorithm>
+#include <cmath>
 #include <cfloat>
 
 #include "spk_common.cuh"
@@ -302,6 +303,182 @@ __global__ void __launch_bounds__(NU_THREADS) nudft_forward_kernel(const FwdPara
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// fp64 kernels (the default, SPK_NUDFT_FP64).  Same decomposition as above with fp64
+// tables and DFMA products.  density_compensation's fixed-point iteration amplifies
+// relative noise in forward(adjoint(w)) by ~1e6 (a 1e-7 perturbation moves the weights by
+// ~20% on a 3D radial pattern), so the reference's results are reproduced only with fp64
+// products; the mixed kernels above are the opt-in fast mode.
+constexpr int ND_CH = 64;            // samples per chunk
+constexpr int ND_AS = NU_UT + 1;     // double2 row strides
+constexpr int ND_BS = NU_VT + 1;  // odd row stride: the row-per-thread B generation
+                                 // would otherwise put a quarter-warp on the same banks
+
+__global__ void __launch_bounds__(NU_THREADS, 2) nudft_adjoint64_kernel(const AdjParams P) {
+    extern __shared__ __align__(16) char sm[];
+    double2* At = reinterpret_cast<double2*>(sm);        // [ND_CH][ND_AS]
+    double2* Bt = At + ND_CH * ND_AS;                    // [ND_CH][ND_BS]
+    const int tid = threadIdx.x;
+    const long long u0 = (long long)blockIdx.x * NU_UT;
+    const long long v0 = (long long)blockIdx.y * NU_VT;
+    const int slice = blockIdx.z;
+    const long long i_begin = P.p * slice / P.slices;
+    const long long i_end = P.p * (slice + 1) / P.slices;
+    const int u_loc = tid % NU_UT;
+    const int vg = tid / NU_UT;
+    double re[NU_VPT], im[NU_VPT];
+#pragma unroll
+    for (int k = 0; k < NU_VPT; ++k) re[k] = im[k] = 0.0;
+    const int h0 = P.n0 / 2, h1 = P.n1 / 2, h2 = P.n2 / 2;
+
+    for (long long c0 = i_begin; c0 < i_end; c0 += ND_CH) {
+        const int cnt = (int)min((long long)ND_CH, i_end - c0);
+        for (int r = tid; r < 2 * ND_CH; r += NU_THREADS) {
+            const bool rowA = r < ND_CH;
+            const int j = rowA ? r : r - ND_CH;
+            if (j >= cnt) continue;  // rows past cnt are never read
+            const long long i = c0 + j;
+            const double k0 = P.pts[i * P.dims];
+            const double k1 = P.pts[i * P.dims + 1];
+            const double2 wi = make_double2(P.w[2 * i], P.w[2 * i + 1]);
+            double2* row = rowA ? At + j * ND_AS : Bt + j * ND_BS;
+            if (P.dims == 3) {
+                if (rowA) {
+                    int a = (int)(u0 / P.n1), b = (int)(u0 - (long long)a * P.n1);
+                    double2 e0 = cispi(k0 * (double)(a - h0));
+                    double2 e1 = cispi(k1 * (double)(b - h1));
+                    const double2 z1 = cispi(k1);
+                    for (int q = 0; q < NU_UT; ++q) {
+                        row[q] = cmul(e0, e1);
+                        if (++b == P.n1) {
+                            b = 0;
+                            ++a;
+                            e0 = cispi(k0 * (double)(a - h0));
+                            e1 = cispi(k1 * (double)(b - h1));
+                        } else {
+                            e1 = cmul(e1, z1);
+                        }
+                    }
+                } else {
+                    const double k2 = P.pts[i * P.dims + 2];
+                    double2 e2 = cmul(wi, cispi(k2 * (double)(v0 - h2)));
+                    const double2 z2 = cispi(k2);
+                    for (int q = 0; q < NU_VT; ++q) {
+                        row[q] = e2;
+                        e2 = cmul(e2, z2);
+                    }
+                }
+            } else if (rowA) {
+                double2 e0 = cmul(wi, cispi(k0 * (double)(u0 - h0)));
+                const double2 z0 = cispi(k0);
+                for (int q = 0; q < NU_UT; ++q) {
+                    row[q] = e0;
+                    e0 = cmul(e0, z0);
+                }
+            } else {
+                double2 e1 = cispi(k1 * (double)(v0 - h1));
+                const double2 z1 = cispi(k1);
+                for (int q = 0; q < NU_VT; ++q) {
+                    row[q] = e1;
+                    e1 = cmul(e1, z1);
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int j = 0; j < cnt; ++j) {
+            const double2 a = At[j * ND_AS + u_loc];
+            const double2* brow = Bt + j * ND_BS + vg * NU_VPT;
+#pragma unroll
+            for (int k = 0; k < NU_VPT; ++k) {
+                const double2 b = brow[k];
+                re[k] = fma(a.x, b.x, re[k]);
+                re[k] = fma(-a.y, b.y, re[k]);
+                im[k] = fma(a.x, b.y, im[k]);
+                im[k] = fma(a.y, b.x, im[k]);
+            }
+        }
+        __syncthreads();
+    }
+    const long long u = u0 + u_loc;
+    if (u >= P.U) return;
+    double* out = P.part + ((size_t)slice * P.U + u) * P.V * 2;
+#pragma unroll
+    for (int k = 0; k < NU_VPT; ++k) {
+        const long long v = v0 + vg * NU_VPT + k;
+        if (v < P.V) {
+            out[2 * v] = re[k];
+            out[2 * v + 1] = im[k];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NU_THREADS) nudft_forward64_kernel(const FwdParams P) {
+    extern __shared__ __align__(16) char sm[];
+    double2* rows = reinterpret_cast<double2*>(sm);  // [NF_UT][V]
+    const int tid = threadIdx.x;
+    const long long i = (long long)blockIdx.x * NU_THREADS + tid;
+    const int slice = blockIdx.y;
+    const long long ub = P.U * slice / P.slices, ue = P.U * (slice + 1) / P.slices;
+    const bool live = i < P.p;
+    const long long ii = live ? i : P.p - 1;
+    const double k0 = P.pts[ii * P.dims];
+    const double k1 = P.pts[ii * P.dims + 1];
+    const double kv = P.dims == 3 ? P.pts[ii * P.dims + 2] : k1;
+    const int hv = (P.dims == 3 ? P.n2 : P.n1) / 2;
+    const double2 z = cispi(-kv);
+    const double2 shift = cispi(kv * (double)hv);
+    const double2 w = cispi(-(P.dims == 3 ? k1 : k0));
+    double fr = 0.0, fi = 0.0;
+    for (long long s0 = ub; s0 < ue; s0 += NF_UT) {
+        const int nu = (int)min((long long)NF_UT, ue - s0);
+        __syncthreads();
+        const double2* src = reinterpret_cast<const double2*>(P.img) + (size_t)s0 * P.V;
+        for (long long e = tid; e < (long long)nu * P.V; e += NU_THREADS) rows[e] = src[e];
+        __syncthreads();
+        double2 A = make_double2(0.0, 0.0);
+        int a = 0, b = 0;
+        for (int q = 0; q < nu; ++q) {
+            const long long u = s0 + q;
+            bool seed = q == 0;
+            if (P.dims == 3) {
+                if (q == 0) {
+                    a = (int)(u / P.n1);
+                    b = (int)(u - (long long)a * P.n1);
+                } else if (++b == P.n1) {
+                    b = 0;
+                    ++a;
+                    seed = true;
+                }
+            }
+            if (seed) {
+                const double t = P.dims == 3
+                                     ? k0 * (double)(a - P.n0 / 2) + k1 * (double)(b - P.n1 / 2)
+                                     : k0 * (double)(u - P.n0 / 2);
+                A = cispi(-t);
+            } else {
+                A = cmul(A, w);
+            }
+            const double2* row = rows + (size_t)q * P.V;
+            double pr = 0.0, pi = 0.0;
+            for (long long v = P.V - 1; v >= 0; --v) {
+                const double2 g = row[v];
+                const double nr = fma(pr, z.x, fma(-pi, z.y, g.x));
+                pi = fma(pr, z.y, fma(pi, z.x, g.y));
+                pr = nr;
+            }
+            fr = fma(A.x, pr, fma(-A.y, pi, fr));
+            fi = fma(A.x, pi, fma(A.y, pr, fi));
+        }
+    }
+    if (live) {
+        const double2 f = cmul(make_double2(fr, fi), shift);
+        double* out = P.part + ((size_t)slice * P.p + i) * 2;
+        out[0] = f.x;
+        out[1] = f.y;
+    }
+}
+
 // density_compensation update (analysis.py:90-96): w_i <- w_i / max(|back_i|, 1e-12)
 __global__ void dcf_update_kernel(double* __restrict__ w, const double* __restrict__ back,
                                   long long p) {
@@ -335,18 +512,31 @@ size_t spk_nudft_workspace_bytes(int64_t p, int dims, const int64_t* grid) {
     return adj > fwd ? adj : fwd;
 }
 
-static int adj_slices(long long U, long long V, long long p) {
+// Sample slices (split-K) of the adjoint: at least ~2 waves of resident CTAs, and among
+// the candidates the one whose last wave is fullest (tiles x slices vs the resident slots).
+static int adj_slices(long long U, long long V, long long p, int chunk, int slots) {
     const long long tiles = ((U + NU_UT - 1) / NU_UT) * ((V + NU_VT - 1) / NU_VT);
-    const long long want = 2LL * num_sms() * 2;  // ~2 waves of 2 CTAs per SM
-    long long s = (want + tiles - 1) / tiles;
-    s = std::max(1LL, std::min(s, std::min(16LL, (p + NU_CH - 1) / NU_CH)));
-    return (int)s;
+    const long long smax = std::max(1LL, std::min(16LL, (p + chunk - 1) / chunk));
+    const long long smin = std::min(smax, std::max(1LL, (2LL * slots + tiles - 1) / tiles));
+    long long best = smin;
+    double best_eff = -1.0;
+    for (long long s = smin; s <= smax; ++s) {
+        const double waves = (double)(tiles * s) / slots;
+        const double eff = waves / std::ceil(waves) - 0.002 * (double)s;
+        if (eff > best_eff + 1e-12) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return (int)best;
 }
 
 int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int dims,
-                      const int64_t* grid, double* out, void* ws, size_t ws_bytes,
+                      const int64_t* grid, int mode, double* out, void* ws, size_t ws_bytes,
                       spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(mode == SPK_NUDFT_FP64 || mode == SPK_NUDFT_MIXED, SPK_ERR_ARG,
+                "nudft: unknown mode %d", mode);
     SPK_REQUIRE(p >= 1, SPK_ERR_ARG, "nudft: empty sample set");
     AdjParams P{};
     P.pts = pts;
@@ -358,17 +548,25 @@ int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int d
     P.n2 = dims == 3 ? (int)grid[2] : 1;
     P.U = dims == 3 ? (long long)P.n0 * P.n1 : P.n0;
     P.V = dims == 3 ? P.n2 : P.n1;
-    P.slices = adj_slices(P.U, P.V, p);
+    const bool f64 = mode == SPK_NUDFT_FP64;
+    const void* kern = f64 ? (const void*)nudft_adjoint64_kernel : (const void*)nudft_adjoint_kernel;
+    const size_t smem =
+        f64 ? (size_t)ND_CH * (ND_AS + ND_BS) * sizeof(double2)
+            : ((size_t)((NU_CH * NU_AS + 1) & ~1) + (size_t)NU_CH * NU_BS) * sizeof(C2);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NU_THREADS, smem);
+    P.slices = adj_slices(P.U, P.V, p, f64 ? ND_CH : NU_CH, std::max(1, per_sm) * num_sms());
     SPK_REQUIRE(ws_bytes >= (size_t)P.slices * P.U * P.V * 16, SPK_ERR_WORKSPACE,
                 "nudft adjoint: workspace too small");
     P.part = static_cast<double*>(ws);
-    const size_t smem = ((size_t)((NU_CH * NU_AS + 1) & ~1) + (size_t)NU_CH * NU_BS) * sizeof(C2);
-    cudaFuncSetAttribute(nudft_adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
     dim3 grid3((unsigned)((P.U + NU_UT - 1) / NU_UT), (unsigned)((P.V + NU_VT - 1) / NU_VT),
                (unsigned)P.slices);
     cudaStream_t s = (cudaStream_t)stream;
-    nudft_adjoint_kernel<<<grid3, NU_THREADS, smem, s>>>(P);
+    if (f64)
+        nudft_adjoint64_kernel<<<grid3, NU_THREADS, smem, s>>>(P);
+    else
+        nudft_adjoint_kernel<<<grid3, NU_THREADS, smem, s>>>(P);
     SPK_CHECK_LAUNCH("spk_nudft_adjoint");
     const long long n = P.U * P.V * 2;
     nudft_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P.part, P.slices, n, out);
@@ -377,9 +575,11 @@ int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int d
 }
 
 int spk_nudft_forward(const double* pts, const double* image, int64_t p, int dims,
-                      const int64_t* grid, double* out, void* ws, size_t ws_bytes,
+                      const int64_t* grid, int mode, double* out, void* ws, size_t ws_bytes,
                       spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(mode == SPK_NUDFT_FP64 || mode == SPK_NUDFT_MIXED, SPK_ERR_ARG,
+                "nudft: unknown mode %d", mode);
     SPK_REQUIRE(p >= 1, SPK_ERR_ARG, "nudft: empty sample set");
     FwdParams P{};
     P.pts = pts;
@@ -401,12 +601,19 @@ int spk_nudft_forward(const double* pts, const double* image, int64_t p, int dim
     SPK_REQUIRE(ws_bytes >= (size_t)P.slices * p * 16, SPK_ERR_WORKSPACE,
                 "nudft forward: workspace too small");
     P.part = static_cast<double*>(ws);
-    const size_t smem = (size_t)NF_UT * P.V * sizeof(float2);
-    cudaFuncSetAttribute(nudft_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max(smem, (size_t)1));
     dim3 grid2((unsigned)blocks, (unsigned)P.slices);
     cudaStream_t s = (cudaStream_t)stream;
-    nudft_forward_kernel<<<grid2, NU_THREADS, smem, s>>>(P);
+    if (mode == SPK_NUDFT_FP64) {
+        const size_t smem = (size_t)NF_UT * P.V * sizeof(double2);
+        cudaFuncSetAttribute(nudft_forward64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)std::max(smem, (size_t)1));
+        nudft_forward64_kernel<<<grid2, NU_THREADS, smem, s>>>(P);
+    } else {
+        const size_t smem = (size_t)NF_UT * P.V * sizeof(float2);
+        cudaFuncSetAttribute(nudft_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)std::max(smem, (size_t)1));
+        nudft_forward_kernel<<<grid2, NU_THREADS, smem, s>>>(P);
+    }
     SPK_CHECK_LAUNCH("spk_nudft_forward");
     const long long n = p * 2;
     nudft_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P.part, P.slices, n, out);

@@ -39,14 +39,14 @@ for name, (n_c, n_s, d), grid in CASES:
     vox = int(np.prod(grid))
     w = torch.zeros((p, 2), dtype=torch.float64, device=pts.device)
     w[:, 0] = 1.0
-    img = an.nudft_adjoint_device(pts, w, grid)
-    t_adj = dev_time(lambda: an.nudft_adjoint_device(pts, w, grid))
-    t_fwd = dev_time(lambda: an.nudft_forward_device(pts, img, grid))
+    rec = dict(case=name, p=p, voxels=vox, products=p * vox)
+    for prec in ("fp64", "mixed"):
+        img = an.nudft_adjoint_device(pts, w, grid, prec)
+        t_adj = dev_time(lambda: an.nudft_adjoint_device(pts, w, grid, prec))
+        t_fwd = dev_time(lambda: an.nudft_forward_device(pts, img, grid, prec))
+        rec[prec] = dict(adjoint_s=t_adj, adjoint_products_per_s=p * vox / t_adj,
+                         forward_s=t_fwd, forward_products_per_s=p * vox / t_fwd)
     t0 = time.perf_counter()
     psf = spk.compute_psf(k, grid, allow_slow=True)
-    t_psf = time.perf_counter() - t0
-    rec = dict(case=name, p=p, voxels=vox, products=p * vox,
-               adjoint_s=t_adj, adjoint_products_per_s=p * vox / t_adj,
-               forward_s=t_fwd, forward_products_per_s=p * vox / t_fwd,
-               compute_psf_wall_s=t_psf, psf_peak=psf.peak_value)
+    rec.update(compute_psf_wall_s=time.perf_counter() - t0, psf_peak=psf.peak_value)
     print(json.dumps(rec), flush=True)

@@ -324,6 +324,14 @@ def analysis_fixtures():
         m = an.psf_metrics(psf)
         out[f"{name}_metrics"] = np.array(list(m.fwhm) + [m.psl_db, m.pnl_db,
                                                           float(m.fwhm_bounded)])
+    # the acceptance-test PSF leg (test_acceptance.py:310-317): radial 64 x 128 3D init,
+    # 10 density-compensation iterations on 32^3 -- an ill-conditioned fixed point that
+    # pins the NUDFT's fp64 accuracy end to end
+    kr = om.init_radial(64, 128, 3)
+    out["dcfr3"] = an.density_compensation(kr, (32, 32, 32), iters=10)
+    mr = an.psf_metrics(an.compute_psf(kr, (32, 32, 32), out["dcfr3"]))
+    out["dcfr3_metrics"] = np.array(list(mr.fwhm) + [mr.psl_db, mr.pnl_db,
+                                                     float(mr.fwhm_bounded)])
     # a smooth synthetic PSF (Gaussian) for the FWHM interpolation
     ax = np.arange(33) - 16
     g = np.exp(-0.5 * (ax[:, None] ** 2 + ax[None, :] ** 2) / 2.0 ** 2)
