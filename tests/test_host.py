@@ -137,3 +137,33 @@ def test_spkt_spkd_bytes_identical_to_reference(host, tmp_path):
     assert (tmp_path / "t.spkt").read_bytes() == host["spkt_bytes"].tobytes()
     spk_io.write_spkd(tmp_path / "d.spkd", host["dens_2d_16"])
     assert (tmp_path / "d.spkd").read_bytes() == host["spkd_bytes"].tobytes()
+
+
+def test_trajectory_csv_roundtrip_and_dispatch(tmp_path):
+    """io.py:96-126,162-169: CSV header, 9-digit round trip, SPKT/CSV dispatch, errors."""
+    rng = np.random.default_rng(5)
+    for dims in (2, 3):
+        coords = rng.uniform(-1, 1, (3, 16, dims))
+        pat = spk.SamplingPattern(coords)
+        csv = tmp_path / f"t{dims}.csv"
+        spk_io.write_trajectory_csv(csv, pat)
+        assert csv.read_text().splitlines()[0] == "shot,sample," + ",".join("kx ky kz".split()[:dims])
+        assert np.allclose(spk_io.read_trajectory_csv(csv).coords, coords, rtol=1e-8, atol=1e-9)
+        spkt = tmp_path / f"t{dims}.spkt"
+        spk_io.write_spkt(spkt, pat, (100.0,) * dims, 1e-5)
+        assert np.allclose(spk_io.load_trajectory(spkt).coords, coords, atol=1e-7)
+        assert np.allclose(spk_io.load_trajectory(csv).coords, coords, atol=1e-8)
+    # rows in any order
+    lines = (tmp_path / "t2.csv").read_text().splitlines()
+    (tmp_path / "r.csv").write_text("\n".join([lines[0]] + lines[1:][::-1]) + "\n")
+    assert np.array_equal(spk_io.read_trajectory_csv(tmp_path / "r.csv").coords,
+                          spk_io.read_trajectory_csv(tmp_path / "t2.csv").coords)
+    (tmp_path / "e.csv").write_text("shot,sample,kx,ky\n")
+    with pytest.raises(spk_io.FileFormatError, match="empty"):
+        spk_io.read_trajectory_csv(tmp_path / "e.csv")
+    (tmp_path / "m.csv").write_text("\n".join(lines[:-1]) + "\n")
+    with pytest.raises(spk_io.FileFormatError, match="rows"):
+        spk_io.read_trajectory_csv(tmp_path / "m.csv")
+    (tmp_path / "c.csv").write_text("shot,sample,kx\n0,0,0.5\n")
+    with pytest.raises(spk_io.FileFormatError, match="columns"):
+        spk_io.read_trajectory_csv(tmp_path / "c.csv")
