@@ -278,7 +278,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or os.environ.get("SPK_BENCH_DIST") == "1"
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2108_02991_b200 as spk
     from paper_2108_02991_b200 import _native, engine
@@ -328,7 +329,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     ops.record = True
     _native.reset_launch_count()
@@ -344,11 +345,11 @@ def run_ours(args):
             times.append((s, e))
         torch.cuda.synchronize()
     launches = _native.launch_count()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     total_ms = sum(s.elapsed_time(e) for s, e in times)
     nb_ms = [s.elapsed_time(e) for s, e in ops.ev]
-    if world > 1:
+    if use_dist:
         t = torch.tensor([total_ms, float(np.mean(nb_ms))], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, nb_mean = float(t[0]), float(t[1])
@@ -383,7 +384,7 @@ def run_ours(args):
     # end-to-end through the public drop-in API with host buffers
     if args.no_e2e:
         e2e = None
-    elif world == 1:
+    elif not use_dist:
         e2e = run_e2e(args, spk, fld, pcfg) if rank == 0 else None
     else:
         e2e = run_e2e_sharded(args, run, step, world)
@@ -429,7 +430,7 @@ def run_ours(args):
                           f"{cb['t_sample']:.1f} s; projection 16 shots scaled to {N_C}",
                 "s_per_iteration_extrapolated": cb["s_per_iteration"]}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
@@ -443,7 +444,8 @@ def run_tree(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or os.environ.get("SPK_BENCH_DIST") == "1"
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2108_02991_b200 as spk
     from paper_2108_02991_b200 import _native, engine
@@ -484,7 +486,7 @@ def run_tree(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     _native.reset_launch_count()
     times = []
@@ -500,7 +502,7 @@ def run_tree(args):
         torch.cuda.synchronize()
     launches = _native.launch_count()
     total_ms = sum(s.elapsed_time(e) for s, e in times)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t[0])
@@ -524,7 +526,7 @@ def run_tree(args):
             "clocks": clk.summary(), "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
