@@ -641,11 +641,20 @@ __device__ unsigned long long spk_polish_prof[3][7];
 #define SPK_PROF_MARK(L, i)
 #endif
 
-// Ring lanes lag by 4 steps (+1 per warp boundary), the minimum for which the windows of
-// consecutive sweeps never overlap out of order.  (A variant running S(t) and A(t-3)
-// concurrently at lag 5 was measured slower: the per-step latency is dominated by
-// control flow, not by the S -> A fp64 chain.)
-__device__ __forceinline__ int ring_offset(int g) { return PL_LAG * g + (g >> 5); }
+// Ring lanes lag by 4 steps, the minimum for which the windows of consecutive sweeps
+// never overlap out of order.  (A variant running S(t) and A(t-3) concurrently at lag 5
+// was measured slower: the per-step latency is dominated by control flow, not by the
+// S -> A fp64 chain.)  Across a warp boundary the lag is 4 + RING_K: the sample lane 31 of
+// warp w-1 emits at step s is consumed by lane 0 of warp w at step s + RING_K, through a
+// 2 RING_K-deep shared-memory slot ring, so the CTA only needs a barrier every RING_K
+// steps (a producer write and its consumer read always straddle one) instead of every
+// step.  The period grows from 4 B + W to 4 B + RING_K W.
+#ifndef SPK_RING_K
+#define SPK_RING_K 4
+#endif
+constexpr int RING_K = SPK_RING_K;
+static_assert(RING_K >= 1 && (RING_K & (RING_K - 1)) == 0, "RING_K must be a power of two");
+__device__ __forceinline__ int ring_offset(int g) { return PL_LAG * g + RING_K * (g >> 5); }
 
 // One global step of the ring.  R = st mod 4 fixes which window slot plays w0..w3
 // (w0 = s[t-2] = slot[R], ..., w3 = s[t+1] = slot[R+3]); the received sample s[t+2]
@@ -659,7 +668,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
                                           double pv1, double pv2, double tol,
                                           const double* __restrict__ s0, double* snap0,
                                           double* res, double* xfer, double* wrap0,
-                                          int wstride, int* stop_sh) {
+                                          int wstride, int* stop_sh) {  // stop_sh[2]
     Sample<D>& w0 = L.slot[R & 3];
     Sample<D>& w1 = L.slot[(R + 1) & 3];
     Sample<D>& w2 = L.slot[(R + 2) & 3];
@@ -696,7 +705,9 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
             }
         }
 #endif
-        if (t == ns + 1 && L.worst <= tol) atomicMin(stop_sh, L.k);
+        // stop flags alternate per barrier block: a lane already in the next block cannot
+        // change the flag the others are about to read at the end of this one
+        if (t == ns + 1 && L.worst <= tol) atomicMin(&stop_sh[(st / RING_K) & 1], L.k);
     }
     // hand the finished sample w0 (= s[t-2]) to the next sweep; it is replaced in slot R
     Sample<D> recv;
@@ -704,7 +715,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
     for (int l = 0; l < D; ++l) recv.v[l] = __shfl_up_sync(0xffffffffu, w0.v[l], 1);
 #ifndef SPK_EXP_NOXFER
     if (lane == 31) {
-        double* x = xfer + ((warp * 2 + (st & 1)) * D);
+        double* x = xfer + ((warp * 2 * RING_K + (st & (2 * RING_K - 1))) * D);
 #pragma unroll
         for (int l = 0; l < D; ++l) x[l] = w0.v[l];
     }
@@ -721,7 +732,9 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
             }
 #ifndef SPK_EXP_NOXFER
             else if (lane == 0) {
-                const double* x = xfer + (((warp - 1) * 2 + ((st - 1) & 1)) * D);
+                // emitted by lane 31 of warp - 1 at step st - RING_K
+                const double* x =
+                    xfer + (((warp - 1) * 2 * RING_K + ((st + RING_K) & (2 * RING_K - 1))) * D);
 #pragma unroll
                 for (int l = 0; l < D; ++l) recv.v[l] = x[l];
             }
@@ -746,7 +759,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
     }
     SPK_PROF_MARK(L, 4)
 #ifndef SPK_EXP_NOSYNC
-    __syncthreads();
+    if (((st + 1) & (RING_K - 1)) == 0) __syncthreads();
 #endif
 #ifdef SPK_POLISH_PROF
     SPK_PROF_MARK(L, 5)
@@ -771,16 +784,16 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     // wrap_mode 2: two wrap buffers in shared memory (round parity), which double as the
     // replay snapshot -- no global snapshot stores on the ring's critical path;
     // 1: one shared wrap buffer + global ping-pong snapshots; 0: wrap in the workspace.
-    extern __shared__ __align__(16) double xfer[];  // [W][2][D], then wrap [1|2][ns][D]
-    __shared__ int stop_sh;
+    extern __shared__ __align__(16) double xfer[];  // [W][2 RING_K][D], then wrap [1|2][ns][D]
+    __shared__ int stop_sh[2];
     const long long c = blockIdx.x;
     const int B = blockDim.x;
     const int W = B >> 5;
-    const int P = max(4 * B + W, ns + 4);
+    const int P = max(4 * B + RING_K * W, ns + 4);
     const int nd4 = ns * D;
     // wrap buffer(s) in shared memory, or (very long shots) in the per-shot workspace
     double* wrap0 = wrap_mode == 0 ? ws + blockIdx.x * (size_t)(4 * nd4) + 3 * nd4
-                                   : xfer + W * 2 * D;
+                                   : xfer + W * 2 * RING_K * D;
     const int wstride = wrap_mode == 2 ? nd4 : 0;
     double* wrap1 = wrap0 + wstride;
     const int g = threadIdx.x;
@@ -793,7 +806,7 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     double* snap0 = ws + c * (size_t)(4 * nd);
     double* snap1 = snap0 + nd;
     double* res = snap1 + nd;
-    if (g == 0) stop_sh = 0x7fffffff;
+    if (g == 0) stop_sh[0] = stop_sh[1] = 0x7fffffff;
     // stage the initial state in the wrap buffer: lane 0 then reads round 0 from it like
     // every later round (no global-load latency on the ring's critical path).  Lane B-1
     // overwrites position q only 4 + ring_offset(B-1) steps after lane 0 has read it.
@@ -818,8 +831,11 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     {                                                                                      \
         ring_step<D, R>(L, st + R, ns, B, P, g, lane, warp, max_sweeps, kl, a, b, pin,     \
                         pv0, pv1, pv2, tol, s0, snap0, res, xfer, wrap0, wstride,          \
-                        &stop_sh);                                                         \
-        if (stop_sh != 0x7fffffff || st + R >= last_step) break;                           \
+                        stop_sh);                                                          \
+        if (((st + R + 1) & (RING_K - 1)) == 0 &&                                          \
+            stop_sh[((st + R) / RING_K) & 1] != 0x7fffffff)                                \
+            break;                                                                         \
+        if (st + R >= last_step) break;                                                    \
     }
     for (int st = 0;; st += 4) {
         SPK_RING_STEP(0)
@@ -835,7 +851,8 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
             for (int q = 0; q < 7; ++q) spk_polish_prof[slot][q] = L.prof[q];
     }
 #endif
-    const int kstar = stop_sh;
+    __syncthreads();  // the last_step exit can fall between barriers
+    const int kstar = min(stop_sh[0], stop_sh[1]);
     int total = max_sweeps;
     if (kstar != 0x7fffffff) {
         const int jj = kstar / B;
@@ -860,7 +877,8 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
 // Ring width: W warps; SPK_POLISH_WARPS overrides (fewer warps -> more shots resident
 // per SM, longer per-sweep latency).
 inline int polish_warps(int ns) {
-    int w = (ns + 4 + 128) / 129;  // 4 B + W >= ns + 4: no idle lane in the ring
+    // 4 B + RING_K W >= ns + 4: no idle lane in the ring
+    int w = (ns + 4 + 127 + RING_K) / (128 + RING_K);
     if (const char* e = getenv("SPK_POLISH_WARPS")) w = atoi(e);
     return w < 1 ? 1 : (w > 32 ? 32 : w);
 }
@@ -1164,7 +1182,7 @@ int spk_project_all(const double* in, const double* grad, double eta,
     // polish: systolic ring, one CTA of 32*pw lanes per shot; snapshots + result in the
     // (now free) FISTA workspace, warp hand-over slots in shared memory
     const int pw = polish_warps(n_s);
-    const size_t xb = (size_t)pw * 2 * dims * sizeof(double);
+    const size_t xb = (size_t)pw * 2 * RING_K * dims * sizeof(double);
     const size_t wb = (size_t)n_s * dims * sizeof(double);
     const int wrap_mode = xb + 2 * wb <= 200 * 1024 ? 2 : xb + wb <= 200 * 1024 ? 1 : 0;
     const size_t psm = xb + (wrap_mode == 2 ? 2 * wb : wrap_mode == 1 ? wb : 0);
