@@ -48,7 +48,7 @@ def release_workspaces() -> None:
 
 
 def h2d(arr: np.ndarray, dtype=torch.float64) -> torch.Tensor:
-    """Copy a host array to the device (pinned staging for large arrays)."""
+    """Copy a host array to the device (synchronous; pageable source)."""
     host = torch.from_numpy(np.ascontiguousarray(arr))
     if host.dtype != dtype:
         host = host.to(dtype)
