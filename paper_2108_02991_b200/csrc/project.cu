@@ -874,6 +874,12 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     if (g == 0 && sweeps_out) sweeps_out[c] = total;
 }
 
+// CTAs per SM the <= 8-warp polish instantiation is register-budgeted for.
+#ifndef SPK_POLISH_MINB
+#define SPK_POLISH_MINB 3
+#endif
+constexpr int PL_MINB = SPK_POLISH_MINB;
+
 // Ring width: W warps; SPK_POLISH_WARPS overrides (fewer warps -> more shots resident
 // per SM, longer per-sweep latency).
 inline int polish_warps(int ns) {
@@ -1186,9 +1192,9 @@ int spk_project_all(const double* in, const double* grad, double eta,
     const size_t wb = (size_t)n_s * dims * sizeof(double);
     const int wrap_mode = xb + 2 * wb <= 200 * 1024 ? 2 : xb + wb <= 200 * 1024 ? 1 : 0;
     const size_t psm = xb + (wrap_mode == 2 ? 2 * wb : wrap_mode == 1 ? wb : 0);
-    cudaFuncSetAttribute(polish_kernel<3, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(polish_kernel<3, 256, PL_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)psm);
-    cudaFuncSetAttribute(polish_kernel<2, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(polish_kernel<2, 256, PL_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)psm);
     cudaFuncSetAttribute(polish_kernel<3, 1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)psm);
@@ -1200,11 +1206,11 @@ int spk_project_all(const double* in, const double* grad, double eta,
     const dim3 grid((unsigned)n_shots), block(32 * pw);
     if (pw <= 8) {
         if (dims == 3)
-            polish_kernel<3, 256, 3><<<grid, block, psm, stream>>>(
+            polish_kernel<3, 256, PL_MINB><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
                 (float4*)pos4, wrap_mode);
         else
-            polish_kernel<2, 256, 3><<<grid, block, psm, stream>>>(
+            polish_kernel<2, 256, PL_MINB><<<grid, block, psm, stream>>>(
                 out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
                 (float4*)pos4, wrap_mode);
     } else {
