@@ -133,3 +133,19 @@ def test_anisotropic_grid_sums_match_cubic_when_isotropic():
         h = np.sqrt(1e-3 + (d * d).sum(0))
         assert abs(v1[t] - (rho * h).sum()) <= 1e-12 * v1[t]
         assert np.abs(g1[t] - (rho * d / h).reshape(3, -1).sum(1)).max() <= 1e-12
+
+
+def test_projection_oracle_solves_the_qp():
+    """The oracle's FISTA + polish at n_pit=1000 vs an independent QP solve (SLSQP) of the
+    reference's acceptance-test problem (test_acceptance.py:153-173): <= 1e-4 there,
+    measured ~2e-7."""
+    from paper_2108_02991_b200.projection import stacked_operator_norm
+    from qp_ref import qp_reference
+
+    rng = np.random.default_rng(7)
+    a, b = 0.3, 0.15
+    tau = 1.0 / stacked_operator_norm(8, -1)
+    for _ in range(20):
+        shot = rng.uniform(-1.5, 1.5, (8, 2))
+        out, _ = orc.project_all(shot[None], a, b, -1, np.zeros(2), 1000, tau, 1e-7)
+        assert np.abs(out[0] - qp_reference(shot, a, b)).max() <= 1e-5
