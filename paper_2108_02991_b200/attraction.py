@@ -11,9 +11,10 @@ Two evaluations share one ``KernelField``:
   (/root/reference/pkg/src/vdtraj/attraction.py:267-308): multilinear interpolation of
   the potential (and force) grids, fp64, in ``spk_field_eval`` (csrc/project.cu),
   bit-identical to the numba kernels for the same grids.  The grids
-  (``precompute_field``, attraction.py:62-113) are produced by K2 with the grid nodes as
-  targets -- the same linear convolution the reference evaluates by FFT -- and are
-  computed lazily on first use.
+  (``precompute_field``, attraction.py:62-113) are the same zero-padded fp64 FFT
+  convolution the reference evaluates with scipy, run on the device with cuFFT
+  (torch.fft) and computed lazily on first use: they match the reference's grids to FFT
+  round-off (~1e-15 of the maximum).
 """
 
 from __future__ import annotations
@@ -37,20 +38,35 @@ class AttractionResult(NamedTuple):
     n_clamped: int
 
 
+def next_fast_len(target: int) -> int:
+    """Smallest 5-smooth integer >= target (scipy.fft.next_fast_len(target, real=True),
+    the reference's FFT pad, attraction.py:92)."""
+    n = max(1, int(target))
+    while True:
+        m = n
+        for f in (2, 3, 5):
+            while m % f == 0:
+                m //= f
+        if m == 1:
+            return n
+        n += 1
+
+
 def field_workspace_bytes(grid_n: int, dims: int) -> int:
-    """Device bytes needed to build the field: lattice weights + node records (20 B),
-    potential + force (8 (1 + d) B) and the K2 partial-sum slots (<= 64 chunks x 32 B)
-    per node."""
-    nodes = (2 * grid_n + 1) ** dims
-    return nodes * (20 + 8 * (1 + dims) + 64 * 32)
+    """Peak workspace of the field FFT (attraction.py:52-59): the real pad buffer, its
+    rfft and the retained density rfft."""
+    pad = next_fast_len(6 * grid_n + 1)
+    per_axis_c = pad // 2 + 1
+    return 8 * pad ** dims + 2 * 16 * per_axis_c * pad ** (dims - 1)
 
 
 class KernelField:
     """Attraction potential/force grids on the (2N+1)^d density grid (attraction.py:26-43).
 
     Constructed either with explicit ``potential`` / ``force`` arrays (drop-in) or from a
-    ``density`` by :func:`precompute_field`, in which case the grids are evaluated by K2
-    the first time they are needed.  ``density`` also feeds ``grad_mode="exact"``.
+    ``density`` by :func:`precompute_field`, in which case the grids are evaluated on the
+    device (fp64 cuFFT convolution) the first time they are needed.  ``density`` also
+    feeds ``grad_mode="exact"``.
     """
 
     def __init__(self, potential=None, force=None, grid_n: int | None = None,
@@ -153,14 +169,35 @@ class KernelField:
                 self._dev["pot"] = _device.h2d(self._potential.reshape(-1))
                 self._dev["force"] = _device.h2d(self._force.reshape(self.dims, -1))
             else:
-                nodes = self.device_nodes()
-                g = nodes.shape[0]
-                val = torch.empty(g, dtype=torch.float64, device=nodes.device)
-                grad = torch.empty((g, self.dims), dtype=torch.float64, device=nodes.device)
-                grid_sums_device(nodes, self, self.kernel_eps ** 2, val, grad)
-                self._dev["pot"] = val
-                self._dev["force"] = grad.t().contiguous()
+                self._dev["pot"], self._dev["force"] = self._fft_grids()
         return self._dev["pot"], self._dev["force"]
+
+    def _fft_grids(self):
+        """precompute_field's convolutions (attraction.py:92-113) on the device in fp64:
+        the kernel sqrt(|x|^2 + eps^2) and its d partials x_l / h sampled on [-2, 2]^d at
+        the grid spacing (same operation order as the reference, so the sampled kernels
+        are bit-identical), zero-padded linear convolution with the density by cuFFT,
+        central (2N+1)^d block.  Returns (potential [G], force [d, G])."""
+        self._require_cubic()
+        n, d, eps = self.grid_n, self.dims, self.kernel_eps
+        dev = _device.device()
+        shape = (next_fast_len(6 * n + 1),) * d
+        rho_f = torch.fft.rfftn(_device.h2d(self.density.grid), s=shape)
+        axis = torch.arange(-2 * n, 2 * n + 1, dtype=torch.float64, device=dev) / n
+        grids = torch.meshgrid(*([axis] * d), indexing="ij")
+        r2 = grids[0] * grids[0]
+        for g in grids[1:]:
+            r2 = r2 + g * g
+        h = torch.sqrt(r2 + eps ** 2)
+        block = (slice(2 * n, 4 * n + 1),) * d
+
+        def conv(kernel):
+            full = torch.fft.irfftn(torch.fft.rfftn(kernel, s=shape) * rho_f, s=shape)
+            return full[block].reshape(-1).contiguous()
+
+        pot = conv(h)
+        force = torch.stack([conv(grids[ax] / h) for ax in range(d)])
+        return pot, force
 
 
 def grid_sums_device(tgt4, field: "KernelField", eps2, val=None, grad=None):
