@@ -137,9 +137,10 @@ def test_field_grids_match_reference_precompute(spk):
         rho = spk.TargetDensity(att[f"{name}_rho"], int(att[f"{name}_n"]))
         fld = spk.precompute_field(rho, kernel_eps=float(att[f"{name}_eps"]))
         pot = att[f"{name}_potential"]
-        assert np.abs(fld.potential - pot).max() <= 1e-6 * np.abs(pot).max(), name
+        # same fp64 FFT convolution as the reference (cuFFT vs pocketfft round-off)
+        assert np.abs(fld.potential - pot).max() <= 1e-13 * np.abs(pot).max(), name
         force = att[f"{name}_force"]
-        assert np.abs(fld.force - force).max() <= 1e-5 * np.abs(force).max(), name
+        assert np.abs(fld.force - force).max() <= 1e-12 * np.abs(force).max(), name
 
 
 def test_fused_equals_separate(spk):
