@@ -470,6 +470,10 @@ __device__ __forceinline__ void speed_pair(Sample<D>& x0, Sample<D>& x1, int n, 
         df[l] = x1.v[l] - x0.v[l];
         nrm += df[l] * df[l];
     }
+    // exact early out: a*a*(1 - 1e-15) < a^2 in real arithmetic, so nrm^2 below it means
+    // sqrt(nrm^2) < a, i.e. the reference's `nrm > a` is false -- skips the IEEE sqrt
+    // for the (typically many) pairs well inside the bound; NaN takes the full path
+    if (nrm <= a * a * (1.0 - 1e-15)) return;
     nrm = sqrt(nrm);
     if (!(nrm > a)) return;
     if (nrm - a > worst) worst = nrm - a;
@@ -505,6 +509,7 @@ __device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sampl
         w[l] = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
         nrm += w[l] * w[l];
     }
+    if (nrm <= b * b * (1.0 - 1e-15)) return;  // exact early out, as in speed_pair
     nrm = sqrt(nrm);
     if (!(nrm > b)) return;
     if (nrm - b > worst) worst = nrm - b;
