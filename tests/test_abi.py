@@ -5,6 +5,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 import paper_2108_02991_b200 as spk
 from paper_2108_02991_b200 import _build, _native
 
@@ -64,3 +66,22 @@ def test_no_cpu_fallback_without_cuda(monkeypatch):
         spk.eval_repulsion_direct(np.zeros((4, 3)))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _device.device()
+
+
+def test_plain_c_consumer_compiles_and_links():
+    """examples/abi_demo.c uses the header as plain C (no C++, no torch types) and links
+    against the built library (run on the GPU by tests/test_gpu_abi_demo.py)."""
+    import shutil
+    import subprocess
+    import tempfile
+
+    REPO = os.path.dirname(_build.INCLUDE)
+    if shutil.which("gcc") is None or not os.path.exists("/usr/local/cuda/include/cuda_runtime.h"):
+        pytest.skip("gcc / CUDA headers not available")
+    lib = os.path.join(REPO, "paper_2108_02991_b200", "_lib")
+    with tempfile.TemporaryDirectory() as d:
+        subprocess.run(["gcc", "-O2", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(REPO, "include"),
+                        "-I", "/usr/local/cuda/include", os.path.join(REPO, "examples", "abi_demo.c"),
+                        "-L", lib, "-lsparkling_b200", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                        "-o", os.path.join(d, "abi_demo")], check=True)
+
