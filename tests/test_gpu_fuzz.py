@@ -1,0 +1,105 @@
+"""Randomised parity (hypothesis, derandomised).  Projection: shot length, dims, pin
+position (incl. the ends), bounds, monotone mode, n_pit and the sweep cap drawn at
+random; the GPU K3 must equal the CPU oracle bit for bit, outputs and sweep counts.
+The ring's edge cases -- N_s below one warp, a pin at sample 0 / N_s - 1, caps that stop
+inside a ring round -- are all in the drawn space."""
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@st.composite
+def cases(draw):
+    dims = draw(st.sampled_from([2, 3]))
+    ns = draw(st.sampled_from([3, 4, 5, 7, 16, 31, 33, 64, 100, 129, 257, 300, 700, 1030]))
+    n_c = draw(st.integers(1, 6))
+    pin = draw(st.sampled_from([-1, 0, ns // 2, ns - 1]))
+    a = draw(st.sampled_from([0.02, 0.05, 0.2, 0.5]))
+    b = draw(st.sampled_from([0.005, 0.01, 0.05, 0.3]))
+    mono = draw(st.booleans())
+    n_pit = draw(st.sampled_from([1, 5, 40]))
+    cap = draw(st.sampled_from([1, 7, 33, 300, 50000]))
+    seed = draw(st.integers(0, 2 ** 31 - 1))
+    scale = draw(st.sampled_from([0.3, 1.0, 1.4]))
+    return dims, ns, n_c, pin, a, b, mono, n_pit, cap, seed, scale
+
+
+@settings(max_examples=150, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(cases())
+def test_projection_bitwise_random(case):
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.projection import project_device
+    import torch
+
+    dims, ns, n_c, pin, a, b, mono, n_pit, cap, seed, scale = case
+    rng = np.random.default_rng(seed)
+    shots = rng.uniform(-scale, scale, (n_c, ns, dims))
+    pv = rng.uniform(-0.3, 0.3, dims) if pin >= 0 else None
+    pc = None if pin < 0 else spk.LinearConstraint(pin, pv)
+    cfg = spk.ProjectionConfig(alpha=a, beta=b, raster_dt=1.0, n_pit=n_pit, pin=pc,
+                               monotone=mono)
+    tau = 1.0 / spk.projection.stacked_operator_norm(ns, pin)
+    dev = _device.h2d(shots)
+    sw = torch.zeros(n_c, dtype=torch.int32, device=dev.device)
+    out = _device.d2h(project_device(dev, cfg, tau=tau, sweeps=sw, max_sweeps=cap))
+    ref, rsw = orc.project_all(shots, a, b, pin, pv, n_pit, tau, 0.1 * cfg.feas_tol,
+                               monotone=mono, max_sweeps=cap)
+    assert np.array_equal(_device.d2h(sw), rsw), case
+    assert np.array_equal(out, ref), (case, np.abs(out - ref).max())
+
+
+@st.composite
+def clouds(draw):
+    dims = draw(st.sampled_from([2, 3]))
+    p = draw(st.sampled_from([1, 2, 31, 513, 4099, 20000]))
+    kind = draw(st.sampled_from(["uniform", "radial", "clustered", "duplicates"]))
+    eps = draw(st.sampled_from([0.0, 1e-3, 0.05]))
+    return dims, p, kind, eps, draw(st.integers(0, 2 ** 31 - 1))
+
+
+def _cloud(dims, p, kind, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "uniform":
+        return rng.uniform(-1, 1, (p, dims))
+    if kind == "radial":
+        v = rng.normal(size=(p, dims))
+        return (rng.uniform(0, 1, p) ** 2)[:, None] * v / np.linalg.norm(v, axis=1, keepdims=True)
+    if kind == "clustered":
+        c = rng.uniform(-0.8, 0.8, (4, dims))
+        return c[rng.integers(0, 4, p)] + 1e-3 * rng.normal(size=(p, dims))
+    base = rng.uniform(-1, 1, (max(1, p // 3), dims))
+    return base[rng.integers(0, base.shape[0], p)]  # exact duplicates
+
+
+@settings(max_examples=40, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(clouds())
+def test_direct_sums_random_clouds(case):
+    """K1 vs the fp64 oracle on random clouds (incl. exact duplicates with eps = 0, where
+    coincident pairs contribute nothing): value rel l2 <= 1e-5, gradient <= 1e-4."""
+    import paper_2108_02991_b200  # noqa: F401
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.repulsion import direct_sums_device
+
+    dims, p, kind, eps, seed = case
+    pts = _cloud(dims, p, kind, seed)
+    p4 = _device.pack_positions(_device.h2d(pts))
+    val, grad = direct_sums_device(p4, p4, dims, eps * eps)
+    vref, gref = orc.direct_sums(pts, eps * eps)
+    val, grad = _device.d2h(val), _device.d2h(grad)
+    if np.linalg.norm(vref) > 0:
+        assert np.linalg.norm(val - vref) / np.linalg.norm(vref) <= 1e-5, case
+    else:
+        assert np.all(val == 0.0), case
+    gn = np.linalg.norm(gref)
+    if gn > 1e-12 * max(1.0, np.linalg.norm(vref)):
+        assert np.linalg.norm(grad - gref) / gn <= 1e-4, case
+    assert np.all(np.isfinite(grad)), case
