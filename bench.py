@@ -462,7 +462,7 @@ def run_tree(args):
     t0 = time.perf_counter()
     fld.source_tree()
     from paper_2108_02991_b200 import tree as _tree
-    fld.source_tree().static_proxies(_tree.auto_params(W["att_prec"])[0])
+    fld.source_tree().static_proxies(_tree.auto_params(W["att_prec"], DIMS)[0])
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     run = engine.ShardedRun(np.ascontiguousarray(start_pattern().coords), cfg, fld)

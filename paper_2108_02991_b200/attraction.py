@@ -229,7 +229,7 @@ def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg
     the same targets (shared with a treecode repulsion)."""
     from . import tree
 
-    params = tree.auto_params(precision)
+    params = tree.auto_params(precision, field.dims)
     if params is None:
         return grid_sums_device(tgt4, field, eps2)
     order, theta = params

@@ -93,10 +93,10 @@ def eval_repulsion_direct(k, eps: float = 1e-3) -> tuple[float, np.ndarray]:
     return cost, grad_h
 
 
-def auto_tree_params(precision: float) -> tuple[int, float]:
+def auto_tree_params(precision: float, dims: int = 3) -> tuple[int, float]:
     """Interpolation order and opening threshold for a precision (repulsion.py:90-96);
     (MAX_INTERP_ORDER, 0.0) -- i.e. exact sums -- below the fp32 floor."""
-    params = tree.auto_params(precision)
+    params = tree.auto_params(precision, dims)
     return params if params is not None else (MAX_INTERP_ORDER, 0.0)
 
 
@@ -120,7 +120,7 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
     returns the target groups (tree.TargetGroups, or None on the direct path) so that a
     treecode attraction can reuse the targets' sort."""
     eps2 = cfg.kernel_eps * cfg.kernel_eps
-    params = tree.auto_params(cfg.tree_precision)
+    params = tree.auto_params(cfg.tree_precision, dims)
     n_src = src4.shape[0]
 
     def done(val, grad, tg=None):

@@ -71,9 +71,23 @@ def far_parent_cap(n_targets: int) -> int | None:
     return FAR_PARENT_CAP if n_targets >= FAR_LEVEL_MIN else None
 
 
-def auto_params(precision: float) -> tuple[int, float] | None:
+# 2D rows: a q^2 proxy is cheap, and dense-centre 2D clouds (radius ~ u^2) need higher
+# orders than the 3D table gives -- (6, 0.7) reached 2.2e-5 on them for the 1e-5 row
+# (scripts/tree_calib2d.py, profiles/r01_tree_calib2d.jsonl; found by tests/test_gpu_fuzz).
+# Worst gradient error over dense-centre radial (150k, 1M), uniform, clustered and 2D
+# spoke clouds: 1.5e-4 / 2.2e-5 / 8.1e-7 / 5.0e-7 for the 1e-3 .. 1e-6 rows.
+AUTO_PARAMS_2D = (
+    (1e-2, 3, 0.8),
+    (1e-3, 4, 0.7),
+    (1e-4, 6, 0.7),
+    (1e-5, 7, 0.6),
+    (1e-6, 8, 0.6),
+)
+
+
+def auto_params(precision: float, dims: int = 3) -> tuple[int, float] | None:
     """(order, theta) for a precision, or None when only the exact kernel meets it."""
-    for floor, order, theta in AUTO_PARAMS:
+    for floor, order, theta in (AUTO_PARAMS_2D if dims == 2 else AUTO_PARAMS):
         if precision >= floor:
             return order, theta
     return None

@@ -103,3 +103,20 @@ def test_direct_sums_random_clouds(case):
     if gn > 1e-12 * max(1.0, np.linalg.norm(vref)):
         assert np.linalg.norm(grad - gref) / gn <= 1e-4, case
     assert np.all(np.isfinite(grad)), case
+
+
+@settings(max_examples=12, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.sampled_from(["uniform", "radial", "clustered", "duplicates"]),
+       st.sampled_from([1e-2, 1e-3, 1e-4, 1e-5]), st.integers(0, 2 ** 31 - 1))
+def test_treecode_precision_contract_random_clouds(dims, kind, prec, seed):
+    """eval_repulsion_tree meets tree_precision on cost and gradient l2 on random clouds
+    large enough (150k) to run the treecode, incl. clustered and duplicated points."""
+    import paper_2108_02991_b200 as spk
+
+    pts = _cloud(dims, 150_000, kind, seed)
+    cfg = spk.RepulsionConfig(backend="tree", tree_precision=prec)
+    c_t, g_t = spk.eval_repulsion_tree(pts, cfg)
+    c_d, g_d = spk.eval_repulsion_direct(pts, cfg.kernel_eps)
+    assert abs(c_t - c_d) / abs(c_d) <= prec, (dims, kind, prec)
+    assert np.linalg.norm(g_t - g_d) / np.linalg.norm(g_d) <= prec, (dims, kind, prec)

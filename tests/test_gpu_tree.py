@@ -68,12 +68,15 @@ def test_precision_contract_auto_params(spk, precision):
     from paper_2108_02991_b200 import _device, tree
     from paper_2108_02991_b200.repulsion import direct_sums_device
 
-    order, theta = tree.auto_params(precision)
+    rng = np.random.default_rng(5)
+    v = rng.normal(size=(150_000, 2))
+    dense_2d = (rng.uniform(0, 1, 150_000) ** 2)[:, None] * v / np.linalg.norm(v, axis=1, keepdims=True)
     clouds = [spk.perturb(spk.init_radial(64, 512, 2), 0.25, 0).points(),
               spk.perturb(spk.init_radial(256, 512, 3), 0.25, 1).points(),
-              np.random.default_rng(5).uniform(-1, 1, (60000, 3))]
+              rng.uniform(-1, 1, (60000, 3)), dense_2d]
     for pts in clouds:
         d = pts.shape[1]
+        order, theta = tree.auto_params(precision, d)
         pos4 = _device.pack_positions(_device.h2d(pts))
         vt, gt = tree.tree_sums_device(pos4, pos4, d, 1e-6, order, theta)
         vd, gd = direct_sums_device(pos4, pos4, d, 1e-6)
