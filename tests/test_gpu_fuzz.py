@@ -120,3 +120,53 @@ def test_treecode_precision_contract_random_clouds(dims, kind, prec, seed):
     c_d, g_d = spk.eval_repulsion_direct(pts, cfg.kernel_eps)
     assert abs(c_t - c_d) / abs(c_d) <= prec, (dims, kind, prec)
     assert np.linalg.norm(g_t - g_d) / np.linalg.norm(g_d) <= prec, (dims, kind, prec)
+
+
+@settings(max_examples=16, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.sampled_from(["uniform", "radial", "clustered"]),
+       st.sampled_from([1e-2, 1e-3, 1e-4, 1e-5]), st.sampled_from([0.1, 0.25, 0.5]),
+       st.sampled_from([0.0, 1.0, 2.0, 4.0]), st.integers(0, 2 ** 31 - 1))
+def test_attraction_treecode_precision_random(dims, kind, prec, cutoff, decay, seed):
+    """The lattice treecode (attraction_tree_precision) meets its precision on the cost
+    and the gradient l2 against exact K2, for random densities and target clouds."""
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.attraction import grid_sums_device, tree_grid_sums_device
+
+    n = 96 if dims == 2 else 24
+    fld = spk.precompute_field(spk.discretize(spk.DensityParams(cutoff, decay), n, dims))
+    pts = np.clip(_cloud(dims, 100_000, kind, seed), -1.0, 1.0)
+    p4 = _device.pack_positions(_device.h2d(pts))
+    eps2 = fld.kernel_eps ** 2
+    v0, g0 = (_device.d2h(x) for x in grid_sums_device(p4, fld, eps2))
+    v1, g1 = (_device.d2h(x) for x in tree_grid_sums_device(p4, fld, eps2, prec))
+    case = (dims, kind, prec, cutoff, decay)
+    assert abs(v1.sum() - v0.sum()) / abs(v0.sum()) <= prec, case
+    assert np.linalg.norm(g1 - g0) / np.linalg.norm(g0) <= prec, case
+
+
+@settings(max_examples=30, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.integers(1, 3000), st.integers(1, 70), st.integers(1, 70),
+       st.integers(1, 40), st.sampled_from(["fp64", "mixed"]), st.integers(0, 2 ** 31 - 1))
+def test_nudft_random_shapes(dims, p, n0, n1, n2, precision, seed):
+    """Adjoint and forward NUDFT on random sample counts and grid shapes (odd, even,
+    1-wide axes) vs the numpy dense-phase oracle: 1e-12 (fp64) / 2e-5 (mixed) of max."""
+    from oracle import nudft_oracle as no
+    from paper_2108_02991_b200.analysis import nudft_adjoint, nudft_forward
+
+    grid = (n0, n1) if dims == 2 else (n0, n1, n2)
+    if p * int(np.prod(grid)) > 4_000_000:  # keep the numpy oracle small
+        p = max(1, 4_000_000 // int(np.prod(grid)))
+    rng = np.random.default_rng(seed)
+    pts = rng.uniform(-1, 1, (p, dims))
+    w = rng.normal(size=p) + 1j * rng.normal(size=p)
+    img = rng.normal(size=grid) + 1j * rng.normal(size=grid)
+    tol = 1e-12 if precision == "fp64" else 2e-5
+    ref = no.nudft_adjoint(pts, w, grid)
+    got = nudft_adjoint(pts, w, grid, precision=precision)
+    assert np.abs(got - ref).max() <= tol * np.abs(ref).max(), (grid, p, precision)
+    ref = no.nudft_forward(pts, img)
+    got = nudft_forward(pts, img, precision=precision)
+    assert np.abs(got - ref).max() <= tol * np.abs(ref).max(), (grid, p, precision)
