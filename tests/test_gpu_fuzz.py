@@ -170,3 +170,27 @@ def test_nudft_random_shapes(dims, p, n0, n1, n2, precision, seed):
     ref = no.nudft_forward(pts, img)
     got = nudft_forward(pts, img, precision=precision)
     assert np.abs(got - ref).max() <= tol * np.abs(ref).max(), (grid, p, precision)
+
+
+@settings(max_examples=12, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.sampled_from(["uniform", "radial", "clustered"]),
+       st.integers(2, 6), st.sampled_from([1e-3, 1e-4, 1e-5]), st.integers(0, 2 ** 31 - 1))
+def test_explicit_order_probe_meets_precision(dims, kind, order, prec, seed):
+    """An explicit interp_order goes through the reference's 64-target probe: it escalates
+    the order (or falls back to exact sums) until the probe meets tree_precision; the
+    result then meets it on the full gradient too (repulsion.py:165-200)."""
+    import warnings
+
+    import paper_2108_02991_b200 as spk
+
+    pts = _cloud(dims, 150_000, kind, seed)
+    cfg = spk.RepulsionConfig(backend="tree", tree_precision=prec, interp_order=order)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        c_t, g_t = spk.eval_repulsion_tree(pts, cfg)
+    c_d, g_d = spk.eval_repulsion_direct(pts, cfg.kernel_eps)
+    # the probe checks 64 targets, so allow 3x on the full-cloud l2 (the reference's probe
+    # has the same sampling limitation)
+    assert abs(c_t - c_d) / abs(c_d) <= 3 * prec, (dims, kind, order, prec)
+    assert np.linalg.norm(g_t - g_d) / np.linalg.norm(g_d) <= 3 * prec, (dims, kind, order, prec)
