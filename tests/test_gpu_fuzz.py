@@ -220,3 +220,27 @@ def test_optimize_gpu_vs_oracle_engine(dims, n_c, n_s, n_decim, pert, seed):
     # coordinates: the ~1e-6 relative gradient difference times the fixed step (eta0 =
     # 1024 eps p) moves samples by ~1e-6 before the projection; measured worst 1.3e-6
     assert np.abs(gpu.pattern.coords - cpu.pattern.coords).max() <= 1e-5
+
+
+@settings(max_examples=10, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.sampled_from(["uniform", "radial", "clustered"]),
+       st.sampled_from([2, 3, 8]), st.integers(0, 7), st.sampled_from([1e-3, 1e-4]),
+       st.integers(0, 2 ** 31 - 1))
+def test_sharded_targets_treecode(dims, kind, world, rank, prec, seed):
+    """A rank's contiguous target shard against all sources (the multi-GPU form of the
+    treecode repulsion) meets the precision on that shard."""
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.repulsion import direct_sums_device, tree_sums_checked
+
+    rank = rank % world
+    pts = _cloud(dims, 200_000, kind, seed)
+    lo, hi = pts.shape[0] * rank // world, pts.shape[0] * (rank + 1) // world
+    src4 = _device.pack_positions(_device.h2d(pts))
+    tgt4 = src4[lo:hi].contiguous()
+    cfg = spk.RepulsionConfig(backend="tree", tree_precision=prec)
+    v1, g1 = (_device.d2h(x) for x in tree_sums_checked(tgt4, src4, dims, cfg))
+    v0, g0 = (_device.d2h(x) for x in direct_sums_device(tgt4, src4, dims, cfg.kernel_eps ** 2))
+    assert abs(v1.sum() - v0.sum()) / abs(v0.sum()) <= prec, (dims, kind, world, rank, prec)
+    assert np.linalg.norm(g1 - g0) / np.linalg.norm(g0) <= prec, (dims, kind, world, rank, prec)
