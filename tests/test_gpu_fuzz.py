@@ -244,3 +244,27 @@ def test_sharded_targets_treecode(dims, kind, world, rank, prec, seed):
     v0, g0 = (_device.d2h(x) for x in direct_sums_device(tgt4, src4, dims, cfg.kernel_eps ** 2))
     assert abs(v1.sum() - v0.sum()) / abs(v0.sum()) <= prec, (dims, kind, world, rank, prec)
     assert np.linalg.norm(g1 - g0) / np.linalg.norm(g0) <= prec, (dims, kind, world, rank, prec)
+
+
+@settings(max_examples=10, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.sampled_from(["uniform", "radial", "clustered", "duplicates"]),
+       st.sampled_from([128, 512, 1024]), st.sampled_from([(4, 0.7, 1e-3), (5, 0.7, 1e-4)]),
+       st.integers(0, 2 ** 31 - 1))
+def test_far_level_random_clouds(dims, kind, cap, row, seed):
+    """The far level (P2L at parents' Chebyshev points + L2P; the repulsion uses it from
+    4M targets) on random clouds and parent capacities: every source counted once, the
+    row's precision met (same bar as the plain walk)."""
+    from paper_2108_02991_b200 import _device, tree
+    from paper_2108_02991_b200.repulsion import direct_sums_device
+
+    order, theta, prec = row
+    pts = _cloud(dims, 200_000, kind, seed)
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    src = tree.SourceTree(pos4, dims)
+    tg = tree.TargetGroups(pos4, dims, same_as=src, parent_cap=cap)
+    vt, gt = (_device.d2h(x) for x in tree.tree_eval(tg, src, order, theta, 1e-6, static=True))
+    vd, gd = (_device.d2h(x) for x in direct_sums_device(pos4, pos4, dims, 1e-6))
+    case = (dims, kind, cap, row)
+    assert abs(vt.sum() - vd.sum()) / abs(vd.sum()) <= prec, case
+    assert np.linalg.norm(gt - gd) / np.linalg.norm(gd) <= prec, case
