@@ -268,3 +268,55 @@ def test_far_level_random_clouds(dims, kind, cap, row, seed):
     case = (dims, kind, cap, row)
     assert abs(vt.sum() - vd.sum()) / abs(vd.sum()) <= prec, case
     assert np.linalg.norm(gt - gd) / np.linalg.norm(gd) <= prec, case
+
+
+def _residuals_numpy(coords, speed_bound, accel_bound, pin):
+    """feasibility_residuals restated in numpy (projection.py:435-452)."""
+    amp = float(np.max(np.abs(coords)) - 1.0)
+    d1 = np.linalg.norm(np.diff(coords, axis=1), axis=2)
+    d2 = np.linalg.norm(np.diff(coords, 2, axis=1), axis=2)
+    res = {"amplitude": max(amp, 0.0),
+           "speed": max(float(d1.max() - speed_bound) if d1.size else -np.inf, 0.0),
+           "acceleration": max(float(d2.max() - accel_bound) if d2.size else -np.inf, 0.0)}
+    if pin is not None:
+        res["pin"] = float(np.abs(coords[:, pin.pinned_index, :] - pin.pinned_value).max())
+    res["max"] = max(res.values())
+    return res
+
+
+@settings(max_examples=60, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.integers(1, 5), st.sampled_from([2, 3, 5, 64, 257]),
+       st.booleans(), st.sampled_from([0.3, 1.0, 1.3]), st.integers(0, 2 ** 31 - 1),
+       st.sampled_from([0.0, 1e-3, 0.3]))
+def test_step_projection_and_residuals(dims, n_c, ns, pinned, scale, seed, eta):
+    """The optimizer's fused step + projection (in = coords - eta * grad, per-shot eta
+    too) bit-identical to the oracle on the stepped input, and feasibility_residuals
+    bit-identical to the reference's numpy formula."""
+    import torch
+
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import _device
+    from paper_2108_02991_b200.projection import project_device
+
+    rng = np.random.default_rng(seed)
+    coords = rng.uniform(-scale, scale, (n_c, ns, dims))
+    grad = rng.normal(size=coords.shape)
+    pin = spk.LinearConstraint(ns // 2, rng.uniform(-0.2, 0.2, dims)) if pinned else None
+    cfg = spk.ProjectionConfig(alpha=0.08, beta=0.02, raster_dt=1.0, n_pit=15, pin=pin)
+    pin_idx = -1 if pin is None else pin.pinned_index
+    tau = 1.0 / spk.projection.stacked_operator_norm(ns, pin_idx)
+    etas = rng.uniform(0, 2 * eta, n_c) if eta > 0 else np.zeros(n_c)
+    for per_shot in (False, True):
+        stepped = coords - (etas[:, None, None] if per_shot else eta) * grad
+        d_eta = _device.h2d(etas) if per_shot else None
+        out = _device.d2h(project_device(_device.h2d(coords), cfg, grad=_device.h2d(grad),
+                                         eta=eta, tau=tau, eta_per_shot=d_eta))
+        ref, _ = orc.project_all(stepped, cfg.speed_bound, cfg.accel_bound, pin_idx,
+                                 None if pin is None else pin.pinned_value, 15, tau,
+                                 0.1 * cfg.feas_tol)
+        assert np.array_equal(out, ref), (dims, n_c, ns, pinned, per_shot)
+    for pat in (coords, ref):
+        got = spk.feasibility_residuals(spk.SamplingPattern(pat), cfg)
+        want = _residuals_numpy(pat, cfg.speed_bound, cfg.accel_bound, pin)
+        assert got == want, (got, want)
