@@ -6,7 +6,7 @@ inside a ring round -- are all in the drawn space."""
 
 import numpy as np
 import pytest
-from hypothesis import HealthCheck, given, settings
+from hypothesis import HealthCheck, assume, given, settings
 from hypothesis import strategies as st
 
 from oracle import oracle as orc
@@ -105,15 +105,23 @@ def test_direct_sums_random_clouds(case):
     assert np.all(np.isfinite(grad)), case
 
 
-@settings(max_examples=12, deadline=None, derandomize=True,
+@settings(max_examples=24, deadline=None, derandomize=True,
           suppress_health_check=[HealthCheck.too_slow])
 @given(st.sampled_from([2, 3]), st.sampled_from(["uniform", "radial", "clustered", "duplicates"]),
-       st.sampled_from([1e-2, 1e-3, 1e-4, 1e-5]), st.integers(0, 2 ** 31 - 1))
+       st.sampled_from([1e-2, 1e-3, 1e-4, 1e-5, 1e-6]), st.integers(0, 2 ** 31 - 1))
 def test_treecode_precision_contract_random_clouds(dims, kind, prec, seed):
     """eval_repulsion_tree meets tree_precision on cost and gradient l2 on random clouds
     large enough (150k) to run the treecode, incl. clustered and duplicated points."""
     import paper_2108_02991_b200 as spk
 
+    # Against the exact fp32-pair kernel: its own distance to fp64 is ~4e-8 on spread
+    # clouds but ~3e-6 on clouds clustered at the eps scale (fp32 cancellation in
+    # t - s; scripts/fp32_floor.py), within the north star's 1e-4 (checked against the
+    # oracle by test_direct_sums_random_clouds) -- so the 1e-6 row is a contract on the
+    # approximation, not on fp64 agreement, for such clouds.
+    # On eps-scale clusters the fp32 arithmetic of the proxies and of the exact kernel
+    # differ by ~1e-6 themselves, so the 1e-6 row is only asserted on the other clouds.
+    assume(not (kind == "clustered" and prec < 1e-5))
     pts = _cloud(dims, 150_000, kind, seed)
     cfg = spk.RepulsionConfig(backend="tree", tree_precision=prec)
     c_t, g_t = spk.eval_repulsion_tree(pts, cfg)
