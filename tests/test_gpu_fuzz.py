@@ -328,3 +328,23 @@ def test_step_projection_and_residuals(dims, n_c, ns, pinned, scale, seed, eta):
         got = spk.feasibility_residuals(spk.SamplingPattern(pat), cfg)
         want = _residuals_numpy(pat, cfg.speed_bound, cfg.accel_bound, pin)
         assert got == want, (got, want)
+
+
+@settings(max_examples=20, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.integers(2, 40), st.integers(2, 40), st.integers(2, 20),
+       st.sampled_from([0.1, 0.25, 0.5]), st.sampled_from([0.0, 2.0, 4.0]),
+       st.integers(1, 3000), st.integers(0, 2 ** 31 - 1))
+def test_exact_attraction_anisotropic_random(dims, n0, n1, n2, cutoff, decay, p, seed):
+    """K2 over random anisotropic (2 N_a + 1 per axis) lattices and random targets
+    (incl. outside [-1, 1]) vs the fp64 oracle: cost 1e-5, gradient rel l2 1e-4."""
+    import paper_2108_02991_b200 as spk
+
+    ns = (n0, n1) if dims == 2 else (n0, n1, n2)
+    rho = spk.discretize_anisotropic(spk.DensityParams(cutoff, decay), ns, dims)
+    fld = spk.precompute_field(rho)
+    pts = np.random.default_rng(seed).uniform(-1.1, 1.1, (p, dims))
+    res = spk.eval_attraction(spk.SamplingPattern(pts[None]), fld, "exact")
+    cref, gref = orc.attraction_exact(pts, rho.grid, fld.kernel_eps)
+    assert abs(res.cost - cref) <= 1e-5 * abs(cref), ns
+    assert np.linalg.norm(res.grad - gref) <= 1e-4 * max(np.linalg.norm(gref), 1e-300), ns
