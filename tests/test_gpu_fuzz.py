@@ -348,3 +348,26 @@ def test_exact_attraction_anisotropic_random(dims, n0, n1, n2, cutoff, decay, p,
     cref, gref = orc.attraction_exact(pts, rho.grid, fld.kernel_eps)
     assert abs(res.cost - cref) <= 1e-5 * abs(cref), ns
     assert np.linalg.norm(res.grad - gref) <= 1e-4 * max(np.linalg.norm(gref), 1e-300), ns
+
+
+@settings(max_examples=8, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.sampled_from([4, 9]), st.sampled_from([32, 64]),
+       st.sampled_from([0, 1]), st.sampled_from(["exact", "consistent", "smooth"]),
+       st.integers(1, 5), st.integers(0, 1000))
+def test_stack_vs_individual_random(dims, n_c, n_s, n_decim, mode, n_prob, seed):
+    """optimize_stack (independent problems as one device batch) follows each
+    single-problem optimize(): same init, costs to 1e-9, coordinates to 1e-6."""
+    import paper_2108_02991_b200 as spk
+
+    hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                          dwell_dt=1e-5, fov=0.192, matrix=32, dims=dims)
+    cfg = spk.OptimizerConfig(n_c=n_c, n_s=n_s, dims=dims, n_decim=n_decim, n_git=3,
+                              perturbation=0.25, seed=seed, grad_mode=mode, grid_n=8)
+    batch = spk.optimize_stack(cfg, hw, n_prob)
+    for q, res in enumerate(batch):
+        single = spk.optimize(spk.OptimizerConfig(**{**cfg.__dict__, "seed": seed + q}), hw)
+        assert np.array_equal(res.initial.coords, single.initial.coords)
+        c1, c2 = res.trace.costs(), single.trace.costs()
+        assert np.abs(c1 - c2).max() <= 1e-9 * np.abs(c2).max(), (q, c1, c2)
+        assert np.abs(res.pattern.coords - single.pattern.coords).max() <= 1e-6
