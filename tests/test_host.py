@@ -167,3 +167,15 @@ def test_trajectory_csv_roundtrip_and_dispatch(tmp_path):
     (tmp_path / "c.csv").write_text("shot,sample,kx\n0,0,0.5\n")
     with pytest.raises(spk_io.FileFormatError, match="columns"):
         spk_io.read_trajectory_csv(tmp_path / "c.csv")
+
+
+def test_default_density_grid_guard():
+    """full3d.cfg's cubic default (grid_n = 2 * 384 -> 1537^3 cells, 29 GB) raises a
+    MemoryError with guidance before allocating (the reference would run out of host
+    memory); no GPU is touched before the check."""
+    hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                          dwell_dt=2e-6, fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208),
+                          dims=3)
+    cfg = spk.OptimizerConfig(n_c=4096, n_s=2048, dims=3, n_decim=6, grad_mode="exact")
+    with pytest.raises(MemoryError, match="discretize_anisotropic"):
+        spk.optimize(cfg, hw)
