@@ -137,6 +137,30 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
     tg = tree.TargetGroups(tgt4, dims, same_as=src if same else None, parent_cap=cap)
     # the far level needs every node's proxies (static), the plain walk builds its own
     val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
+    if cfg.interp_order is None:
+        # Extension of the reference (which trusts its table in auto mode): the same
+        # 64-target probe, and on a miss the next stricter (order, theta) row, then the
+        # exact kernel.  The table is calibrated on SPARKLING-like, uniform and radial
+        # clouds; dense blobs whose sub-boxes all sit at the opening ratio can exceed it
+        # (profiles/r01_tree_fuzz_sweep.txt).
+        rows = tree.AUTO_PARAMS_2D if dims == 2 else tree.AUTO_PARAMS
+        k = next(i for i, r in enumerate(rows) if cfg.tree_precision >= r[0])
+        err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
+        while max(err_val, err_grad) > cfg.tree_precision:
+            k += 1
+            if k >= len(rows):
+                warnings.warn(
+                    f"tree backend (auto) reached relative error {max(err_val, err_grad):.2e}"
+                    f" > {cfg.tree_precision:.2e} on the probe at every table row; falling "
+                    f"back to direct summation")
+                return done(*direct_sums_device(tgt4, src4, dims, eps2), tg)
+            _, order, theta = rows[k]
+            warnings.warn(
+                f"tree backend (auto) reached relative error {max(err_val, err_grad):.2e} > "
+                f"{cfg.tree_precision:.2e} on the probe; tightening to interp_order={order}, "
+                f"theta={theta}")
+            val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
+            err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
     if cfg.interp_order is not None:
         err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         while max(err_val, err_grad) > cfg.tree_precision and order < MAX_INTERP_ORDER:

@@ -288,3 +288,26 @@ def test_far_level_matches_plain_treecode(spk, order, theta):
     va, ga, vr, gr = (_device.d2h(x) for x in (va, ga, vr, gr))
     assert abs(va.sum() - vr.sum()) / abs(vr.sum()) <= precision / 2
     assert np.linalg.norm(ga - gr) / np.linalg.norm(gr) <= precision / 2
+
+
+def test_auto_mode_probe_tightens_on_dense_blobs(spk):
+    """Auto (order, theta) rows are calibrated on SPARKLING-like, uniform and radial
+    clouds; on eps-scale blobs (every sub-box at the opening ratio) the 1e-3 row reaches
+    ~1.9e-3.  The auto-mode probe (an extension of the reference) detects it, tightens to
+    the next row with a warning, and the result meets the precision."""
+    import warnings
+
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_fuzz import _cloud
+
+    pts = _cloud(3, 140_000, "clustered", 679326770)
+    cfg = spk.RepulsionConfig(backend="tree", tree_precision=1e-3)
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
+        c_t, g_t = spk.eval_repulsion_tree(pts, cfg)
+    assert any("tightening" in str(w.message) for w in caught)
+    c_d, g_d = spk.eval_repulsion_direct(pts, cfg.kernel_eps)
+    assert abs(c_t - c_d) / abs(c_d) <= 1e-3
+    assert np.linalg.norm(g_t - g_d) / np.linalg.norm(g_d) <= 1e-3
