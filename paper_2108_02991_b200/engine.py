@@ -33,6 +33,7 @@ class CudaOps:
 
     def __init__(self):
         self.device = _device.device()
+        self._tree_rows = {}  # treecode auto-mode rows validated by the probe (per level)
 
     def empty(self, shape, dtype=torch.float64):
         return torch.empty(shape, dtype=dtype, device=self.device)
@@ -54,7 +55,8 @@ class CudaOps:
             # sort is shared when both run
             tg = None
             if cfg.repulsion.backend == "tree":
-                vr, gr, tg = tree_sums_checked(tgt4, src4, d, cfg.repulsion, return_groups=True)
+                vr, gr, tg = tree_sums_checked(tgt4, src4, d, cfg.repulsion, return_groups=True,
+                                               row_cache=self._tree_rows)
             else:
                 vr, gr = direct_sums_device(tgt4, src4, d, eps2_rep)
             if att_tree:

@@ -114,11 +114,13 @@ def _probe_error(tgt4, src4, dims, eps2, val, grad) -> tuple[float, float]:
 
 
 def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
-                      return_groups: bool = False):
+                      return_groups: bool = False, row_cache: dict | None = None):
     """Device raw sums for backend="tree" with the reference's order selection, probe,
     escalation and direct fallback (repulsion.py:165-200).  With ``return_groups`` also
     returns the target groups (tree.TargetGroups, or None on the direct path) so that a
-    treecode attraction can reuse the targets' sort."""
+    treecode attraction can reuse the targets' sort.  ``row_cache`` (the optimizer's):
+    the auto-mode probe runs once per (sizes, precision) and its validated table row is
+    reused -- once per optimizer level instead of every iteration."""
     eps2 = cfg.kernel_eps * cfg.kernel_eps
     params = tree.auto_params(cfg.tree_precision, dims)
     n_src = src4.shape[0]
@@ -130,6 +132,13 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
         # small problems (exact kernel is faster) and precisions below the fp32 floor
         return done(*direct_sums_device(tgt4, src4, dims, eps2))
     auto_order, theta = params
+    rows = tree.AUTO_PARAMS_2D if dims == 2 else tree.AUTO_PARAMS
+    ckey = (tgt4.shape[0], n_src, dims, cfg.tree_precision)
+    cached = None if row_cache is None or cfg.interp_order is not None else row_cache.get(ckey)
+    if cached is not None:
+        if cached >= len(rows):
+            return done(*direct_sums_device(tgt4, src4, dims, eps2))
+        _, auto_order, theta = rows[cached]
     order = cfg.interp_order if cfg.interp_order is not None else auto_order
     same = tgt4.data_ptr() == src4.data_ptr() and tgt4.shape[0] == n_src
     src = tree.SourceTree(src4, dims)
@@ -137,13 +146,12 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
     tg = tree.TargetGroups(tgt4, dims, same_as=src if same else None, parent_cap=cap)
     # the far level needs every node's proxies (static), the plain walk builds its own
     val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
-    if cfg.interp_order is None:
+    if cfg.interp_order is None and cached is None:
         # Extension of the reference (which trusts its table in auto mode): the same
         # 64-target probe, and on a miss the next stricter (order, theta) row, then the
         # exact kernel.  The table is calibrated on SPARKLING-like, uniform and radial
         # clouds; dense blobs whose sub-boxes all sit at the opening ratio can exceed it
         # (profiles/r01_tree_fuzz_sweep.txt).
-        rows = tree.AUTO_PARAMS_2D if dims == 2 else tree.AUTO_PARAMS
         k = next(i for i, r in enumerate(rows) if cfg.tree_precision >= r[0])
         err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         while max(err_val, err_grad) > cfg.tree_precision:
@@ -153,6 +161,8 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
                     f"tree backend (auto) reached relative error {max(err_val, err_grad):.2e}"
                     f" > {cfg.tree_precision:.2e} on the probe at every table row; falling "
                     f"back to direct summation")
+                if row_cache is not None:
+                    row_cache[ckey] = k
                 return done(*direct_sums_device(tgt4, src4, dims, eps2), tg)
             _, order, theta = rows[k]
             warnings.warn(
@@ -161,6 +171,8 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
                 f"theta={theta}")
             val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
             err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
+        if row_cache is not None:
+            row_cache[ckey] = k
     if cfg.interp_order is not None:
         err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         while max(err_val, err_grad) > cfg.tree_precision and order < MAX_INTERP_ORDER:
