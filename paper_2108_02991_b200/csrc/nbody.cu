@@ -98,8 +98,9 @@ __device__ __forceinline__ float rsqrt_sfu(float x) {
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
 // Positions tile against this thread's NB_TPT targets (difference form).
-// G: guard r2 == 0 (eps2 == 0 => coincident points contribute value 0, gradient 0,
-// like the reference's `if h > 0` at _treecode.py:525).
+// G: guard r2 below the fp32 normal range (eps2 < FLT_MIN, incl. eps = 0 => coincident
+// points contribute value 0, gradient 0, like the reference's `if h > 0` at
+// _treecode.py:525; for 0 < eps < 1.1e-19 the dropped value is eps itself).
 template <int D, bool G>
 __device__ __forceinline__ void tile_positions(const float4* __restrict__ tile, int cnt,
                                                const float2 (&X)[NB_PAIRS],
@@ -129,8 +130,8 @@ __device__ __forceinline__ void tile_positions(const float4* __restrict__ tile, 
             inv.x = rsqrt_sfu(r2.x);
             inv.y = rsqrt_sfu(r2.y);
             if (G) {
-                inv.x = r2.x > 0.0f ? inv.x : 0.0f;
-                inv.y = r2.y > 0.0f ? inv.y : 0.0f;
+                inv.x = r2.x >= FLT_MIN ? inv.x : 0.0f;  // rsqrt.approx.ftz flushes subnormal r2
+                inv.y = r2.y >= FLT_MIN ? inv.y : 0.0f;
             }
             av[k] = __ffma2_rn(r2, inv, av[k]);  // sum h = sum r2 / h
             ax[k] = __ffma2_rn(dx, inv, ax[k]);
@@ -200,8 +201,8 @@ __device__ __forceinline__ void tile_lattice(const float* __restrict__ tile, lon
                 inv.x = rsqrt_sfu(r2.x);
                 inv.y = rsqrt_sfu(r2.y);
                 if (G) {
-                    inv.x = r2.x > 0.0f ? inv.x : 0.0f;
-                    inv.y = r2.y > 0.0f ? inv.y : 0.0f;
+                    inv.x = r2.x >= FLT_MIN ? inv.x : 0.0f;  // rsqrt.approx.ftz flushes subnormal r2
+                    inv.y = r2.y >= FLT_MIN ? inv.y : 0.0f;
                 }
                 const float2 winv = __fmul2_rn(inv, bc(w));
                 av[q] = __ffma2_rn(r2, winv, av[q]);

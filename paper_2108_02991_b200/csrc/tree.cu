@@ -748,8 +748,8 @@ __device__ __forceinline__ void pair_step(const float4 s, float2 X, float2 Y, fl
     inv.x = rsqrt_approx(r2.x);
     inv.y = rsqrt_approx(r2.y);
     if (G) {
-        inv.x = r2.x > 0.0f ? inv.x : 0.0f;
-        inv.y = r2.y > 0.0f ? inv.y : 0.0f;
+        inv.x = r2.x >= FLT_MIN ? inv.x : 0.0f;  // rsqrt.approx.ftz flushes subnormal r2
+        inv.y = r2.y >= FLT_MIN ? inv.y : 0.0f;
     }
     const float2 wi = __fmul2_rn(inv, bcast(s.w));
     av = __ffma2_rn(r2, wi, av);  // w h = w r2 / h

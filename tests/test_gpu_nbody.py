@@ -226,3 +226,19 @@ def test_c4_scale_row_subset(spk):
     aref, agref = orc.grid_sums(pts[rows], rho.grid, fld.kernel_eps ** 2)
     assert rel_l2(va, aref) <= VAL_TOL
     assert rel_l2(ga, agref) <= GRAD_TOL
+
+
+def test_subnormal_eps_squared_stays_finite(spk):
+    """eps below 1.1e-19 has a subnormal fp32 square, which the rsqrt.approx.ftz flushes:
+    the guard must drop those coincident pairs (as for eps = 0) instead of producing
+    inf / NaN (found by scripts/nbody_extreme.py)."""
+    rng = np.random.default_rng(4)
+    for d in (2, 3):
+        pts = rng.uniform(-1, 1, (500, d))
+        cost, grad = spk.eval_repulsion_direct(pts, eps=1e-20)
+        assert np.isfinite(cost) and np.all(np.isfinite(grad))
+        cref, gref = orc.repulsion(pts, 1e-20)
+        assert abs(cost - cref) <= VAL_TOL * abs(cref)
+        assert rel_l2(grad, gref) <= GRAD_TOL
+        c1, g1 = spk.eval_repulsion_direct(pts[:1], eps=1e-20)
+        assert np.isfinite(c1) and abs(c1) <= 1e-19 and np.all(g1 == 0.0)
