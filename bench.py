@@ -1,17 +1,24 @@
 """Benchmark: pair-interactions/s and s/iteration of the SPARKLING hot path.
 
-Workload (BASELINE.json configs[1], "C2"): 3D, 1024 shots x 1024 samples (p = 2^20),
-129^3 density grid (N = 64, "128^3"), exact attraction (north star), eps_rep = 1e-3,
-eps_att = 1/(2N), full3d hardware limits, pin at N_s/2, perturbed radial init
-(P = 0.25, seed 0).  One step = one optimize() iteration on the device: fused K1+K2
+Headline workload (BASELINE.json configs[1], "C2"): 3D, 1024 shots x 1024 samples
+(p = 2^20), 129^3 density grid (N = 64, "128^3"), exact attraction (north star),
+eps_rep = 1e-3, eps_att = 1/(2N), full3d hardware limits, pin at N_s/2, perturbed radial
+init (P = 0.25, seed 0).  One step = one optimize() iteration on the device: fused K1+K2
 N-body, gradient combine + BB dots, step + K3 projection (FISTA 100 it + polish),
 feasibility residuals, position all-gather.
 
+The metric is quoted at ~10^7 samples (configs[3], "C4": 4096 x 2048), so the default run
+appends two sub-records measured in the same invocation: ``c4`` (exact sums, as the
+headline) and ``c4t`` (the reference's full3d.cfg backends: repulsion treecode 1e-3,
+attraction treecode 1e-4).
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's CPU path (the
-bit-exact C port in oracle/, all host threads) on bounded row samples of the same
-workload.
+``--gpus N`` is authoritative: without torchrun's WORLD_SIZE and N > 1 the script
+re-launches itself under ``torch.distributed.run`` with N ranks (failing loudly when the
+node has fewer than N GPUs); under torchrun WORLD_SIZE must equal N.  Prints ONE JSON
+line (rank 0).  ``--impl reference`` times the reference's CPU path (the bit-exact C
+port in oracle/, all host threads) on bounded samples of the same workload.
 """
 
 from __future__ import annotations
@@ -19,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -30,8 +38,9 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-# Workloads (SURVEY 8 shapes).  The bench line is C2 (BASELINE configs[1], the config
-# the metric is quoted on for one GPU); the others are selectable with --config.
+# Workloads (SURVEY 8 shapes).  The bench line is C2 (BASELINE configs[1], the largest
+# config whose exact step fits the per-run budget at 20+5 steps); C4 / C4t ride along as
+# sub-records; the others are selectable with --config.
 WORKLOADS = {
     "c2": dict(name="C2: 3D SPARKLING 1024 shots x 1024 samples, 129^3 density grid",
                n_c=1024, n_s=1024, dims=3, grid_n=(64, 64, 64), pert=0.25,
@@ -60,8 +69,20 @@ WORKLOADS = {
                n_c=64, n_s=512, dims=2, grid_n=(128, 128), pert=0.25,
                fov=0.192, matrix=64, dwell=2e-6, stack=64),
 }
+# sub-records of the default (c2) run: key -> (timed steps, warm-up steps); None = the
+# run's own --steps / --warmup
+SUBRECORDS = {"c4": (2, 3), "c4t": (None, None)}
 W = dict(WORKLOADS["c2"])
 EPS_REP = 1e-3
+FLOPS = {3: (17, 19), 2: (12, 14)}  # (repulsion, attraction) algorithmic flops per pair
+# executed FP32 lane-ops per pair (csrc/nbody.cu): positions 3D 3 FADD + 3 FFMA (r2) +
+# 4 FFMA (value, gradient); 2D 2 + 2 + 3; lattice 6 (dl, r2, w/h, value, S, g_last) in
+# both; one MUFU.RSQ per pair everywhere
+LANE_OPS = {3: (10, 6), 2: (7, 6)}
+# FMA-pipe cost of one rsqrt evaluated without the SFU (integer seed + 2 Newton steps):
+# 8 lane-ops; used for the balanced-pipe bound below
+RSQRT_FMA_LANE_OPS = 8
+METRIC = "pair-interactions/s"
 
 
 def select_workload(key: str) -> None:
@@ -83,18 +104,24 @@ def density():
     if len(set(GRID_NS)) == 1:
         return spk.discretize(params, GRID_NS[0], DIMS)
     return spk.discretize_anisotropic(params, GRID_NS, DIMS)
-FLOPS = {3: (17, 19), 2: (12, 14)}  # (repulsion, attraction) flops per pair
-METRIC = "pair-interactions/s"
 
 
 def workload_config():
-    return {"workload": W["name"] + " (exact attraction + exact repulsion + projection)",
-            "n_c": N_C, "n_s": N_S, "p": N_C * N_S, "grid": [2 * n + 1 for n in GRID_NS],
-            "grad_mode": "exact", "eps_rep": EPS_REP, "eps_att": 1.0 / (2 * GRID_N),
-            "n_pit": 100,
-            "hardware": f"G 40 mT/m, S 180 T/m/s, raster 10 us, matrix {W['matrix']}, "
-                        f"fov {W['fov']} m",
-            "l2": "flushed between steps (256 MiB memset outside the per-step events)"}
+    """The workload keys, identical in both arms (the parallelism is a top-level key)."""
+    cfg = {"workload": W["name"] + (" (exact attraction + exact repulsion + projection)"
+                                    if not W.get("tree") else ""),
+           "n_c": N_C, "n_s": N_S, "p": N_C * N_S, "grid": [2 * n + 1 for n in GRID_NS],
+           "grad_mode": "exact", "eps_rep": EPS_REP, "eps_att": 1.0 / (2 * GRID_N),
+           "n_pit": 100,
+           "hardware": f"G 40 mT/m, S 180 T/m/s, raster 10 us, matrix {W['matrix']}, "
+                       f"fov {W['fov']} m",
+           "l2": "flushed between steps (256 MiB memset outside the per-step events)"}
+    if W.get("tree"):
+        cfg["repulsion"] = f"tree, tree_precision {W['rep_prec']}"
+        cfg["attraction"] = f"treecode, precision {W['att_prec']}"
+    if W.get("stack"):
+        cfg["stack"] = W["stack"]
+    return cfg
 
 
 def hardware():
@@ -183,47 +210,92 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- helpers
 def measured_peaks():
-    path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
-        with open(path) as fh:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
             return json.load(fh)
     except OSError:
         return {}
 
 
-def fp32_peak_tflops(sm_mhz):
-    # 148 SMs x 128 FP32 lanes x 2 flop (FMA) x clock
-    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-
-
 def measured_fp32_peak():
-    """FP32 TFLOP/s measured by scripts/micro/fp32_peak.cu (profiles/fp32_peak.json)."""
+    """(FP32 TFLOP/s, MUFU.RSQ per clk per SM, clock MHz) measured by
+    scripts/micro/fp32_peak.cu on a B200 (profiles/fp32_peak.json); MEASURED_PEAKS.json
+    has HBM and bf16 entries only."""
     try:
         with open(os.path.join(REPO, "profiles", "fp32_peak.json")) as fh:
             d = json.load(fh)
-        return float(d["fp32_tflops"]), float(d["sm_mhz"])
+        return (float(d["fp32_tflops"]), float(d.get("mufu_rsq_per_clk_per_sm", 15.87)),
+                float(d["sm_mhz"]), "measured (scripts/micro/fp32_peak.cu, "
+                                    "profiles/fp32_peak.json)")
     except (OSError, ValueError, KeyError):
-        return None, None
+        mhz = float(measured_peaks().get("sm_max_mhz", 1965.0))
+        return (148 * 128 * 2 * mhz * 1e6 / 1e12, 16.0, mhz,
+                "nominal 148 SM x 128 FP32 lanes x 2 and 16 MUFU/clk/SM at the max clock")
 
 
-def sfu_pairs_per_s(mhz):
-    """Measured MUFU.RSQ throughput x 148 SMs (one rsqrt per pair)."""
-    per_clk = 15.87
+def committed_traffic(key: str):
+    """DRAM bytes per fused N-body launch for this workload from an ncu capture
+    (profiles/nbody_traffic.json, keyed by workload), or None when not captured."""
     try:
-        with open(os.path.join(REPO, "profiles", "fp32_peak.json")) as fh:
-            per_clk = float(json.load(fh)["mufu_rsq_per_clk_per_sm"])
-    except (OSError, ValueError, KeyError):
-        pass
-    return per_clk * 148 * mhz * 1e6
-
-
-def committed_traffic():
-    path = os.path.join(REPO, "profiles", "nbody_traffic.json")
-    try:
-        with open(path) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+        with open(os.path.join(REPO, "profiles", "nbody_traffic.json")) as fh:
+            d = json.load(fh)
     except (OSError, ValueError):
-        return None
+        return None, None
+    rec = d.get("workloads", {}).get(key)
+    if rec is None:
+        return None, None
+    return rec.get("dram_bytes_per_launch"), rec.get("source")
+
+
+def nbody_roofline(key, dims, rep_pairs, att_pairs, launch_ms, clocks):
+    """Roofline of the fused N-body launch.
+
+    The path is rsqrt-bound: each pair costs FP32 lane-ops on the FMA pipe and
+    one MUFU.RSQ on the SFU.  The bound is the balanced-pipe time of the executed mix:
+    FMA work L = rep * lane_rep + att * lane_att lane-ops at the measured FP32 rate, SFU work
+    M = rep + att rsqrts at the measured MUFU rate, where the hardware may move x rsqrts to
+    the FMA pipe at RSQRT_FMA_LANE_OPS each: T = min_x max((L + c x)/fma_rate,
+    (M - x)/sfu_rate).  ``peak`` is the algorithmic TFLOP/s the launch would reach at that
+    bound (17/19 flops per pair), so frac = achieved / peak = T / launch time
+    and never exceeds 1."""
+    f_rep, f_att = FLOPS[dims]
+    l_rep, l_att = LANE_OPS[dims]
+    tflops, mufu_clk, mhz, src = measured_fp32_peak()
+    fma_rate = tflops * 1e12 / 2.0            # lane-ops/s
+    sfu_rate = mufu_clk * 148 * mhz * 1e6     # rsqrt/s
+    lanes = rep_pairs * l_rep + att_pairs * l_att
+    mufu = rep_pairs + att_pairs
+    c = RSQRT_FMA_LANE_OPS
+    x = max(0.0, min(mufu, (mufu * fma_rate / sfu_rate - lanes) / (c + fma_rate / sfu_rate)))
+    bound_s = max((lanes + c * x) / fma_rate, (mufu - x) / sfu_rate)
+    overlap_s = max(lanes / fma_rate, mufu / sfu_rate)
+    flops = rep_pairs * f_rep + att_pairs * f_att
+    achieved = flops / (launch_ms / 1e3) / 1e12
+    peak = flops / bound_s / 1e12
+    traffic, tsrc = committed_traffic(key)
+    sm = clocks.get("sm_mhz") if clocks else None
+    return {
+        "bound": "fp32+sfu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak,
+        "frac_at_measured_clock": (achieved / (peak * sm / mhz)) if sm else None,
+        "traffic": traffic,
+        "traffic_source": tsrc if traffic is not None else
+        "no ncu DRAM capture for this workload (the kernel reads ~0 bytes per pair)",
+        "kernel": "nbody_kernel (fused K1+K2) + finalize", "launch_ms": launch_ms,
+        "hw_bound_ms": bound_s * 1e3,
+        "overlap_bound_ms_no_offload": overlap_s * 1e3,
+        "algorithmic_tflops_vs_fp32_peak": achieved / tflops,
+        "peak_source": f"{src}: FP32 {tflops:.2f} TFLOP/s and MUFU.RSQ {mufu_clk:.2f}/clk/SM "
+                       f"at {mhz:.0f} MHz",
+        "work": {"repulsion_pairs": rep_pairs, "attraction_pairs": att_pairs,
+                 "flops_per_pair": {"repulsion": f_rep, "attraction": f_att},
+                 "lane_ops_per_pair": {"repulsion": l_rep, "attraction": l_att},
+                 "mufu_per_pair": 1, "rsqrt_on_fma_lane_ops": c},
+        "note": "peak = algorithmic flops at the balanced FP32+SFU bound of the executed "
+                "mix (hw_bound_ms); frac = hw_bound_ms / launch_ms.  "
+                "algorithmic_tflops_vs_fp32_peak is secondary: the lattice segment runs "
+                "fewer lane-ops than its 19 algorithmic flops, so it can exceed 1.",
+    }
 
 
 def cpu_model():
@@ -237,10 +309,25 @@ def cpu_model():
     return "unknown"
 
 
+def inloop_shots():
+    """In-loop shots for the CPU projection sample: the stepped (pre-projection) shots of
+    optimize iteration 6 of this workload, recorded on a B200 by
+    scripts/make_inloop_shots.py (bench_data/).  Fresh-init shots need several times more
+    polish sweeps than in-loop ones and would inflate the CPU time."""
+    key = "c4" if W["key"].startswith("c4") else W["key"]
+    path = os.path.join(REPO, "bench_data", f"inloop_{key}.npz")
+    if os.path.exists(path):
+        d = np.load(path)
+        return d["shots"], f"{d['shots'].shape[0]} in-loop shots (optimize iteration " \
+                           f"{int(d['iteration'])}, bench_data/inloop_{key}.npz)"
+    return start_pattern().coords[:16], "16 fresh-init shots (no in-loop fixture)"
+
+
 def cpu_reference_sample(rows: int, threads: int = 0):
     """Reference CPU path (bit-exact C port of direct_sums / the weighted attraction sum
-    / _project_all, OpenMP over all host threads) on bounded row samples of the workload.
-    Returns pairs/s and an extrapolated s/iteration."""
+    / _project_all, OpenMP over the host threads) on bounded samples of the workload:
+    ``rows`` target rows against all sources, and a sample of in-loop shots through the
+    projection.  Returns pairs/s and an extrapolated s/iteration."""
     from oracle import oracle as orc
     import paper_2108_02991_b200 as spk
 
@@ -255,37 +342,172 @@ def cpu_reference_sample(rows: int, threads: int = 0):
     orc.grid_sums(pts[idx], rho.grid, (1.0 / (2 * GRID_N)) ** 2, threads)
     t_att = time.perf_counter() - t0
     rate = (rows * p + rows * g) / (t_rep + t_att)
-    # projection: a bounded shot sample at full size, scaled to all shots
     cfg = proj_config()
-    n_sh = 16
-    shots = start_pattern().coords[:n_sh]
+    shots, what = inloop_shots()
     tau = 1.0 / spk.projection.stacked_operator_norm(N_S, N_S // 2)
     t0 = time.perf_counter()
     orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, N_S // 2, np.zeros(DIMS), 100,
                     tau, 0.1 * cfg.feas_tol, nthreads=threads)
-    t_proj = (time.perf_counter() - t0) * (N_C / n_sh)
+    t_proj = (time.perf_counter() - t0) * (N_C / shots.shape[0])
     s_per_it = rep_pairs / (rows * p / t_rep) + att_pairs / (rows * g / t_att) + t_proj
     return {"pairs_per_s": rate, "s_per_iteration": s_per_it, "t_sample": t_rep + t_att,
-            "rows": rows, "proj_s_extrapolated": t_proj}
+            "rows": rows, "proj_s_extrapolated": t_proj, "proj_sample": what}
 
 
-# ---------------------------------------------------------------- our arm
-def run_ours(args):
+def cpu_baseline_record(rows):
+    cb = cpu_reference_sample(rows)
+    p, g, _, _ = pairs_per_step()
+    return {"value": cb["pairs_per_s"], "unit": "pairs/s", "cores": os.cpu_count(),
+            "kind": "port", "cpu": cpu_model(),
+            "sample": f"{cb['rows']} target rows x all p={p} sources (repulsion) + "
+                      f"{cb['rows']} rows x all {g} grid cells (attraction), fp64, "
+                      f"{cb['t_sample']:.1f} s; projection: {cb['proj_sample']}, scaled to "
+                      f"{N_C} shots",
+            "s_per_iteration_extrapolated": cb["s_per_iteration"],
+            "proj_s_extrapolated": cb["proj_s_extrapolated"]}
+
+
+# ---------------------------------------------------------------- process group
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def ensure_world(args) -> None:
+    """Make ``--gpus N`` authoritative for our arm (one process per GPU)."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank "
+                     f"per GPU (torchrun --nproc-per-node {args.gpus})")
+        if args.gpus > 1:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        return
+    if args.gpus <= 1:
+        return
     import torch
-    import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    use_dist = world > 1 or os.environ.get("SPK_BENCH_DIST") == "1"
-    if use_dist:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import paper_2108_02991_b200 as spk
-    from paper_2108_02991_b200 import _native, engine
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} requested but this node has {have} CUDA "
+                 f"device(s); refusing to report a {args.gpus}-GPU number")
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr,
+          flush=True)
+    os.execve(sys.executable, cmd, env)
+
+
+class Ctx:
+    """This process's rank / device / process group."""
+
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dist = self.world > 1 or os.environ.get("SPK_BENCH_DIST") == "1"
+        if self.dist:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+
+    def barrier(self):
+        if self.dist:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def max(self, *vals):
+        if not self.dist:
+            return vals
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return tuple(float(x) for x in t.tolist())
+
+    def close(self):
+        if self.dist:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+def timed_loop(ctx, step, steps, warmup, on_record=None):
+    """W untimed warm-up steps, then K device-timed steps (CUDA events on the launching
+    stream, L2 flushed before each step outside the events), barrier + synchronize on
+    both sides.  Returns (total_ms max over ranks, clocks, our kernel launches)."""
+    import torch
+    from paper_2108_02991_b200 import _native
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    if on_record:
+        on_record()
+    _native.reset_launch_count()
+    times = []
+    with ClockSampler(ctx.local) as clk:
+        torch.cuda.synchronize()
+        for _ in range(steps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step()
+            e.record()
+            times.append((s, e))
+        torch.cuda.synchronize()
+    launches = _native.launch_count()
+    ctx.barrier()
+    total_ms = sum(s.elapsed_time(e) for s, e in times)
+    del flush
+    return total_ms, clk.summary(), launches
+
+
+def optimizer_step(run, cfg):
+    """One optimizer iteration on the device (optimizer.py:301-344 through ShardedRun)."""
     from paper_2108_02991_b200.optimizer import _bb_step, default_eta0
 
+    state = {"eta0": default_eta0(run.p, EPS_REP), "it": 0, "have": False}
+    state["eta"] = state["eta0"]
+    pcfg = proj_config()
+
+    def step():
+        state["it"] += 1
+        att, rep, bad, dots = run.evaluate()
+        if bad or not np.isfinite(att - rep):
+            raise RuntimeError("non-finite during bench")
+        state["eta"] = _bb_step(state["it"], state["eta"], dots[0], dots[1], state["have"],
+                                state["eta0"], cfg.fixed_step_iters)
+        state["have"] = True
+        run.step_project(pcfg, state["eta"])
+        run.residual_max(pcfg)
+        return att - rep
+
+    return step, state
+
+
+# ---------------------------------------------------------------- our arm: exact sums
+def measure_exact(args, ctx, steps, warmup, with_e2e, with_cpu):
+    import torch
+
+    import paper_2108_02991_b200 as spk
+    from paper_2108_02991_b200 import engine
+
     class TimedOps(engine.CudaOps):
+        """Records CUDA events around the fused N-body launch (same stream)."""
+
         def __init__(self):
             super().__init__()
             self.record = False
@@ -301,236 +523,92 @@ def run_ours(args):
             self.ev.append((s, e))
             return out
 
-    hw = hardware()
     cfg = spk.OptimizerConfig(n_c=N_C, n_s=N_S, dims=DIMS, n_pit=100, grad_mode="exact",
                               grid_n=GRID_N, seed=0, perturbation=W["pert"])
-    rho = density()
-    fld = spk.precompute_field(rho)
+    fld = spk.precompute_field(density())
     pcfg = proj_config()
     ops = TimedOps()
     run = engine.ShardedRun(np.ascontiguousarray(start_pattern().coords), cfg, fld, ops=ops)
     run.project(pcfg)
-    eta0 = default_eta0(run.p, EPS_REP)
-    state = {"eta": eta0, "it": 0, "have": False}
+    step, _ = optimizer_step(run, cfg)
 
-    def step():
-        state["it"] += 1
-        att, rep, bad, dots = run.evaluate()
-        if bad or not np.isfinite(att - rep):
-            raise RuntimeError("non-finite during bench")
-        state["eta"] = _bb_step(state["it"], state["eta"], dots[0], dots[1], state["have"],
-                                eta0, cfg.fixed_step_iters)
-        state["have"] = True
-        run.step_project(pcfg, state["eta"])
-        run.residual_max(pcfg)
-        return att - rep
+    def on_record():
+        ops.record = True
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if use_dist:
-        dist.barrier()
-    ops.record = True
-    _native.reset_launch_count()
-    times = []
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            flush.zero_()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            step()
-            e.record()
-            times.append((s, e))
-        torch.cuda.synchronize()
-    launches = _native.launch_count()
-    if use_dist:
-        dist.barrier()
-    total_ms = sum(s.elapsed_time(e) for s, e in times)
-    nb_ms = [s.elapsed_time(e) for s, e in ops.ev]
-    if use_dist:
-        t = torch.tensor([total_ms, float(np.mean(nb_ms))], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, nb_mean = float(t[0]), float(t[1])
-    else:
-        nb_mean = float(np.mean(nb_ms))
+    total_ms, clocks, launches = timed_loop(ctx, step, steps, warmup, on_record)
+    nb_mean = float(np.mean([s.elapsed_time(e) for s, e in ops.ev]))
+    total_ms, nb_mean = ctx.max(total_ms, nb_mean)
     p, g, rep_pairs, att_pairs = pairs_per_step()
-    value = (rep_pairs + att_pairs) * args.steps / (total_ms / 1e3)
-
-    # roofline of the dominant kernel (fused K1+K2 launch on this rank)
     local_t = run.local * N_S
-    f_rep, f_att = FLOPS[DIMS]
-    flops = local_t * p * f_rep + local_t * g * f_att
-    achieved = flops / (nb_mean / 1e3) / 1e12
-    peaks = measured_peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak, peak_mhz = measured_fp32_peak()
-    if peak is None:
-        peak, peak_mhz = fp32_peak_tflops(sm_max), sm_max
-        peak_source = (f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_max} MHz "
-                       f"(MEASURED_PEAKS.json clock)")
-    else:
-        peak_source = (f"measured FFMA2 throughput {peak:.2f} TFLOP/s at {peak_mhz:.0f} MHz "
-                       f"(scripts/micro/fp32_peak.cu, profiles/fp32_peak.json); "
-                       f"MEASURED_PEAKS.json has no FP32 entry")
-    clocks = clk.summary()
-    # hardware-bound time of the launch: repulsion pairs at the FP32 roofline (f_rep flops
-    # per pair), attraction pairs at the measured SFU rate (the lattice kernel spends 6
-    # FP32 lane-ops + 1 MUFU per pair, so the SFU binds, profiles/fp32_peak.json)
-    sfu_rate = sfu_pairs_per_s(peak_mhz)
-    bound_ms = (local_t * p / (peak * 1e12 / f_rep) + local_t * g / sfu_rate) * 1e3
-
-    # end-to-end through the public drop-in API with host buffers
-    if args.no_e2e:
-        e2e = None
-    elif not use_dist:
-        e2e = run_e2e(args, spk, fld, pcfg) if rank == 0 else None
-    else:
-        e2e = run_e2e_sharded(args, run, step, world)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "s_per_iteration": total_ms / args.steps / 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
-            "config": workload_config() | {"parallelism": f"shots sharded over {world} GPU(s)"},
-            "roofline": {"bound": "fp32+sfu", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak,
-                         "frac_at_measured_clock": (
-                             achieved / (peak * clocks["sm_mhz"] / peak_mhz)
-                             if clocks.get("sm_mhz") else None),
-                         "traffic": committed_traffic(),
-                         "kernel": "nbody_kernel (fused K1+K2) + finalize",
-                         "flops_per_pair": {"repulsion": f_rep, "attraction": f_att},
-                         "launch_ms": nb_mean,
-                         "peak_source": peak_source,
-                         "hw_bound_ms": bound_ms,
-                         "frac_of_hw_bound": bound_ms / nb_mean,
-                         "hw_bound_note": "repulsion pairs at the FP32 peak / 17 flops, "
-                                          "attraction pairs at the measured MUFU.RSQ rate "
-                                          f"({sfu_rate:.3g}/s): the lattice kernel does fewer "
-                                          "than the algorithmic 19 flops per pair, so "
-                                          "'frac' (algorithmic flops / FP32 peak) can "
-                                          "approach 1 while frac_of_hw_bound stays honest"},
-            "clocks": clocks,
-            "gpu_launches": launches,
-        }
-        if e2e is not None:
-            line["e2e"] = e2e
-        if not args.no_cpu_baseline and world == 1:
-            cb = cpu_reference_sample(args.cpu_rows)
-            line["cpu_baseline"] = {
-                "value": cb["pairs_per_s"], "unit": "pairs/s", "cores": os.cpu_count(),
-                "kind": "port", "cpu": cpu_model(),
-                "sample": f"{cb['rows']} target rows x all p={p} sources (repulsion) + "
-                          f"{cb['rows']} rows x all {g} grid cells (attraction), fp64, "
-                          f"{cb['t_sample']:.1f} s; projection 16 shots scaled to {N_C}",
-                "s_per_iteration_extrapolated": cb["s_per_iteration"]}
-        print(json.dumps(line), flush=True)
-    if use_dist:
-        dist.destroy_process_group()
+    rec = {
+        "metric": METRIC, "value": (rep_pairs + att_pairs) * steps / (total_ms / 1e3),
+        "unit": "pairs/s", "n_gpus": ctx.world, "steps": steps, "warmup": warmup,
+        "ms_per_step": total_ms / steps, "s_per_iteration": total_ms / steps / 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
+        "config": workload_config(),
+        "parallelism": f"shots sharded over {ctx.world} GPU(s)",
+        "roofline": nbody_roofline(W["key"], DIMS, local_t * p, local_t * g, nb_mean, clocks),
+        "clocks": clocks, "gpu_launches": launches,
+    }
+    if with_e2e:
+        if not ctx.dist:
+            rec["e2e"] = run_e2e(args, spk, fld, pcfg, steps)
+        else:
+            rec["e2e"] = run_e2e_sharded(ctx, run, step, steps)
+    del run, ops, fld
+    if with_cpu and ctx.world == 1 and ctx.rank == 0:
+        rec["cpu_baseline"] = cpu_baseline_record(args.cpu_rows if W["key"] == "c2" else
+                                                  args.cpu_rows // 16)
+    return rec
 
 
-def run_tree(args):
+# ---------------------------------------------------------------- our arm: treecodes
+def measure_tree(args, ctx, steps, warmup):
     """Treecode workloads (c2t, c4t): s/iteration of the full optimizer iteration with
     RepulsionConfig(backend="tree") and the treecode attraction, through ShardedRun."""
     import torch
-    import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    use_dist = world > 1 or os.environ.get("SPK_BENCH_DIST") == "1"
-    if use_dist:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2108_02991_b200 as spk
-    from paper_2108_02991_b200 import _native, engine
-    from paper_2108_02991_b200.optimizer import _bb_step, default_eta0
+    from paper_2108_02991_b200 import engine
+    from paper_2108_02991_b200 import tree as _tree
 
-    hw = hardware()
     cfg = spk.OptimizerConfig(n_c=N_C, n_s=N_S, dims=DIMS, n_pit=100, grad_mode="exact",
                               grid_n=GRID_N, seed=0, perturbation=W["pert"],
                               attraction_tree_precision=W["att_prec"],
                               repulsion=spk.RepulsionConfig(backend="tree",
                                                             tree_precision=W["rep_prec"]))
     fld = spk.precompute_field(density())
-    pcfg = proj_config()
     t0 = time.perf_counter()
-    fld.source_tree()
-    from paper_2108_02991_b200 import tree as _tree
     fld.source_tree().static_proxies(_tree.auto_params(W["att_prec"], DIMS)[0])
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     run = engine.ShardedRun(np.ascontiguousarray(start_pattern().coords), cfg, fld)
-    run.project(pcfg)
-    eta0 = default_eta0(run.p, EPS_REP)
-    state = {"eta": eta0, "it": 0, "have": False}
-
-    def step():
-        state["it"] += 1
-        att, rep, bad, dots = run.evaluate()
-        if bad or not np.isfinite(att - rep):
-            raise RuntimeError("non-finite during bench")
-        state["eta"] = _bb_step(state["it"], state["eta"], dots[0], dots[1], state["have"],
-                                eta0, cfg.fixed_step_iters)
-        state["have"] = True
-        run.step_project(pcfg, state["eta"])
-        run.residual_max(pcfg)
-        return att - rep
-
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if use_dist:
-        dist.barrier()
-    _native.reset_launch_count()
-    times = []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            step()
-            e.record()
-            times.append((s, e))
-        torch.cuda.synchronize()
-    launches = _native.launch_count()
-    total_ms = sum(s.elapsed_time(e) for s, e in times)
-    if use_dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t[0])
+    run.project(proj_config())
+    step, _ = optimizer_step(run, cfg)
+    total_ms, clocks, launches = timed_loop(ctx, step, steps, warmup)
+    (total_ms,) = ctx.max(total_ms)
     p, g, rep_pairs, att_pairs = pairs_per_step()
-    s_it = total_ms / args.steps / 1e3
-    if rank == 0:
-        line = {
-            "metric": "s/iteration", "value": s_it, "unit": "s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_it * 1e3,
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
-            "config": workload_config() | {
-                "parallelism": f"shots sharded over {world} GPU(s)",
-                "workload": W["name"], "repulsion": f"tree, tree_precision {W['rep_prec']}",
-                "attraction": f"treecode, precision {W['att_prec']}"},
-            "equivalent_direct_pairs_per_s": (rep_pairs + att_pairs) / s_it,
-            "setup_s": {"lattice_tree_and_proxies": t_setup},
-            "roofline": None,
-            "roofline_note": "treecode lists vary per iteration; the kernel roofline is "
-                             "reported on the exact C2 line",
-            "clocks": clk.summary(), "gpu_launches": launches,
-        }
-        print(json.dumps(line), flush=True)
-    if use_dist:
-        dist.destroy_process_group()
+    s_it = total_ms / steps / 1e3
+    del run, fld
+    return {
+        "metric": "s/iteration", "value": s_it, "unit": "s", "n_gpus": ctx.world,
+        "steps": steps, "warmup": warmup, "ms_per_step": s_it * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
+        "config": workload_config(),
+        "parallelism": f"shots sharded over {ctx.world} GPU(s)",
+        "equivalent_direct_pairs_per_s": (rep_pairs + att_pairs) / s_it,
+        "setup_s": {"lattice_tree_and_proxies": t_setup},
+        "roofline": None,
+        "roofline_note": "treecode interaction lists change every iteration; the kernel "
+                         "roofline is reported on the exact lines",
+        "clocks": clocks, "gpu_launches": launches,
+    }
 
 
-def run_stack(args):
+# ---------------------------------------------------------------- our arm: C3 stack
+def measure_stack(args, ctx, steps, warmup):
     """C3: one stacked optimize iteration of G independent problems per step (1 GPU)."""
     import torch
 
@@ -538,7 +616,6 @@ def run_stack(args):
     from paper_2108_02991_b200 import _native, stack
     from paper_2108_02991_b200.optimizer import _bb_step, default_eta0
 
-    torch.cuda.set_device(0)
     G = W["stack"]
     cfg = spk.OptimizerConfig(n_c=N_C, n_s=N_S, dims=DIMS, n_pit=100, grad_mode="exact",
                               grid_n=GRID_N, seed=0, perturbation=W["pert"])
@@ -577,61 +654,41 @@ def run_stack(args):
         run.step_project(pcfg, st["etas"])
         run.residual_max(pcfg)
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    st["record"] = True
-    _native.reset_launch_count()
-    times = []
-    with ClockSampler(0) as clk:
-        for _ in range(args.steps):
-            flush.zero_()
-            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record()
-            step()
-            e0.record()
-            times.append((s0, e0))
-        torch.cuda.synchronize()
-    _native.call = orig_call
-    total_ms = sum(a.elapsed_time(b) for a, b in times)
+    def on_record():
+        st["record"] = True
+
+    try:
+        total_ms, clocks, launches = timed_loop(ctx, step, steps, warmup, on_record)
+    finally:
+        _native.call = orig_call
     nb_ms = float(np.mean([a.elapsed_time(b) for a, b in nb_events]))
     p, g, rep_pairs, att_pairs = pairs_per_step()
     pairs = G * (rep_pairs + att_pairs)
-    f_rep, f_att = FLOPS[DIMS]
-    peak, peak_mhz = measured_fp32_peak() if measured_fp32_peak()[0] else (
-        fp32_peak_tflops(1965.0), 1965.0)
-    achieved = G * (rep_pairs * f_rep + att_pairs * f_att) / (nb_ms / 1e3) / 1e12
-    bound_ms = G * (rep_pairs / (peak * 1e12 / f_rep) + att_pairs / sfu_pairs_per_s(peak_mhz)) * 1e3
-    line = {
-        "metric": METRIC, "value": pairs * args.steps / (total_ms / 1e3), "unit": "pairs/s",
-        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "s_per_iteration": total_ms / args.steps / 1e3,
+    return {
+        "metric": METRIC, "value": pairs * steps / (total_ms / 1e3), "unit": "pairs/s",
+        "n_gpus": 1, "steps": steps, "warmup": warmup,
+        "ms_per_step": total_ms / steps, "s_per_iteration": total_ms / steps / 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 pair math, f64 accumulation / projection", "data": "synthetic",
-        "config": workload_config() | {"stack": G, "parallelism": "one device batch"},
-        "roofline": {"bound": "fp32+sfu", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "launch_ms": nb_ms,
-                     "hw_bound_ms": bound_ms, "frac_of_hw_bound": bound_ms / nb_ms,
-                     "kernel": "nbody_kernel batched (spk_fused_sums_batched)"},
-        "clocks": clk.summary(), "gpu_launches": _native.launch_count(),
+        "config": workload_config(), "parallelism": "one device batch",
+        "roofline": nbody_roofline("c3", DIMS, G * rep_pairs, G * att_pairs, nb_ms, clocks)
+        | {"kernel": "nbody_kernel batched (spk_fused_sums_batched)"},
+        "clocks": clocks, "gpu_launches": launches,
     }
-    print(json.dumps(line), flush=True)
 
 
-def run_e2e_sharded(args, run, step, world):
+# ---------------------------------------------------------------- end to end
+def run_e2e_sharded(ctx, run, step, steps):
     """N > 1: the sharded optimize iteration with this rank's shots copied H2D from pinned
     host memory before, and the projected shots + scalars copied D2H after, every step
     (device-timed per step, max over ranks)."""
     import torch
-    import torch.distributed as dist
 
     host_in = torch.empty(run.coords.shape, dtype=torch.float64, pin_memory=True)
     host_in.copy_(run.coords)
     host_out = torch.empty_like(host_in, pin_memory=True)
-    steps = max(1, min(args.steps, args.e2e_steps))
     torch.cuda.synchronize()
-    dist.barrier()
+    ctx.barrier()
     total = 0.0
     for _ in range(steps):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -643,18 +700,17 @@ def run_e2e_sharded(args, run, step, world):
         torch.cuda.synchronize()
         total += s.elapsed_time(e)
         host_in.copy_(host_out)
-    t = torch.tensor([total], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    (total,) = ctx.max(total)
     p, g, rep_pairs, att_pairs = pairs_per_step()
     nbytes = host_in.numel() * 8
-    return {"value": (rep_pairs + att_pairs) * steps / (float(t[0]) / 1e3), "unit": "pairs/s",
-            "s_per_iteration": float(t[0]) / 1e3 / steps, "steps": steps,
-            "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world + 48,
+    return {"value": (rep_pairs + att_pairs) * steps / (total / 1e3), "unit": "pairs/s",
+            "s_per_iteration": total / 1e3 / steps, "steps": steps,
+            "h2d_bytes_per_step": nbytes * ctx.world, "d2h_bytes_per_step": nbytes * ctx.world + 48,
             "api": "sharded optimize iteration (engine.ShardedRun) with per-step pinned "
                    "H2D of every rank's shots and D2H of the projected shots"}
 
 
-def run_e2e(args, spk, fld, pcfg):
+def run_e2e(args, spk, fld, pcfg, steps):
     """The reference's loop body (optimizer.py:301-344) through the public API with numpy
     host arrays; every call copies its inputs H2D and results D2H."""
     import torch
@@ -665,7 +721,7 @@ def run_e2e(args, spk, fld, pcfg):
     eta0 = default_eta0(pattern.n_samples, EPS_REP)
     prev_c = prev_g = None
     eta = eta0
-    steps = max(1, min(args.steps, args.e2e_steps))
+    steps = max(1, min(steps, args.e2e_steps))
     bi = bo = 0
     nbytes = pattern.coords.nbytes
     for it in range(1, steps + 2):  # first iteration is warm-up
@@ -715,12 +771,13 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": s_it * 1e3, "s_per_iteration": s_it, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config() | {"parallelism": "host CPU threads"},
+        "config": workload_config(), "parallelism": f"{threads} host CPU threads",
         "cpu_baseline": {"value": rate, "unit": "pairs/s", "cores": threads, "kind": "port",
                          "cpu": cpu_model(),
                          "sample": f"per step {args.ref_rows} target rows x all {p} sources "
-                                   f"+ {args.ref_rows} rows x {g} grid cells, fp64, plus 16 "
-                                   f"shots of projection; s/iteration extrapolated"},
+                                   f"+ {args.ref_rows} rows x {g} grid cells, fp64, plus "
+                                   f"{samples[0]['proj_sample']} through the projection; "
+                                   f"s/iteration extrapolated"},
         "e2e": {"value": rate, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -735,20 +792,49 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-rows", type=int, default=16384)
     ap.add_argument("--ref-rows", type=int, default=2048)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true",
+                    help="skip the c4 / c4t sub-records of the default c2 run")
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     select_workload(args.config)
     if args.impl == "reference":
         run_reference(args)
-    elif W.get("stack"):
-        run_stack(args)
+        return
+    ensure_world(args)
+    ctx = Ctx()
+    from paper_2108_02991_b200 import _device
+
+    if W.get("stack"):
+        line = measure_stack(args, ctx, args.steps, args.warmup)
     elif W.get("tree"):
-        run_tree(args)
+        line = measure_tree(args, ctx, args.steps, args.warmup)
     else:
-        run_ours(args)
+        line = measure_exact(args, ctx, args.steps, args.warmup, not args.no_e2e,
+                             not args.no_cpu_baseline)
+    if args.config == "c2" and not args.no_sub:
+        line["subrecords"] = {}
+        for key, (k, w) in SUBRECORDS.items():
+            _device.release_workspaces()
+            select_workload(key)
+            k = args.steps if k is None else min(k, args.steps)
+            w = args.warmup if w is None else w
+            t0 = time.perf_counter()
+            if W.get("tree"):
+                rec = measure_tree(args, ctx, k, w)
+            else:
+                rec = measure_exact(args, ctx, k, w, False, not args.no_cpu_baseline)
+            rec["wall_s"] = time.perf_counter() - t0
+            line["subrecords"][key] = rec
+            if ctx.rank == 0:
+                print(f"bench.py: {key}: {rec['ms_per_step'] / 1e3:.3f} s/it "
+                      f"({rec['wall_s']:.0f} s wall)", file=sys.stderr, flush=True)
+        select_workload(args.config)
+    if ctx.rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
 
 
 if __name__ == "__main__":

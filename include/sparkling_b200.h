@@ -238,8 +238,9 @@ int spk_tree_node_boxes(const void* rec, int64_t n_nodes, const int32_t* first_c
  * nodes with more than m = order^dims particles become proxy slots (node order), other
  * far nodes and opened leaves contribute their particle ranges (contiguous ranges merge).
  * Count pass: slot_of/slot_node [n_nodes] i32, slot_box [n_nodes][6] f32 (center, half),
- * slot_unit_off [n_nodes + 1] i64, seg_off [n_groups + 1] i64, totals [3] i64 = segments,
- * slots, P2M units (device).  Write pass fills seg_start/seg_count and the P2M units.
+ * slot_unit_off [n_nodes + 1] i64, seg_off [n_groups + 1] i64, totals [4] i64 = segments,
+ * slots, P2M units, traversal-stack overflows (device; the lists are invalid unless
+ * totals[3] == 0 -- the Python wrapper raises).  Write pass fills seg_start/seg_count and the P2M units.
  * Optional far level: parent_box [n_parents][6] and group_parent [n_groups]; nodes far
  * from a group's parent (same opening test) are skipped -- the parent's P2L/L2P covers
  * them; far_only = 1 emits far nodes only (the parents' own walk, for their P2L). */

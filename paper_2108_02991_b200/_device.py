@@ -67,3 +67,10 @@ def pack_positions(coords: torch.Tensor, out: torch.Tensor | None = None) -> tor
         out = torch.empty((p, 4), dtype=torch.float32, device=coords.device)
     _native.call("spk_pack_positions", ptr(coords), p, d, ptr(out), stream())
     return out
+
+
+def release_workspaces() -> None:
+    """Drop the cached workspaces (e.g. between problem sizes in one process)."""
+    _WS.clear()
+    if torch.cuda.is_available():
+        torch.cuda.empty_cache()

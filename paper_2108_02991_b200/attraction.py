@@ -221,13 +221,16 @@ def grid_sums_device(tgt4, field: "KernelField", eps2, val=None, grad=None):
     return val, grad
 
 
-def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg=None):
+def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg=None,
+                          row_cache: dict | None = None):
     """Treecode approximation of :func:`grid_sums_device` (tree.py) within ``precision``
     relative error of the cost and of the gradient l2 norm: the density lattice is a
     static weighted source set, so its octree and the Chebyshev proxies of every node are
     built once per field and reused every iteration; per call only the targets are
     sorted and the interaction lists rebuilt.  ``tg``: precomputed tree.TargetGroups of
-    the same targets (shared with a treecode repulsion)."""
+    the same targets (shared with a treecode repulsion).  ``row_cache`` (the run's, see
+    engine.CudaOps): reuse the probe-validated table row, re-probing every
+    ``tree.REPROBE_EVERY`` calls; without it every call probes."""
     from . import tree
 
     params = tree.auto_params(precision, field.dims)
@@ -238,12 +241,13 @@ def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg
     # treecode repulsion's auto mode; a random sweep found clustered targets on a sharp
     # density reaching 2.2e-5 at the 1e-5 row, scripts/att_tree_fuzz_many.py).  A probe of
     # 64 targets against the whole lattice costs ~20-40 ms at C4 (the K2 kernel is built
-    # for thousands of targets), so the validated row is cached per (target count,
-    # precision) and the probe runs on the first call of each -- once per optimizer level.
-    key = ("tree_row", tgt4.shape[0], precision)
-    k = field._dev.get(key)
-    probe = k is None
-    if probe:
+    # for thousands of targets), so inside optimize() the validated row is kept on the
+    # run's cache (never on the field, which callers reuse across runs) and re-probed every
+    # tree.REPROBE_EVERY calls.
+    key = ("att", tgt4.shape[0], precision)
+    k, reprobe = tree.cached_row(row_cache, key)
+    probe = k is None or reprobe
+    if k is None:
         k = next(i for i, r in enumerate(rows) if precision >= r[0])
     if k >= len(rows):
         return grid_sums_device(tgt4, field, eps2)
@@ -261,14 +265,14 @@ def tree_grid_sums_device(tgt4, field: "KernelField", eps2, precision: float, tg
         if k >= len(rows):
             warnings.warn(f"lattice treecode reached relative error {err:.2e} > {precision:.2e} "
                           f"on the probe at every table row; using exact sums")
-            field._dev[key] = k
+            tree.store_row(row_cache, key, k)
             return grid_sums_device(tgt4, field, eps2)
         _, order, theta = rows[k]
         warnings.warn(f"lattice treecode reached relative error {err:.2e} > {precision:.2e} on "
                       f"the probe; tightening to interp_order={order}, theta={theta}")
         val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=True, far=False)
         err = _probe_grid_error(tgt4, field, eps2, val, grad)
-    field._dev[key] = k
+    tree.store_row(row_cache, key, k)
     return val, grad
 
 

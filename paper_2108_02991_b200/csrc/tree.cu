@@ -436,8 +436,14 @@ struct TravParams {
     const float* pbox;         // optional far-level parents: [n_parents][6]
     const int32_t* gparent;    // group -> parent
     int far_only;              // parents' own walk: emit far nodes only (no near leaves)
+    unsigned long long* overflow;  // pass 0: groups whose walk overflowed the stack
 };
-constexpr int TR_STACK = 224;  // >= 31 levels x 7 pending siblings + 1
+// Stack bound: a depth-first walk holds at most (children - 1) pending siblings per level
+// plus the current node.  Keys have 21 bits per axis in 3D (21 levels of 8 children) and
+// 31 in 2D (31 levels of 4 children).
+constexpr int TR_STACK = 224;
+static_assert(TR_STACK >= 21 * 7 + 1 && TR_STACK >= 31 * 3 + 1,
+              "traversal stack too small for the Morton key depth");
 
 // One thread per target group walks the source octree (dual_traverse's opening test,
 // _treecode.py:173-244, applied group-to-node).  Pass 0 counts segments and flags proxy
@@ -494,7 +500,10 @@ __global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
             free_sub = pb.r >= __fmul_rn(P.theta, __fadd_rn(__fsqrt_rn(pd2), sb.r));
             if (!free_sub && P.nchild[v] != 0) {
                 const int nc = P.nchild[v];
-                if (sp + nc > TR_STACK) continue;
+                if (sp + nc > TR_STACK) {  // cannot happen within the key depth (above)
+                    if (PASS == 0) atomicAdd(P.overflow, 1ULL);
+                    continue;
+                }
                 for (int c = nc - 1; c >= 0; --c) stk[sp++] = P.fchild[v] + c;
                 continue;
             }
@@ -522,7 +531,10 @@ __global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
             }
         } else {
             const int nc = P.nchild[v];
-            if (sp + nc > TR_STACK) continue;  // unreachable for <= 31 levels
+            if (sp + nc > TR_STACK) {  // cannot happen within the key depth (above)
+                if (PASS == 0) atomicAdd(P.overflow, 1ULL);
+                continue;
+            }
             const int32_t flag = free_sub ? FREE : 0;
             for (int c = nc - 1; c >= 0; --c) stk[sp++] = (P.fchild[v] + c) | flag;
         }
@@ -579,6 +591,7 @@ __global__ void totals_kernel(const long long* __restrict__ seg_off, long long n
     totals[0] = seg_off[n_groups];
     totals[1] = (long long)slot_of[n_nodes - 1] + is_proxy[n_nodes - 1];
     totals[2] = slot_unit_off[n_nodes];  // units_per_slot is zero past the last slot
+    // totals[3]: stack overflows counted by the traversal (the caller fails on nonzero)
 }
 
 
@@ -1061,6 +1074,8 @@ int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
     P.pbox = parent_box;
     P.gparent = group_parent;
     P.far_only = far_only;
+    P.overflow = reinterpret_cast<unsigned long long*>(totals + 3);
+    cudaMemsetAsync(totals + 3, 0, sizeof(int64_t), s);
     traverse_kernel<0><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
     SPK_CHECK_LAUNCH("spk_tree_plan_count(traverse)");
     size_t t = cub_bytes;

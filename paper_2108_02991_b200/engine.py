@@ -33,7 +33,8 @@ class CudaOps:
 
     def __init__(self):
         self.device = _device.device()
-        self._tree_rows = {}  # treecode auto-mode rows validated by the probe (per level)
+        # treecode auto-mode rows validated by the probe (repulsion and lattice), per run
+        self._tree_rows = {}
 
     def empty(self, shape, dtype=torch.float64):
         return torch.empty(shape, dtype=dtype, device=self.device)
@@ -61,7 +62,8 @@ class CudaOps:
                 vr, gr = direct_sums_device(tgt4, src4, d, eps2_rep)
             if att_tree:
                 va, ga = tree_grid_sums_device(tgt4, fld, fld.kernel_eps ** 2,
-                                               cfg.attraction_tree_precision, tg=tg)
+                                               cfg.attraction_tree_precision, tg=tg,
+                                               row_cache=self._tree_rows)
             elif cfg.grad_mode == "exact":
                 va, ga = grid_sums_device(tgt4, fld, fld.kernel_eps ** 2)
             else:
@@ -125,6 +127,11 @@ class ShardedRun:
         self.world = dist.get_world_size(group) if group is not None else 1
         self.rank = dist.get_rank(group) if group is not None else 0
         n_c, n_s, d = start.shape
+        if n_c < self.world:
+            # every rank must own at least one shot: the kernels need targets, and a rank
+            # without any would fail while the others wait in the collectives
+            raise ValueError(f"{n_c} shots cannot be sharded over {self.world} ranks; "
+                             f"use at most {n_c} ranks")
         base, extra = divmod(n_c, self.world)
         self.counts = [base + (1 if r < extra else 0) for r in range(self.world)]
         self.offsets = [sum(self.counts[:r]) for r in range(self.world)]
@@ -209,8 +216,10 @@ class ShardedRun:
         return att_cost, rep_cost, int(tot[4]), (float(tot[2]), float(tot[3]))
 
     def set_host_gradient(self, grad: np.ndarray):
-        """Patched-evaluator path (single rank): install a host gradient, return the BB
-        dot products computed with numpy exactly as step_size does."""
+        """Patched-evaluator path: install a host gradient of ALL shots (every rank
+        evaluates the same gathered pattern), keep this rank's rows, and return the BB
+        dot products computed with numpy over the whole pattern exactly as step_size
+        does (identical on every rank)."""
         coords = self.gather_coords()
         dots = (0.0, 0.0)
         if self.host_prev is not None:
@@ -219,7 +228,9 @@ class ShardedRun:
             dg = grad - pg
             dots = (float(np.vdot(dk, dg)), float(np.vdot(dg, dg)))
         self.host_prev = (coords.copy(), grad)
-        self.grad.copy_(torch.from_numpy(np.ascontiguousarray(grad, dtype=np.float64)))
+        lo = self.offsets[self.rank]
+        mine = np.ascontiguousarray(grad[lo:lo + self.local], dtype=np.float64)
+        self.grad.copy_(torch.from_numpy(mine))
         return dots
 
     def step_project(self, proj_cfg, eta: float) -> bool:

@@ -31,7 +31,13 @@ MAX_INTERP_ORDER = 8
 
 @dataclass
 class RepulsionConfig:
-    """Same fields and validation as the reference (repulsion.py:33-60)."""
+    """Same fields and validation as the reference (repulsion.py:33-60).
+
+    ``backend="tree"`` meets ``tree_precision`` (relative error of the cost and of the
+    gradient l2 norm) as checked by a 64-target probe against the exact kernel: on every
+    call through the public API, and inside ``optimize`` on the first call of a level and
+    then every ``tree.REPROBE_EVERY`` iterations (between probes the validated row is
+    trusted, as the reference trusts its table)."""
 
     kernel_eps: float = 1e-3
     backend: str = "direct"
@@ -119,8 +125,9 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
     escalation and direct fallback (repulsion.py:165-200).  With ``return_groups`` also
     returns the target groups (tree.TargetGroups, or None on the direct path) so that a
     treecode attraction can reuse the targets' sort.  ``row_cache`` (the optimizer's):
-    the auto-mode probe runs once per (sizes, precision) and its validated table row is
-    reused -- once per optimizer level instead of every iteration."""
+    the auto-mode probe runs on the first call per (sizes, precision) and its validated
+    table row is reused, with a re-probe every ``tree.REPROBE_EVERY`` calls (the points
+    move within a level); without a cache (the public API) every call probes."""
     eps2 = cfg.kernel_eps * cfg.kernel_eps
     params = tree.auto_params(cfg.tree_precision, dims)
     n_src = src4.shape[0]
@@ -133,8 +140,9 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
         return done(*direct_sums_device(tgt4, src4, dims, eps2))
     auto_order, theta = params
     rows = tree.AUTO_PARAMS_2D if dims == 2 else tree.AUTO_PARAMS
-    ckey = (tgt4.shape[0], n_src, dims, cfg.tree_precision)
-    cached = None if row_cache is None or cfg.interp_order is not None else row_cache.get(ckey)
+    ckey = ("rep", tgt4.shape[0], n_src, dims, cfg.tree_precision)
+    cached, reprobe = (None, False) if cfg.interp_order is not None else \
+        tree.cached_row(row_cache, ckey)
     if cached is not None:
         if cached >= len(rows):
             return done(*direct_sums_device(tgt4, src4, dims, eps2))
@@ -146,13 +154,15 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
     tg = tree.TargetGroups(tgt4, dims, same_as=src if same else None, parent_cap=cap)
     # the far level needs every node's proxies (static), the plain walk builds its own
     val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
-    if cfg.interp_order is None and cached is None:
+    if cfg.interp_order is None and (cached is None or reprobe):
         # Extension of the reference (which trusts its table in auto mode): the same
         # 64-target probe, and on a miss the next stricter (order, theta) row, then the
         # exact kernel.  The table is calibrated on SPARKLING-like, uniform and radial
         # clouds; dense blobs whose sub-boxes all sit at the opening ratio can exceed it
-        # (profiles/r01_tree_fuzz_sweep.txt).
-        k = next(i for i, r in enumerate(rows) if cfg.tree_precision >= r[0])
+        # (profiles/r01_tree_fuzz_sweep.txt).  Inside optimize() the validated row is
+        # re-probed every tree.REPROBE_EVERY calls, starting from that row.
+        k = cached if reprobe else next(i for i, r in enumerate(rows)
+                                        if cfg.tree_precision >= r[0])
         err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         while max(err_val, err_grad) > cfg.tree_precision:
             k += 1
@@ -161,8 +171,7 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
                     f"tree backend (auto) reached relative error {max(err_val, err_grad):.2e}"
                     f" > {cfg.tree_precision:.2e} on the probe at every table row; falling "
                     f"back to direct summation")
-                if row_cache is not None:
-                    row_cache[ckey] = k
+                tree.store_row(row_cache, ckey, k)
                 return done(*direct_sums_device(tgt4, src4, dims, eps2), tg)
             _, order, theta = rows[k]
             warnings.warn(
@@ -171,8 +180,7 @@ def tree_sums_checked(tgt4, src4, dims: int, cfg: RepulsionConfig, *,
                 f"theta={theta}")
             val, grad = tree.tree_eval(tg, src, order, theta, eps2, static=cap is not None)
             err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
-        if row_cache is not None:
-            row_cache[ckey] = k
+        tree.store_row(row_cache, ckey, k)
     if cfg.interp_order is not None:
         err_val, err_grad = _probe_error(tgt4, src4, dims, eps2, val, grad)
         while max(err_val, err_grad) > cfg.tree_precision and order < MAX_INTERP_ORDER:

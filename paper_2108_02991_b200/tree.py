@@ -14,7 +14,7 @@ out for the B200 (csrc/tree.cu, csrc/tree_host.cpp):
   3. GPU: tight node boxes (leaves reduce, levels merge bottom-up) and group boxes.
   4. GPU: one thread per target group walks the octree -> segments of near particles and
      of far-node proxies (q^d tensor Chebyshev points on the node's box); count pass,
-     one 24-byte read-back of the totals, write pass.
+     one 32-byte read-back of the totals, write pass.
   5. GPU: P2M proxy weights; one warp per target group (<= 64 targets) sums the weighted
      kernel over its segments (packed f32x2 FMA + MUFU.RSQ, fp64 accumulation per
      256-record batch).
@@ -52,6 +52,30 @@ LEAF_CAP = 256  # source particles per octree leaf
 # At or below this many sources the exact kernel is faster than building and walking a
 # tree on the B200 (C1 32k: 0.4 vs 1.0 ms; 65k: 1.7 vs 2.5 ms; 1M: 362 vs 19 ms).
 DIRECT_BELOW = 1 << 17
+# Auto-mode probe cadence inside optimize(): a table row validated by the 64-target probe
+# is reused for this many calls with the same sizes, then probed again (starting from the
+# validated row) because the points move and can cluster within a level.
+REPROBE_EVERY = 10
+
+
+def cached_row(row_cache, key):
+    """(row, reprobe): the validated table row for ``key`` while it is fresh (row, False);
+    (row, True) when the re-probe is due (start probing at that row); (None, False) when
+    nothing is cached."""
+    if row_cache is None:
+        return None, False
+    entry = row_cache.get(key)
+    if entry is None:
+        return None, False
+    entry[1] += 1
+    if entry[1] < REPROBE_EVERY:
+        return entry[0], False
+    return entry[0], True
+
+
+def store_row(row_cache, key, row):
+    if row_cache is not None:
+        row_cache[key] = [row, 0]
 # Target octrees are split down to at least this level (cells of 1/16 of the domain):
 # sparse targets (coarse decimation levels) would otherwise form groups spanning whole
 # spokes, whose near field against the dense lattice is huge (131k targets against the
@@ -356,6 +380,13 @@ class TargetGroups:
                      self.d_ge.data_ptr(), dims, self.box.data_ptr(), st)
 
 
+def _check_overflow(n: int) -> None:
+    """The traversal stack bound holds for the Morton key depth (static_assert in
+    tree.cu); a nonzero count would mean dropped subtrees, so fail instead of summing."""
+    if n:
+        raise _native.NativeError(f"tree plan: traversal stack overflow in {n} walks")
+
+
 def _static_plan(src: SourceTree, boxes: torch.Tensor, n_groups: int, theta: float,
                  order: int, slot_of: torch.Tensor, pbox=None, gparent=None, far_only=False):
     """Interaction lists against the source tree's static (all-node) proxies."""
@@ -367,7 +398,7 @@ def _static_plan(src: SourceTree, boxes: torch.Tensor, n_groups: int, theta: flo
     tmp_b = torch.empty((n_nodes, 6), dtype=torch.float32, device=dev)
     tmp_u = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
     seg_off = torch.empty(n_groups + 1, dtype=torch.int64, device=dev)
-    totals = torch.empty(3, dtype=torch.int64, device=dev)
+    totals = torch.empty(4, dtype=torch.int64, device=dev)
     ws = _device.workspace(_native.query("spk_tree_plan_workspace_bytes", n_nodes, n_groups),
                            "tree_plan")
     args = (src.d_nb.data_ptr(), src.d_ne.data_ptr(), src.d_fc.data_ptr(), src.d_nc.data_ptr(),
@@ -377,7 +408,8 @@ def _static_plan(src: SourceTree, boxes: torch.Tensor, n_groups: int, theta: flo
                  tmp_b.data_ptr(), tmp_u.data_ptr(), seg_off.data_ptr(), totals.data_ptr(),
                  _device.ptr(pbox), _device.ptr(gparent), int(far_only), ws.data_ptr(),
                  ws.numel(), st)
-    n_seg = int(totals[0].item())
+    n_seg, _, _, overflow = (int(x) for x in totals.cpu().numpy())
+    _check_overflow(overflow)
     seg_start = torch.empty(max(n_seg, 1), dtype=torch.int64, device=dev)
     seg_count = torch.empty(max(n_seg, 1), dtype=torch.int32, device=dev)
     _native.call("spk_tree_plan_write", *args, slot_of.data_ptr(), tmp_n.data_ptr(),
@@ -451,7 +483,7 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
     slot_box = torch.empty((n_nodes, 6), dtype=torch.float32, device=dev)
     slot_unit_off = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
     seg_off = torch.empty(n_groups + 1, dtype=torch.int64, device=dev)
-    totals = torch.empty(3, dtype=torch.int64, device=dev)
+    totals = torch.empty(4, dtype=torch.int64, device=dev)
     ws = _device.workspace(_native.query("spk_tree_plan_workspace_bytes", n_nodes, n_groups),
                            "tree_plan")
     _native.call("spk_tree_plan_count", src.d_nb.data_ptr(), src.d_ne.data_ptr(),
@@ -460,7 +492,8 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  slot_of.data_ptr(), slot_node.data_ptr(), slot_box.data_ptr(),
                  slot_unit_off.data_ptr(), seg_off.data_ptr(), totals.data_ptr(), None, None,
                  0, ws.data_ptr(), ws.numel(), st)
-    n_seg, n_slots, n_units = (int(x) for x in totals.cpu().numpy())
+    n_seg, n_slots, n_units, overflow = (int(x) for x in totals.cpu().numpy())
+    _check_overflow(overflow)
     mark("plan_count")
     if static:
         rec, write_slot_of = src.static_proxies(order)

@@ -1,0 +1,115 @@
+"""Per-rank share of one optimizer iteration at N = 2, 4, 8 ranks, timed on ONE B200.
+
+With shots sharded contiguously (engine.ShardedRun), rank r of N evaluates its own
+targets against ALL sources (fused K1 + K2), combines, and projects its own shots; the
+ranks then meet in the position all-gather.  So the N-rank iteration takes
+max_r (sums_r + combine_r + project_r + residuals_r) + all-gather.  This script brings a
+single-GPU run to the in-loop state (bench.py's 5 warm-up iterations), then times every
+rank's share of the next iterations in isolation on the same device and reports the
+projected strong-scaling efficiency t_1 / (N t_N).  The all-gather (16 B per sample over
+NVLink 5, 16 MiB at C2) is added as an estimate at 600 GB/s.
+
+    python scripts/rank_share.py [--config c2|c4] [--iters 3] > profiles/r02_rank_share_c2.jsonl
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+import bench  # noqa: E402
+import paper_2108_02991_b200 as spk  # noqa: E402
+from paper_2108_02991_b200 import engine  # noqa: E402
+from paper_2108_02991_b200.optimizer import _bb_step  # noqa: E402
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--ranks", default="1,2,4,8")
+    args = ap.parse_args()
+    bench.select_workload(args.config)
+    cfg = spk.OptimizerConfig(n_c=bench.N_C, n_s=bench.N_S, dims=bench.DIMS, n_pit=100,
+                              grad_mode="exact", grid_n=bench.GRID_N, seed=0,
+                              perturbation=bench.W["pert"])
+    fld = spk.precompute_field(bench.density())
+    pcfg = bench.proj_config()
+    run = engine.ShardedRun(np.ascontiguousarray(bench.start_pattern().coords), cfg, fld)
+    run.project(pcfg)
+    step, state = bench.optimizer_step(run, cfg)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ops, ns, d = run.ops, run.n_s, run.d
+    worlds = [int(x) for x in args.ranks.split(",")]
+    rows = {n: [] for n in worlds}
+    for it in range(args.iters):
+        # this iteration's step size, from the full evaluation (as every rank would get)
+        state["it"] += 1
+        att, rep, bad, dots = run.evaluate()
+        eta = _bb_step(state["it"], state["eta"], dots[0], dots[1], state["have"],
+                       state["eta0"], cfg.fixed_step_iters)
+        for n in worlds:
+            base, extra = divmod(bench.N_C, n)
+            counts = [base + (1 if r < extra else 0) for r in range(n)]
+            offs = [sum(counts[:r]) for r in range(n)]
+            per = []
+            for r in range(n):
+                lo, cnt = offs[r], counts[r]
+                coords = run.coords[lo:lo + cnt]
+                tgt = run.pos4_all[lo * ns:(lo + cnt) * ns]
+                grad = torch.empty((cnt, ns, d), dtype=torch.float64, device="cuda")
+                out = torch.empty_like(grad)
+                pos4 = torch.empty((cnt * ns, 4), dtype=torch.float32, device="cuda")
+                flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+                e = [ev() for _ in range(4)]
+                torch.cuda.synchronize()
+                e[0].record()
+                va, ga, vr, gr = ops.sums(tgt, run.pos4_all, coords, fld, cfg)
+                ops.combine(va, ga, vr, gr, run.p, coords, None, None, grad.view(-1, d))
+                e[1].record()
+                sw = ops.project(coords, pcfg, grad, float(eta), out, pos4, flag)
+                e[2].record()
+                ops.residuals(out, pcfg)
+                e[3].record()
+                torch.cuda.synchronize()
+                per.append({"rank": r, "shots": cnt, "sums_ms": e[0].elapsed_time(e[1]),
+                            "project_ms": e[1].elapsed_time(e[2]),
+                            "residual_ms": e[2].elapsed_time(e[3])})
+            gather_ms = 16.0 * bench.N_C * ns * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
+            tot = [p["sums_ms"] + p["project_ms"] + p["residual_ms"] for p in per]
+            rows[n].append({"iteration": state["it"], "eta": eta, "max_rank_ms": max(tot),
+                            "allgather_est_ms": gather_ms,
+                            "step_ms": max(tot) + gather_ms,
+                            "max_sums_ms": max(p["sums_ms"] for p in per),
+                            "max_project_ms": max(p["project_ms"] for p in per),
+                            "ranks": per})
+        # advance the real single-GPU run by this iteration
+        state["eta"] = eta
+        state["have"] = True
+        run.step_project(pcfg, eta)
+        run.residual_max(pcfg)
+    t1 = np.mean([x["step_ms"] for x in rows[1]]) if 1 in rows else None
+    for n in worlds:
+        tn = float(np.mean([x["step_ms"] for x in rows[n]]))
+        rec = {"config": args.config, "n_ranks": n, "step_ms": tn,
+               "sums_ms": float(np.mean([x["max_sums_ms"] for x in rows[n]])),
+               "project_ms": float(np.mean([x["max_project_ms"] for x in rows[n]])),
+               "efficiency": (t1 / (n * tn)) if t1 else None,
+               "iterations": rows[n]}
+        print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()

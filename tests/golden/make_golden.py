@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -286,6 +287,98 @@ def optimize_fixture():
     np.savez_compressed(os.path.join(OUT, "optimize.npz"), **out)
 
 
+# ---------------------------------------------------------------------------- trajectories
+# End-to-end trajectories of the reference's own ``optimize`` (optimizer.py:239-349) at
+# BASELINE configs[0] (C1: 2D, 64 shots x 512 samples, 257^2 density grid) and on a reduced
+# 3D multi-resolution schedule, for tests/test_gpu_trajectory.py.  Each case also records
+# the reference's OWN sensitivity: the same run with 1e-6 relative noise injected into its
+# repulsion gradient (the size of the fp32 pair-sum error of the GPU kernels), three noise
+# seeds; the test bounds the GPU drift against that.
+
+sys.path.insert(0, os.path.dirname(OUT))
+import trajectory_cases as _tc  # noqa: E402  (the case table, shared with the GPU tests)
+
+TRAJ_CASES = _tc.CASES
+TRAJ_NOISE = _tc.NOISE
+TRAJ_NOISE_SEEDS = _tc.NOISE_SEEDS
+
+
+def _run_reference(cfg_kw, hw_kw, patched_exact, noise_seed=None):
+    """One reference optimize; returns (per-level final coords, trace arrays)."""
+    from vdtraj import repulsion as rp
+
+    repo = os.path.dirname(os.path.dirname(OUT))
+    sys.path.insert(0, repo)
+    from oracle import oracle as orc
+
+    hw = core.HardwareSpec(**_tc.hardware_kwargs(hw_kw))
+    cfg = om.OptimizerConfig(repulsion=om.RepulsionConfig(backend="direct"), **cfg_kw)
+    levels = []
+    saved = (om.eval_attraction, om.eval_repulsion, om.upsample_shots)
+
+    def capture_upsample(k):
+        levels.append(k.coords.copy())
+        return saved[2](k)
+
+    om.upsample_shots = capture_upsample
+    if patched_exact:
+        def exact_attraction(k, fld, grad_mode="consistent"):
+            cost, grad = orc.attraction_exact(k.points(), fld_holder["rho"].grid,
+                                              fld.kernel_eps)
+            n_out = int(np.count_nonzero((np.abs(k.points()) > 1.0).any(axis=1)))
+            return at.AttractionResult(cost=cost, grad=grad, n_clamped=n_out)
+        om.eval_attraction = exact_attraction
+    if noise_seed is not None:
+        rng = np.random.default_rng(noise_seed)
+
+        def noisy(k, c):
+            cost, g = rp.eval_repulsion(k, c)
+            return (cost * (1 + 0.1 * TRAJ_NOISE * rng.standard_normal()),
+                    g * (1 + TRAJ_NOISE * rng.standard_normal(g.shape)))
+        om.eval_repulsion = noisy
+    fld_holder = {}
+    try:
+        rho = density.discretize(cfg.density, cfg.grid_n, cfg.dims)
+        fld_holder["rho"] = rho
+        res = om.optimize(cfg, hw, rho=rho)
+    finally:
+        om.eval_attraction, om.eval_repulsion, om.upsample_shots = saved
+    levels.append(res.pattern.coords.copy())
+    recs = res.trace.records
+    trace = {k: np.array([getattr(r, k) for r in recs])
+             for k in ("level", "cost", "attraction", "repulsion", "step", "feas_residual")}
+    return levels, trace
+
+
+def trajectory_fixtures():
+    out = {}
+    for name, (cfg_kw, hw_kw, patched) in TRAJ_CASES.items():
+        t0 = time.perf_counter()
+        levels, trace = _run_reference(cfg_kw, hw_kw, patched)
+        for li, c in enumerate(levels):
+            out[f"{name}_level{li}"] = c
+        for k, v in trace.items():
+            out[f"{name}_{k}"] = v
+        # the reference's own drift under 1e-6 relative repulsion-gradient noise
+        nd = np.zeros((len(TRAJ_NOISE_SEEDS), len(levels)))
+        nl2 = np.zeros_like(nd)
+        ncost = np.zeros(len(TRAJ_NOISE_SEEDS))
+        for si, s in enumerate(TRAJ_NOISE_SEEDS):
+            nlev, ntr = _run_reference(cfg_kw, hw_kw, patched, noise_seed=s)
+            for li, (a, b) in enumerate(zip(nlev, levels)):
+                nd[si, li] = np.abs(a - b).max()
+                nl2[si, li] = np.linalg.norm(a - b) / np.linalg.norm(b)
+            ncost[si] = np.abs(ntr["cost"] - trace["cost"]).max() / np.abs(trace["cost"]).max()
+        out[f"{name}_noise_max"] = nd.max(axis=0)
+        out[f"{name}_noise_rel_l2"] = nl2.max(axis=0)
+        out[f"{name}_noise_cost_rel"] = np.float64(ncost.max())
+        print(f"{name}: {time.perf_counter() - t0:.1f} s; noise drift per level "
+              f"{nd.max(axis=0)}, cost {ncost.max():.2e}", flush=True)
+    out["names"] = np.array(list(TRAJ_CASES))
+    out["noise"] = np.float64(TRAJ_NOISE)
+    np.savez_compressed(os.path.join(OUT, "trajectory.npz"), **out)
+
+
 def analysis_fixtures():
     """NUDFT adjoint / forward, density compensation, PSF + metrics, dwell resampling and
     density compliance (analysis.py, core.py:286-311)."""
@@ -366,7 +459,7 @@ def analysis_fixtures():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["repulsion", "attraction", "projection", "host", "optimize",
-                             "analysis"]
+                             "analysis", "trajectory"]
     if "repulsion" in which:
         repulsion_fixtures()
     if "attraction" in which:
@@ -379,6 +472,8 @@ if __name__ == "__main__":
         optimize_fixture()
     if "analysis" in which:
         analysis_fixtures()
+    if "trajectory" in which:
+        trajectory_fixtures()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

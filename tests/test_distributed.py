@@ -77,3 +77,79 @@ def test_multilevel_ranks_match_one(tmp_path, world, n_c):
     assert np.allclose(got["costs"], single.trace.costs(), rtol=1e-12, atol=0)
     assert np.allclose(got["steps"], [r.step for r in single.trace.records], rtol=1e-9)
     assert np.abs(got["coords"] - single.pattern.coords).max() <= 1e-9
+
+
+def _worker_too_few(rank, world, port, out_dir):
+    from cpu_ops import OracleOps
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        try:
+            spk.optimize(_cfg(2, 0), _hw(), ops=OracleOps())
+            msg = "no error"
+        except ValueError as exc:
+            msg = str(exc)
+        with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as fh:
+            fh.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fewer_shots_than_ranks_raises_everywhere(tmp_path):
+    """2 shots over 3 ranks: every rank raises ValueError before any collective (no rank
+    waits in an all-gather for a rank that has no targets)."""
+    mp.spawn(_worker_too_few, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    for r in range(3):
+        msg = (tmp_path / f"r{r}.txt").read_text()
+        assert "cannot be sharded over 3 ranks" in msg, (r, msg)
+
+
+def _patched_attraction(k, fld, grad_mode="consistent"):
+    """A host evaluator in the reference's shape (what tests monkeypatch into
+    optimizer.eval_attraction, reference tests/test_optimizer.py:224): the fp64 exact sum."""
+    from oracle import oracle as orc
+
+    cost, grad = orc.attraction_exact(k.points(), fld.density.grid, fld.kernel_eps)
+    return spk.AttractionResult(cost=cost, grad=grad, n_clamped=0)
+
+
+def _patched_repulsion(k, cfg):
+    from oracle import oracle as orc
+
+    return orc.repulsion(k.points(), cfg.kernel_eps)
+
+
+def _worker_patched(rank, world, port, n_c, out_path):
+    from cpu_ops import OracleOps
+    import paper_2108_02991_b200.optimizer as om
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    om.eval_attraction = _patched_attraction
+    om.eval_repulsion = _patched_repulsion
+    try:
+        res = spk.optimize(_cfg(n_c), _hw(), ops=OracleOps())
+        if rank == 0:
+            np.savez(out_path, coords=res.pattern.coords, costs=res.trace.costs())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_patched_evaluator_two_ranks_match_one(tmp_path, monkeypatch):
+    """The patched-evaluator path (host gradient of the whole pattern) sharded over two
+    ranks keeps each rank's rows and reproduces the single-rank run."""
+    from cpu_ops import OracleOps
+    import paper_2108_02991_b200.optimizer as om
+
+    monkeypatch.setattr(om, "eval_attraction", _patched_attraction)
+    monkeypatch.setattr(om, "eval_repulsion", _patched_repulsion)
+    single = spk.optimize(_cfg(5), _hw(), ops=OracleOps())
+    monkeypatch.undo()
+    out = str(tmp_path / "p.npz")
+    mp.spawn(_worker_patched, args=(2, _free_port(), 5, out), nprocs=2, join=True)
+    got = np.load(out)
+    assert np.allclose(got["costs"], single.trace.costs(), rtol=1e-12, atol=0)
+    assert np.abs(got["coords"] - single.pattern.coords).max() <= 1e-9
