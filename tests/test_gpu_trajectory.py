@@ -28,8 +28,8 @@ pytestmark = pytest.mark.gpu
 # The GPU's perturbation is of the same size (fp32 pair sums, ~1e-6 relative) but not the
 # same distribution (it is correlated across iterations, where the injected noise is
 # not), so a small multiple is allowed.
-K_COORDS = 10.0
-K_COST = 10.0
+K_COORDS = 3.0
+K_COST = 3.0
 
 
 @pytest.fixture(scope="module")
