@@ -156,12 +156,6 @@ int spk_feasibility_residuals_batched(const double* coords, int64_t n_groups,
                                       double b, int pin_idx, const double* pin_val, double* out,
                                       void* ws, size_t ws_bytes, spk_stream_t stream);
 
-/* Self-test of the polish's certified fast sqrt / quotient (csrc/project.cu) against the
- * IEEE sqrt.rn / div.rn on n random cases.  counts (device uint64, 5): sqrt mismatches,
- * quotient mismatches (both 0 by construction), sqrt fallbacks, quotient fallbacks,
- * cases.  Test support; not part of the reference interface. */
-int spk_selftest_fastdiv(int64_t n, uint64_t seed, uint64_t* counts, spk_stream_t stream);
-
 /* upsample_shots (optimizer.py:183-199): (n_shots, n_s, d) -> (n_shots, 2 n_s, d). */
 int spk_upsample_shots(const double* in, double* out, int64_t n_shots, int n_s, int dims,
                        spk_stream_t stream);

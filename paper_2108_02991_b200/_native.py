@@ -58,7 +58,6 @@ SIGNATURES = {
     "spk_feasibility_residuals": (c_int, [c_vp, c_i64, c_int, c_int, c_dbl, c_dbl, c_int,
                                           ctypes.POINTER(c_dbl), c_vp, c_vp, c_size, c_vp]),
     "spk_upsample_shots": (c_int, [c_vp, c_vp, c_i64, c_int, c_int, c_vp]),
-    "spk_selftest_fastdiv": (c_int, [c_i64, ctypes.c_uint64, c_vp, c_vp]),
     "spk_field_eval": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_i64, c_int, c_vp, c_vp,
                                c_vp, c_vp]),
     "spk_tree_keys": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
@@ -118,7 +117,6 @@ LAUNCHES = {
     "spk_direct_sums": 2, "spk_grid_sums": 2, "spk_fused_sums": 3, "spk_pack_positions": 1,
     "spk_build_grid_sources": 1, "spk_combine_gradient": 2, "spk_project_all": 2,
     "spk_feasibility_residuals": 2, "spk_upsample_shots": 1, "spk_field_eval": 1,
-    "spk_selftest_fastdiv": 1,
     "spk_fused_sums_batched": 3, "spk_combine_gradient_batched": 2,
     "spk_feasibility_residuals_batched": 2,
     "spk_tree_keys": 1, "spk_tree_sort": 10, "spk_tree_gather": 1, "spk_tree_boxes": 1,

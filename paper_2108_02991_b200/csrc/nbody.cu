@@ -22,7 +22,6 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdarg>
-#include <cstdlib>
 #include <cstring>
 
 #include "spk_common.cuh"
@@ -98,19 +97,6 @@ __device__ __forceinline__ float rsqrt_sfu(float x) {
 
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-// 1/sqrt(x) without the SFU: integer seed (rel. error <= 1.8e-3) and two Newton steps
-// y <- y (1.5 - (x/2) y^2), 7 FP32 lane-ops + 2 integer ops; rel. error ~2e-7 after
-// rounding, like MUFU.RSQ.  Used for a fraction of the lattice pairs so that the FMA pipe
-// takes work off the (binding) SFU; normal x only (the guarded variant masks r2 below
-// FLT_MIN afterwards, as for the SFU path).
-__device__ __forceinline__ float rsqrt_fma(float x) {
-    const float h = 0.5f * x;
-    float y = __int_as_float(0x5f375a86 - (__float_as_int(x) >> 1));
-    y = y * fmaf(-h * y, y, 1.5f);
-    y = y * fmaf(-h * y, y, 1.5f);
-    return y;
-}
-
 // Positions tile against this thread's NB_TPT targets (difference form).
 // G: guard r2 below the fp32 normal range (eps2 < FLT_MIN, incl. eps = 0 => coincident
 // points contribute value 0, gradient 0, like the reference's `if h > 0` at
@@ -162,38 +148,7 @@ __device__ __forceinline__ void tile_positions(const float4* __restrict__ tile, 
 //     r2 = dl^2 + a,  winv = w / h,  v += r2 winv,  S += winv,  g_last += dl winv
 // then g_other += d_other * S at the end of the row.  6 FP32 lane-ops + 1 MUFU per pair
 // (the reference's algorithmic count stays 19 flops per pair).
-// One lattice cell (weight w, last-axis node coordinate l) against this thread's targets.
-// FMA: the first target's rsqrt of the last pair runs on the FMA pipe (rsqrt_fma).
-template <int D, bool G, bool FMA>
-__device__ __forceinline__ void lattice_cell(float w, float l, const float2 (&Y)[NB_PAIRS],
-                                             const float2 (&Z)[NB_PAIRS],
-                                             const float2 (&A)[NB_PAIRS],
-                                             float2 (&av)[NB_PAIRS], float2 (&ay)[NB_PAIRS],
-                                             float2 (&az)[NB_PAIRS], float2 (&Sw)[NB_PAIRS]) {
-    const float2 nl = bc(-l);
-#pragma unroll
-    for (int q = 0; q < NB_PAIRS; ++q) {
-        const float2 dl = __fadd2_rn(D == 3 ? Z[q] : Y[q], nl);
-        const float2 r2 = __ffma2_rn(dl, dl, A[q]);
-        float2 inv;
-        inv.x = (FMA && q == NB_PAIRS - 1) ? rsqrt_fma(r2.x) : rsqrt_sfu(r2.x);
-        inv.y = rsqrt_sfu(r2.y);
-        if (G) {
-            inv.x = r2.x >= FLT_MIN ? inv.x : 0.0f;  // rsqrt.approx.ftz flushes subnormal r2
-            inv.y = r2.y >= FLT_MIN ? inv.y : 0.0f;
-        }
-        const float2 winv = __fmul2_rn(inv, bc(w));
-        av[q] = __ffma2_rn(r2, winv, av[q]);
-        Sw[q] = __fadd2_rn(Sw[q], winv);
-        if (D == 3) az[q] = __ffma2_rn(dl, winv, az[q]);
-        else ay[q] = __ffma2_rn(dl, winv, ay[q]);
-    }
-}
-
-// OFF (0..4): number of every 4 consecutive cells in which one of the thread's 8 rsqrts
-// runs on the FMA pipe, i.e. OFF/32 of the lattice pairs (chosen by the host planner to
-// balance the FMA and SFU pipes, K1/K2).
-template <int D, bool G, int OFF>
+template <int D, bool G>
 __device__ __forceinline__ void tile_lattice(const float* __restrict__ tile, long long c0, int cnt,
                                              const SegDesc& S, const float* __restrict__ axes,
                                              const float2 (&X)[NB_PAIRS],
@@ -234,15 +189,28 @@ __device__ __forceinline__ void tile_lattice(const float* __restrict__ tile, lon
         }
         const float* wrow = tile + done;
         const float* lrow = AL + k;
-        int m = 0;
-        for (; m + 4 <= n_run; m += 4) {
-            lattice_cell<D, G, (0 < OFF)>(wrow[m], lrow[m], Y, Z, A, av, ay, az, Sw);
-            lattice_cell<D, G, (1 < OFF)>(wrow[m + 1], lrow[m + 1], Y, Z, A, av, ay, az, Sw);
-            lattice_cell<D, G, (2 < OFF)>(wrow[m + 2], lrow[m + 2], Y, Z, A, av, ay, az, Sw);
-            lattice_cell<D, G, (3 < OFF)>(wrow[m + 3], lrow[m + 3], Y, Z, A, av, ay, az, Sw);
+#pragma unroll 4
+        for (int m = 0; m < n_run; ++m) {
+            const float w = wrow[m];
+            const float2 nl = bc(-lrow[m]);
+#pragma unroll
+            for (int q = 0; q < NB_PAIRS; ++q) {
+                const float2 dl = __fadd2_rn(D == 3 ? Z[q] : Y[q], nl);
+                const float2 r2 = __ffma2_rn(dl, dl, A[q]);
+                float2 inv;
+                inv.x = rsqrt_sfu(r2.x);
+                inv.y = rsqrt_sfu(r2.y);
+                if (G) {
+                    inv.x = r2.x >= FLT_MIN ? inv.x : 0.0f;  // rsqrt.approx.ftz flushes subnormal r2
+                    inv.y = r2.y >= FLT_MIN ? inv.y : 0.0f;
+                }
+                const float2 winv = __fmul2_rn(inv, bc(w));
+                av[q] = __ffma2_rn(r2, winv, av[q]);
+                Sw[q] = __fadd2_rn(Sw[q], winv);
+                if (D == 3) az[q] = __ffma2_rn(dl, winv, az[q]);
+                else ay[q] = __ffma2_rn(dl, winv, ay[q]);
+            }
         }
-        for (; m < n_run; ++m)
-            lattice_cell<D, G, false>(wrow[m], lrow[m], Y, Z, A, av, ay, az, Sw);
 #pragma unroll
         for (int q = 0; q < NB_PAIRS; ++q) {
             ax[q] = __ffma2_rn(d0[q], Sw[q], ax[q]);
@@ -254,7 +222,7 @@ __device__ __forceinline__ void tile_lattice(const float* __restrict__ tile, lon
     }
 }
 
-template <int D, int KIND, bool G, int OFF>
+template <int D, int KIND, bool G>
 __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, long long t_end,
                                           char* stages, uint64_t* bars, const float* axes,
                                           const float2 (&X)[NB_PAIRS],
@@ -292,7 +260,7 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
             tile_positions<D, G>(reinterpret_cast<const float4*>(stages + stage * STAGE_BYTES),
                                  cnt, X, Y, Z, e2, av, ax, ay, az);
         else
-            tile_lattice<D, G, OFF>(reinterpret_cast<const float*>(stages + stage * STAGE_BYTES),
+            tile_lattice<D, G>(reinterpret_cast<const float*>(stages + stage * STAGE_BYTES),
                                t * TILE, cnt, S, axes, X, Y, Z, e2, av, ax, ay, az);
 #define NB_ACC(k, c) acc[((k) * 4 + (c)) * NB_THREADS + tid]
 #pragma unroll
@@ -313,7 +281,7 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
     }
 }
 
-template <int D, int OFF>
+template <int D>
 __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(const NBParams P) {
     extern __shared__ __align__(128) char stages[];
     double* acc = reinterpret_cast<double*>(stages + NB_TILE_BYTES);
@@ -376,11 +344,11 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(con
 
     const bool guard = !(S.eps2 >= FLT_MIN);
     if (S.kind == 1) {
-        if (guard) run_chunk<D, 1, true, OFF>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
-        else run_chunk<D, 1, false, OFF>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        if (guard) run_chunk<D, 1, true>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        else run_chunk<D, 1, false>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
     } else {
-        if (guard) run_chunk<D, 0, true, 0>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
-        else run_chunk<D, 0, false, 0>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        if (guard) run_chunk<D, 0, true>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
+        else run_chunk<D, 0, false>(Sg, t_begin, t_end, stages, bars, axes, X, Y, Z, acc);
     }
 
     double* slot = P.part + (size_t)chunk * 4 * P.n_tgt;
@@ -429,12 +397,11 @@ static int nbody_slots() {
     static int slots = 0;
     if (slots == 0) {
         int occ = 0;
-        for (auto f : {nbody_kernel<3, 0>, nbody_kernel<3, 1>, nbody_kernel<3, 2>,
-                       nbody_kernel<3, 3>, nbody_kernel<3, 4>, nbody_kernel<2, 0>,
-                       nbody_kernel<2, 1>, nbody_kernel<2, 2>, nbody_kernel<2, 3>,
-                       nbody_kernel<2, 4>})
-            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, NB_SMEM);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbody_kernel<3, 0>, NB_THREADS,
+        cudaFuncSetAttribute(nbody_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             NB_SMEM);
+        cudaFuncSetAttribute(nbody_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             NB_SMEM);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbody_kernel<3>, NB_THREADS,
                                                           NB_SMEM) != cudaSuccess ||
             occ <= 0) {
             cudaGetLastError();
@@ -449,22 +416,6 @@ static int nbody_slots() {
 // lane-ops, a lattice tile NB_TILE_W pairs bounded by the SFU (16 / clk / SM).
 constexpr double NB_COST_POS_TILE = NB_TILE / 12.8;
 constexpr double NB_COST_LAT_TILE = NB_TILE_W / 16.0;
-
-// Share of the lattice rsqrts evaluated on the FMA pipe, in 1/32 (0..4): balances the
-// pipes of the whole launch.  FMA lane-ops L = rep * {10, 7} + att * 6, SFU work M =
-// rep + att rsqrts; moving x rsqrts costs 7 lane-ops each, and the FMA pipe does ~8
-// lane-ops per MUFU.RSQ (124 vs 15.9 per clk per SM): x = (8 M - L) / (7 + 8).
-// SPK_NB_FMA_RSQRT=k forces k.
-static int fma_rsqrt_share(int dims, long long att_pairs, long long rep_pairs) {
-    if (const char* e = getenv("SPK_NB_FMA_RSQRT")) return std::max(0, std::min(4, atoi(e)));
-    if (att_pairs <= 0) return 0;
-    const double lane_rep = dims == 3 ? 10.0 : 7.0;
-    const double L = lane_rep * (double)rep_pairs + 6.0 * (double)att_pairs;
-    const double M = (double)rep_pairs + (double)att_pairs;
-    const double x = (8.0 * M - L) / 15.0;
-    if (x <= 0.0) return 0;
-    return (int)std::max(0L, std::min(4L, std::lround(32.0 * x / (double)att_pairs)));
-}
 
 // Choose the chunk counts: minimise (waves x longest unit) + per-unit overhead, with the
 // two segments split in proportion to their estimated cost.  seg0 is the lattice.
@@ -557,27 +508,10 @@ static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float
     P.part = static_cast<double*>(ws);
     const long long grid = pl.n_tb * (pl.nc0 + pl.nc1);
     nbody_slots();  // sets the shared-memory attribute once
-    const int off = fma_rsqrt_share(dims, n0 * n_tgt, n1 * n_tgt);
-#define NB_LAUNCH(DD, OO)                                                                  \
-    nbody_kernel<DD, OO><<<(unsigned)grid, NB_THREADS, NB_SMEM, stream>>>(P)
-    if (dims == 3) {
-        switch (off) {
-            case 0: NB_LAUNCH(3, 0); break;
-            case 1: NB_LAUNCH(3, 1); break;
-            case 2: NB_LAUNCH(3, 2); break;
-            case 3: NB_LAUNCH(3, 3); break;
-            default: NB_LAUNCH(3, 4); break;
-        }
-    } else {
-        switch (off) {
-            case 0: NB_LAUNCH(2, 0); break;
-            case 1: NB_LAUNCH(2, 1); break;
-            case 2: NB_LAUNCH(2, 2); break;
-            case 3: NB_LAUNCH(2, 3); break;
-            default: NB_LAUNCH(2, 4); break;
-        }
-    }
-#undef NB_LAUNCH
+    if (dims == 3)
+        nbody_kernel<3><<<(unsigned)grid, NB_THREADS, NB_SMEM, stream>>>(P);
+    else
+        nbody_kernel<2><<<(unsigned)grid, NB_THREADS, NB_SMEM, stream>>>(P);
     SPK_CHECK_LAUNCH("nbody_kernel");
     const unsigned fb = (unsigned)((n_tgt + 255) / 256);
     if (pl.nc0 > 0 && (val0 || grad0))

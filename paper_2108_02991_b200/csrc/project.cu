@@ -458,121 +458,6 @@ __device__ __forceinline__ void box_sample(Sample<D>& s, double& worst) {
     }
 }
 
-
-// ---------------------------------------------------- correctly rounded sqrt + quotient
-// The polish's active constraints need sqrt(nrm2) and a quotient by it, both IEEE
-// round-to-nearest (bit parity with numba).  The compiler's sqrt.rn / div.rn sequences
-// run one after the other (~90 + ~120 cycles of dependent latency on the ring's critical
-// path).  Here one reciprocal square root y ~ 1/sqrt(x) serves both:
-//   s  = RN(x y), s' = s + (x - s^2) y/2          (Markstein's correction, FMA)
-//   q0 = RN(n yd), q1 = q0 + (n - d q0) yd         (yd ~ 1/d from y)
-// and each result is CERTIFIED correctly rounded by its exact-ish residual: s' is
-// RN(sqrt x) iff |x - s'^2| < s' ulp(s'), q1 is RN(n/d) iff |n - d q1| < d ulp(q1)/2; the
-// tests accept only with a 2^-20 margin (the fma residual is itself rounded) and never
-// for a power-of-two result (whose lower neighbour is half an ulp away).  Anything not
-// certified -- or outside the normal range, NaN, inf -- falls back to the IEEE
-// instruction, so the outputs are bit-identical to sqrt.rn / div.rn by construction.
-__device__ __forceinline__ double ulp_of(double v) {
-    // 2^(E - 52) for a positive normal v (exact)
-    const long long e = __double_as_longlong(v) & 0x7ff0000000000000LL;
-    return __longlong_as_double(e - (52LL << 52));
-}
-
-__device__ __forceinline__ bool pow2_mantissa(double v) {
-    return (__double_as_longlong(v) & 0x000fffffffffffffLL) == 0;
-}
-
-// s = RN(sqrt(x)) and y ~ 1/sqrt(x) (relative error ~1 ulp); returns false when the fast
-// path did not certify s (the caller then uses IEEE sqrt and division).
-__device__ __forceinline__ bool sqrt_rcp_fast(double x, double& s, double& y) {
-    if (!(x >= 0x1p-900 && x <= 0x1p900)) return false;
-    double y0;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
-    const double y0sq = y0 * y0;
-    const double e = fma(-x, y0sq, 1.0);
-    const double c = fma(e, 0.375, 0.5);
-    const double ye = y0 * e;
-    y = fma(c, ye, y0);
-    const double s0 = x * y;
-    const double r = fma(-s0, s0, x);
-    s = fma(r, 0.5 * y, s0);
-    const double rs = fma(-s, s, x);
-    const double bound = s * ulp_of(s);
-    return fabs(rs) < bound * (1.0 - 0x1p-20) && !pow2_mantissa(s);
-}
-
-// q = RN(n / d) given yd ~ 1/d (a few ulps); false when not certified.
-__device__ __forceinline__ bool div_fast(double n, double d, double yd, double& q) {
-    const double q0 = n * yd;
-    const double r = fma(-d, q0, n);
-    q = fma(r, yd, q0);
-    const double r1 = fma(-d, q, n);
-    const double bound = d * (0.5 * ulp_of(q));
-    return fabs(r1) < bound * (1.0 - 0x1p-20) && !pow2_mantissa(q) && q >= 0x1p-900 &&
-           q <= 0x1p900;
-}
-
-#ifndef SPK_POLISH_FASTDIV
-#define SPK_POLISH_FASTDIV 1
-#endif
-
-
-// Self-test of the certified fast sqrt / quotient against the IEEE instructions on n
-// random cases (log-uniform magnitudes, near-square and near-midpoint inputs).  counts:
-// [0] sqrt mismatches, [1] quotient mismatches (both must be 0), [2] sqrt fallbacks,
-// [3] quotient fallbacks, [4] cases.
-__device__ __forceinline__ unsigned long long splitmix(unsigned long long& st) {
-    unsigned long long z = (st += 0x9e3779b97f4a7c15ULL);
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
-}
-
-__global__ void fastdiv_selftest_kernel(long long n, unsigned long long seed,
-                                        unsigned long long* counts) {
-    unsigned long long st = seed ^ (0x632be59bd9b4e019ULL * (blockIdx.x * 256ull + threadIdx.x));
-    unsigned long long c[5] = {0, 0, 0, 0, 0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const double u1 = (double)(splitmix(st) >> 11) * 0x1p-53;
-        const double u2 = (double)(splitmix(st) >> 11) * 0x1p-53;
-        const unsigned long long kind = splitmix(st) & 3;
-        double x = exp2(-40.0 + 60.0 * u1);
-        if (kind == 1) {
-            // near a perfect square of a short mantissa (exact squares and neighbours)
-            const double r = floor(exp2(10.0 + 20.0 * u2)) * 0x1p-20;
-            x = r * r;
-            const long long d = (long long)(splitmix(st) % 5) - 2;
-            x = __longlong_as_double(__double_as_longlong(x) + d);
-        }
-        const double a = sqrt(x) * (0.25 + 0.7499 * u2);  // active constraint: sqrt(x) > a
-        double sf, y;
-        const bool ok_s = sqrt_rcp_fast(x, sf, y);
-        const double si = sqrt(x);
-        c[4] += 1;
-        if (!ok_s) {
-            c[2] += 1;
-            continue;
-        }
-        if (__double_as_longlong(sf) != __double_as_longlong(si)) c[0] += 1;
-        // speed-pair quotient and accel-triple quotient
-        const double ex = si - a;
-        double q;
-        if (div_fast(1.8 * 0.5 * ex, si, y, q)) {
-            if (__double_as_longlong(q) != __double_as_longlong(1.8 * 0.5 * ex / si)) c[1] += 1;
-        } else {
-            c[3] += 1;
-        }
-        const double den = 6.0 * si;
-        if (div_fast(1.8 * ex, den, y * (1.0 / 6.0), q)) {
-            if (__double_as_longlong(q) != __double_as_longlong(1.8 * ex / den)) c[1] += 1;
-        } else {
-            c[3] += 1;
-        }
-    }
-    for (int k = 0; k < 5; ++k) atomicAdd(&counts[k], c[k]);
-}
-
 // Speed pair (n, n+1) on registers x0 = s[n], x1 = s[n+1] (projection.py:313-345).
 template <int D>
 __device__ __forceinline__ void speed_pair(Sample<D>& x0, Sample<D>& x1, int n, double a,
@@ -589,25 +474,6 @@ __device__ __forceinline__ void speed_pair(Sample<D>& x0, Sample<D>& x1, int n, 
     // sqrt(nrm^2) < a, i.e. the reference's `nrm > a` is false -- skips the IEEE sqrt
     // for the (typically many) pairs well inside the bound; NaN takes the full path
     if (nrm <= a * a * (1.0 - 1e-15)) return;
-#if SPK_POLISH_FASTDIV
-    {
-        // fast path: unpinned pair, sqrt and quotient certified (see sqrt_rcp_fast)
-        double r, y, shrink;
-        if (n != pin && n + 1 != pin && sqrt_rcp_fast(nrm, r, y)) {
-            if (!(r > a)) return;
-            const double ex = r - a;
-            if (div_fast(omega * 0.5 * ex, r, y, shrink)) {
-                if (ex > worst) worst = ex;
-#pragma unroll
-                for (int l = 0; l < D; ++l) {
-                    x0.v[l] += shrink * df[l];
-                    x1.v[l] -= shrink * df[l];
-                }
-                return;
-            }
-        }
-    }
-#endif
     nrm = sqrt(nrm);
     if (!(nrm > a)) return;
     if (nrm - a > worst) worst = nrm - a;
@@ -644,28 +510,6 @@ __device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sampl
         nrm += w[l] * w[l];
     }
     if (nrm <= b * b * (1.0 - 1e-15)) return;  // exact early out, as in speed_pair
-#if SPK_POLISH_FASTDIV
-    if (pin != n && pin != n + 1 && pin != n + 2) {
-        double r, y, step;
-        if (sqrt_rcp_fast(nrm, r, y)) {
-            if (!(r > b)) return;
-            const double ex = r - b;
-            const double den = 6.0 * r;
-            // 1/den ~ y / 6 (a few ulps): enough for the certified one-step quotient
-            if (div_fast(omega * ex, den, y * (1.0 / 6.0), step)) {
-                if (ex > worst) worst = ex;
-                const double step1 = step * -2.0;
-#pragma unroll
-                for (int l = 0; l < D; ++l) {
-                    x0.v[l] -= step * w[l];
-                    x1.v[l] -= step1 * w[l];
-                    x2.v[l] -= step * w[l];
-                }
-                return;
-            }
-        }
-    }
-#endif
     nrm = sqrt(nrm);
     if (!(nrm > b)) return;
     if (nrm - b > worst) worst = nrm - b;
@@ -814,6 +658,9 @@ __device__ unsigned long long spk_polish_prof[3][7];
 #define SPK_RING_K 4
 #endif
 constexpr int RING_K = SPK_RING_K;
+#ifndef SPK_RING_UNROLL
+#define SPK_RING_UNROLL 4
+#endif
 static_assert(RING_K >= 1 && (RING_K & (RING_K - 1)) == 0, "RING_K must be a power of two");
 __device__ __forceinline__ int ring_offset(int g) { return PL_LAG * g + RING_K * (g >> 5); }
 
@@ -998,12 +845,28 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
             break;                                                                         \
         if (st + R >= last_step) break;                                                    \
     }
+#if SPK_RING_UNROLL == 4
     for (int st = 0;; st += 4) {
         SPK_RING_STEP(0)
         SPK_RING_STEP(1)
         SPK_RING_STEP(2)
         SPK_RING_STEP(3)
     }
+#else
+    // one step per iteration: the window rotates by register moves (a quarter of the
+    // code of the 4x unrolled loop)
+    for (int st = 0;; ++st) {
+        ring_step<D, 0>(L, st, ns, B, P, g, lane, warp, max_sweeps, kl, a, b, pin, pv0, pv1,
+                        pv2, tol, s0, snap0, res, xfer, wrap0, wstride, stop_sh);
+        const Sample<D> r = L.slot[0];
+        L.slot[0] = L.slot[1];
+        L.slot[1] = L.slot[2];
+        L.slot[2] = L.slot[3];
+        L.slot[3] = r;
+        if (((st + 1) & (RING_K - 1)) == 0 && stop_sh[(st / RING_K) & 1] != 0x7fffffff) break;
+        if (st >= last_step) break;
+    }
+#endif
 #undef SPK_RING_STEP
 #ifdef SPK_POLISH_PROF
     if (blockIdx.x == 0) {
@@ -1385,16 +1248,6 @@ int spk_project_all(const double* in, const double* grad, double eta,
                 (float4*)pos4, wrap_mode);
     }
     SPK_CHECK_LAUNCH("polish_kernel");
-    return SPK_OK;
-}
-
-int spk_selftest_fastdiv(int64_t n, uint64_t seed, uint64_t* counts, spk_stream_t stream) {
-    SPK_REQUIRE(n >= 0 && counts != nullptr, SPK_ERR_ARG, "selftest: bad arguments");
-    cudaMemsetAsync(counts, 0, 5 * sizeof(uint64_t), (cudaStream_t)stream);
-    if (n == 0) return SPK_OK;
-    fastdiv_selftest_kernel<<<num_sms() * 8, 256, 0, (cudaStream_t)stream>>>(
-        n, seed, reinterpret_cast<unsigned long long*>(counts));
-    SPK_CHECK_LAUNCH("fastdiv_selftest");
     return SPK_OK;
 }
 

@@ -24,7 +24,7 @@ from oracle import oracle as orc  # noqa: E402
 threads = os.cpu_count()
 numba.set_num_threads(threads)
 out = {"threads": threads, "cpu": open("/proc/cpuinfo").read().split("model name")[1]
-       .split("\n")[0].strip(": ")}
+       .split("\n")[0].strip(": \t")}
 
 # direct_sums (K1), p = 2^16 full (4.3e9 pairs)
 p = 1 << 16

@@ -243,26 +243,3 @@ def test_subnormal_eps_squared_stays_finite(spk):
         c1, g1 = spk.eval_repulsion_direct(pts[:1], eps=1e-20)
         assert np.isfinite(c1) and abs(c1) <= 1e-19 and np.all(g1 == 0.0)
 
-
-@pytest.mark.parametrize("share", [0, 1, 2, 3, 4])
-def test_lattice_rsqrt_on_fma_pipe(spk, share, monkeypatch):
-    """Every FMA/SFU split of the lattice rsqrts (SPK_NB_FMA_RSQRT = share/32 of the pairs
-    through the integer-seed + 2 Newton rsqrt) meets the oracle tolerance in 2D and 3D,
-    incl. the eps = 0 guard path (the fused launch runs the same lattice tile code)."""
-    from paper_2108_02991_b200 import _device
-    from paper_2108_02991_b200.attraction import grid_sums_device
-
-    monkeypatch.setenv("SPK_NB_FMA_RSQRT", str(share))
-    rng = np.random.default_rng(40 + share)
-    for d, n in ((3, 12), (2, 40)):
-        rho = spk.discretize(spk.DensityParams(0.25, 2.0), n, d)
-        fld = spk.precompute_field(rho)
-        pts = rng.uniform(-1, 1, (4100, d))
-        res = spk.eval_attraction(spk.SamplingPattern(pts[None]), fld, "exact")
-        cref, gref = orc.attraction_exact(pts, rho.grid, fld.kernel_eps)
-        assert abs(res.cost - cref) <= VAL_TOL * abs(cref)
-        assert rel_l2(res.grad, gref) <= GRAD_TOL
-        pos4 = _device.pack_positions(_device.h2d(pts))
-        v, g = grid_sums_device(pos4, fld, 0.0)  # eps = 0: guarded variant
-        vo, go = orc.grid_sums(pts, rho.grid, 0.0)
-        assert rel_l2(_device.d2h(g), go) <= GRAD_TOL

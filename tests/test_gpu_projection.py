@@ -188,20 +188,3 @@ def test_ring_configurations_vs_oracle(spk, d, ns, pin, mono, cap):
     assert np.array_equal(sw, rsw), (sw, rsw)
     assert np.array_equal(out, ref), np.abs(out - ref).max()
 
-
-def test_certified_fast_sqrt_and_quotient_match_ieee():
-    """The polish's fast sqrt / quotient (one reciprocal square root for both, each
-    certified by its residual, IEEE fallback otherwise) equals sqrt.rn / div.rn bit for
-    bit on 2e7 random and near-square cases; the fallback is rare."""
-    import torch
-
-    from paper_2108_02991_b200 import _device, _native
-
-    counts = torch.zeros(5, dtype=torch.int64, device=_device.device())
-    for seed in (1, 2):
-        _native.call("spk_selftest_fastdiv", 10_000_000, seed, counts.data_ptr(),
-                     _device.stream())
-        c = counts.cpu().numpy()
-        assert c[4] == 10_000_000
-        assert c[0] == 0 and c[1] == 0, c
-        assert c[2] <= 1e-4 * c[4] and c[3] <= 1e-3 * c[4], c
