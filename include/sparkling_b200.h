@@ -66,6 +66,16 @@ int spk_grid_sums(const void* tgt, int64_t n_tgt, const float* grid_w, const int
                   int dims, float eps2, double* val, double* grad, void* ws,
                   size_t ws_bytes, spk_stream_t stream);
 
+/* K2 for the rows of a shot subset (the multi-GPU path's attraction of shots whose polish
+ * has finished, overlapped with the polish of the others): targets are the n_s records
+ * of each listed shot in tgt (shot-major), results go to the same rows of val [.] and
+ * grad [.][dims] (other rows untouched).  Same arithmetic as spk_grid_sums. */
+size_t spk_grid_sums_shots_workspace_bytes(int64_t n_ids, int n_s, int64_t n_cells);
+int spk_grid_sums_shots(const void* tgt, const int32_t* shot_ids, int64_t n_ids, int n_s,
+                        const float* grid_w, const int64_t* side, int dims, float eps2,
+                        double* val, double* grad, void* ws, size_t ws_bytes,
+                        spk_stream_t stream);
+
 /* Both sums in ONE launch (the optimize() hot loop, optimizer.py:302-303): segment 0 =
  * the density lattice (attraction), segment 1 = positions (repulsion).  Either segment
  * may be empty (grid_w = NULL or n_pos = 0). */
@@ -142,6 +152,21 @@ int spk_project_all(const double* in, const double* grad, double eta,
                     const double* pin_val, int n_pit, double tau, int monotone, double tol,
                     int max_sweeps, void* pos4, int32_t* sweeps, double* trace,
                     int32_t* nonfinite, void* ws, size_t ws_bytes, spk_stream_t stream);
+
+/* The two halves of spk_project_all, for callers that schedule the polish themselves:
+ * FISTA for all shots (out = FISTA result, the workspace keeps no state the polish
+ * needs), then the polish of a subset of shots shot_ids[0..n_ids) (null = all n_shots) in
+ * place on `shots`, with the workspace of spk_project_workspace_bytes(n_shots, ...).
+ * Several disjoint subsets may be polished concurrently on different streams. */
+int spk_project_fista(const double* in, const double* grad, double eta,
+                      const double* eta_per_shot, double* out, int64_t n_shots, int n_s,
+                      int dims, double a, double b, int pin_idx, const double* pin_val,
+                      int n_pit, double tau, int monotone, double* trace, int32_t* nonfinite,
+                      void* ws, size_t ws_bytes, spk_stream_t stream);
+int spk_polish_shots(double* shots, const int32_t* shot_ids, int64_t n_ids, int64_t n_shots,
+                     int n_s, int dims, double a, double b, int pin_idx, const double* pin_val,
+                     double tol, int max_sweeps, void* pos4, int32_t* sweeps, void* ws,
+                     size_t ws_bytes, spk_stream_t stream);
 
 /* feasibility_residuals (projection.py:435-452): out[0..4] = amplitude, speed,
  * acceleration, pin (0 if no pin), max -- each already clipped at 0 like the reference. */

@@ -54,6 +54,15 @@ SIGNATURES = {
     "spk_project_all": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_vp, c_i64, c_int, c_int, c_dbl, c_dbl,
                                 c_int, ctypes.POINTER(c_dbl), c_int, c_dbl, c_int, c_dbl,
                                 c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "spk_project_fista": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_vp, c_i64, c_int, c_int, c_dbl,
+                                  c_dbl, c_int, ctypes.POINTER(c_dbl), c_int, c_dbl, c_int,
+                                  c_vp, c_vp, c_vp, c_size, c_vp]),
+    "spk_polish_shots": (c_int, [c_vp, c_vp, c_i64, c_i64, c_int, c_int, c_dbl, c_dbl, c_int,
+                                 ctypes.POINTER(c_dbl), c_dbl, c_int, c_vp, c_vp, c_vp, c_size,
+                                 c_vp]),
+    "spk_grid_sums_shots_workspace_bytes": (c_size, [c_i64, c_int, c_i64]),
+    "spk_grid_sums_shots": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, ctypes.POINTER(c_i64),
+                                    c_int, ctypes.c_float, c_vp, c_vp, c_vp, c_size, c_vp]),
     "spk_residuals_workspace_bytes": (c_size, [c_i64]),
     "spk_feasibility_residuals": (c_int, [c_vp, c_i64, c_int, c_int, c_dbl, c_dbl, c_int,
                                           ctypes.POINTER(c_dbl), c_vp, c_vp, c_size, c_vp]),
@@ -125,6 +134,7 @@ LAUNCHES = {
     "spk_tree_l2p": 1,
     "spk_tree_plan_write": 2, "spk_nudft_adjoint": 2, "spk_nudft_forward": 2,
     "spk_dcf_update": 1, "spk_psf_magnitude": 1,
+    "spk_project_fista": 1, "spk_polish_shots": 1, "spk_grid_sums_shots": 4,
 }
 _launched = [0]
 

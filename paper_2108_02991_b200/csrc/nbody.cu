@@ -639,6 +639,29 @@ void set_error(const char* fmt, ...) {
     va_end(ap);
 }
 
+// Rows of a shot subset: gather the listed shots' target records into a contiguous
+// buffer, and scatter per-target results back to their rows (val [n], grad [n][dims]).
+__global__ void gather_shot_rows_kernel(const float4* __restrict__ src,
+                                        const int32_t* __restrict__ ids, long long n_ids,
+                                        int n_s, float4* __restrict__ dst) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_ids * n_s) return;
+    const long long k = i / n_s;
+    dst[i] = src[(long long)ids[k] * n_s + (i - k * n_s)];
+}
+
+__global__ void scatter_shot_rows_kernel(const double* __restrict__ v, const double* __restrict__ g,
+                                         const int32_t* __restrict__ ids, long long n_ids,
+                                         int n_s, int dims, double* __restrict__ val,
+                                         double* __restrict__ grad) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_ids * n_s) return;
+    const long long k = i / n_s;
+    const long long r = (long long)ids[k] * n_s + (i - k * n_s);
+    val[r] = v[i];
+    for (int l = 0; l < dims; ++l) grad[r * dims + l] = g[i * dims + l];
+}
+
 }  // namespace spk
 
 using namespace spk;
@@ -681,6 +704,44 @@ int spk_grid_sums(const void* tgt, int64_t n_tgt, const float* grid_w, const int
                   spk_stream_t stream) {
     return launch_sums((const float4*)tgt, n_tgt, dims, grid_w, side, eps2, nullptr, 0, 0.f,
                        val, grad, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+static size_t shot_rows_scratch(int64_t n_rows) {
+    return ((size_t)n_rows * (16 + 8 + 24) + 255) & ~(size_t)255;
+}
+
+size_t spk_grid_sums_shots_workspace_bytes(int64_t n_ids, int n_s, int64_t n_cells) {
+    return shot_rows_scratch(n_ids * n_s) + spk_nbody_workspace_bytes(n_ids * n_s, n_cells, 0);
+}
+
+int spk_grid_sums_shots(const void* tgt, const int32_t* shot_ids, int64_t n_ids, int n_s,
+                        const float* grid_w, const int64_t* side, int dims, float eps2,
+                        double* val, double* grad, void* ws, size_t ws_bytes,
+                        spk_stream_t stream_) {
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
+    SPK_REQUIRE(n_ids >= 0 && n_s >= 1, SPK_ERR_ARG, "shot subset: bad sizes");
+    if (n_ids == 0) return SPK_OK;
+    SPK_REQUIRE(shot_ids != nullptr, SPK_ERR_ARG, "shot subset: null shot list");
+    const long long n = n_ids * n_s;
+    long long n_cells = 1;
+    for (int a = 0; a < dims; ++a) n_cells *= side[a];
+    SPK_REQUIRE(ws != nullptr && ws_bytes >= spk_grid_sums_shots_workspace_bytes(n_ids, n_s, n_cells),
+                SPK_ERR_WORKSPACE, "grid sums (shot subset): workspace too small");
+    cudaStream_t stream = (cudaStream_t)stream_;
+    char* p = static_cast<char*>(ws);
+    float4* t4 = reinterpret_cast<float4*>(p);
+    double* v = reinterpret_cast<double*>(p + (size_t)n * 16);
+    double* g = v + n;
+    const size_t scratch = shot_rows_scratch(n);
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    gather_shot_rows_kernel<<<nb, 256, 0, stream>>>((const float4*)tgt, shot_ids, n_ids, n_s, t4);
+    SPK_CHECK_LAUNCH("grid_sums_shots(gather)");
+    const int rc = launch_sums(t4, n, dims, grid_w, side, eps2, nullptr, 0, 0.f, v, g, nullptr,
+                               nullptr, p + scratch, ws_bytes - scratch, stream);
+    if (rc != SPK_OK) return rc;
+    scatter_shot_rows_kernel<<<nb, 256, 0, stream>>>(v, g, shot_ids, n_ids, n_s, dims, val, grad);
+    SPK_CHECK_LAUNCH("grid_sums_shots(scatter)");
+    return SPK_OK;
 }
 
 int spk_fused_sums(const void* tgt, int64_t n_tgt, int dims, const float* grid_w,

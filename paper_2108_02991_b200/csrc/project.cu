@@ -438,6 +438,9 @@ __global__ void __launch_bounds__(PJ_THREADS) fista_kernel(const ProjArgs A) {
 // sweep, the batch is replayed with j + 1 lanes.  Every element sees the same IEEE fp64
 // operations in the same order as the reference => bit-identical results and sweep count.
 constexpr int PL_LAG = 4;
+#ifndef SPK_BOX_FAST
+#define SPK_BOX_FAST 1
+#endif
 
 template <int D>
 struct Sample {
@@ -446,9 +449,16 @@ struct Sample {
 
 template <int D>
 __device__ __forceinline__ void box_sample(Sample<D>& s, double& worst) {
-    // branch-free and short: the excess |v| - 1 equals the reference's v - 1 / -1 - v
-    // bit for bit, and fmax leaves worst (>= 0) unchanged when |v| <= 1 or v is NaN;
-    // only |v| > 1 replaces v, by +-1 with v's sign (NaN and +-0 pass through)
+#if SPK_BOX_FAST
+    // almost every sample is inside the box: one compare per axis (|v| > 1 is false for
+    // |v| <= 1 and for NaN, exactly the reference's no-op cases) and a warp-uniform skip
+    bool out = fabs(s.v[0]) > 1.0 || fabs(s.v[1]) > 1.0;
+    if (D == 3) out = out || fabs(s.v[D - 1]) > 1.0;
+    if (!out) return;
+#endif
+    // the excess |v| - 1 equals the reference's v - 1 / -1 - v bit for bit, and fmax
+    // leaves worst (>= 0) unchanged when |v| <= 1 or v is NaN; only |v| > 1 replaces v,
+    // by +-1 with v's sign (NaN and +-0 pass through)
 #pragma unroll
     for (int l = 0; l < D; ++l) {
         const double v = s.v[l];
@@ -685,12 +695,19 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
     const bool on = t >= -2 && t <= ns + 1 && L.k < max_sweeps;
     if (on) {
         if (t == -2) L.worst = 0.0;
+#ifdef SPK_EXP_SA_INDEP
+        Sample<D> w2c = w2;  // experiment: A reads sample t before S(t) (wrong results)
+#endif
 #ifndef SPK_EXP_NOSPEED
         if (t >= 0 && t <= ns - 2) speed_pair<D>(w2, w3, t, a, pin, L.worst);
 #endif
         SPK_PROF_MARK(L, 0)
 #ifndef SPK_EXP_NOACCEL
+#ifdef SPK_EXP_SA_INDEP
+        if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2c, t - 2, b, pin, L.worst);
+#else
         if (t >= 2 && t <= ns - 1) accel_triple<D>(w0, w1, w2, t - 2, b, pin, L.worst);
+#endif
 #endif
         SPK_PROF_MARK(L, 1)
 #ifndef SPK_EXP_NOSNAP
@@ -788,19 +805,21 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
                                                       double pv1, double pv2, double tol,
                                                       int max_sweeps, double* ws,
                                                       int32_t* sweeps_out, float4* pos4,
-                                                      int wrap_mode) {
+                                                      int wrap_mode,
+                                                      const int32_t* __restrict__ shot_ids) {
     // wrap_mode 2: two wrap buffers in shared memory (round parity), which double as the
     // replay snapshot -- no global snapshot stores on the ring's critical path;
     // 1: one shared wrap buffer + global ping-pong snapshots; 0: wrap in the workspace.
     extern __shared__ __align__(16) double xfer[];  // [W][2 RING_K][D], then wrap [1|2][ns][D]
     __shared__ int stop_sh[2];
-    const long long c = blockIdx.x;
+    // shot of this CTA: the launch's shot list (a subset in any order) or blockIdx.x
+    const long long c = shot_ids ? (long long)shot_ids[blockIdx.x] : (long long)blockIdx.x;
     const int B = blockDim.x;
     const int W = B >> 5;
     const int P = max(4 * B + RING_K * W, ns + 4);
     const int nd4 = ns * D;
     // wrap buffer(s) in shared memory, or (very long shots) in the per-shot workspace
-    double* wrap0 = wrap_mode == 0 ? ws + blockIdx.x * (size_t)(4 * nd4) + 3 * nd4
+    double* wrap0 = wrap_mode == 0 ? ws + c * (size_t)(4 * nd4) + 3 * nd4
                                    : xfer + W * 2 * RING_K * D;
     const int wstride = wrap_mode == 2 ? nd4 : 0;
     double* wrap1 = wrap0 + wstride;
@@ -1157,23 +1176,11 @@ size_t spk_project_workspace_bytes(int64_t n_shots, int n_s, int dims, int with_
     return (size_t)n_shots * proj_state_doubles(n_s, dims) * sizeof(double) + 256;
 }
 
-int spk_project_all(const double* in, const double* grad, double eta,
-                    const double* eta_per_shot, double* out,
-                    int64_t n_shots, int n_s, int dims, double a, double b, int pin_idx,
-                    const double* pin_val, int n_pit, double tau, int monotone, double tol,
-                    int max_sweeps, void* pos4, int32_t* sweeps, double* trace,
-                    int32_t* nonfinite, void* ws, size_t ws_bytes, spk_stream_t stream_) {
-    cudaStream_t stream = (cudaStream_t)stream_;
-    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
-    SPK_REQUIRE(n_s >= 2, SPK_ERR_ARG, "projection needs at least 2 samples per shot");
-    SPK_REQUIRE(n_pit >= 1, SPK_ERR_ARG, "n_pit must be >= 1");
-    SPK_REQUIRE(pin_idx < n_s, SPK_ERR_ARG, "pinned_index %d out of range for N_s=%d",
-                pin_idx, n_s);
-    SPK_REQUIRE(max_sweeps >= 1, SPK_ERR_ARG, "max_sweeps must be >= 1");
-    if (n_shots <= 0) return SPK_OK;
-    const size_t need = spk_project_workspace_bytes(n_shots, n_s, dims, trace != nullptr);
-    SPK_REQUIRE(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE,
-                "projection workspace too small: need %zu, got %zu", need, ws_bytes);
+static int launch_fista(const double* in, const double* grad, double eta,
+                        const double* eta_per_shot, double* out, int64_t n_shots, int n_s,
+                        int dims, double a, double b, int pin_idx, const double* pin_val,
+                        int n_pit, double tau, int monotone, double* trace,
+                        int32_t* nonfinite, void* ws, cudaStream_t stream) {
     ProjArgs A;
     A.in = in;
     A.grad = grad;
@@ -1209,8 +1216,21 @@ int spk_project_all(const double* in, const double* grad, double eta,
         fista_kernel<2><<<(unsigned)n_shots, nt, dyn, stream>>>(A);
     }
     SPK_CHECK_LAUNCH("fista_kernel");
-    // polish: systolic ring, one CTA of 32*pw lanes per shot; snapshots + result in the
-    // (now free) FISTA workspace, warp hand-over slots in shared memory
+    return SPK_OK;
+}
+
+// Polish (systolic ring, one CTA of 32 pw lanes per shot) of n_ids shots: shot_ids[i]
+// (or i when shot_ids is null).  Snapshots + result live in that shot's slot of the FISTA
+// workspace, warp hand-over slots and wrap buffers in shared memory.
+static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, int n_s,
+                         int dims, double a, double b, int pin_idx, const double* pin_val,
+                         double tol, int max_sweeps, void* pos4, int32_t* sweeps, void* ws,
+                         cudaStream_t stream) {
+    if (n_ids <= 0) return SPK_OK;
+    const int pin = pin_idx < 0 ? -1 : pin_idx;
+    double pv[3] = {0, 0, 0};
+    for (int l = 0; l < dims; ++l)
+        if (pin_idx >= 0) pv[l] = pin_val[l];
     const int pw = polish_warps(n_s);
     const size_t xb = (size_t)pw * 2 * RING_K * dims * sizeof(double);
     const size_t wb = (size_t)n_s * dims * sizeof(double);
@@ -1227,28 +1247,80 @@ int spk_project_all(const double* in, const double* grad, double eta,
     double* pws = static_cast<double*>(ws);
     // <= 8 warps (N_s <= 1283): a register budget of 80 keeps the ring window in registers
     // with 3 CTAs per SM; wider rings use the 1024-thread instantiation
-    const dim3 grid((unsigned)n_shots), block(32 * pw);
+    const dim3 grid((unsigned)n_ids), block(32 * pw);
+#define PL_LAUNCH(DD, TT, MB)                                                              \
+    polish_kernel<DD, TT, MB><<<grid, block, psm, stream>>>(                               \
+        shots, n_s, a, b, pin, pv[0], pv[1], pv[2], tol, max_sweeps, pws, sweeps,           \
+        (float4*)pos4, wrap_mode, shot_ids)
     if (pw <= 8) {
-        if (dims == 3)
-            polish_kernel<3, 256, PL_MINB><<<grid, block, psm, stream>>>(
-                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_mode);
-        else
-            polish_kernel<2, 256, PL_MINB><<<grid, block, psm, stream>>>(
-                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_mode);
+        if (dims == 3) PL_LAUNCH(3, 256, PL_MINB);
+        else PL_LAUNCH(2, 256, PL_MINB);
     } else {
-        if (dims == 3)
-            polish_kernel<3, 1024, 1><<<grid, block, psm, stream>>>(
-                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_mode);
-        else
-            polish_kernel<2, 1024, 1><<<grid, block, psm, stream>>>(
-                out, n_s, a, b, A.pin, A.pv[0], A.pv[1], A.pv[2], tol, max_sweeps, pws, sweeps,
-                (float4*)pos4, wrap_mode);
+        if (dims == 3) PL_LAUNCH(3, 1024, 1);
+        else PL_LAUNCH(2, 1024, 1);
     }
+#undef PL_LAUNCH
     SPK_CHECK_LAUNCH("polish_kernel");
     return SPK_OK;
+}
+
+#define SPK_PROJECT_CHECKS                                                                 \
+    SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);  \
+    SPK_REQUIRE(n_s >= 2, SPK_ERR_ARG, "projection needs at least 2 samples per shot");    \
+    SPK_REQUIRE(pin_idx < n_s, SPK_ERR_ARG, "pinned_index %d out of range for N_s=%d",     \
+                pin_idx, n_s)
+
+int spk_project_all(const double* in, const double* grad, double eta,
+                    const double* eta_per_shot, double* out,
+                    int64_t n_shots, int n_s, int dims, double a, double b, int pin_idx,
+                    const double* pin_val, int n_pit, double tau, int monotone, double tol,
+                    int max_sweeps, void* pos4, int32_t* sweeps, double* trace,
+                    int32_t* nonfinite, void* ws, size_t ws_bytes, spk_stream_t stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    SPK_PROJECT_CHECKS;
+    SPK_REQUIRE(n_pit >= 1, SPK_ERR_ARG, "n_pit must be >= 1");
+    SPK_REQUIRE(max_sweeps >= 1, SPK_ERR_ARG, "max_sweeps must be >= 1");
+    if (n_shots <= 0) return SPK_OK;
+    const size_t need = spk_project_workspace_bytes(n_shots, n_s, dims, trace != nullptr);
+    SPK_REQUIRE(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE,
+                "projection workspace too small: need %zu, got %zu", need, ws_bytes);
+    int rc = launch_fista(in, grad, eta, eta_per_shot, out, n_shots, n_s, dims, a, b, pin_idx,
+                          pin_val, n_pit, tau, monotone, trace, nonfinite, ws, stream);
+    if (rc != SPK_OK) return rc;
+    return launch_polish(out, nullptr, n_shots, n_s, dims, a, b, pin_idx, pin_val, tol,
+                         max_sweeps, pos4, sweeps, ws, stream);
+}
+
+int spk_project_fista(const double* in, const double* grad, double eta,
+                      const double* eta_per_shot, double* out, int64_t n_shots, int n_s,
+                      int dims, double a, double b, int pin_idx, const double* pin_val,
+                      int n_pit, double tau, int monotone, double* trace, int32_t* nonfinite,
+                      void* ws, size_t ws_bytes, spk_stream_t stream) {
+    SPK_PROJECT_CHECKS;
+    SPK_REQUIRE(n_pit >= 1, SPK_ERR_ARG, "n_pit must be >= 1");
+    if (n_shots <= 0) return SPK_OK;
+    const size_t need = spk_project_workspace_bytes(n_shots, n_s, dims, trace != nullptr);
+    SPK_REQUIRE(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE,
+                "projection workspace too small: need %zu, got %zu", need, ws_bytes);
+    return launch_fista(in, grad, eta, eta_per_shot, out, n_shots, n_s, dims, a, b, pin_idx,
+                        pin_val, n_pit, tau, monotone, trace, nonfinite, ws,
+                        (cudaStream_t)stream);
+}
+
+int spk_polish_shots(double* shots, const int32_t* shot_ids, int64_t n_ids, int64_t n_shots,
+                     int n_s, int dims, double a, double b, int pin_idx, const double* pin_val,
+                     double tol, int max_sweeps, void* pos4, int32_t* sweeps, void* ws,
+                     size_t ws_bytes, spk_stream_t stream) {
+    SPK_PROJECT_CHECKS;
+    SPK_REQUIRE(max_sweeps >= 1, SPK_ERR_ARG, "max_sweeps must be >= 1");
+    SPK_REQUIRE(n_ids >= 0 && n_ids <= n_shots, SPK_ERR_ARG, "polish: %lld ids for %lld shots",
+                (long long)n_ids, (long long)n_shots);
+    if (n_ids <= 0) return SPK_OK;
+    const size_t need = spk_project_workspace_bytes(n_shots, n_s, dims, 0);
+    SPK_REQUIRE(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE,
+                "projection workspace too small: need %zu, got %zu", need, ws_bytes);
+    return launch_polish(shots, shot_ids, n_ids, n_s, dims, a, b, pin_idx, pin_val, tol,
+                         max_sweeps, pos4, sweeps, ws, (cudaStream_t)stream);
 }
 
 size_t spk_residuals_workspace_bytes(int64_t n_shots) {

@@ -18,13 +18,15 @@ the gloo backend.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _device, _native
 from .attraction import field_eval_device, grid_sums_device, tree_grid_sums_device
-from .projection import project_device, residuals_device
+from .projection import project_device, project_overlap_device, residuals_device
 from .repulsion import direct_sums_device, tree_sums_checked
 
 
@@ -106,6 +108,41 @@ class CudaOps:
     def residuals(self, coords, proj_cfg):
         return residuals_device(coords, proj_cfg)
 
+    # ---- K2-under-polish overlap (ShardedRun.overlap)
+    OVERLAP_GROUPS = 8
+
+    def overlap_capable(self, cfg, n_local_shots: int) -> bool:
+        """The overlap pays when the polish is tail-bound: few shots per SM (a rank of a
+        multi-GPU run), exact lattice attraction, exact repulsion.  SPK_OVERLAP=0/1
+        forces it off/on."""
+        env = os.environ.get("SPK_OVERLAP")
+        eligible = (cfg.grad_mode == "exact" and cfg.attraction_tree_precision is None
+                    and cfg.repulsion.backend == "direct")
+        if env is not None:
+            return eligible and env == "1"
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        return eligible and n_local_shots <= 2 * sms
+
+    def _overlap_streams(self):
+        if not hasattr(self, "_ostreams"):
+            g = self.OVERLAP_GROUPS
+            self._ostreams = ([torch.cuda.Stream(priority=-1) for _ in range(g)],
+                              [torch.cuda.Stream(priority=0) for _ in range(g)])
+        return self._ostreams
+
+    def project_overlap(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, fld,
+                        att_val, att_grad, sweeps, order):
+        n_c = coords.shape[0]
+        ps, ks = self._overlap_streams()
+        g = max(1, min(len(ps), n_c // 8))
+        return project_overlap_device(coords, proj_cfg, grad=grad, eta=eta, out=out,
+                                      pos4=pos4, nonfinite=nonfinite, field=fld,
+                                      att_val=att_val, att_grad=att_grad, sweeps=sweeps,
+                                      order=order, polish_streams=ps[:g], k2_streams=ks[:g])
+
+    def repulsion_sums(self, tgt4, src4, cfg):
+        return direct_sums_device(tgt4, src4, cfg.dims, cfg.repulsion.kernel_eps ** 2)
+
     def upsample(self, coords):
         n_c, n_s, d = coords.shape
         out = self.empty((n_c, 2 * n_s, d))
@@ -160,6 +197,16 @@ class ShardedRun:
         self.flag = ops.empty(1, torch.int32)
         self.have_prev = False
         self.host_prev = None
+        # K2-under-polish overlap: the lattice sums of the positions the last projection
+        # produced (att_pre), and the polish sweep counts that order the next one
+        self.overlap = (hasattr(ops, "overlap_capable")
+                        and ops.overlap_capable(self.cfg, self.local))
+        self.att_pre = None
+        self.sweeps_prev = None
+        if self.overlap:
+            self.att_val = ops.empty(self.local * n_s)
+            self.att_grad = ops.empty((self.local * n_s, d))
+            self.sweeps = ops.empty(self.local, torch.int32)
 
     # ------------------------------------------------------------ communication
     def _gather_pos4(self):
@@ -193,6 +240,7 @@ class ShardedRun:
         self._gather_pos4()
         self.have_prev = False
         self.host_prev = None
+        self.att_pre = None
 
     def _pos4_target(self):
         n = self.local * self.n_s
@@ -201,7 +249,14 @@ class ShardedRun:
     def evaluate(self):
         """Fused device evaluation -> (att_cost, rep_cost, n_nonfinite, (dkdg, dgdg))."""
         tgt = self._pos4_target()
-        va, ga, vr, gr = self.ops.sums(tgt, self.pos4_all, self.coords, self.fld, self.cfg)
+        if self.att_pre is not None:
+            # K2 already ran under the last polish; only K1 needs the gathered sources
+            va, ga = self.att_pre
+            self.att_pre = None
+            vr, gr = self.ops.repulsion_sums(tgt, self.pos4_all, self.cfg)
+        else:
+            va, ga, vr, gr = self.ops.sums(tgt, self.pos4_all, self.coords, self.fld,
+                                           self.cfg)
         prev_c = self.prev if self.have_prev else None
         prev_g = self.prev_grad if self.have_prev else None
         scal = self.ops.combine(va, ga, vr, gr, self.p, self.coords, prev_c, prev_g,
@@ -236,8 +291,20 @@ class ShardedRun:
     def step_project(self, proj_cfg, eta: float) -> bool:
         """coords <- P(coords - eta * grad); returns False if the step was non-finite."""
         self.flag.zero_()
-        out = self.ops.project(self.coords, proj_cfg, self.grad, float(eta), self.next,
-                               self._pos4_target(), self.flag)
+        if self.overlap:
+            order = None
+            if self.sweeps_prev is not None:
+                order = torch.argsort(self.sweeps_prev, descending=True,
+                                      stable=True).to(torch.int32)
+            out = self.ops.project_overlap(self.coords, proj_cfg, self.grad, float(eta),
+                                           self.next, self._pos4_target(), self.flag,
+                                           self.fld, self.att_val, self.att_grad,
+                                           self.sweeps, order)
+            self.att_pre = (self.att_val, self.att_grad)
+            self.sweeps_prev = self.sweeps.clone()
+        else:
+            out = self.ops.project(self.coords, proj_cfg, self.grad, float(eta), self.next,
+                                   self._pos4_target(), self.flag)
         # rotate: prev <- coords, coords <- out, next <- old prev
         self.prev, self.coords, self.next = self.coords, out, self.prev
         self.prev_grad, self.grad = self.grad, self.prev_grad

@@ -184,3 +184,73 @@ def feasibility_residuals(k: SamplingPattern, cfg: ProjectionConfig) -> dict:
         res["pin"] = float(vals[3])
     res["max"] = max(res.values())
     return res
+
+
+def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad, eta,
+                           out: torch.Tensor, pos4: torch.Tensor, nonfinite, field,
+                           att_val: torch.Tensor, att_grad: torch.Tensor,
+                           sweeps: torch.Tensor, order: torch.Tensor | None,
+                           polish_streams, k2_streams) -> torch.Tensor:
+    """K3 with the lattice attraction (K2) of every shot started as soon as its polish
+    group is done, so that K2 runs under the polish of the slower shots.
+
+    The polish time of a shot varies by ~3x between shots and the iteration waits for the
+    slowest; on a rank with few shots (multi-GPU) most SMs idle
+    during that tail.  Shots are polished in groups, longest first by the previous
+    iteration's sweep counts (``order``, device int32; None = shot order), each group on
+    its own high-priority stream, and each group's K2 (spk_grid_sums_shots) follows on a
+    low-priority stream.  The projection itself is unchanged (bit-identical per shot);
+    K2 writes ``att_val`` [n_shots * n_s] / ``att_grad`` [n_shots * n_s, d] for the NEW
+    positions ``pos4``.  Returns ``out``; ``sweeps`` receives this call's sweep counts."""
+    n_c, n_s, dims = coords.shape
+    pin_idx, pin_val = _pin_arrays(cfg, dims)
+    tau = 1.0 / stacked_operator_norm(n_s, pin_idx)
+    nbytes = _native.query("spk_project_workspace_bytes", n_c, n_s, dims, 0)
+    ws = _device.workspace(nbytes, "project")
+    pv = _native.f64_array(list(pin_val) + [0.0] * (3 - dims))
+    main = torch.cuda.current_stream()
+    _native.call("spk_project_fista", coords.data_ptr(), _device.ptr(grad), float(eta), None,
+                 out.data_ptr(), n_c, n_s, dims, cfg.speed_bound, cfg.accel_bound, pin_idx, pv,
+                 cfg.n_pit, float(tau), int(bool(cfg.monotone)), None, _device.ptr(nonfinite),
+                 ws.data_ptr(), ws.numel(), main.cuda_stream)
+    if order is None:
+        order = torch.arange(n_c, dtype=torch.int32, device=coords.device)
+    G = len(polish_streams)
+    bounds = [n_c * g // G for g in range(G + 1)]
+    fista_done = torch.cuda.Event()
+    fista_done.record(main)
+    w = field.device_sources()
+    sides = field.sides
+    n_cells = int(np.prod(sides))
+    eps2 = float(field.kernel_eps ** 2)
+    side_arr = _native.i64_array(sides)
+    done = []
+    for g in range(G):
+        lo, hi = bounds[g], bounds[g + 1]
+        if hi <= lo:
+            continue
+        ids = order[lo:hi]
+        ps, ks = polish_streams[g], k2_streams[g]
+        ps.wait_event(fista_done)
+        _native.call("spk_polish_shots", out.data_ptr(), ids.data_ptr(), hi - lo, n_c, n_s,
+                     dims, cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 0.1 * cfg.feas_tol,
+                     MAX_POLISH_SWEEPS, pos4.data_ptr(), sweeps.data_ptr(), ws.data_ptr(),
+                     ws.numel(), ps.cuda_stream)
+        polished = torch.cuda.Event()
+        polished.record(ps)
+        ks.wait_event(polished)
+        kb = _native.query("spk_grid_sums_shots_workspace_bytes", hi - lo, n_s, n_cells)
+        kws = _device.workspace(kb, f"k2_overlap_{g}")
+        _native.call("spk_grid_sums_shots", pos4.data_ptr(), ids.data_ptr(), hi - lo, n_s,
+                     w.data_ptr(), side_arr, dims, eps2, att_val.data_ptr(),
+                     att_grad.data_ptr(), kws.data_ptr(), kws.numel(), ks.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(ks)
+        # the shot list (a slice of the caller's order tensor) is read on both streams
+        ids.record_stream(ps)
+        ids.record_stream(ks)
+        done.append((ps, ev))
+    for ps, ev in done:
+        main.wait_stream(ps)
+        main.wait_event(ev)
+    return out

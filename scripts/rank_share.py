@@ -9,6 +9,11 @@ rank's share of the next iterations in isolation on the same device and reports 
 projected strong-scaling efficiency t_1 / (N t_N).  The all-gather (16 B per sample over
 NVLink 5, 16 MiB at C2) is added as an estimate at 600 GB/s.
 
+Each share is timed twice: the plain schedule (fused K1 + K2, combine, projection) and the
+overlap schedule the engine uses on tail-bound ranks (ShardedRun.overlap): projection with
+every polish group's K2 on a side stream, then K1 alone; the polish order comes from the
+previous iteration's sweep counts of the same shots, as in the engine.
+
     python scripts/rank_share.py [--config c2|c4] [--iters 3] > profiles/r02_rank_share_c2.jsonl
 """
 import argparse
@@ -26,6 +31,7 @@ import bench  # noqa: E402
 import paper_2108_02991_b200 as spk  # noqa: E402
 from paper_2108_02991_b200 import engine  # noqa: E402
 from paper_2108_02991_b200.optimizer import _bb_step  # noqa: E402
+from paper_2108_02991_b200.projection import project_device  # noqa: E402
 
 
 def ev():
@@ -35,7 +41,7 @@ def ev():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ranks", default="1,2,4,8")
     args = ap.parse_args()
@@ -54,6 +60,7 @@ def main():
     ops, ns, d = run.ops, run.n_s, run.d
     worlds = [int(x) for x in args.ranks.split(",")]
     rows = {n: [] for n in worlds}
+    prev_sweeps = {}
     for it in range(args.iters):
         # this iteration's step size, from the full evaluation (as every rank would get)
         state["it"] += 1
@@ -73,25 +80,52 @@ def main():
                 out = torch.empty_like(grad)
                 pos4 = torch.empty((cnt * ns, 4), dtype=torch.float32, device="cuda")
                 flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+                sw = torch.empty(cnt, dtype=torch.int32, device="cuda")
                 e = [ev() for _ in range(4)]
                 torch.cuda.synchronize()
                 e[0].record()
                 va, ga, vr, gr = ops.sums(tgt, run.pos4_all, coords, fld, cfg)
                 ops.combine(va, ga, vr, gr, run.p, coords, None, None, grad.view(-1, d))
                 e[1].record()
-                sw = ops.project(coords, pcfg, grad, float(eta), out, pos4, flag)
+                project_device(coords, pcfg, grad=grad, eta=float(eta), out=out, pos4=pos4,
+                               nonfinite=flag, sweeps=sw)
                 e[2].record()
                 ops.residuals(out, pcfg)
                 e[3].record()
                 torch.cuda.synchronize()
-                per.append({"rank": r, "shots": cnt, "sums_ms": e[0].elapsed_time(e[1]),
-                            "project_ms": e[1].elapsed_time(e[2]),
-                            "residual_ms": e[2].elapsed_time(e[3])})
+                rec = {"rank": r, "shots": cnt, "sums_ms": e[0].elapsed_time(e[1]),
+                       "project_ms": e[1].elapsed_time(e[2]),
+                       "residual_ms": e[2].elapsed_time(e[3])}
+                # overlap schedule: order by the previous iteration's sweeps of these shots
+                key = (n, r)
+                order = prev_sweeps.get(key)
+                if order is not None:
+                    order = torch.argsort(order, descending=True, stable=True).to(torch.int32)
+                av = torch.empty(cnt * ns, dtype=torch.float64, device="cuda")
+                ag = torch.empty((cnt * ns, d), dtype=torch.float64, device="cuda")
+                sw2 = torch.empty(cnt, dtype=torch.int32, device="cuda")
+                f = [ev() for _ in range(3)]
+                torch.cuda.synchronize()
+                f[0].record()
+                ops.project_overlap(coords, pcfg, grad, float(eta), out, pos4, flag, fld, av,
+                                    ag, sw2, order)
+                f[1].record()
+                vr2, gr2 = ops.repulsion_sums(tgt, run.pos4_all, cfg)
+                ops.combine(av, ag, vr2, gr2, run.p, coords, None, None, grad.view(-1, d))
+                ops.residuals(out, pcfg)
+                f[2].record()
+                torch.cuda.synchronize()
+                rec["overlap_project_k2_ms"] = f[0].elapsed_time(f[1])
+                rec["overlap_k1_combine_ms"] = f[1].elapsed_time(f[2])
+                prev_sweeps[key] = sw.clone()
+                per.append(rec)
             gather_ms = 16.0 * bench.N_C * ns * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
             tot = [p["sums_ms"] + p["project_ms"] + p["residual_ms"] for p in per]
+            tot_o = [p["overlap_project_k2_ms"] + p["overlap_k1_combine_ms"] for p in per]
             rows[n].append({"iteration": state["it"], "eta": eta, "max_rank_ms": max(tot),
                             "allgather_est_ms": gather_ms,
                             "step_ms": max(tot) + gather_ms,
+                            "overlap_step_ms": max(tot_o) + gather_ms,
                             "max_sums_ms": max(p["sums_ms"] for p in per),
                             "max_project_ms": max(p["project_ms"] for p in per),
                             "ranks": per})
@@ -100,13 +134,18 @@ def main():
         state["have"] = True
         run.step_project(pcfg, eta)
         run.residual_max(pcfg)
-    t1 = np.mean([x["step_ms"] for x in rows[1]]) if 1 in rows else None
+    # the first iteration has no previous sweep counts (shot-order polish groups); the
+    # averages below skip it
+    t1 = np.mean([x["step_ms"] for x in rows[1][1:]]) if 1 in rows else None
     for n in worlds:
-        tn = float(np.mean([x["step_ms"] for x in rows[n]]))
+        tn = float(np.mean([x["step_ms"] for x in rows[n][1:]]))
+        to = float(np.mean([x["overlap_step_ms"] for x in rows[n][1:]]))
         rec = {"config": args.config, "n_ranks": n, "step_ms": tn,
-               "sums_ms": float(np.mean([x["max_sums_ms"] for x in rows[n]])),
-               "project_ms": float(np.mean([x["max_project_ms"] for x in rows[n]])),
+               "sums_ms": float(np.mean([x["max_sums_ms"] for x in rows[n][1:]])),
+               "project_ms": float(np.mean([x["max_project_ms"] for x in rows[n][1:]])),
                "efficiency": (t1 / (n * tn)) if t1 else None,
+               "overlap_step_ms": to,
+               "overlap_efficiency": (t1 / (n * to)) if t1 else None,
                "iterations": rows[n]}
         print(json.dumps(rec), flush=True)
 
