@@ -101,9 +101,9 @@ class CudaOps:
                      out.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
         return out
 
-    def project(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite):
+    def project(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, sweeps=None):
         return project_device(coords, proj_cfg, grad=grad, eta=eta, out=out, pos4=pos4,
-                              nonfinite=nonfinite)
+                              nonfinite=nonfinite, sweeps=sweeps)
 
     def residuals(self, coords, proj_cfg):
         return residuals_device(coords, proj_cfg)
@@ -111,17 +111,11 @@ class CudaOps:
     # ---- K2-under-polish overlap (ShardedRun.overlap)
     OVERLAP_GROUPS = 8
 
-    def overlap_capable(self, cfg, n_local_shots: int) -> bool:
-        """The overlap pays when the polish is tail-bound: few shots per SM (a rank of a
-        multi-GPU run), exact lattice attraction, exact repulsion.  SPK_OVERLAP=0/1
-        forces it off/on."""
-        env = os.environ.get("SPK_OVERLAP")
-        eligible = (cfg.grad_mode == "exact" and cfg.attraction_tree_precision is None
-                    and cfg.repulsion.backend == "direct")
-        if env is not None:
-            return eligible and env == "1"
-        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
-        return eligible and n_local_shots <= 2 * sms
+    def overlap_capable(self, cfg) -> bool:
+        """Eligible for the K2-under-polish schedule: exact lattice attraction and exact
+        repulsion (the fused N-body splits into K2 per polish group + K1)."""
+        return (cfg.grad_mode == "exact" and cfg.attraction_tree_precision is None
+                and cfg.repulsion.backend == "direct")
 
     def _overlap_streams(self):
         if not hasattr(self, "_ostreams"):
@@ -199,8 +193,7 @@ class ShardedRun:
         self.host_prev = None
         # K2-under-polish overlap: the lattice sums of the positions the last projection
         # produced (att_pre), and the polish sweep counts that order the next one
-        self.overlap = (hasattr(ops, "overlap_capable")
-                        and ops.overlap_capable(self.cfg, self.local))
+        self.overlap = hasattr(ops, "overlap_capable") and ops.overlap_capable(self.cfg)
         self.att_pre = None
         self.sweeps_prev = None
         if self.overlap:
@@ -288,10 +281,28 @@ class ShardedRun:
         self.grad.copy_(torch.from_numpy(mine))
         return dots
 
+    # Overlap pays when the polish is heavy next to the N-body: splitting the fused launch
+    # into K1 + per-group K2 costs ~6 % of the N-body (the pipes no longer mix), the K2
+    # hidden under the polish is ~40 % of the polish time (C2, profiles/
+    # r02_rank_share_c2.jsonl).  Polish time per sample ~1.5e-11 s per sweep, N-body time
+    # per target ~2.6e-13 s per source: overlap iff mean sweeps >= 2.7e-3 (G + p).  The
+    # rule uses the previous projection's sweep counts, so it is deterministic.
+    OVERLAP_MIN_SWEEPS_PER_SOURCE = 2.7e-3
+
+    def _use_overlap(self) -> bool:
+        env = os.environ.get("SPK_OVERLAP")
+        if env is not None:
+            return env == "1"
+        if self.sweeps_prev is None:
+            return False
+        n_src = self.p + int(np.prod(self.fld.sides))
+        mean = float(self.sweeps_prev.to(torch.float64).mean().item())
+        return mean >= self.OVERLAP_MIN_SWEEPS_PER_SOURCE * n_src
+
     def step_project(self, proj_cfg, eta: float) -> bool:
         """coords <- P(coords - eta * grad); returns False if the step was non-finite."""
         self.flag.zero_()
-        if self.overlap:
+        if self.overlap and self._use_overlap():
             order = None
             if self.sweeps_prev is not None:
                 order = torch.argsort(self.sweeps_prev, descending=True,
@@ -301,6 +312,11 @@ class ShardedRun:
                                            self.fld, self.att_val, self.att_grad,
                                            self.sweeps, order)
             self.att_pre = (self.att_val, self.att_grad)
+            self.sweeps_prev = self.sweeps.clone()
+        elif self.overlap:
+            # plain schedule, but keep the sweep counts that decide and order the overlap
+            out = self.ops.project(self.coords, proj_cfg, self.grad, float(eta), self.next,
+                                   self._pos4_target(), self.flag, self.sweeps)
             self.sweeps_prev = self.sweeps.clone()
         else:
             out = self.ops.project(self.coords, proj_cfg, self.grad, float(eta), self.next,

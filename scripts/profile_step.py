@@ -40,8 +40,9 @@ class PhaseOps(engine.CudaOps):
     def combine(self, *a, **k):
         return self._t("combine", super().combine, *a, **k)
 
-    def project(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite):
-        sw = torch.empty(coords.shape[0], dtype=torch.int32, device=coords.device)
+    def project(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, sweeps=None):
+        sw = sweeps if sweeps is not None else torch.empty(coords.shape[0], dtype=torch.int32,
+                                                           device=coords.device)
         r = self._t("project", project_device, coords, proj_cfg, grad=grad, eta=eta, out=out,
                     pos4=pos4, nonfinite=nonfinite, sweeps=sw)
         self.sweeps.append(sw)
