@@ -2,7 +2,7 @@
   polish  -- single shot / 1024 shots at 1600 fixed sweeps, and the real in-loop C2
              projection (5 warm-up optimizer iterations, then 3 timed step+projections)
   nbody   -- fused K1+K2 at C2 and on a C4 target subset (1/16 of the targets against all
-             sources and the whole lattice) for each FMA/SFU rsqrt split SPK_NB_FMA_RSQRT
+             sources and the whole lattice)
     python scripts/ab_r02.py polish|nbody
 """
 import os
@@ -85,16 +85,10 @@ def nbody():
         n_t = pos4.shape[0] // frac
         tgt = pos4[:n_t]
         ops = engine.CudaOps()
-        for k in ("auto", "0", "1", "2", "3", "4"):
-            if k == "auto":
-                os.environ.pop("SPK_NB_FMA_RSQRT", None)
-            else:
-                os.environ["SPK_NB_FMA_RSQRT"] = k
-            ops.sums(tgt, pos4, coords[:n_t // bench.N_S], fld, cfg)
+        ops.sums(tgt, pos4, coords[:n_t // bench.N_S], fld, cfg)
+        for rep in range(2):
             t = timed(lambda: ops.sums(tgt, pos4, coords[:n_t // bench.N_S], fld, cfg), 2)
-            print(f"{key} (targets {n_t}) fused N-body, FMA rsqrt share {k}/32: {t:.1f} ms",
-                  flush=True)
-        os.environ.pop("SPK_NB_FMA_RSQRT", None)
+            print(f"{key} (targets {n_t}) fused N-body: {t:.1f} ms", flush=True)
         del fld, pos4, coords
         _device.release_workspaces()
 
