@@ -233,13 +233,9 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
     constexpr int TILE = KIND == 0 ? NB_TILE : NB_TILE_W;
     constexpr int REC = KIND == 0 ? 16 : 4;
     constexpr int STAGE_BYTES = NB_TILE * 16;
-    // A stage holds TPS consecutive tiles (lattice: 4 x 512 fp32 weights = 8 KB, the size
-    // of one 512-record position tile), so the CTA barrier that frees a stage for the
-    // next TMA comes once per TPS tiles.
-    constexpr int TPS = KIND == 0 ? 1 : (NB_TILE * 16) / (NB_TILE_W * 4);
-    auto issue = [&](long long t, int stage) {  // tiles t .. t + TPS - 1 (clipped)
+    auto issue = [&](long long t, int stage) {
         const long long first = t * TILE;
-        const long long cnt = min((long long)TILE * TPS, min(t_end * TILE, S.n) - first);
+        const long long cnt = min((long long)TILE, S.n - first);
         const uint32_t bytes = (uint32_t)(((cnt * REC) + 15) & ~15LL);  // weights padded
         mbar_expect_tx(&bars[stage], bytes);
         tma_load_1d(stages + stage * STAGE_BYTES,
@@ -247,27 +243,24 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
     };
     if (tid == 0) {
         for (int s = 0; s < NB_STAGES; ++s)
-            if (t_begin + (long long)s * TPS < t_end) issue(t_begin + (long long)s * TPS, s);
+            if (t_begin + s < t_end) issue(t_begin + s, s);
     }
     for (long long t = t_begin; t < t_end; ++t) {
         const long long i = t - t_begin;
-        const long long grp = i / TPS;
-        const int sub = (int)(i - grp * TPS);
-        const int stage = (int)(grp % NB_STAGES);
-        const uint32_t parity = (uint32_t)((grp / NB_STAGES) & 1);
+        const int stage = (int)(i % NB_STAGES);
+        const uint32_t parity = (uint32_t)((i / NB_STAGES) & 1);
         const int cnt = (int)min((long long)TILE, S.n - t * TILE);
         float2 av[NB_PAIRS], ax[NB_PAIRS], ay[NB_PAIRS], az[NB_PAIRS];
 #pragma unroll
         for (int k = 0; k < NB_PAIRS; ++k) {
             av[k] = ax[k] = ay[k] = az[k] = bc(0.f);
         }
-        if (sub == 0) mbar_wait(&bars[stage], parity);
+        mbar_wait(&bars[stage], parity);
         if (KIND == 0)
             tile_positions<D, G>(reinterpret_cast<const float4*>(stages + stage * STAGE_BYTES),
                                  cnt, X, Y, Z, e2, av, ax, ay, az);
         else
-            tile_lattice<D, G>(reinterpret_cast<const float*>(stages + stage * STAGE_BYTES) +
-                                   sub * TILE,
+            tile_lattice<D, G>(reinterpret_cast<const float*>(stages + stage * STAGE_BYTES),
                                t * TILE, cnt, S, axes, X, Y, Z, e2, av, ax, ay, az);
 #define NB_ACC(k, c) acc[((k) * 4 + (c)) * NB_THREADS + tid]
 #pragma unroll
@@ -283,11 +276,8 @@ __device__ __forceinline__ void run_chunk(const SegDesc& S, long long t_begin, l
                 NB_ACC(2 * k + 1, 3) += az[k].y;
             }
         }
-        if (sub == TPS - 1 || t + 1 == t_end) {
-            __syncthreads();  // every warp is done with this stage
-            const long long next = t_begin + (grp + NB_STAGES) * TPS;
-            if (tid == 0 && next < t_end) issue(next, stage);
-        }
+        __syncthreads();  // every warp is done with this stage
+        if (tid == 0 && t + NB_STAGES < t_end) issue(t + NB_STAGES, stage);
     }
 }
 
