@@ -243,10 +243,14 @@ class ShardedRun:
         """Fused device evaluation -> (att_cost, rep_cost, n_nonfinite, (dkdg, dgdg))."""
         tgt = self._pos4_target()
         if self.att_pre is not None:
-            # K2 already ran under the last polish; only K1 needs the gathered sources
-            va, ga = self.att_pre
+            # K2 ran (or is still running) under the last polish; only K1 needs the
+            # gathered sources, and it co-runs with the tail of K2
+            va, ga, k2_events = self.att_pre
             self.att_pre = None
             vr, gr = self.ops.repulsion_sums(tgt, self.pos4_all, self.cfg)
+            cur = torch.cuda.current_stream()
+            for ev in k2_events:
+                cur.wait_event(ev)
         else:
             va, ga, vr, gr = self.ops.sums(tgt, self.pos4_all, self.coords, self.fld,
                                            self.cfg)
@@ -307,11 +311,10 @@ class ShardedRun:
             if self.sweeps_prev is not None:
                 order = torch.argsort(self.sweeps_prev, descending=True,
                                       stable=True).to(torch.int32)
-            out = self.ops.project_overlap(self.coords, proj_cfg, self.grad, float(eta),
-                                           self.next, self._pos4_target(), self.flag,
-                                           self.fld, self.att_val, self.att_grad,
-                                           self.sweeps, order)
-            self.att_pre = (self.att_val, self.att_grad)
+            out, k2_events = self.ops.project_overlap(
+                self.coords, proj_cfg, self.grad, float(eta), self.next, self._pos4_target(),
+                self.flag, self.fld, self.att_val, self.att_grad, self.sweeps, order)
+            self.att_pre = (self.att_val, self.att_grad, k2_events)
             self.sweeps_prev = self.sweeps.clone()
         elif self.overlap:
             # plain schedule, but keep the sweep counts that decide and order the overlap

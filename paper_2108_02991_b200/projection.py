@@ -201,7 +201,9 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
     its own high-priority stream, and each group's K2 (spk_grid_sums_shots) follows on a
     low-priority stream.  The projection itself is unchanged (bit-identical per shot);
     K2 writes ``att_val`` [n_shots * n_s] / ``att_grad`` [n_shots * n_s, d] for the NEW
-    positions ``pos4``.  Returns ``out``; ``sweeps`` receives this call's sweep counts."""
+    positions ``pos4``.  Returns ``(out, k2_events)``: the caller's stream has waited for
+    the projection; wait on ``k2_events`` before reading ``att_val`` / ``att_grad``.
+    ``sweeps`` receives this call's sweep counts."""
     n_c, n_s, dims = coords.shape
     pin_idx, pin_val = _pin_arrays(cfg, dims)
     tau = 1.0 / stacked_operator_norm(n_s, pin_idx)
@@ -246,11 +248,17 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
                      att_grad.data_ptr(), kws.data_ptr(), kws.numel(), ks.cuda_stream)
         ev = torch.cuda.Event()
         ev.record(ks)
-        # the shot list (a slice of the caller's order tensor) is read on both streams
-        ids.record_stream(ps)
-        ids.record_stream(ks)
+        # buffers used on the side streams stay reserved until that work completes, even
+        # if the caller drops them first (caching-allocator stream semantics)
+        for t, st in ((ids, ps), (ids, ks), (out, ps), (sweeps, ps), (pos4, ps), (pos4, ks),
+                      (att_val, ks), (att_grad, ks)):
+            t.record_stream(st)
         done.append((ps, ev))
+    # the caller's stream waits for the polish only: K1 (which needs the gathered
+    # positions, not K2) can then co-run with the tail of the SFU-bound K2 launches; the
+    # returned events must be waited on before the K2 results are read
+    k2_events = []
     for ps, ev in done:
         main.wait_stream(ps)
-        main.wait_event(ev)
-    return out
+        k2_events.append(ev)
+    return out, k2_events

@@ -107,14 +107,17 @@ def main():
                 f = [ev() for _ in range(3)]
                 torch.cuda.synchronize()
                 f[0].record()
-                ops.project_overlap(coords, pcfg, grad, float(eta), out, pos4, flag, fld, av,
-                                    ag, sw2, order)
+                _, k2ev = ops.project_overlap(coords, pcfg, grad, float(eta), out, pos4, flag,
+                                              fld, av, ag, sw2, order)
                 f[1].record()
                 vr2, gr2 = ops.repulsion_sums(tgt, run.pos4_all, cfg)
+                for e_ in k2ev:
+                    torch.cuda.current_stream().wait_event(e_)
                 ops.combine(av, ag, vr2, gr2, run.p, coords, None, None, grad.view(-1, d))
                 ops.residuals(out, pcfg)
                 f[2].record()
                 torch.cuda.synchronize()
+                # projection (K2 may continue past f[1]), then K1 co-running with K2's tail
                 rec["overlap_project_k2_ms"] = f[0].elapsed_time(f[1])
                 rec["overlap_k1_combine_ms"] = f[1].elapsed_time(f[2])
                 prev_sweeps[key] = sw.clone()
