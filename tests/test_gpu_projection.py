@@ -188,3 +188,79 @@ def test_ring_configurations_vs_oracle(spk, d, ns, pin, mono, cap):
     assert np.array_equal(sw, rsw), (sw, rsw)
     assert np.array_equal(out, ref), np.abs(out - ref).max()
 
+
+
+@pytest.mark.parametrize("d,ns", [(3, 256), (2, 100), (3, 1030)])
+def test_fista_then_polish_subsets_equal_project_all(spk, d, ns):
+    """spk_project_fista + spk_polish_shots on shuffled disjoint shot lists, launched on
+    two streams, equal spk_project_all bit for bit (outputs, positions, sweep counts) --
+    the building blocks of the multi-GPU overlap schedule."""
+    from paper_2108_02991_b200 import _device, _native
+    from paper_2108_02991_b200.projection import _pin_arrays, project_device, stacked_operator_norm
+
+    rng = np.random.default_rng(ns + d)
+    n = 11
+    shots = rng.uniform(-1.1, 1.1, (n, ns, d)) * np.linspace(0.2, 1.0, ns)[None, :, None]
+    cfg = spk.ProjectionConfig(alpha=0.05, beta=0.004, raster_dt=1.0, n_pit=80,
+                               pin=spk.LinearConstraint(ns // 2, np.zeros(d)))
+    dev = _device.h2d(shots)
+    ref = torch.empty_like(dev)
+    ref4 = torch.empty((n * ns, 4), dtype=torch.float32, device=dev.device)
+    ref_sw = torch.empty(n, dtype=torch.int32, device=dev.device)
+    project_device(dev, cfg, out=ref, pos4=ref4, sweeps=ref_sw)
+    pin_idx, pin_val = _pin_arrays(cfg, d)
+    pv = _native.f64_array(list(pin_val) + [0.0] * (3 - d))
+    tau = 1.0 / stacked_operator_norm(ns, pin_idx)
+    ws = _device.workspace(_native.query("spk_project_workspace_bytes", n, ns, d, 0), "t_split")
+    out = torch.empty_like(dev)
+    pos4 = torch.empty_like(ref4)
+    sw = torch.empty_like(ref_sw)
+    _native.call("spk_project_fista", dev.data_ptr(), None, 0.0, None, out.data_ptr(), n, ns, d,
+                 cfg.speed_bound, cfg.accel_bound, pin_idx, pv, cfg.n_pit, tau, 0, None, None,
+                 ws.data_ptr(), ws.numel(), _device.stream())
+    perm = torch.tensor(rng.permutation(n), dtype=torch.int32, device=dev.device)
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(main)
+    for ids, st in ((perm[:5], main), (perm[5:], side)):
+        _native.call("spk_polish_shots", out.data_ptr(), ids.data_ptr(), ids.numel(), n, ns, d,
+                     cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 0.1 * cfg.feas_tol,
+                     50000, pos4.data_ptr(), sw.data_ptr(), ws.data_ptr(), ws.numel(),
+                     st.cuda_stream)
+    main.wait_stream(side)
+    assert torch.equal(out, ref) and torch.equal(pos4, ref4) and torch.equal(sw, ref_sw)
+    # argument errors are reported, not executed
+    with pytest.raises(ValueError):
+        _native.call("spk_polish_shots", out.data_ptr(), perm.data_ptr(), n + 1, n, ns, d,
+                     cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 1e-7, 50000, None, None,
+                     ws.data_ptr(), ws.numel(), _device.stream())
+
+
+def test_grid_sums_on_shot_subset(spk):
+    """spk_grid_sums_shots fills exactly the rows of the listed shots with the lattice
+    sums (fp32 pair math: <= 1e-4 relative l2 of the gradient vs the fp64 oracle, like
+    spk_grid_sums) and leaves the other rows untouched."""
+    from paper_2108_02991_b200 import _device, _native
+
+    rng = np.random.default_rng(5)
+    n, ns, d = 9, 300, 3
+    pts = rng.uniform(-1, 1, (n * ns, d))
+    rho = spk.discretize(spk.DensityParams(0.25, 2.0), 10, d)
+    fld = spk.precompute_field(rho)
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    ids = torch.tensor([7, 2, 4], dtype=torch.int32, device=pos4.device)
+    val = torch.full((n * ns,), -7.0, dtype=torch.float64, device=pos4.device)
+    grad = torch.full((n * ns, d), -7.0, dtype=torch.float64, device=pos4.device)
+    w = fld.device_sources()
+    nb = _native.query("spk_grid_sums_shots_workspace_bytes", 3, ns, int(np.prod(fld.sides)))
+    ws = _device.workspace(nb, "t_gs")
+    _native.call("spk_grid_sums_shots", pos4.data_ptr(), ids.data_ptr(), 3, ns, w.data_ptr(),
+                 _native.i64_array(fld.sides), d, float(fld.kernel_eps ** 2), val.data_ptr(),
+                 grad.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
+    v, g = _device.d2h(val), _device.d2h(grad)
+    rows = np.concatenate([np.arange(s * ns, (s + 1) * ns) for s in (7, 2, 4)])
+    other = np.setdiff1d(np.arange(n * ns), rows)
+    assert np.all(v[other] == -7.0) and np.all(g[other] == -7.0)
+    vo, go = orc.grid_sums(pts[rows], rho.grid, fld.kernel_eps ** 2)
+    assert np.linalg.norm(g[rows] - go) <= 1e-4 * np.linalg.norm(go)
+    assert np.abs(v[rows] - vo).max() <= 1e-5 * np.abs(vo).max()
