@@ -5,7 +5,8 @@ tree 1e-3, attraction treecode 1e-4), timed on ONE B200.
 The schedule runs for real on one GPU.  At iteration --probe of every level (inside the
 fixed-step phase, so every rank would use the same step eta0) each rank's share of that
 iteration at N = 1, 2, 4, 8 is timed in isolation: its targets against all sources
-(treecode repulsion and lattice attraction, incl. the per-rank tree builds), the
+(treecode repulsion and lattice attraction, incl. the per-rank tree builds; the
+auto-mode probe, which a run does once per level, is warmed untimed), the
 combine, the projection of its shots.  The N-rank iteration is the slowest rank plus the
 position all-gather (estimated at 600 GB/s).  Per level the projected time is
 n_git x that; the sum over levels is the projected schedule time.
@@ -60,6 +61,12 @@ while True:
             base, extra = divmod(cfg.n_c, n)
             counts = [base + (1 if r < extra else 0) for r in range(n)]
             offs = [sum(counts[:r]) for r in range(n)]
+            # the treecodes' auto-mode probe runs once per (sizes, precision) and level
+            # in a real run (row cache): warm it for this share size, untimed
+            g0 = torch.empty((counts[0], ns, d), dtype=torch.float64, device="cuda")
+            ops.sums(run.pos4_all[:counts[0] * ns], run.pos4_all, run.coords[:counts[0]],
+                     state.fld, cfg)
+            del g0
             per = []
             for r in range(n):
                 lo, cnt = offs[r], counts[r]
