@@ -248,9 +248,10 @@ class ShardedRun:
             va, ga, k2_events = self.att_pre
             self.att_pre = None
             vr, gr = self.ops.repulsion_sums(tgt, self.pos4_all, self.cfg)
-            cur = torch.cuda.current_stream()
-            for ev in k2_events:
-                cur.wait_event(ev)
+            if k2_events:
+                cur = torch.cuda.current_stream()
+                for ev in k2_events:
+                    cur.wait_event(ev)
         else:
             va, ga, vr, gr = self.ops.sums(tgt, self.pos4_all, self.coords, self.fld,
                                            self.cfg)

@@ -55,7 +55,7 @@ class OracleOps:
         out[4] = np.count_nonzero(~np.isfinite(g))
         return torch.from_numpy(out)
 
-    def project(self, coords, cfg, grad, eta, out, pos4, nonfinite):
+    def project(self, coords, cfg, grad, eta, out, pos4, nonfinite, sweeps=None):
         k = coords.numpy()
         if grad is not None:
             k = k - eta * grad.numpy()
@@ -65,12 +65,15 @@ class OracleOps:
         pin = -1 if cfg.pin is None else cfg.pin.pinned_index
         pv = np.zeros(d) if cfg.pin is None else cfg.pin.pinned_value
         tau = 1.0 / stacked_operator_norm(n_s, pin)
-        res, _ = orc.project_all(k, cfg.speed_bound, cfg.accel_bound, pin, pv, cfg.n_pit,
-                                 tau, 0.1 * cfg.feas_tol, monotone=cfg.monotone)
+        res, sw = orc.project_all(k, cfg.speed_bound, cfg.accel_bound, pin, pv, cfg.n_pit,
+                                  tau, 0.1 * cfg.feas_tol, monotone=cfg.monotone)
         out.copy_(torch.from_numpy(res))
         if pos4 is not None:
             self._fill_pos4(out, pos4)
+        if sweeps is not None:
+            sweeps.copy_(torch.from_numpy(sw.astype(np.int32)))
         return out
+
 
     def residuals(self, coords, cfg):
         c = coords.numpy()
@@ -92,3 +95,36 @@ class OracleOps:
         up[:, 1:-1:2] = 0.5 * (c[:, :-1] + c[:, 1:])
         up[:, -1] = c[:, -1] + 0.5 * (c[:, -1] - c[:, -2])
         return torch.from_numpy(np.clip(up, -1.0, 1.0))
+
+
+class OverlapOracleOps(OracleOps):
+    """OracleOps with the engine's K2-under-polish schedule (engine.ShardedRun.overlap):
+    the projection of each polish group (shots in ``order``) followed by that group's
+    lattice sums, synchronously -- exercises the schedule's bookkeeping (shot order from
+    the previous sweeps, per-rank K2 rows, K1 alone afterwards) on the CPU."""
+
+    OVERLAP_GROUPS = 3
+
+    def overlap_capable(self, cfg):
+        return cfg.grad_mode == "exact"
+
+    def project_overlap(self, coords, cfg, grad, eta, out, pos4, nonfinite, fld, att_val,
+                        att_grad, sweeps, order):
+        self.overlap_calls = getattr(self, "overlap_calls", 0) + 1
+        self.project(coords, cfg, grad, eta, out, pos4, nonfinite, sweeps)
+        n_c, n_s, d = coords.shape
+        ids = np.arange(n_c) if order is None else order.numpy()
+        assert sorted(ids.tolist()) == list(range(n_c))
+        for grp in np.array_split(ids, self.OVERLAP_GROUPS):
+            for c in grp:
+                t = pos4[c * n_s:(c + 1) * n_s, :d].double().numpy()
+                va, ga = orc.grid_sums(t, fld.density.grid, fld.kernel_eps ** 2)
+                att_val[c * n_s:(c + 1) * n_s] = torch.from_numpy(va)
+                att_grad[c * n_s:(c + 1) * n_s] = torch.from_numpy(ga)
+        return out, []
+
+    def repulsion_sums(self, tgt4, src4, cfg):
+        d = cfg.dims
+        vr, gr = orc.cross_sums(tgt4[:, :d].double().numpy(), src4[:, :d].double().numpy(),
+                                cfg.repulsion.kernel_eps ** 2)
+        return torch.from_numpy(vr), torch.from_numpy(gr)

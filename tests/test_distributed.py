@@ -153,3 +153,37 @@ def test_patched_evaluator_two_ranks_match_one(tmp_path, monkeypatch):
     got = np.load(out)
     assert np.allclose(got["costs"], single.trace.costs(), rtol=1e-12, atol=0)
     assert np.abs(got["coords"] - single.pattern.coords).max() <= 1e-9
+
+
+def _worker_overlap(rank, world, port, n_c, out_path):
+    from cpu_ops import OverlapOracleOps
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["SPK_OVERLAP"] = "1"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops = OverlapOracleOps()
+        res = spk.optimize(_cfg(n_c), _hw(), ops=ops)
+        if rank == 0:
+            np.savez(out_path, coords=res.pattern.coords, costs=res.trace.costs(),
+                     calls=np.int64(ops.overlap_calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlap_schedule_two_ranks_matches_plain(tmp_path, monkeypatch):
+    """The K2-under-polish schedule (per-rank K2 rows computed with the projection, K1
+    alone in the next evaluation, polish groups ordered by the previous sweeps) on two
+    gloo ranks reproduces the plain single-rank loop: the oracle's lattice sums are
+    row-wise fp64, so the results must match to the rank-order reduction of the scalars."""
+    from cpu_ops import OracleOps
+
+    monkeypatch.setenv("SPK_OVERLAP", "0")
+    single = spk.optimize(_cfg(5), _hw(), ops=OracleOps())
+    out = str(tmp_path / "o.npz")
+    mp.spawn(_worker_overlap, args=(2, _free_port(), 5, out), nprocs=2, join=True)
+    got = np.load(out)
+    assert int(got["calls"]) > 0
+    assert np.allclose(got["costs"], single.trace.costs(), rtol=1e-12, atol=0)
+    assert np.abs(got["coords"] - single.pattern.coords).max() <= 1e-9
