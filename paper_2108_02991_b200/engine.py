@@ -137,6 +137,23 @@ class CudaOps:
     def repulsion_sums(self, tgt4, src4, cfg):
         return direct_sums_device(tgt4, src4, cfg.dims, cfg.repulsion.kernel_eps ** 2)
 
+    # ---- spatial target partition for the treecodes (ShardedRun.spatial)
+    def spatial_capable(self, cfg) -> bool:
+        """Treecode sums cost per target depends on how densely a rank's targets fill
+        space: a shot-sharded rank holds every 1/N-th spoke everywhere, so its target
+        groups are sparse.  With the treecodes the N-body targets are therefore split by
+        Morton order (compact blocks) instead of by shot."""
+        return cfg.grad_mode == "exact" and (cfg.repulsion.backend == "tree"
+                                             or cfg.attraction_tree_precision is not None)
+
+    def spatial_order(self, pos4, dims):
+        """Permutation of the samples along the Morton curve (device int64; the same on
+        every rank for the same positions)."""
+        from . import tree
+
+        _, perm = tree._sort(pos4, dims)
+        return perm.long()
+
     def upsample(self, coords):
         n_c, n_s, d = coords.shape
         out = self.empty((n_c, 2 * n_s, d))
@@ -194,6 +211,9 @@ class ShardedRun:
         # K2-under-polish overlap: the lattice sums of the positions the last projection
         # produced (att_pre), and the polish sweep counts that order the next one
         self.overlap = hasattr(ops, "overlap_capable") and ops.overlap_capable(self.cfg)
+        env = os.environ.get("SPK_SPATIAL")
+        self.spatial = (hasattr(ops, "spatial_capable") and ops.spatial_capable(self.cfg)
+                        and (self.world > 1 if env is None else env == "1"))
         self.att_pre = None
         self.sweeps_prev = None
         if self.overlap:
@@ -242,7 +262,9 @@ class ShardedRun:
     def evaluate(self):
         """Fused device evaluation -> (att_cost, rep_cost, n_nonfinite, (dkdg, dgdg))."""
         tgt = self._pos4_target()
-        if self.att_pre is not None:
+        if self.spatial:
+            va, ga, vr, gr = self._spatial_sums()
+        elif self.att_pre is not None:
             # K2 ran (or is still running) under the last polish; only K1 needs the
             # gathered sources, and it co-runs with the tail of K2
             va, ga, k2_events = self.att_pre
@@ -267,6 +289,35 @@ class ShardedRun:
         att_cost = float(tot[0] / p)
         rep_cost = float(tot[1] / (2.0 * p * p))
         return att_cost, rep_cost, int(tot[4]), (float(tot[2]), float(tot[3]))
+
+    def _spatial_sums(self):
+        """N-body sums with the targets split by Morton order: rank r evaluates the r-th
+        contiguous block of the sorted samples against all sources, the blocks' results
+        are all-gathered (p x (2 + 2d) fp64, rank order) and every rank keeps the rows of
+        its own shots.  Deterministic for a given world size."""
+        d, p = self.d, self.p
+        perm = self.ops.spatial_order(self.pos4_all, d)
+        bounds = [p * r // self.world for r in range(self.world + 1)]
+        lo, hi = bounds[self.rank], bounds[self.rank + 1]
+        tgt = self.pos4_all[perm[lo:hi]].contiguous()
+        va, ga, vr, gr = self.ops.sums(tgt, self.pos4_all, None, self.fld, self.cfg)
+        w = 2 + 2 * d
+        pack = torch.cat([va.reshape(-1, 1), ga.reshape(-1, d), vr.reshape(-1, 1),
+                          gr.reshape(-1, d)], dim=1)
+        if self.world > 1:
+            m = max(bounds[r + 1] - bounds[r] for r in range(self.world))
+            pad = self.ops.empty((m, w))
+            pad[:hi - lo] = pack
+            buf = self.ops.empty((self.world * m, w))
+            dist.all_gather_into_tensor(buf, pad, group=self.group)
+            pack = torch.cat([buf[r * m:r * m + bounds[r + 1] - bounds[r]]
+                              for r in range(self.world)])
+        full = self.ops.empty((p, w))
+        full.index_copy_(0, perm, pack)
+        n_s = self.n_s
+        mine = full[self.offsets[self.rank] * n_s:(self.offsets[self.rank] + self.local) * n_s]
+        return (mine[:, 0].contiguous(), mine[:, 1:1 + d].contiguous(),
+                mine[:, 1 + d].contiguous(), mine[:, 2 + d:].contiguous())
 
     def set_host_gradient(self, grad: np.ndarray):
         """Patched-evaluator path: install a host gradient of ALL shots (every rank

@@ -8,7 +8,10 @@ iteration at N = 1, 2, 4, 8 is timed in isolation: its targets against all sourc
 (treecode repulsion and lattice attraction, incl. the per-rank tree builds; the
 auto-mode probe, which a run does once per level, is warmed untimed), the
 combine, the projection of its shots.  The N-rank iteration is the slowest rank plus the
-position all-gather (estimated at 600 GB/s).  Per level the projected time is
+position all-gather (estimated at 600 GB/s).  Two layouts of the N-body targets are timed:
+by shot (each rank's own samples) and spatial (engine.ShardedRun.spatial: rank r takes the
+r-th Morton-order block of all samples; plus the all-gather that returns the results to
+the shots' owners, estimated likewise).  Per level the projected time is
 n_git x that; the sum over levels is the projected schedule time.
 
     python scripts/rank_share_schedule.py [--n-git 100] [--probe 10] > profiles/r02_rank_share_full3d.json
@@ -68,6 +71,11 @@ while True:
                      state.fld, cfg)
             del g0
             per = []
+            perm = ops.spatial_order(run.pos4_all, d)
+            sb = [run.p * r // n for r in range(n + 1)]
+            # warm the probe for the spatial block size too
+            ops.sums(run.pos4_all[perm[sb[0]:sb[1]]].contiguous(), run.pos4_all, None,
+                     state.fld, cfg)
             for r in range(n):
                 lo, cnt = offs[r], counts[r]
                 coords = run.coords[lo:lo + cnt]
@@ -75,7 +83,7 @@ while True:
                 grad = torch.empty((cnt, ns, d), dtype=torch.float64, device="cuda")
                 out = torch.empty_like(grad)
                 pos4 = torch.empty((cnt * ns, 4), dtype=torch.float32, device="cuda")
-                e = [ev() for _ in range(3)]
+                e = [ev() for _ in range(5)]
                 torch.cuda.synchronize()
                 e[0].record()
                 va, ga, vr, gr = ops.sums(tgt, run.pos4_all, coords, state.fld, cfg)
@@ -84,12 +92,26 @@ while True:
                 ops.project(coords, state.proj_cfg, grad, float(state.eta0), out, pos4, None)
                 ops.residuals(out, state.proj_cfg)
                 e[2].record()
+                # spatial layout (engine.ShardedRun.spatial): this rank's Morton block
+                blk = run.pos4_all[perm[sb[r]:sb[r + 1]]].contiguous()
+                e[3].record()
+                ops.sums(blk, run.pos4_all, None, state.fld, cfg)
+                e[4].record()
                 torch.cuda.synchronize()
-                per.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])))
+                per.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]),
+                            e[3].elapsed_time(e[4])))
             gather = 16.0 * run.p * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
-            step = max(s + p for s, p in per) + gather
-            rec["ranks"][n] = {"step_ms": step, "max_sums_ms": max(s for s, _ in per),
-                               "max_project_ms": max(p for _, p in per), "allgather_est_ms": gather}
+            exch = 8.0 * (2 + 2 * d) * run.p * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
+            step = max(s + p for s, p, _ in per) + gather
+            # spatial: sums of the Morton block + combine (same cost as in the shot
+            # layout's sums column, dominated by the sums), projection of the shots
+            step_sp = max(sp for _, _, sp in per) + max(p for _, p, _ in per) + gather + exch
+            rec["ranks"][n] = {"step_ms": step, "max_sums_ms": max(s for s, _, _ in per),
+                               "max_project_ms": max(p for _, p, _ in per),
+                               "allgather_est_ms": gather,
+                               "spatial_step_ms": step_sp,
+                               "spatial_max_sums_ms": max(sp for _, _, sp in per),
+                               "spatial_exchange_est_ms": exch}
         levels.append(rec)
         print(json.dumps(rec), file=sys.stderr, flush=True)
     if om.step(state) is None:
@@ -101,8 +123,11 @@ summary = {"schedule": "full3d.cfg: 4096 x 2048, n_decim 6, n_git %d, repulsion 
            "one_gpu_wall_s_incl_probes": wall, "levels": levels, "projected": {}}
 for n in worlds:
     tot = sum(cfg.n_git * lv["ranks"][n]["step_ms"] for lv in levels) / 1e3
-    summary["projected"][n] = {"schedule_s": tot}
+    tsp = sum(cfg.n_git * lv["ranks"][n]["spatial_step_ms"] for lv in levels) / 1e3
+    summary["projected"][n] = {"schedule_s": tot, "spatial_schedule_s": tsp}
 t1 = summary["projected"][worlds[0]]["schedule_s"]
 for n in worlds:
     summary["projected"][n]["efficiency"] = t1 / (n * summary["projected"][n]["schedule_s"])
+    summary["projected"][n]["spatial_efficiency"] = (
+        t1 / (n * summary["projected"][n]["spatial_schedule_s"]))
 print(json.dumps(summary))

@@ -41,6 +41,23 @@ class OracleOps:
         vr, gr = orc.cross_sums(t, s, cfg.repulsion.kernel_eps ** 2)
         return tuple(torch.from_numpy(x) for x in (va, ga, vr, gr))
 
+    def spatial_capable(self, cfg):
+        # the spatial target partition (engine.ShardedRun.spatial) only when a test asks
+        import os
+
+        return os.environ.get("SPK_SPATIAL") == "1"
+
+    def spatial_order(self, pos4, dims):
+        """Morton order of the samples (21 bits per axis), deterministic, like the
+        device sort."""
+        q = np.clip(((pos4[:, :dims].double().numpy() + 1.0) * 0.5 * (1 << 21)).astype(np.int64),
+                    0, (1 << 21) - 1)
+        key = np.zeros(q.shape[0], dtype=np.int64)
+        for bit in range(21):
+            for a in range(dims):
+                key |= ((q[:, a] >> bit) & 1) << (bit * dims + a)
+        return torch.from_numpy(np.argsort(key, kind="stable"))
+
     def combine(self, va, ga, vr, gr, p, coords, prev_c, prev_g, grad_out):
         g = ga.numpy() / float(p) - gr.numpy() / (float(p) * float(p))
         grad_out.copy_(torch.from_numpy(g))

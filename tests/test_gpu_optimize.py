@@ -199,3 +199,24 @@ def test_k2_under_polish_overlap_matches_plain_loop(spk, monkeypatch, dims, n_c)
     rel = np.abs(ovl.trace.costs() - plain.trace.costs()) / np.abs(plain.trace.costs())
     assert rel.max() <= 1e-6, rel.max()
     assert np.abs(ovl.pattern.coords - plain.pattern.coords).max() <= 1e-5
+
+
+def test_spatial_target_partition_on_device(spk, monkeypatch):
+    """The treecodes' spatial layout (ShardedRun.spatial: N-body targets in Morton-order
+    blocks, results returned to the shot owners; forced on a single GPU with
+    SPK_SPATIAL=1) gives the same iteration as the shot layout to the treecode's
+    precision: the lattice treecode groups a differently ordered target set."""
+    hw = desk_hw(spk, dims=3, matrix=16)
+    cfg = spk.OptimizerConfig(n_c=16, n_s=64, dims=3, n_decim=1, n_git=4, grad_mode="exact",
+                              seed=4, grid_n=12, attraction_tree_precision=1e-4)
+    monkeypatch.setenv("SPK_SPATIAL", "0")
+    plain = spk.optimize(cfg, hw)
+    monkeypatch.setenv("SPK_SPATIAL", "1")
+    from paper_2108_02991_b200 import optimizer as om
+
+    st = om.start(cfg, hw)
+    assert st.run.spatial
+    sp = om.finish(st)
+    rel = np.abs(sp.trace.costs() - plain.trace.costs()) / np.abs(plain.trace.costs())
+    assert rel.max() <= 1e-4, rel.max()
+    assert np.abs(sp.pattern.coords - plain.pattern.coords).max() <= 1e-3
