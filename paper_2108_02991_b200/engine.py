@@ -109,7 +109,7 @@ class CudaOps:
         return residuals_device(coords, proj_cfg)
 
     # ---- K2-under-polish overlap (ShardedRun.overlap)
-    OVERLAP_GROUPS = 8
+    OVERLAP_GROUPS = int(os.environ.get("SPK_OVERLAP_GROUPS", "8"))
 
     def overlap_capable(self, cfg) -> bool:
         """Eligible for the K2-under-polish schedule: exact lattice attraction and exact
