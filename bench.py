@@ -853,9 +853,11 @@ def main():
                 print(f"bench.py: {key}: {rec['ms_per_step'] / 1e3:.3f} s/it "
                       f"({rec['wall_s']:.0f} s wall)", file=sys.stderr, flush=True)
         select_workload(args.config)
+    # after the process group is destroyed: NCCL's INIT-subsystem INFO lines (which go to
+    # stdout, N > 1) then all precede the JSON line, which stays the last line
+    ctx.close()
     if ctx.rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
 
 
 if __name__ == "__main__":
