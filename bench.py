@@ -382,8 +382,13 @@ def ensure_world(args) -> None:
             sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank "
                      f"per GPU (torchrun --nproc-per-node {args.gpus})")
         if args.gpus > 1:
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            # rank 0's NCCL INIT lines show the N-rank communicator; the other ranks stay
+            # quiet so that nothing can follow rank 0's JSON line on the shared stdout
+            if os.environ.get("RANK", "0") == "0":
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            else:
+                os.environ["NCCL_DEBUG"] = "WARN"
         return
     if args.gpus <= 1:
         return
@@ -394,8 +399,6 @@ def ensure_world(args) -> None:
         sys.exit(f"bench.py: --gpus {args.gpus} requested but this node has {have} CUDA "
                  f"device(s); refusing to report a {args.gpus}-GPU number")
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
            f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
