@@ -441,9 +441,6 @@ constexpr int PL_LAG = 4;
 #ifndef SPK_BOX_FAST
 #define SPK_BOX_FAST 1
 #endif
-#ifndef SPK_POLISH_BRANCHFREE
-#define SPK_POLISH_BRANCHFREE 0
-#endif
 
 template <int D>
 struct Sample {
@@ -483,27 +480,6 @@ __device__ __forceinline__ void speed_pair(Sample<D>& x0, Sample<D>& x1, int n, 
         df[l] = x1.v[l] - x0.v[l];
         nrm += df[l] * df[l];
     }
-#if SPK_POLISH_BRANCHFREE
-    if (n != pin && n + 1 != pin) {
-        // unpinned pair without branches: in-loop some lane of a warp is active in almost
-        // every step, so the warp pays sqrt + div anyway; straight-line code lets the
-        // scheduler interleave this chain with the rest of the step.  Inactive (or NaN)
-        // pairs keep their samples bit for bit through the selects.
-        const double r = sqrt(nrm);
-        const bool act = r > a;
-        const double ex = r - a;
-        const double shrink = omega * 0.5 * ex / r;
-        worst = (act && ex > worst) ? ex : worst;
-#pragma unroll
-        for (int l = 0; l < D; ++l) {
-            const double t = shrink * df[l];
-            const double u0 = x0.v[l] + t, u1 = x1.v[l] - t;
-            x0.v[l] = act ? u0 : x0.v[l];
-            x1.v[l] = act ? u1 : x1.v[l];
-        }
-        return;
-    }
-#endif
     // exact early out: a*a*(1 - 1e-15) < a^2 in real arithmetic, so nrm^2 below it means
     // sqrt(nrm^2) < a, i.e. the reference's `nrm > a` is false -- skips the IEEE sqrt
     // for the (typically many) pairs well inside the bound; NaN takes the full path
@@ -543,27 +519,6 @@ __device__ __forceinline__ void accel_triple(Sample<D>& x0, Sample<D>& x1, Sampl
         w[l] = x0.v[l] - 2.0 * x1.v[l] + x2.v[l];
         nrm += w[l] * w[l];
     }
-#if SPK_POLISH_BRANCHFREE
-    if (pin != n && pin != n + 1 && pin != n + 2) {
-        // unpinned triple without branches (see speed_pair)
-        const double r = sqrt(nrm);
-        const bool act = r > b;
-        const double ex = r - b;
-        const double step = omega * ex / (6.0 * r);
-        const double step1 = step * -2.0;
-        worst = (act && ex > worst) ? ex : worst;
-#pragma unroll
-        for (int l = 0; l < D; ++l) {
-            const double u0 = x0.v[l] - step * w[l];
-            const double u1 = x1.v[l] - step1 * w[l];
-            const double u2 = x2.v[l] - step * w[l];
-            x0.v[l] = act ? u0 : x0.v[l];
-            x1.v[l] = act ? u1 : x1.v[l];
-            x2.v[l] = act ? u2 : x2.v[l];
-        }
-        return;
-    }
-#endif
     if (nrm <= b * b * (1.0 - 1e-15)) return;  // exact early out, as in speed_pair
     nrm = sqrt(nrm);
     if (!(nrm > b)) return;
