@@ -59,3 +59,34 @@ def test_library_usable_after_errors(env):
 
     cost, grad = spk.eval_repulsion_direct(np.array([[0.0, 0.0], [1.0, 0.0]]), eps=0.0)
     assert abs(cost - 0.25) < 1e-7 and np.abs(grad).max() == pytest.approx(0.25, rel=1e-7)
+
+
+def test_round2_entry_point_errors(env):
+    """spk_grid_sums_shots / spk_polish_shots / spk_project_fista reject bad arguments and
+    undersized workspaces like the other entry points."""
+    _device, _native = env
+    dev = _device.device()
+    p4 = _device.pack_positions(_device.h2d(np.zeros((32, 3))))
+    val = torch.empty(32, dtype=torch.float64, device=dev)
+    grad = torch.empty((32, 3), dtype=torch.float64, device=dev)
+    w = torch.zeros(28, dtype=torch.float32, device=dev)
+    side = _native.i64_array([3, 3, 3])
+    ids = torch.tensor([1, 3], dtype=torch.int32, device=dev)
+    tiny = torch.empty(16, dtype=torch.uint8, device=dev)
+    with pytest.raises(ValueError, match="null shot list"):
+        _native.call("spk_grid_sums_shots", p4.data_ptr(), None, 2, 8, w.data_ptr(), side, 3,
+                     1e-4, val.data_ptr(), grad.data_ptr(), tiny.data_ptr(), tiny.numel(),
+                     _device.stream())
+    with pytest.raises(_native.NativeError, match="workspace"):
+        _native.call("spk_grid_sums_shots", p4.data_ptr(), ids.data_ptr(), 2, 8, w.data_ptr(),
+                     side, 3, 1e-4, val.data_ptr(), grad.data_ptr(), tiny.data_ptr(),
+                     tiny.numel(), _device.stream())
+    shots = _device.h2d(np.zeros((4, 8, 3)))
+    with pytest.raises(_native.NativeError, match="workspace"):
+        _native.call("spk_polish_shots", shots.data_ptr(), ids.data_ptr(), 2, 4, 8, 3, 0.1, 0.1,
+                     -1, _native.f64_array([0, 0, 0]), 1e-7, 100, None, None, tiny.data_ptr(),
+                     tiny.numel(), _device.stream())
+    with pytest.raises(ValueError, match="n_pit"):
+        _native.call("spk_project_fista", shots.data_ptr(), None, 0.0, None, shots.data_ptr(),
+                     4, 8, 3, 0.1, 0.1, -1, _native.f64_array([0, 0, 0]), 0, 0.05, 0, None,
+                     None, tiny.data_ptr(), tiny.numel(), _device.stream())
