@@ -636,7 +636,6 @@ struct RingLane {
     Sample<D> slot[4];  // register window, roles rotate with the global step (mod 4)
     double worst;
     int t, j, k;        // local step in the current round, round, sweep index
-    int jm;             // j modulo the number of wrap buffers
 #ifdef SPK_POLISH_PROF
     unsigned long long prof[7];
     unsigned long long tp;
@@ -669,34 +668,8 @@ __device__ unsigned long long spk_polish_prof[3][7];
 #define SPK_RING_K 4
 #endif
 constexpr int RING_K = SPK_RING_K;
-constexpr int RING_K_SHIFT = RING_K == 1 ? 0 : RING_K == 2 ? 1 : RING_K == 4 ? 2 : RING_K == 8 ? 3 : 4;
-// stop-test (CTA barrier) period with three wrap buffers; neighbour pairs in between
-#ifndef SPK_PL_STOP_SHIFT
-#define SPK_PL_STOP_SHIFT 5
-#endif
-constexpr int PL_STOP_SHIFT = SPK_PL_STOP_SHIFT;
-#ifndef SPK_PAIR_BAR
-#define SPK_PAIR_BAR 0
-#endif
 static_assert(RING_K >= 1 && (RING_K & (RING_K - 1)) == 0, "RING_K must be a power of two");
 __device__ __forceinline__ int ring_offset(int g) { return PL_LAG * g + RING_K * (g >> 5); }
-
-// Neighbour-only barrier of the ring: the only per-step cross-warp traffic is the
-// hand-over from warp w - 1 to warp w, so between the CTA-wide barriers (which the stop
-// test needs) warps w and w + 1 synchronise pairwise (named barrier w + 1, 64 threads):
-// first the pairs (0,1), (2,3), ..., then (1,2), (3,4), ... -- two levels, no chain.
-__device__ __forceinline__ void named_bar(int id) {
-    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
-}
-__device__ __forceinline__ void pair_sync(int warp, int W) {
-    if (warp & 1) {
-        named_bar(warp);
-        if (warp + 1 < W) named_bar(warp + 1);
-    } else {
-        if (warp + 1 < W) named_bar(warp + 1);
-        if (warp > 0) named_bar(warp);
-    }
-}
 
 // One global step of the ring.  R = st mod 4 fixes which window slot plays w0..w3
 // (w0 = s[t-2] = slot[R], ..., w3 = s[t+1] = slot[R+3]); the received sample s[t+2]
@@ -710,8 +683,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
                                           double pv1, double pv2, double tol,
                                           const double* __restrict__ s0, double* snap0,
                                           double* res, double* xfer, double* wrap0,
-                                          int wstride, int nwrap, int stop_shift,
-                                          int* stop_sh) {  // stop_sh[2]
+                                          int wstride, int* stop_sh) {  // stop_sh[2]
     Sample<D>& w0 = L.slot[R & 3];
     Sample<D>& w1 = L.slot[(R + 1) & 3];
     Sample<D>& w2 = L.slot[(R + 2) & 3];
@@ -740,7 +712,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
             if (g == B - 1) {
                 // round j's output stream: wrap buffer j & 1 (both the same buffer when
                 // single-buffered, which then needs the global ping-pong snapshots)
-                double* wb = wrap0 + L.jm * wstride;
+                double* wb = wrap0 + (L.j & 1) * wstride;
 #pragma unroll
                 for (int l = 0; l < D; ++l) wb[(t - 2) * D + l] = w0.v[l];
                 if (wstride == 0) {  // single wrap buffer: ping-pong snapshots in global
@@ -757,7 +729,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
 #endif
         // stop flags alternate per barrier block: a lane already in the next block cannot
         // change the flag the others are about to read at the end of this one
-        if (t == ns + 1 && L.worst <= tol) atomicMin(&stop_sh[(st >> stop_shift) & 1], L.k);
+        if (t == ns + 1 && L.worst <= tol) atomicMin(&stop_sh[(st / RING_K) & 1], L.k);
     }
     // hand the finished sample w0 (= s[t-2]) to the next sweep; it is replaced in slot R
     Sample<D> recv;
@@ -776,8 +748,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
             if (g == 0) {
                 // first sweep of a round: the previous round's last sweep (the initial
                 // state for round 0, staged at kernel start), through the wrap buffer
-                const double* rb =
-                    wrap0 + (L.jm == 0 ? nwrap - 1 : L.jm - 1) * wstride;  // round j - 1's
+                const double* rb = wrap0 + ((L.j + 1) & 1) * wstride;  // round j - 1's stream
 #pragma unroll
                 for (int l = 0; l < D; ++l) recv.v[l] = rb[m * D + l];
             }
@@ -806,16 +777,11 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
     if (++L.t == P - 2) {
         L.t = -2;
         ++L.j;
-        L.jm = L.jm + 1 == nwrap ? 0 : L.jm + 1;
         L.k += B;
     }
     SPK_PROF_MARK(L, 4)
 #ifndef SPK_EXP_NOSYNC
-    if (((st + 1) & (RING_K - 1)) == 0) {
-        // CTA-wide at the stop-test period, neighbour pairs in between (pair_sync)
-        if (((st + 1) >> stop_shift) << stop_shift == st + 1) __syncthreads();
-        else pair_sync(warp, B >> 5);
-    }
+    if (((st + 1) & (RING_K - 1)) == 0) __syncthreads();
 #endif
 #ifdef SPK_POLISH_PROF
     SPK_PROF_MARK(L, 5)
@@ -838,12 +804,10 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
                                                       int32_t* sweeps_out, float4* pos4,
                                                       int wrap_mode,
                                                       const int32_t* __restrict__ shot_ids) {
-    // wrap_mode 3: three wrap buffers in shared memory (round mod 3) -- the replay source
-    // (round j* - 1) then survives a stop detected up to a round late, so the stop test
-    // (and the CTA barrier) runs every PL_STOP_K steps with neighbour-pair barriers in
-    // between; 2: two wrap buffers (round parity), which double as the replay snapshot;
+    // wrap_mode 2: two wrap buffers in shared memory (round parity), which double as the
+    // replay snapshot -- no global snapshot stores on the ring's critical path;
     // 1: one shared wrap buffer + global ping-pong snapshots; 0: wrap in the workspace.
-    extern __shared__ __align__(16) double xfer[];  // [W][2 RING_K][D], then wrap [1|2|3][ns][D]
+    extern __shared__ __align__(16) double xfer[];  // [W][2 RING_K][D], then wrap [1|2][ns][D]
     __shared__ int stop_sh[2];
     // shot of this CTA: the launch's shot list (a subset in any order) or blockIdx.x
     const long long c = shot_ids ? (long long)shot_ids[blockIdx.x] : (long long)blockIdx.x;
@@ -854,9 +818,7 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     // wrap buffer(s) in shared memory, or (very long shots) in the per-shot workspace
     double* wrap0 = wrap_mode == 0 ? ws + c * (size_t)(4 * nd4) + 3 * nd4
                                    : xfer + W * 2 * RING_K * D;
-    const int wstride = wrap_mode >= 2 ? nd4 : 0;
-    const int nwrap = wrap_mode == 3 ? 3 : 2;
-    const int stop_shift = wrap_mode == 3 ? PL_STOP_SHIFT : RING_K_SHIFT;
+    const int wstride = wrap_mode == 2 ? nd4 : 0;
     double* wrap1 = wrap0 + wstride;
     const int g = threadIdx.x;
     const int lane = g & 31;
@@ -872,9 +834,7 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     // stage the initial state in the wrap buffer: lane 0 then reads round 0 from it like
     // every later round (no global-load latency on the ring's critical path).  Lane B-1
     // overwrites position q only 4 + ring_offset(B-1) steps after lane 0 has read it.
-    // round 0 reads buffer (0 - 1) mod nwrap
-    double* wrap_init = wrap0 + (nwrap - 1) * wstride;
-    for (int i = g; i < nd; i += B) wrap_init[i] = s0[i];
+    for (int i = g; i < nd; i += B) wrap1[i] = s0[i];  // round 0 reads buffer (0 - 1) & 1
     __syncthreads();
     const int kl = max_sweeps - 1;
     const int last_step = (kl / B) * P + ring_offset(kl % B) + ns + 3;
@@ -890,16 +850,14 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     L.tp = clock64();
 #endif
     L.j = 0;
-    L.jm = 0;
     L.k = g;
-    const int stop_mask = (1 << stop_shift) - 1;
 #define SPK_RING_STEP(R)                                                                   \
     {                                                                                      \
         ring_step<D, R>(L, st + R, ns, B, P, g, lane, warp, max_sweeps, kl, a, b, pin,     \
-                        pv0, pv1, pv2, tol, s0, snap0, res, xfer, wrap0, wstride, nwrap,   \
-                        stop_shift, stop_sh);                                              \
-        if (((st + R + 1) & stop_mask) == 0 &&                                             \
-            stop_sh[((st + R) >> stop_shift) & 1] != 0x7fffffff)                           \
+                        pv0, pv1, pv2, tol, s0, snap0, res, xfer, wrap0, wstride,          \
+                        stop_sh);                                                          \
+        if (((st + R + 1) & (RING_K - 1)) == 0 &&                                          \
+            stop_sh[((st + R) / RING_K) & 1] != 0x7fffffff)                                \
             break;                                                                         \
         if (st + R >= last_step) break;                                                    \
     }
@@ -922,10 +880,9 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     int total = max_sweeps;
     if (kstar != 0x7fffffff) {
         const int jj = kstar / B;
-        const double* src = jj == 0      ? s0
-                            : nwrap == 3 ? wrap0 + ((jj - 1) % 3) * wstride
-                            : wstride    ? ((jj - 1) & 1 ? wrap1 : wrap0)
-                                         : ((jj - 1) & 1 ? snap1 : snap0);
+        const double* src = jj == 0    ? s0
+                            : wstride ? ((jj - 1) & 1 ? wrap1 : wrap0)
+                                     : ((jj - 1) & 1 ? snap1 : snap0);
         __syncthreads();
         systolic_batch<D>(src, res, xfer, ns, a, b, pin, pv, kstar - jj * B + 1);
         total = kstar + 1;
@@ -1258,11 +1215,8 @@ static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, 
     const int pw = polish_warps(n_s);
     const size_t xb = (size_t)pw * 2 * RING_K * dims * sizeof(double);
     const size_t wb = (size_t)n_s * dims * sizeof(double);
-    const int wrap_mode = (SPK_PAIR_BAR && xb + 3 * wb <= 200 * 1024) ? 3
-                          : xb + 2 * wb <= 200 * 1024                ? 2
-                          : xb + wb <= 200 * 1024                    ? 1
-                                                                     : 0;
-    const size_t psm = xb + (size_t)(wrap_mode == 3 ? 3 : wrap_mode == 2 ? 2 : wrap_mode) * wb;
+    const int wrap_mode = xb + 2 * wb <= 200 * 1024 ? 2 : xb + wb <= 200 * 1024 ? 1 : 0;
+    const size_t psm = xb + (wrap_mode == 2 ? 2 * wb : wrap_mode == 1 ? wb : 0);
     cudaFuncSetAttribute(polish_kernel<3, 256, PL_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)psm);
     cudaFuncSetAttribute(polish_kernel<2, 256, PL_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
