@@ -190,7 +190,7 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
                            out: torch.Tensor, pos4: torch.Tensor, nonfinite, field,
                            att_val: torch.Tensor, att_grad: torch.Tensor,
                            sweeps: torch.Tensor, order: torch.Tensor | None,
-                           polish_streams, k2_streams) -> torch.Tensor:
+                           polish_streams, k2_streams, eta_per_shot=None) -> torch.Tensor:
     """K3 with the lattice attraction (K2) of every shot started as soon as its polish
     group is done, so that K2 runs under the polish of the slower shots.
 
@@ -211,8 +211,8 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
     ws = _device.workspace(nbytes, "project")
     pv = _native.f64_array(list(pin_val) + [0.0] * (3 - dims))
     main = torch.cuda.current_stream()
-    _native.call("spk_project_fista", coords.data_ptr(), _device.ptr(grad), float(eta), None,
-                 out.data_ptr(), n_c, n_s, dims, cfg.speed_bound, cfg.accel_bound, pin_idx, pv,
+    _native.call("spk_project_fista", coords.data_ptr(), _device.ptr(grad), float(eta),
+                 _device.ptr(eta_per_shot), out.data_ptr(), n_c, n_s, dims, cfg.speed_bound, cfg.accel_bound, pin_idx, pv,
                  cfg.n_pit, float(tau), int(bool(cfg.monotone)), None, _device.ptr(nonfinite),
                  ws.data_ptr(), ws.numel(), main.cuda_stream)
     if order is None:

@@ -11,6 +11,11 @@ Barzilai-Borwein step and trace; the batch shares the kernel launches:
 * one ``spk_project_all`` launch over all shots with a per-shot step size;
 * one batched residual launch.
 
+With exact sums and a polish that is heavy next to the N-body (the engine's rule,
+engine.ShardedRun), the lattice sums run per polish group under the slower shots' polish
+(projection.project_overlap_device) and the next evaluation launches the batched K1
+alone.
+
 A single problem of C1 size (32k samples) leaves most of the 148 SMs idle; 64 of them
 fill the GPU.
 """
@@ -39,7 +44,12 @@ from .optimizer import (
     perturb,
 )
 from .core import SamplingPattern
-from .projection import ProjectionConfig, _pin_arrays, project_device
+from .projection import (
+    ProjectionConfig,
+    _pin_arrays,
+    project_device,
+    project_overlap_device,
+)
 
 
 class StackedRun:
@@ -66,11 +76,35 @@ class StackedRun:
         self.prev_grad = self._empty((shots, n_s, self.d))
         self.flag = self._empty(1, torch.int32)
         self.have_prev = False
+        # K2-under-polish (see the module docstring): lattice sums of the last
+        # projection's positions, and the sweep counts that decide and order the next
+        self.overlap = self.cfg.grad_mode == "exact"
+        self.att_pre = None
+        self.sweeps = self._empty(shots, torch.int32)
+        self.sweeps_prev = None
+        if self.overlap:
+            self.att_val = self._empty(self.G * self.p)
+            self.att_grad = self._empty((self.G * self.p, self.d))
 
     def project(self, pcfg):
         out = project_device(self.coords, pcfg, out=self.next, pos4=self.pos4)
         self.coords, self.next = out, self.coords
         self.have_prev = False
+        self.att_pre = None
+
+    def _use_overlap(self) -> bool:
+        import os
+
+        from .engine import ShardedRun
+
+        env = os.environ.get("SPK_OVERLAP")
+        if env is not None:
+            return self.overlap and env == "1"
+        if not self.overlap or self.sweeps_prev is None:
+            return False
+        n_src = self.p + int(np.prod(self.fld.sides))
+        mean = float(self.sweeps_prev.to(torch.float64).mean().item())
+        return mean >= ShardedRun.OVERLAP_MIN_SWEEPS_PER_SOURCE * n_src
 
     def evaluate(self):
         """Per-problem (att_cost, rep_cost, n_nonfinite, dkdg, dgdg) arrays."""
@@ -79,7 +113,14 @@ class StackedRun:
         va, vr = self._empty(n), self._empty(n)
         ga, gr = self._empty((n, d)), self._empty((n, d))
         eps2_rep = float(cfg.repulsion.kernel_eps ** 2)
-        if cfg.grad_mode == "exact":
+        k2_events = []
+        if self.att_pre is not None:
+            # K2 ran under the last polish: the batched launch sums the positions only
+            va, ga, k2_events = self.att_pre
+            self.att_pre = None
+            n_cells = 0
+            args = (None, None, 0.0)
+        elif cfg.grad_mode == "exact":
             w = self.fld.device_sources()
             sides = self.fld.sides
             n_cells = int(np.prod(sides))
@@ -95,6 +136,9 @@ class StackedRun:
                      va.data_ptr() if n_cells else None, ga.data_ptr() if n_cells else None,
                      vr.data_ptr(), gr.data_ptr(), ws.data_ptr(), ws.numel(),
                      _device.stream())
+        cur = torch.cuda.current_stream()
+        for ev in k2_events:
+            cur.wait_event(ev)
         out = self._empty((G, 6))
         cws = _device.workspace(_native.query("spk_combine_batched_workspace_bytes", G, p),
                                 "combine")
@@ -112,8 +156,28 @@ class StackedRun:
         """coords <- P(coords - eta_q * grad) per problem; returns a non-finite flag."""
         eta_shot = _device.h2d(np.repeat(np.asarray(etas, dtype=np.float64), self.n_c))
         self.flag.zero_()
-        out = project_device(self.coords, pcfg, grad=self.grad, eta=0.0, out=self.next,
-                             pos4=self.pos4, nonfinite=self.flag, eta_per_shot=eta_shot)
+        if self._use_overlap():
+            from .engine import CudaOps
+
+            ops = getattr(self, "_ops", None) or CudaOps()
+            self._ops = ops
+            order = None
+            if self.sweeps_prev is not None:
+                order = torch.argsort(self.sweeps_prev, descending=True,
+                                      stable=True).to(torch.int32)
+            ps, ks = ops._overlap_streams()
+            out, k2_events = project_overlap_device(
+                self.coords, pcfg, grad=self.grad, eta=0.0, out=self.next, pos4=self.pos4,
+                nonfinite=self.flag, field=self.fld, att_val=self.att_val,
+                att_grad=self.att_grad, sweeps=self.sweeps, order=order, polish_streams=ps,
+                k2_streams=ks, eta_per_shot=eta_shot)
+            self.att_pre = (self.att_val, self.att_grad, k2_events)
+        else:
+            out = project_device(self.coords, pcfg, grad=self.grad, eta=0.0, out=self.next,
+                                 pos4=self.pos4, nonfinite=self.flag, eta_per_shot=eta_shot,
+                                 sweeps=self.sweeps if self.overlap else None)
+        if self.overlap:
+            self.sweeps_prev = self.sweeps.clone()
         self.prev, self.coords, self.next = self.coords, out, self.prev
         self.prev_grad, self.grad = self.grad, self.prev_grad
         self.have_prev = True
