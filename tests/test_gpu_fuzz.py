@@ -371,3 +371,40 @@ def test_stack_vs_individual_random(dims, n_c, n_s, n_decim, mode, n_prob, seed)
         c1, c2 = res.trace.costs(), single.trace.costs()
         assert np.abs(c1 - c2).max() <= 1e-9 * np.abs(c2).max(), (q, c1, c2)
         assert np.abs(res.pattern.coords - single.pattern.coords).max() <= 1e-6
+
+
+@settings(max_examples=10, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from([2, 3]), st.sampled_from([4, 9, 16, 25]), st.sampled_from([32, 64, 96]),
+       st.sampled_from([0, 1]), st.sampled_from([0.25, 0.75]), st.integers(0, 10_000),
+       st.sampled_from(["overlap", "spatial"]))
+def test_schedules_match_plain_loop(dims, n_c, n_s, n_decim, pert, seed, schedule):
+    """The multi-GPU schedules on random configurations, forced on one GPU: K2 under the
+    polish (exact sums) and the Morton-order target layout (lattice treecode) each give
+    the plain loop's trajectory to the accuracy of their sums."""
+    import os
+
+    import paper_2108_02991_b200 as spk
+
+    hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
+                          dwell_dt=1e-5, fov=0.192, matrix=32, dims=dims)
+    extra = {} if schedule == "overlap" else {"attraction_tree_precision": 1e-4}
+    cfg = spk.OptimizerConfig(n_c=n_c, n_s=n_s, dims=dims, n_decim=n_decim, n_git=3, n_pit=40,
+                              grad_mode="exact", grid_n=8, seed=seed, perturbation=pert,
+                              **extra)
+    env = "SPK_OVERLAP" if schedule == "overlap" else "SPK_SPATIAL"
+    old = os.environ.get(env)
+    try:
+        os.environ[env] = "0"
+        plain = spk.optimize(cfg, hw)
+        os.environ[env] = "1"
+        other = spk.optimize(cfg, hw)
+    finally:
+        if old is None:
+            os.environ.pop(env, None)
+        else:
+            os.environ[env] = old
+    tol = 1e-6 if schedule == "overlap" else 1e-4
+    cp, co = plain.trace.costs(), other.trace.costs()
+    assert np.abs(co - cp).max() <= tol * np.abs(cp).max(), (schedule, co, cp)
+    assert np.abs(other.pattern.coords - plain.pattern.coords).max() <= 1e-3
