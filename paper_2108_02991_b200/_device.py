@@ -43,10 +43,6 @@ def workspace(nbytes: int, slot: str = "main") -> torch.Tensor:
     return buf
 
 
-def release_workspaces() -> None:
-    _WS.clear()
-
-
 def h2d(arr: np.ndarray, dtype=torch.float64) -> torch.Tensor:
     """Copy a host array to the device (synchronous; pageable source)."""
     host = torch.from_numpy(np.ascontiguousarray(arr))
@@ -55,8 +51,21 @@ def h2d(arr: np.ndarray, dtype=torch.float64) -> torch.Tensor:
     return host.to(device(), non_blocking=False)
 
 
+# Below this size the pinned staging buys nothing over a plain copy.
+_PINNED_MIN_BYTES = 1 << 16
+
+
 def d2h(t: torch.Tensor) -> np.ndarray:
-    return t.detach().to("cpu").numpy()
+    """Device -> host numpy array through page-locked memory: a pageable D2H runs at
+    ~2 GB/s on the B200 boxes, a pinned one at full PCIe rate, and the array returned is a
+    view of the pinned buffer (torch's caching host allocator keeps it alive and reuses
+    it), so a later h2d of that array is a page-locked copy too."""
+    t = t.detach()
+    if t.device.type != "cuda" or t.numel() * t.element_size() < _PINNED_MIN_BYTES:
+        return t.to("cpu").numpy()
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t)  # synchronous copy into the page-locked buffer
+    return host.numpy()
 
 
 def pack_positions(coords: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
