@@ -422,10 +422,18 @@ class Ctx:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # test hooks (tests/test_gpu_multirank.py): every rank on one device over gloo, a
+        # functional check of the N-rank path on a one-GPU box -- never a measurement
+        backend = os.environ.get("SPK_BENCH_BACKEND", "nccl")
+        if "SPK_BENCH_DEVICE" in os.environ:
+            self.local = int(os.environ["SPK_BENCH_DEVICE"])
         torch.cuda.set_device(self.local)
         self.dist = self.world > 1 or os.environ.get("SPK_BENCH_DIST") == "1"
         if self.dist:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(backend)
 
     def barrier(self):
         if self.dist:
