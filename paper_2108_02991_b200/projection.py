@@ -190,13 +190,13 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
                            out: torch.Tensor, pos4: torch.Tensor, nonfinite, field,
                            att_val: torch.Tensor, att_grad: torch.Tensor,
                            sweeps: torch.Tensor, order: torch.Tensor | None,
-                           polish_streams, k2_streams, eta_per_shot=None) -> torch.Tensor:
+                           polish_streams, k2_streams, eta_per_shot=None):
     """K3 with the lattice attraction (K2) of every shot started as soon as its polish
     group is done, so that K2 runs under the polish of the slower shots.
 
     The polish time of a shot varies by ~3x between shots and the iteration waits for the
-    slowest; on a rank with few shots (multi-GPU) most SMs idle
-    during that tail.  Shots are polished in groups, longest first by the previous
+    slowest, so SMs idle during that tail -- most of them on a rank with few shots
+    (multi-GPU), the last waves' worth on one GPU.  Shots are polished in groups, longest first by the previous
     iteration's sweep counts (``order``, device int32; None = shot order), each group on
     its own high-priority stream, and each group's K2 (spk_grid_sums_shots) follows on a
     low-priority stream.  The projection itself is unchanged (bit-identical per shot);
@@ -212,9 +212,9 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
     pv = _native.f64_array(list(pin_val) + [0.0] * (3 - dims))
     main = torch.cuda.current_stream()
     _native.call("spk_project_fista", coords.data_ptr(), _device.ptr(grad), float(eta),
-                 _device.ptr(eta_per_shot), out.data_ptr(), n_c, n_s, dims, cfg.speed_bound, cfg.accel_bound, pin_idx, pv,
-                 cfg.n_pit, float(tau), int(bool(cfg.monotone)), None, _device.ptr(nonfinite),
-                 ws.data_ptr(), ws.numel(), main.cuda_stream)
+                 _device.ptr(eta_per_shot), out.data_ptr(), n_c, n_s, dims, cfg.speed_bound,
+                 cfg.accel_bound, pin_idx, pv, cfg.n_pit, float(tau), int(bool(cfg.monotone)),
+                 None, _device.ptr(nonfinite), ws.data_ptr(), ws.numel(), main.cuda_stream)
     if order is None:
         order = torch.arange(n_c, dtype=torch.int32, device=coords.device)
     G = len(polish_streams)
