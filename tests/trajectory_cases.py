@@ -26,6 +26,7 @@ CASES = {
     "c1_exact": (dict(C1, grad_mode="smooth"), C1_HW, True),
     "ml3d_smooth": (dict(ML3D, grad_mode="smooth"), FULL3D_HW, False),
     "ml3d_consistent": (dict(ML3D, grad_mode="consistent"), FULL3D_HW, False),
+    "ml3d_exact": (dict(ML3D, grad_mode="smooth"), FULL3D_HW, True),
 }
 NOISE = 1e-6               # relative noise injected into the reference's repulsion gradient
 NOISE_SEEDS = (11, 12, 13)
