@@ -268,7 +268,13 @@ int spk_tree_node_boxes(const void* rec, int64_t n_nodes, const int32_t* first_c
  * totals[3] == 0 -- the Python wrapper raises).  Write pass fills seg_start/seg_count and the P2M units.
  * Optional far level: parent_box [n_parents][6] and group_parent [n_groups]; nodes far
  * from a group's parent (same opening test) are skipped -- the parent's P2L/L2P covers
- * them; far_only = 1 emits far nodes only (the parents' own walk, for their P2L). */
+ * them; far_only = 1 emits far nodes only (the parents' own walk, for their P2L).
+ * Sub-walks (plain traversal only, parent_box == NULL): with sub_off != NULL
+ * ([n_groups * SPK_TREE_FRONT + 1] i64, filled by the count pass and passed unchanged to
+ * the write pass) every group's walk runs as SPK_TREE_FRONT threads split at the tree's
+ * second level (ranges merge only within one; spk_tree_host_plan follows that rule);
+ * NULL = one thread per group. */
+#define SPK_TREE_FRONT 64
 size_t spk_tree_plan_workspace_bytes(int64_t n_nodes, int64_t n_groups);
 int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
                         const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
@@ -276,8 +282,8 @@ int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
                         double theta, int order, int dims, int64_t n_src, int32_t* slot_of,
                         int32_t* slot_node, float* slot_box, int64_t* slot_unit_off,
                         int64_t* seg_off, int64_t* totals, const float* parent_box,
-                        const int32_t* group_parent, int far_only, void* ws, size_t ws_bytes,
-                        spk_stream_t stream);
+                        const int32_t* group_parent, int far_only, int64_t* sub_off, void* ws,
+                        size_t ws_bytes, spk_stream_t stream);
 int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
                         const int32_t* first_child, const int32_t* n_child, int64_t n_nodes,
                         const float* node_box, const float* group_box, int64_t n_groups,
@@ -286,7 +292,8 @@ int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
                         const int64_t* slot_unit_off, int64_t n_slots, const int64_t* seg_off,
                         int64_t* seg_start, int32_t* seg_count, int32_t* unit_slot,
                         int64_t* unit_begin, int64_t* unit_end, const float* parent_box,
-                        const int32_t* group_parent, int far_only, spk_stream_t stream);
+                        const int32_t* group_parent, int far_only, const int64_t* sub_off,
+                        spk_stream_t stream);
 
 /* Far level (target-side interpolation, the m2l + l2p of _treecode.py:330-426): the
  * q^dims tensor Chebyshev points of every parent box (points [n_parents * q^dims] float4,

@@ -103,10 +103,10 @@ SIGNATURES = {
     "spk_tree_plan_workspace_bytes": (c_size, [c_i64, c_i64]),
     "spk_tree_plan_count": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl,
                                     c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                    c_vp, c_vp, c_int, c_vp, c_size, c_vp]),
+                                    c_vp, c_vp, c_int, c_vp, c_vp, c_size, c_vp]),
     "spk_tree_plan_write": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl,
                                     c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp,
-                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
+                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
     "spk_tree_host_slot_nodes": (None, [c_vp, c_vp]),
     "spk_tree_group_size": (c_int, []),
     "spk_tree_host_build": (c_vp, [c_vp, c_i64, c_int, c_i64, c_int]),

@@ -437,7 +437,16 @@ struct TravParams {
     const int32_t* gparent;    // group -> parent
     int far_only;              // parents' own walk: emit far nodes only (no near leaves)
     unsigned long long* overflow;  // pass 0: groups whose walk overflowed the stack
+    long long* sub_cnt;        // sub-walks, pass 0 out [n_groups * TR_FRONT]
+    const long long* sub_off;  // sub-walks, pass 1 in [n_groups * TR_FRONT + 1]
 };
+// Sub-walks of the plain traversal: every group's walk is split at the octree's second
+// level -- one thread per (group, frontier node), TR_FRONT = 8 x 8 (3D) / 4 x 4 (2D)
+// frontier slots -- instead of one thread walking the whole tree.  The outputs
+// concatenated in frontier order are the serial walk's with contiguous particle ranges
+// merged only within a frontier subtree (the host planner follows the same rule).
+constexpr int TR_FRONT = 64;
+static_assert(TR_FRONT == SPK_TREE_FRONT, "sparkling_b200.h SPK_TREE_FRONT");
 // Stack bound: a depth-first walk holds at most (children - 1) pending siblings per level
 // plus the current node.  Keys have 21 bits per axis in 3D (21 levels of 8 children) and
 // 31 in 2D (31 levels of 4 children).
@@ -541,6 +550,122 @@ __global__ void __launch_bounds__(128) traverse_kernel(const TravParams P) {
     }
     flush();
     if (PASS == 0) P.seg_cnt[g] = n_out;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(128) traverse_sub_kernel(const TravParams P, int front,
+                                                           int fan) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= P.n_groups * front) return;
+    const long long g = idx / front;
+    const int f = (int)(idx - g * front);
+    const int c1 = f / fan, c2 = f - (f / fan) * fan;
+    long long pend_start = 0, pend_cnt = 0, n_out = 0;
+    bool pend_direct = false;
+    const long long o = PASS ? P.sub_off[idx] : 0;
+    auto flush = [&]() {
+        if (pend_cnt > 0) {
+            if (PASS) {
+                P.seg_start[o + n_out] = pend_start;
+                P.seg_count[o + n_out] = (int32_t)pend_cnt;
+            }
+            ++n_out;
+            pend_cnt = 0;
+        }
+    };
+    auto done = [&]() {
+        flush();
+        if (PASS == 0) P.sub_cnt[idx] = n_out;
+    };
+    // this slot's frontier node (depth 2, or a leaf above it) and its ancestors, in DFS
+    // order; slots past a node's child count are empty
+    int anc[2];
+    bool first[2];
+    int n_anc = 0, start;
+    if (P.nchild[0] == 0) {
+        if (f != 0) return done();
+        start = 0;
+    } else {
+        if (c1 >= P.nchild[0]) return done();
+        const int n1 = P.fchild[0] + c1;
+        anc[n_anc] = 0;
+        first[n_anc++] = f == 0;
+        if (P.nchild[n1] == 0) {
+            if (c2 != 0) return done();
+            start = n1;
+        } else {
+            if (c2 >= P.nchild[n1]) return done();
+            anc[n_anc] = n1;
+            first[n_anc++] = c2 == 0;
+            start = P.fchild[n1] + c2;
+        }
+    }
+    const CR tb = center_radius(P.gbox + g * 6, P.dims);
+    const float th2 = __fmul_rn(P.theta, P.theta);
+    auto is_far = [&](int v) {
+        const CR sb = center_radius(P.nbox + (size_t)v * 6, P.dims);
+        float d2 = 0.0f;
+        for (int a = 0; a < P.dims; ++a) {
+            const float d = __fsub_rn(tb.c[a], sb.c[a]);
+            d2 = __fadd_rn(d2, __fmul_rn(d, d));
+        }
+        const float lhs = __fadd_rn(tb.r, sb.r);
+        return __fmul_rn(lhs, lhs) < __fmul_rn(th2, d2);
+    };
+    auto emit = [&](int v, bool far) {
+        const long long b = P.nbeg[v], e = P.nend[v];
+        if (far && e - b > P.m) {
+            flush();
+            if (PASS == 0) P.is_proxy[v] = 1;
+            else pend_start = P.n_src + (long long)P.slot_of[v] * P.m;
+            pend_cnt = P.m;
+            pend_direct = false;
+            flush();
+        } else {
+            if (!far && P.far_only) return;
+            if (pend_cnt > 0 && pend_direct && pend_start + pend_cnt == b &&
+                pend_cnt + (e - b) < (1LL << 30)) {
+                pend_cnt += e - b;
+            } else {
+                flush();
+                pend_start = b;
+                pend_cnt = e - b;
+                pend_direct = true;
+            }
+        }
+    };
+    // a far ancestor ends the walk there: the ancestor's first frontier slot emits it
+    for (int k = 0; k < n_anc; ++k) {
+        if (is_far(anc[k])) {
+            if (first[k]) emit(anc[k], true);
+            return done();
+        }
+    }
+    int32_t stk[TR_STACK];
+    int sp = 0;
+    stk[sp++] = start;
+    while (sp > 0) {
+        const int32_t v = stk[--sp];
+        const bool far = is_far(v);
+        if (far || P.nchild[v] == 0) {
+            emit(v, far);
+        } else {
+            const int nc = P.nchild[v];
+            if (sp + nc > TR_STACK) {  // cannot happen within the key depth
+                if (PASS == 0) atomicAdd(P.overflow, 1ULL);
+                continue;
+            }
+            for (int c = nc - 1; c >= 0; --c) stk[sp++] = P.fchild[v] + c;
+        }
+    }
+    done();
+}
+
+// Group offsets from the sub-walk offsets: seg_off[g] = sub_off[g * front].
+__global__ void group_offsets_kernel(const long long* __restrict__ sub_off, long long n_groups,
+                                     int front, long long* __restrict__ seg_off) {
+    const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (g <= n_groups) seg_off[g] = sub_off[g * front];
 }
 
 constexpr long long P2M_UNIT = 4096;  // particles per P2M unit (tree_host.cpp P2M_UNIT)
@@ -1010,13 +1135,14 @@ size_t spk_tree_plan_workspace_bytes(int64_t n_nodes, int64_t n_groups) {
     cub::DeviceScan::ExclusiveSum(nullptr, a, (const int32_t*)nullptr, (int32_t*)nullptr,
                                   (int)n_nodes);
     cub::DeviceScan::ExclusiveSum(nullptr, b, (const long long*)nullptr, (long long*)nullptr,
-                                  (int)(n_groups + 1));
+                                  (int)(n_groups * TR_FRONT + 1));
     cub::DeviceScan::ExclusiveSum(nullptr, c, (const long long*)nullptr, (long long*)nullptr,
                                   (int)(n_nodes + 1));
     const size_t cub_bytes = std::max(a, std::max(b, c));
-    // is_proxy [n_nodes] i32, seg_cnt [n_groups + 1] i64, units_per_slot [n_nodes + 1] i64
+    // is_proxy [n_nodes] i32, seg_cnt [n_groups * TR_FRONT + 1] i64 (per group, or per
+    // sub-walk), units_per_slot [n_nodes + 1] i64
     return ((cub_bytes + 255) & ~(size_t)255) + (size_t)n_nodes * 4 + 256 +
-           (size_t)(n_groups + 1) * 8 + 256 + (size_t)(n_nodes + 1) * 8 + 256;
+           (size_t)(n_groups * TR_FRONT + 1) * 8 + 256 + (size_t)(n_nodes + 1) * 8 + 256;
 }
 
 static void plan_ws(void* ws, int64_t n_nodes, int64_t n_groups, size_t cub_bytes,
@@ -1028,7 +1154,7 @@ static void plan_ws(void* ws, int64_t n_nodes, int64_t n_groups, size_t cub_byte
     *is_proxy = reinterpret_cast<int32_t*>(p);
     p += ((size_t)n_nodes * 4 + 255) & ~(size_t)255;
     *seg_cnt = reinterpret_cast<long long*>(p);
-    p += ((size_t)(n_groups + 1) * 8 + 255) & ~(size_t)255;
+    p += ((size_t)(n_groups * TR_FRONT + 1) * 8 + 255) & ~(size_t)255;
     *units_per_slot = reinterpret_cast<long long*>(p);
 }
 
@@ -1038,14 +1164,17 @@ int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
                         double theta, int order, int dims, int64_t n_src, int32_t* slot_of,
                         int32_t* slot_node, float* slot_box, int64_t* slot_unit_off,
                         int64_t* seg_off, int64_t* totals, const float* parent_box,
-                        const int32_t* group_parent, int far_only, void* ws, size_t ws_bytes,
-                        spk_stream_t stream) {
+                        const int32_t* group_parent, int far_only, int64_t* sub_off, void* ws,
+                        size_t ws_bytes, spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
     SPK_REQUIRE(n_nodes > 0 && n_groups > 0, SPK_ERR_ARG, "tree plan: empty tree or groups");
+    SPK_REQUIRE(sub_off == nullptr || parent_box == nullptr, SPK_ERR_ARG,
+                "tree plan: sub-walks are for the plain traversal (no far-level parents)");
     SPK_REQUIRE(ws_bytes >= spk_tree_plan_workspace_bytes(n_nodes, n_groups), SPK_ERR_WORKSPACE,
                 "tree plan: workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
-    size_t cub_bytes = ws_bytes - ((size_t)n_nodes * 4 + 256 + (size_t)(n_groups + 1) * 8 + 256 +
+    size_t cub_bytes = ws_bytes - ((size_t)n_nodes * 4 + 256 +
+                                   (size_t)(n_groups * TR_FRONT + 1) * 8 + 256 +
                                    (size_t)(n_nodes + 1) * 8 + 256);
     cub_bytes &= ~(size_t)255;
     void* tmp;
@@ -1054,7 +1183,7 @@ int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
     long long* ups;
     plan_ws(ws, n_nodes, n_groups, cub_bytes, &tmp, &is_proxy, &seg_cnt, &ups);
     cudaMemsetAsync(is_proxy, 0, (size_t)n_nodes * 4, s);
-    cudaMemsetAsync(seg_cnt, 0, (size_t)(n_groups + 1) * 8, s);
+    cudaMemsetAsync(seg_cnt, 0, (size_t)(n_groups * TR_FRONT + 1) * 8, s);
     cudaMemsetAsync(ups, 0, (size_t)(n_nodes + 1) * 8, s);
     const int m = dims == 3 ? order * order * order : order * order;
     TravParams P{};
@@ -1076,14 +1205,30 @@ int spk_tree_plan_count(const int64_t* node_begin, const int64_t* node_end,
     P.far_only = far_only;
     P.overflow = reinterpret_cast<unsigned long long*>(totals + 3);
     cudaMemsetAsync(totals + 3, 0, sizeof(int64_t), s);
-    traverse_kernel<0><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
+    const int fan = dims == 3 ? 8 : 4, front = fan * fan;
+    if (sub_off) {
+        P.sub_cnt = seg_cnt;
+        const long long nt = n_groups * front;
+        traverse_sub_kernel<0><<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(P, front, fan);
+    } else {
+        traverse_kernel<0><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
+    }
     SPK_CHECK_LAUNCH("spk_tree_plan_count(traverse)");
     size_t t = cub_bytes;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, t, is_proxy, slot_of, (int)n_nodes, s);
     SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree plan scan: %s", cudaGetErrorString(e));
     t = cub_bytes;
-    e = cub::DeviceScan::ExclusiveSum(tmp, t, seg_cnt, reinterpret_cast<long long*>(seg_off),
-                                      (int)(n_groups + 1), s);
+    if (sub_off) {
+        e = cub::DeviceScan::ExclusiveSum(tmp, t, seg_cnt, reinterpret_cast<long long*>(sub_off),
+                                          (int)(n_groups * front + 1), s);
+        SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree plan scan: %s", cudaGetErrorString(e));
+        group_offsets_kernel<<<(unsigned)((n_groups + 1 + 127) / 128), 128, 0, s>>>(
+            reinterpret_cast<const long long*>(sub_off), n_groups, front,
+            reinterpret_cast<long long*>(seg_off));
+    } else {
+        e = cub::DeviceScan::ExclusiveSum(tmp, t, seg_cnt, reinterpret_cast<long long*>(seg_off),
+                                          (int)(n_groups + 1), s);
+    }
     SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "tree plan scan: %s", cudaGetErrorString(e));
     slots_kernel<<<(unsigned)((n_nodes + 127) / 128), 128, 0, s>>>(
         P.nbeg, P.nend, node_box, is_proxy, slot_of, n_nodes, dims, slot_node, slot_box, ups);
@@ -1107,7 +1252,8 @@ int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
                         const int64_t* slot_unit_off, int64_t n_slots, const int64_t* seg_off,
                         int64_t* seg_start, int32_t* seg_count, int32_t* unit_slot,
                         int64_t* unit_begin, int64_t* unit_end, const float* parent_box,
-                        const int32_t* group_parent, int far_only, spk_stream_t stream) {
+                        const int32_t* group_parent, int far_only, const int64_t* sub_off,
+                        spk_stream_t stream) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
     cudaStream_t s = (cudaStream_t)stream;
     TravParams P{};
@@ -1129,7 +1275,14 @@ int spk_tree_plan_write(const int64_t* node_begin, const int64_t* node_end,
     P.pbox = parent_box;
     P.gparent = group_parent;
     P.far_only = far_only;
-    traverse_kernel<1><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
+    if (sub_off) {
+        const int fan = dims == 3 ? 8 : 4, front = fan * fan;
+        P.sub_off = reinterpret_cast<const long long*>(sub_off);
+        const long long nt = n_groups * front;
+        traverse_sub_kernel<1><<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(P, front, fan);
+    } else {
+        traverse_kernel<1><<<(unsigned)((n_groups + 127) / 128), 128, 0, s>>>(P);
+    }
     SPK_CHECK_LAUNCH("spk_tree_plan_write(traverse)");
     if (n_slots > 0) {
         units_kernel<<<(unsigned)((n_slots + 127) / 128), 128, 0, s>>>(

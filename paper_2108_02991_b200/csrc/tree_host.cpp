@@ -249,6 +249,8 @@ void spk_tree_host_set_leaf_boxes(void* h, const float* leaf_box) {
  * theta: opening parameter (far when r_t + r_s < theta * |c_t - c_s|); order: proxies per
  * axis; n_src: sorted source records before the proxy block.
  * counts[0..4] = segments, slots, units, near pairs (per target), far pairs (per target). */
+static constexpr int32_t BREAK = INT32_MIN;  // raw list: no merge across this mark
+
 int spk_tree_host_plan(void* h, int64_t n_groups, const float* group_box, double theta,
                        int order, int64_t n_src, int64_t* counts) {
     HostTree* t = static_cast<HostTree*>(h);
@@ -263,11 +265,17 @@ int spk_tree_host_plan(void* h, int64_t n_groups, const float* group_box, double
         const Box tb = make_box(group_box + g * 6, dims);
         std::vector<int32_t>& out = raw[(size_t)g];
         int32_t stack[512];
+        uint8_t depth[512];
         int sp = 0;
+        depth[sp] = 0;
         stack[sp++] = 0;
         while (sp > 0) {
             const int32_t v = stack[--sp];
+            const int dv = depth[sp];
             const Node& nd = t->nodes[v];
+            // the device splits every walk into sub-walks at the tree's second level and
+            // merges ranges only within one (tree.cu traverse_sub_kernel): break here too
+            if (dv <= 2) out.push_back(BREAK);
             const Box& sb = t->box[v];
             float d2 = 0.0f;
             for (int a = 0; a < dims; ++a) {
@@ -290,7 +298,10 @@ int spk_tree_host_plan(void* h, int64_t n_groups, const float* group_box, double
                     // cannot happen for depth <= 31 with <= 8 children per level
                     continue;
                 }
-                for (int c = nd.n_child - 1; c >= 0; --c) stack[sp++] = nd.first_child + c;
+                for (int c = nd.n_child - 1; c >= 0; --c) {
+                    depth[sp] = (uint8_t)std::min(dv + 1, 255);
+                    stack[sp++] = nd.first_child + c;
+                }
             }
         }
     }
@@ -336,6 +347,10 @@ int spk_tree_host_plan(void* h, int64_t n_groups, const float* group_box, double
         out.reserve(raw[(size_t)g].size());
         bool last_direct = false;
         for (int32_t e : raw[(size_t)g]) {
+            if (e == BREAK) {
+                last_direct = false;
+                continue;
+            }
             int64_t start, cnt;
             if (e < 0) {
                 start = n_src + (int64_t)slot_of[-1 - e] * m;

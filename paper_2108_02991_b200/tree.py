@@ -48,6 +48,7 @@ AUTO_PARAMS = (
     (1e-6, 6, 0.5),
 )
 MAX_ORDER = 8
+SUB_FRONT = 64  # frontier slots per group walk (sparkling_b200.h SPK_TREE_FRONT)
 LEAF_CAP = 256  # source particles per octree leaf
 # At or below this many sources the exact kernel is faster than building and walking a
 # tree on the B200 (C1 32k: 0.4 vs 1.0 ms; 65k: 1.7 vs 2.5 ms; 1M: 362 vs 19 ms).
@@ -387,6 +388,14 @@ def _check_overflow(n: int) -> None:
         raise _native.NativeError(f"tree plan: traversal stack overflow in {n} walks")
 
 
+def _sub_offsets(n_groups: int, dev) -> torch.Tensor | None:
+    """Per-(group, frontier slot) list offsets of the sub-walk traversal (tree.cu
+    traverse_sub_kernel); SPK_TREE_SUBWALK=0 selects the one-thread-per-group walk."""
+    if os.environ.get("SPK_TREE_SUBWALK", "1") == "0":
+        return None
+    return torch.empty(n_groups * SUB_FRONT + 1, dtype=torch.int64, device=dev)
+
+
 def _static_plan(src: SourceTree, boxes: torch.Tensor, n_groups: int, theta: float,
                  order: int, slot_of: torch.Tensor, pbox=None, gparent=None, far_only=False):
     """Interaction lists against the source tree's static (all-node) proxies."""
@@ -404,10 +413,13 @@ def _static_plan(src: SourceTree, boxes: torch.Tensor, n_groups: int, theta: flo
     args = (src.d_nb.data_ptr(), src.d_ne.data_ptr(), src.d_fc.data_ptr(), src.d_nc.data_ptr(),
             n_nodes, src.node_box.data_ptr(), boxes.data_ptr(), n_groups, float(theta), order,
             src.dims, src.n)
+    sub_off = None if pbox is not None else _sub_offsets(n_groups, dev)
     _native.call("spk_tree_plan_count", *args, tmp_i.data_ptr(), tmp_n.data_ptr(),
                  tmp_b.data_ptr(), tmp_u.data_ptr(), seg_off.data_ptr(), totals.data_ptr(),
-                 _device.ptr(pbox), _device.ptr(gparent), int(far_only), ws.data_ptr(),
-                 ws.numel(), st)
+                 _device.ptr(pbox), _device.ptr(gparent), int(far_only), _device.ptr(sub_off),
+                 ws.data_ptr(), ws.numel(), st)
+    if sub_off is not None:
+        _native.add_launches(1)
     n_seg, _, _, overflow = (int(x) for x in totals.cpu().numpy())
     _check_overflow(overflow)
     seg_start = torch.empty(max(n_seg, 1), dtype=torch.int64, device=dev)
@@ -416,7 +428,7 @@ def _static_plan(src: SourceTree, boxes: torch.Tensor, n_groups: int, theta: flo
                  tmp_u.data_ptr(), 0, seg_off.data_ptr(), seg_start.data_ptr(),
                  seg_count.data_ptr(), tmp_i.data_ptr(), seg_off.data_ptr(),
                  seg_off.data_ptr(), _device.ptr(pbox), _device.ptr(gparent), int(far_only),
-                 st)
+                 _device.ptr(sub_off), st)
     return seg_off, seg_start, seg_count, n_seg
 
 
@@ -484,6 +496,7 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
     slot_unit_off = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
     seg_off = torch.empty(n_groups + 1, dtype=torch.int64, device=dev)
     totals = torch.empty(4, dtype=torch.int64, device=dev)
+    sub_off = _sub_offsets(n_groups, dev)
     ws = _device.workspace(_native.query("spk_tree_plan_workspace_bytes", n_nodes, n_groups),
                            "tree_plan")
     _native.call("spk_tree_plan_count", src.d_nb.data_ptr(), src.d_ne.data_ptr(),
@@ -491,7 +504,9 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  tg.box.data_ptr(), n_groups, float(theta), order, dims, n_s,
                  slot_of.data_ptr(), slot_node.data_ptr(), slot_box.data_ptr(),
                  slot_unit_off.data_ptr(), seg_off.data_ptr(), totals.data_ptr(), None, None,
-                 0, ws.data_ptr(), ws.numel(), st)
+                 0, _device.ptr(sub_off), ws.data_ptr(), ws.numel(), st)
+    if sub_off is not None:
+        _native.add_launches(1)
     n_seg, n_slots, n_units, overflow = (int(x) for x in totals.cpu().numpy())
     _check_overflow(overflow)
     mark("plan_count")
@@ -514,7 +529,7 @@ def tree_eval(tg: TargetGroups, src: SourceTree, order: int, theta: float, eps2:
                  write_slot_of.data_ptr(), slot_node.data_ptr(), slot_unit_off.data_ptr(),
                  0 if static else n_slots, seg_off.data_ptr(), seg_start.data_ptr(),
                  seg_count.data_ptr(), unit_slot.data_ptr(), unit_begin.data_ptr(),
-                 unit_end.data_ptr(), None, None, 0, st)
+                 unit_end.data_ptr(), None, None, 0, _device.ptr(sub_off), st)
     mark("plan_write")
     if not static and n_slots:
         ws2 = _device.workspace(_native.query("spk_tree_p2m_workspace_bytes", n_units, order,

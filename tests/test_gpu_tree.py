@@ -194,6 +194,48 @@ def test_device_lists_match_host_planner(spk, dims):
     assert np.array_equal(seg_count, L["seg_count"])
 
 
+def _canonical_lists(seg_off, seg_start, seg_count, n_src):
+    """Per group, adjacent direct ranges merged completely (proxy segments kept)."""
+    out = []
+    for g in range(len(seg_off) - 1):
+        cur = []
+        for k in range(seg_off[g], seg_off[g + 1]):
+            s, c = int(seg_start[k]), int(seg_count[k])
+            if s < n_src and cur and cur[-1][0] < n_src and sum(cur[-1]) == s:
+                cur[-1] = (cur[-1][0], cur[-1][1] + c)
+            else:
+                cur.append((s, c))
+        out.append(cur)
+    return out
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_subwalk_plan_matches_serial_walk(spk, dims, monkeypatch):
+    """The sub-walk traversal (one thread per group and second-level node) lists the same
+    nodes, proxies and particle ranges as the one-thread-per-group walk; only the
+    merging of contiguous ranges across second-level subtrees differs, and the sums agree
+    to rounding."""
+    from paper_2108_02991_b200 import _device, tree
+
+    pts = (spk.perturb(spk.init_radial(144, 512, 3), 0.25, 5).points() if dims == 3 else
+           spk.perturb(spk.init_radial(128, 512, 2), 0.25, 5).points())
+    pos4 = _device.pack_positions(_device.h2d(pts))
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SPK_TREE_SUBWALK", mode)
+        L = {}
+        v, g = tree.tree_sums_device(pos4, pos4, dims, 1e-6, 4, 0.6, lists=L)
+        tree._native.load().spk_tree_host_free(L["host_tree"][0])
+        res[mode] = (_device.d2h(v), _device.d2h(g), L)
+    (v0, g0, L0), (v1, g1, L1) = res["0"], res["1"]
+    assert np.array_equal(L0["slot_node"], L1["slot_node"])
+    assert L1["seg_off"][-1] >= L0["seg_off"][-1]
+    assert (_canonical_lists(L0["seg_off"], L0["seg_start"], L0["seg_count"], L0["n_src"]) ==
+            _canonical_lists(L1["seg_off"], L1["seg_start"], L1["seg_count"], L1["n_src"]))
+    assert np.abs(v1 - v0).max() <= 1e-12 * np.abs(v0).max()
+    assert np.abs(g1 - g0).max() <= 1e-10 * np.abs(g0).max()
+
+
 @pytest.mark.parametrize("precision", [1e-3, 1e-4, 1e-5])
 def test_attraction_tree_precision(spk, precision):
     """Treecode attraction over the static lattice tree vs the exact K2 sums."""
