@@ -4,7 +4,10 @@ projection alone, K2 for those shots alone, and both launched concurrently on tw
 (projection on a high-priority stream).  Timing-only: K2 reads the pre-projection
 positions.
 
-    python scripts/overlap_probe.py [n_ranks=8]
+    python scripts/overlap_probe.py [n_ranks=8] [k2|fused]
+
+With "fused", the second kernel is the share's full fused K1 + K2 launch (its targets
+against all sources): could the polish hide under the whole N-body?
 """
 import os
 import sys
@@ -22,6 +25,7 @@ from paper_2108_02991_b200.optimizer import _bb_step  # noqa: E402
 from paper_2108_02991_b200.projection import project_device  # noqa: E402
 
 nr = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+what = sys.argv[2] if len(sys.argv) > 2 else "k2"
 bench.select_workload("c2")
 cfg = spk.OptimizerConfig(n_c=bench.N_C, n_s=bench.N_S, dims=3, grad_mode="exact",
                           grid_n=bench.GRID_N, seed=0, perturbation=bench.W["pert"])
@@ -52,7 +56,10 @@ def proj():
 
 
 def k2():
-    grid_sums_device(tgt, fld, eps2)
+    if what == "fused":
+        run.ops.sums(tgt, run.pos4_all, coords, fld, cfg)
+    else:
+        grid_sums_device(tgt, fld, eps2)
 
 
 def timed(fn):
@@ -82,5 +89,5 @@ def both():
 k2()
 for rep in range(2):
     tp, tk, tb = timed(proj), timed(k2), timed(both)
-    print(f"N={nr} ({cnt} shots): projection {tp:.1f} ms, K2 {tk:.1f} ms, sum {tp + tk:.1f}, "
-          f"concurrent {tb:.1f} ms (hidden {tp + tk - tb:.1f} of {tk:.1f})", flush=True)
+    print(f"N={nr} ({cnt} shots): projection {tp:.1f} ms, {what} {tk:.1f} ms, sum {tp + tk:.1f}, "
+          f"concurrent {tb:.1f} ms (hidden {tp + tk - tb:.1f} of {min(tp, tk):.1f})", flush=True)

@@ -44,7 +44,11 @@ def main():
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ranks", default="1,2,4,8")
+    ap.add_argument("--groups", type=int, default=None,
+                    help="polish groups of the overlap schedule (default: the engine's)")
     args = ap.parse_args()
+    if args.groups:
+        engine.CudaOps.OVERLAP_GROUPS = args.groups
     bench.select_workload(args.config)
     cfg = spk.OptimizerConfig(n_c=bench.N_C, n_s=bench.N_S, dims=bench.DIMS, n_pit=100,
                               grad_mode="exact", grid_n=bench.GRID_N, seed=0,
@@ -104,13 +108,14 @@ def main():
                 av = torch.empty(cnt * ns, dtype=torch.float64, device="cuda")
                 ag = torch.empty((cnt * ns, d), dtype=torch.float64, device="cuda")
                 sw2 = torch.empty(cnt, dtype=torch.int32, device="cuda")
-                f = [ev() for _ in range(3)]
+                f = [ev() for _ in range(4)]
                 torch.cuda.synchronize()
                 f[0].record()
                 _, k2ev = ops.project_overlap(coords, pcfg, grad, float(eta), out, pos4, flag,
                                               fld, av, ag, sw2, order)
                 f[1].record()
                 vr2, gr2 = ops.repulsion_sums(tgt, run.pos4_all, cfg)
+                f[3].record()
                 for e_ in k2ev:
                     torch.cuda.current_stream().wait_event(e_)
                 ops.combine(av, ag, vr2, gr2, run.p, coords, None, None, grad.view(-1, d))
@@ -120,6 +125,7 @@ def main():
                 # projection (K2 may continue past f[1]), then K1 co-running with K2's tail
                 rec["overlap_project_k2_ms"] = f[0].elapsed_time(f[1])
                 rec["overlap_k1_combine_ms"] = f[1].elapsed_time(f[2])
+                rec["overlap_k1_ms"] = f[1].elapsed_time(f[3])
                 prev_sweeps[key] = sw.clone()
                 per.append(rec)
             gather_ms = 16.0 * bench.N_C * ns * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
@@ -143,7 +149,8 @@ def main():
     for n in worlds:
         tn = float(np.mean([x["step_ms"] for x in rows[n][1:]]))
         to = float(np.mean([x["overlap_step_ms"] for x in rows[n][1:]]))
-        rec = {"config": args.config, "n_ranks": n, "step_ms": tn,
+        rec = {"config": args.config, "n_ranks": n, "groups": ops.OVERLAP_GROUPS,
+               "step_ms": tn,
                "sums_ms": float(np.mean([x["max_sums_ms"] for x in rows[n][1:]])),
                "project_ms": float(np.mean([x["max_project_ms"] for x in rows[n][1:]])),
                "efficiency": (t1 / (n * tn)) if t1 else None,

@@ -39,8 +39,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n-git", type=int, default=100)
 ap.add_argument("--probe", type=int, default=10)
 ap.add_argument("--ranks", default="1,2,4,8")
+ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 worlds = [int(x) for x in a.ranks.split(",")]
+REPS = a.reps
 
 hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5, dwell_dt=2e-6,
                       fov=(0.23, 0.23, 0.1248), matrix=(384, 384, 208), dims=3)
@@ -88,23 +90,28 @@ while True:
                 grad = torch.empty((cnt, ns, d), dtype=torch.float64, device="cuda")
                 out = torch.empty_like(grad)
                 pos4 = torch.empty((cnt * ns, 4), dtype=torch.float32, device="cuda")
-                e = [ev() for _ in range(5)]
-                torch.cuda.synchronize()
-                e[0].record()
-                va, ga, vr, gr = ops.sums(tgt, run.pos4_all, coords, state.fld, cfg)
-                ops.combine(va, ga, vr, gr, run.p, coords, None, None, grad.view(-1, d))
-                e[1].record()
-                ops.project(coords, state.proj_cfg, grad, float(state.eta0), out, pos4, None)
-                ops.residuals(out, state.proj_cfg)
-                e[2].record()
-                # spatial layout (engine.ShardedRun.spatial): this rank's Morton block
-                blk = run.pos4_all[perm[sb[r]:sb[r + 1]]].contiguous()
-                e[3].record()
-                ops.sums(blk, run.pos4_all, None, state.fld, cfg)
-                e[4].record()
-                torch.cuda.synchronize()
-                per.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]),
-                            e[3].elapsed_time(e[4])))
+                reps = []
+                for _ in range(REPS):
+                    e = [ev() for _ in range(5)]
+                    torch.cuda.synchronize()
+                    e[0].record()
+                    va, ga, vr, gr = ops.sums(tgt, run.pos4_all, coords, state.fld, cfg)
+                    ops.combine(va, ga, vr, gr, run.p, coords, None, None, grad.view(-1, d))
+                    e[1].record()
+                    ops.project(coords, state.proj_cfg, grad, float(state.eta0), out, pos4,
+                                None)
+                    ops.residuals(out, state.proj_cfg)
+                    e[2].record()
+                    # spatial layout (engine.ShardedRun.spatial): this rank's Morton block
+                    blk = run.pos4_all[perm[sb[r]:sb[r + 1]]].contiguous()
+                    e[3].record()
+                    ops.sums(blk, run.pos4_all, None, state.fld, cfg)
+                    e[4].record()
+                    torch.cuda.synchronize()
+                    reps.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]),
+                                 e[3].elapsed_time(e[4])))
+                # median of REPS timings per component (single timings vary by up to 40 %)
+                per.append(tuple(float(np.median([x[k] for x in reps])) for k in range(3)))
             gather = 16.0 * run.p * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
             exch = 8.0 * (2 + 2 * d) * run.p * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
             step = max(s + p for s, p, _ in per) + gather
