@@ -588,12 +588,13 @@ def measure_exact(args, ctx, steps, warmup, with_e2e, with_cpu):
                              "K1 + K2 launch alone"},
         "clocks": clocks, "gpu_launches": launches,
     }
+    del run, ops
+    torch.cuda.empty_cache()
     if with_e2e:
+        rec["e2e"] = run_e2e_step_api(ctx, cfg, fld, steps)
         if not ctx.dist:
-            rec["e2e"] = run_e2e(args, spk, fld, pcfg, steps)
-        else:
-            rec["e2e"] = run_e2e_sharded(ctx, run, step, steps)
-    del run, ops, fld
+            rec["e2e_numpy_api"] = run_e2e(args, spk, fld, pcfg, steps)
+    del fld
     if with_cpu and ctx.world == 1 and ctx.rank == 0:
         rec["cpu_baseline"] = cpu_baseline_record(args.cpu_rows if W["key"] == "c2" else
                                                   args.cpu_rows // 16)
@@ -726,15 +727,30 @@ def measure_stack(args, ctx, steps, warmup):
 
 
 # ---------------------------------------------------------------- end to end
-def run_e2e_sharded(ctx, run, step, steps):
-    """N > 1: the sharded optimize iteration with this rank's shots copied H2D from pinned
-    host memory before, and the projected shots + scalars copied D2H after, every step
-    (device-timed per step, max over ranks)."""
+def run_e2e_step_api(ctx, cfg, fld, steps):
+    """The public per-iteration API -- ``optimizer.start`` once, then ``optimizer.step``
+    (optimize's loop body: evaluate, guards, step size, step + projection, residuals,
+    TraceRecord) -- with the pattern round-tripping through pinned host memory every step:
+    this rank's shots copied H2D into the run before the call, the projected shots copied
+    D2H after it (the step's TraceRecord scalars come back inside the call).  Each step is
+    device-timed with CUDA events around the copies and the call; max over ranks.  The
+    shots a step receives are the previous step's output, so the run progresses like
+    ``optimize``."""
+    import dataclasses
+
     import torch
 
+    from paper_2108_02991_b200 import optimizer as om
+
+    warm = 2  # the first step has no previous sweep counts (plain schedule)
+    cfg_e = dataclasses.replace(cfg, n_decim=0, n_git=warm + steps)
+    state = om.start(cfg_e, hardware(), rho=density(), fld=fld)
+    run = state.run
     host_in = torch.empty(run.coords.shape, dtype=torch.float64, pin_memory=True)
-    host_in.copy_(run.coords)
     host_out = torch.empty_like(host_in, pin_memory=True)
+    for _ in range(warm):
+        om.step(state)
+    host_in.copy_(run.coords)
     torch.cuda.synchronize()
     ctx.barrier()
     total = 0.0
@@ -742,20 +758,26 @@ def run_e2e_sharded(ctx, run, step, steps):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         run.coords.copy_(host_in, non_blocking=True)
-        step()
+        rec = om.step(state)
         host_out.copy_(run.coords, non_blocking=True)
         e.record()
         torch.cuda.synchronize()
         total += s.elapsed_time(e)
+        if rec is None or not np.isfinite(rec.cost):
+            raise RuntimeError("e2e: optimizer.step did not return a finite record")
         host_in.copy_(host_out)
     (total,) = ctx.max(total)
     p, g, rep_pairs, att_pairs = pairs_per_step()
     nbytes = host_in.numel() * 8
+    del state, run
+    torch.cuda.empty_cache()
     return {"value": (rep_pairs + att_pairs) * steps / (total / 1e3), "unit": "pairs/s",
             "s_per_iteration": total / 1e3 / steps, "steps": steps,
-            "h2d_bytes_per_step": nbytes * ctx.world, "d2h_bytes_per_step": nbytes * ctx.world + 48,
-            "api": "sharded optimize iteration (engine.ShardedRun) with per-step pinned "
-                   "H2D of every rank's shots and D2H of the projected shots"}
+            "h2d_bytes_per_step": nbytes * ctx.world,
+            "d2h_bytes_per_step": nbytes * ctx.world + 64 * ctx.world,
+            "api": "optimizer.start + optimizer.step (the public per-iteration entry point, "
+                   "optimize's loop body) with every rank's shots H2D from pinned host "
+                   "memory before and D2H after each step, plus the TraceRecord scalars"}
 
 
 def run_e2e(args, spk, fld, pcfg, steps):
