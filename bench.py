@@ -247,6 +247,17 @@ def committed_traffic(key: str):
     return rec.get("dram_bytes_per_launch"), rec.get("source")
 
 
+def co_issue_ceiling(key):
+    """Measured FFMA2 + MUFU co-issue ceiling of this workload's instruction mix
+    (profiles/mix_peak.json, scripts/micro/mix_peak.cu), or None if not measured."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "mix_peak.json")) as fh:
+            return json.load(fh)["co_issue_ceiling"].get(key)
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def nbody_roofline(key, dims, rep_pairs, att_pairs, launch_ms, clocks):
     """Roofline of the fused N-body launch.
 
@@ -275,6 +286,7 @@ def nbody_roofline(key, dims, rep_pairs, att_pairs, launch_ms, clocks):
     achieved = flops / (launch_ms / 1e3) / 1e12
     peak = flops / bound_s / 1e12
     traffic, tsrc = committed_traffic(key)
+    ceiling = co_issue_ceiling(key)
     sm = clocks.get("sm_mhz") if clocks else None
     return {
         "bound": "fp32+sfu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -285,6 +297,8 @@ def nbody_roofline(key, dims, rep_pairs, att_pairs, launch_ms, clocks):
         "no ncu DRAM capture for this workload (the kernel reads ~0 bytes per pair)",
         "kernel": "nbody_kernel (fused K1+K2) + finalize", "launch_ms": launch_ms,
         "hw_bound_ms": bound_s * 1e3,
+        "co_issue_ceiling": ceiling,
+        "frac_of_co_issue_ceiling": (bound_s / (launch_ms / 1e3) / ceiling) if ceiling else None,
         "frac_of_balanced_offload_bound": balanced_s / (launch_ms / 1e3),
         "balanced_offload_bound_ms": balanced_s * 1e3,
         "algorithmic_tflops_vs_fp32_peak": achieved / tflops,
@@ -297,7 +311,9 @@ def nbody_roofline(key, dims, rep_pairs, att_pairs, launch_ms, clocks):
         "note": "peak = algorithmic flops at the FP32+SFU bound of the executed mix "
                 "(max of FMA-pipe and SFU time, hw_bound_ms); frac = hw_bound_ms / "
                 "launch_ms.  frac_of_balanced_offload_bound also lets rsqrts move to the "
-                "FMA pipe (measured slower here).  algorithmic_tflops_vs_fp32_peak is "
+                "FMA pipe (measured slower here).  co_issue_ceiling = the fraction of "
+                "that bound a dependency-free FFMA2 + MUFU stream of the same mix reaches "
+                "on this GPU (profiles/mix_peak.json).  algorithmic_tflops_vs_fp32_peak is "
                 "secondary: the lattice segment runs fewer lane-ops than its 19 "
                 "algorithmic flops, so it can exceed 1.",
     }
