@@ -3,7 +3,8 @@ keys, target groups and interaction lists.  Structural invariants: the nodes par
 the sorted range level by level, leaves respect the capacity, groups tile the targets
 in order, and every group's list covers every source exactly once (near particle ranges
 plus far nodes) -- the completeness property the reference's dual_traverse guarantees
-(_treecode.py:173-244)."""
+(_treecode.py:173-244) -- and contiguous ranges merge only within a second-level
+subtree, as the device's sub-walks do."""
 
 import numpy as np
 import pytest
@@ -131,5 +132,16 @@ def test_tree_groups_and_lists_cover_every_source_once(dims):
                         v = slot_node[s]
                         cover[beg[v]:end[v]] += 1
             assert np.all(cover == 1), g
+        # merge rule of the device's sub-walks (tree.cu traverse_sub_kernel): a direct
+        # range never spans two second-level subtrees (the frontier: level-2 nodes and
+        # leaves above level 2, which partition the sources)
+        front = np.nonzero((lv == 2) | ((nc == 0) & (lv < 2)))[0]
+        fb = np.sort(beg[front])
+        assert fb[0] == 0 and np.array_equal(np.sort(end[front])[:-1], fb[1:])
+        direct = seg_start < n
+        st, c = seg_start[direct], seg_count[direct].astype(np.int64)
+        k = np.searchsorted(fb, st, side="right") - 1
+        limit = np.append(fb[1:], n)[k]
+        assert np.all(st + c <= limit)
     finally:
         lib.spk_tree_host_free(tree)
