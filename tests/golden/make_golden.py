@@ -220,6 +220,32 @@ def projection_fixtures():
     np.savez_compressed(os.path.join(OUT, "projection.npz"), **out)
 
 
+def nonfinite_fixtures():
+    """The reference's _project_all on shots holding NaN / +-inf samples (numba kernel
+    called directly: SamplingPattern rejects non-finite coordinates at the API)."""
+    rng = np.random.default_rng(20261019)
+    out = {}
+    names = []
+    for d in (2, 3):
+        for ns, pin in ((64, -1), (300, 150)):
+            name = f"nf{d}_{ns}"
+            shots = rng.uniform(-1.3, 1.3, (4, ns, d))
+            shots[0, 10, 0] = np.nan
+            shots[1, 20, d - 1] = np.inf
+            shots[2, 5, 1] = -np.inf
+            shots[2, 7, 0] = np.nan
+            a, b, pv = 0.05, 0.01, np.full(d, 0.05)
+            lam = pr._stacked_operator_norm(ns, pin)
+            res = np.empty_like(shots)
+            pr._project_all(shots, a, b, pin, pv, 50, 1.0 / lam, False, 1e-7, res)
+            out.update({f"{name}_in": shots, f"{name}_out": res, f"{name}_a": np.float64(a),
+                        f"{name}_b": np.float64(b), f"{name}_pin": np.int64(pin),
+                        f"{name}_pinval": pv, f"{name}_lam": np.float64(lam)})
+            names.append(name)
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "projection_nonfinite.npz"), **out)
+
+
 def host_fixtures():
     out = {}
     for n_c, n_s, d in ((8, 33, 2), (16, 32, 3), (4096, 4, 3), (1, 9, 2)):
@@ -459,7 +485,7 @@ def analysis_fixtures():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["repulsion", "attraction", "projection", "host", "optimize",
-                             "analysis", "trajectory"]
+                             "analysis", "trajectory", "nonfinite"]
     if "repulsion" in which:
         repulsion_fixtures()
     if "attraction" in which:
@@ -474,6 +500,8 @@ if __name__ == "__main__":
         analysis_fixtures()
     if "trajectory" in which:
         trajectory_fixtures()
+    if "nonfinite" in which:
+        nonfinite_fixtures()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -107,6 +107,25 @@ def test_random_cases_vs_oracle(spk):
             assert np.array_equal(out, ref), (d, ns, np.abs(out - ref).max())
 
 
+def test_nonfinite_samples_match_reference(spk):
+    """Shots holding NaN / +-inf samples through the K3 kernels: outputs equal the
+    reference's _project_all (NaN positions included) and the sweep counts the oracle's."""
+    nf = golden("projection_nonfinite")
+    for name in nf["names"]:
+        shots = nf[f"{name}_in"]
+        d, pin = shots.shape[2], int(nf[f"{name}_pin"])
+        pc = None if pin < 0 else spk.LinearConstraint(pin, nf[f"{name}_pinval"])
+        cfg = spk.ProjectionConfig(alpha=float(nf[f"{name}_a"]), beta=float(nf[f"{name}_b"]),
+                                   raster_dt=1.0, n_pit=50, pin=pc)
+        tau = 1.0 / float(nf[f"{name}_lam"])
+        out, _, sw = run(spk, shots, cfg, tau)
+        assert np.array_equal(out, nf[f"{name}_out"], equal_nan=True), name
+        _, rsw = orc.project_all(shots, cfg.speed_bound, cfg.accel_bound, pin,
+                                 nf[f"{name}_pinval"] if pin >= 0 else np.zeros(d), 50, tau,
+                                 0.1 * cfg.feas_tol)
+        assert np.array_equal(sw, rsw), name
+
+
 def test_public_api(spk, proj):
     rng = np.random.default_rng(4)
     cfg = spk.ProjectionConfig(alpha=10216.0, beta=4.6e7, raster_dt=1e-5, n_pit=80)

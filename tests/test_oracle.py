@@ -98,6 +98,18 @@ def test_project_all_bitwise(proj):
         assert np.array_equal(out, proj[f"{name}_out"]), name
 
 
+def test_project_all_nonfinite_bitwise():
+    # NaN / +-inf samples through _project_all (numba kernel fixture): NaN spreads and
+    # the polish's comparisons treat it as satisfied, exactly as in the reference
+    nf = golden("projection_nonfinite")
+    for name in nf["names"]:
+        out, _ = orc.project_all(nf[f"{name}_in"], float(nf[f"{name}_a"]),
+                                 float(nf[f"{name}_b"]), int(nf[f"{name}_pin"]),
+                                 nf[f"{name}_pinval"], 50, 1.0 / float(nf[f"{name}_lam"]), 1e-7)
+        assert np.isnan(out).any(), name
+        assert np.array_equal(out, nf[f"{name}_out"], equal_nan=True), name
+
+
 def test_trace_bitwise(proj):
     for name in ("mono2d", "trace3d"):
         c = _case(proj, name)
