@@ -18,6 +18,7 @@ the gloo backend.
 
 from __future__ import annotations
 
+import contextlib
 import os
 
 import numpy as np
@@ -125,17 +126,38 @@ class CudaOps:
         return self._ostreams
 
     def project_overlap(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, fld,
-                        att_val, att_grad, sweeps, order):
+                        att_val, att_grad, sweeps, order, groups_out=None):
         n_c = coords.shape[0]
         ps, ks = self._overlap_streams()
         g = max(1, min(len(ps), n_c // 8))
         return project_overlap_device(coords, proj_cfg, grad=grad, eta=eta, out=out,
                                       pos4=pos4, nonfinite=nonfinite, field=fld,
                                       att_val=att_val, att_grad=att_grad, sweeps=sweeps,
-                                      order=order, polish_streams=ps[:g], k2_streams=ks[:g])
+                                      order=order, polish_streams=ps[:g], k2_streams=ks[:g],
+                                      groups_out=groups_out)
 
     def repulsion_sums(self, tgt4, src4, cfg):
         return direct_sums_device(tgt4, src4, cfg.dims, cfg.repulsion.kernel_eps ** 2)
+
+    def k1_streams(self):
+        """(gather stream, K1 stream) of the pipelined K1 (ShardedRun._k1_pipelined)."""
+        if not hasattr(self, "_k1s"):
+            self._k1s = (torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0))
+        return self._k1s
+
+    def k1_workspace_bytes(self, shapes) -> int:
+        return max(_native.query("spk_nbody_workspace_bytes", t, 0, s) for t, s in shapes)
+
+    def repulsion_block(self, tgt4, src4, cfg, ws):
+        """K1 of a target block against a source block, fresh fp64 outputs, caller-owned
+        workspace (launches on a side stream must not share the cached one)."""
+        n_t, n_s, d = tgt4.shape[0], src4.shape[0], cfg.dims
+        val = torch.empty(n_t, dtype=torch.float64, device=tgt4.device)
+        grad = torch.empty((n_t, d), dtype=torch.float64, device=tgt4.device)
+        _native.call("spk_direct_sums", tgt4.data_ptr(), n_t, src4.data_ptr(), n_s, d,
+                     float(cfg.repulsion.kernel_eps ** 2), val.data_ptr(), grad.data_ptr(),
+                     ws.data_ptr(), ws.numel(), _device.stream())
+        return val, grad
 
     # ---- spatial target partition for the treecodes (ShardedRun.spatial)
     def spatial_capable(self, cfg) -> bool:
@@ -160,6 +182,93 @@ class CudaOps:
         _native.call("spk_upsample_shots", coords.data_ptr(), out.data_ptr(), n_c, n_s, d,
                      _device.stream())
         return out
+
+
+def k1_pipelined(ops, cfg, pos, groups, world, gather):
+    """K1 (repulsion) of the next evaluation computed under the polish, as the polish
+    groups finish (ShardedRun with the overlap schedule on several ranks; DESIGN.md
+    section 7).
+
+    ``pos``: this rank's position records [local shots, n_s, 4] as the projection writes
+    them; ``groups``: (shot ids, polished event) per polish group in launch order, every
+    rank with the same number of equally sized groups; ``gather(q, loc_q, src_q)`` fills
+    ``src_q`` with every rank's q-th group block (``loc_q`` is this rank's; an NCCL
+    all_gather_into_tensor across ranks).  Groups are taken in their expected finishing
+    order (shortest first: the reverse of the longest-first launch order).  For the q-th
+    group its block is gathered on a gather stream; then on a K1 stream the local targets
+    of group q are summed against the gathered groups 0..q and the local targets of groups
+    0..q-1 against gathered group q -- every (target group, source group) block runs
+    once, as soon as both are final.  Sums accumulate per target group in a fixed block
+    order (deterministic).  Returns (val, grad, [event]) in shot order, or None if the
+    groups are unequal."""
+    sizes = {int(ids.numel()) for ids, _ in groups}
+    if len(sizes) != 1:
+        return None
+    G, n_g = len(groups), sizes.pop()
+    local, n_s = pos.shape[0], pos.shape[1]
+    d = cfg.dims
+    ng_t = n_g * n_s
+    cuda = pos.is_cuda
+    dev = pos.device
+    loc = ops.empty((G, ng_t, 4), torch.float32)
+    src = ops.empty((G, world * ng_t, 4), torch.float32)
+    acc_v = torch.zeros((G, ng_t), dtype=torch.float64, device=dev)
+    acc_g = torch.zeros((G, ng_t, d), dtype=torch.float64, device=dev)
+    proc = list(reversed(range(G)))
+    ws = None
+    if cuda:
+        cs, ks = ops.k1_streams()
+        shapes = [(ng_t, (q + 1) * world * ng_t) for q in range(G)]
+        shapes += [(q * ng_t, world * ng_t) for q in range(1, G)]
+        cs.wait_stream(torch.cuda.current_stream())
+        ks.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(ks):
+            ws = torch.empty(ops.k1_workspace_bytes(shapes), dtype=torch.uint8, device=dev)
+
+    def on(stream):
+        return torch.cuda.stream(stream) if cuda else contextlib.nullcontext()
+
+    def block(tgt4, src4):
+        if cuda:
+            return ops.repulsion_block(tgt4, src4, cfg, ws)
+        return ops.repulsion_sums(tgt4, src4, cfg)
+
+    for q, g in enumerate(proc):
+        ids, polished = groups[g]
+        if cuda and polished is not None:
+            cs.wait_event(polished)
+        with on(cs if cuda else None):
+            loc[q].copy_(pos.index_select(0, ids.long()).reshape(ng_t, 4))
+            gather(q, loc[q], src[q])
+        if cuda:
+            ks.wait_stream(cs)
+        with on(ks if cuda else None):
+            v, gg = block(loc[q], src[:q + 1].reshape(-1, 4))
+            acc_v[q] += v
+            acc_g[q] += gg.view(ng_t, d)
+            if q > 0:
+                v, gg = block(loc[:q].reshape(-1, 4), src[q])
+                acc_v[:q] += v.view(q, ng_t)
+                acc_g[:q] += gg.view(q, ng_t, d)
+    with on(ks if cuda else None):
+        ids_all = torch.cat([groups[g][0] for g in proc]).long()
+        vr = ops.empty(local * n_s)
+        gr = ops.empty((local * n_s, d))
+        vr.view(local, n_s)[ids_all] = acc_v.view(G * n_g, n_s)
+        gr.view(local, n_s, d)[ids_all] = acc_g.view(G * n_g, n_s, d)
+    events = []
+    if cuda:
+        ev = torch.cuda.Event()
+        ev.record(ks)
+        events.append(ev)
+        for t in (loc, src, acc_v, acc_g, vr, gr, ws, ids_all):
+            t.record_stream(ks)
+        for t in (loc, src, pos):
+            t.record_stream(cs)
+        for ids, _ in groups:
+            ids.record_stream(cs)
+            ids.record_stream(ks)
+    return vr, gr, events
 
 
 class ShardedRun:
@@ -215,6 +324,7 @@ class ShardedRun:
         self.spatial = (hasattr(ops, "spatial_capable") and ops.spatial_capable(self.cfg)
                         and (self.world > 1 if env is None else env == "1"))
         self.att_pre = None
+        self.rep_pre = None
         self.sweeps_prev = None
         if self.overlap:
             self.att_val = ops.empty(self.local * n_s)
@@ -254,6 +364,7 @@ class ShardedRun:
         self.have_prev = False
         self.host_prev = None
         self.att_pre = None
+        self.rep_pre = None
 
     def _pos4_target(self):
         n = self.local * self.n_s
@@ -269,7 +380,13 @@ class ShardedRun:
             # gathered sources, and it co-runs with the tail of K2
             va, ga, k2_events = self.att_pre
             self.att_pre = None
-            vr, gr = self.ops.repulsion_sums(tgt, self.pos4_all, self.cfg)
+            if self.rep_pre is not None:
+                # K1 too ran under the polish, block by block (_k1_pipelined)
+                vr, gr, k1_events = self.rep_pre
+                self.rep_pre = None
+                k2_events = list(k2_events) + list(k1_events)
+            else:
+                vr, gr = self.ops.repulsion_sums(tgt, self.pos4_all, self.cfg)
             if k2_events:
                 cur = torch.cuda.current_stream()
                 for ev in k2_events:
@@ -355,6 +472,24 @@ class ShardedRun:
         mean = float(self.sweeps_prev.to(torch.float64).mean().item())
         return mean >= self.OVERLAP_MIN_SWEEPS_PER_SOURCE * n_src
 
+    def _use_k1_pipeline(self) -> bool:
+        """K1 block by block under the polish (_k1_pipelined), opt-in with SPK_K1_PIPE=1
+        (even shards only).  Off by default: the per-rank-share projection measured it
+        within +-3 % of the plain overlap schedule at N = 2 / 4 / 8 (the K1 blocks take
+        issue slots from the latency-bound polish on the same SMs)."""
+        return os.environ.get("SPK_K1_PIPE") == "1" and self.even
+
+    def _k1_pipelined(self, groups):
+        """K1 of the next evaluation, block by block under the polish (k1_pipelined)."""
+        def gather(q, loc_q, src_q):
+            if self.world > 1:
+                dist.all_gather_into_tensor(src_q, loc_q, group=self.group)
+            else:
+                src_q.copy_(loc_q)
+
+        pos = self._pos4_target().view(self.local, self.n_s, 4)
+        return k1_pipelined(self.ops, self.cfg, pos, groups, self.world, gather)
+
     def step_project(self, proj_cfg, eta: float) -> bool:
         """coords <- P(coords - eta * grad); returns False if the step was non-finite."""
         self.flag.zero_()
@@ -363,10 +498,13 @@ class ShardedRun:
             if self.sweeps_prev is not None:
                 order = torch.argsort(self.sweeps_prev, descending=True,
                                       stable=True).to(torch.int32)
+            groups = [] if self._use_k1_pipeline() else None
             out, k2_events = self.ops.project_overlap(
                 self.coords, proj_cfg, self.grad, float(eta), self.next, self._pos4_target(),
-                self.flag, self.fld, self.att_val, self.att_grad, self.sweeps, order)
+                self.flag, self.fld, self.att_val, self.att_grad, self.sweeps, order,
+                groups_out=groups)
             self.att_pre = (self.att_val, self.att_grad, k2_events)
+            self.rep_pre = self._k1_pipelined(groups) if groups else None
             self.sweeps_prev = self.sweeps.clone()
         elif self.overlap:
             # plain schedule, but keep the sweep counts that decide and order the overlap

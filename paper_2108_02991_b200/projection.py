@@ -190,7 +190,7 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
                            out: torch.Tensor, pos4: torch.Tensor, nonfinite, field,
                            att_val: torch.Tensor, att_grad: torch.Tensor,
                            sweeps: torch.Tensor, order: torch.Tensor | None,
-                           polish_streams, k2_streams, eta_per_shot=None):
+                           polish_streams, k2_streams, eta_per_shot=None, groups_out=None):
     """K3 with the lattice attraction (K2) of every shot started as soon as its polish
     group is done, so that K2 runs under the polish of the slower shots.
 
@@ -203,7 +203,9 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
     K2 writes ``att_val`` [n_shots * n_s] / ``att_grad`` [n_shots * n_s, d] for the NEW
     positions ``pos4``.  Returns ``(out, k2_events)``: the caller's stream has waited for
     the projection; wait on ``k2_events`` before reading ``att_val`` / ``att_grad``.
-    ``sweeps`` receives this call's sweep counts."""
+    ``sweeps`` receives this call's sweep counts.  ``groups_out`` (a list) receives
+    ``(shot ids, polished event)`` per group in launch order, for work that may start as
+    soon as a group's positions are final (the engine's pipelined K1)."""
     n_c, n_s, dims = coords.shape
     pin_idx, pin_val = _pin_arrays(cfg, dims)
     tau = 1.0 / stacked_operator_norm(n_s, pin_idx)
@@ -241,6 +243,8 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
         polished = torch.cuda.Event()
         polished.record(ps)
         ks.wait_event(polished)
+        if groups_out is not None:
+            groups_out.append((ids, polished))
         kb = _native.query("spk_grid_sums_shots_workspace_bytes", hi - lo, n_s, n_cells)
         kws = _device.workspace(kb, f"k2_overlap_{g}")
         _native.call("spk_grid_sums_shots", pos4.data_ptr(), ids.data_ptr(), hi - lo, n_s,

@@ -126,15 +126,64 @@ def main():
                 rec["overlap_project_k2_ms"] = f[0].elapsed_time(f[1])
                 rec["overlap_k1_combine_ms"] = f[1].elapsed_time(f[2])
                 rec["overlap_k1_ms"] = f[1].elapsed_time(f[3])
+                # pipelined K1 (engine.k1_pipelined, several ranks): every polish group's
+                # block is gathered as it finishes and the K1 blocks run under the polish.
+                # The other ranks' q-th groups are taken from the current positions and
+                # assumed final when ours is (one GPU: their timing cannot be observed).
+                if True:
+                    orders = []
+                    for r2 in range(n):
+                        o2 = prev_sweeps.get((n, r2))
+                        o2 = (torch.argsort(o2, descending=True, stable=True)
+                              if o2 is not None else torch.arange(counts[r2], device="cuda"))
+                        orders.append(o2.long() + offs[r2])
+
+                    def gather(q, loc_q, src_q, orders=orders):
+                        G = ngroups[0]
+                        gl = G - 1 - q
+                        rows = []
+                        for r2 in range(n):
+                            c2 = counts[r2]
+                            sh = orders[r2][c2 * gl // G:c2 * (gl + 1) // G]
+                            rows.append((sh[:, None] * ns + torch.arange(ns, device="cuda")
+                                         ).reshape(-1))
+                        src_q.copy_(run.pos4_all.index_select(0, torch.cat(rows)))
+
+                    groups = []
+                    av3 = torch.empty_like(av)
+                    ag3 = torch.empty_like(ag)
+                    sw3 = torch.empty_like(sw2)
+                    h = [ev() for _ in range(2)]
+                    torch.cuda.synchronize()
+                    h[0].record()
+                    _, k2ev3 = ops.project_overlap(coords, pcfg, grad, float(eta), out, pos4,
+                                                   flag, fld, av3, ag3, sw3, order,
+                                                   groups_out=groups)
+                    ngroups = [len(groups)]
+                    res = engine.k1_pipelined(ops, cfg, pos4.view(cnt, ns, 4), groups, n,
+                                              gather)
+                    if res is not None:
+                        vr3, gr3, k1ev = res
+                        for e_ in list(k2ev3) + list(k1ev):
+                            torch.cuda.current_stream().wait_event(e_)
+                        ops.combine(av3, ag3, vr3, gr3, run.p, coords, None, None,
+                                    grad.view(-1, d))
+                        ops.residuals(out, pcfg)
+                        h[1].record()
+                        torch.cuda.synchronize()
+                        rec["pipelined_step_ms"] = h[0].elapsed_time(h[1])
                 prev_sweeps[key] = sw.clone()
                 per.append(rec)
             gather_ms = 16.0 * bench.N_C * ns * (n - 1) / n / 600e9 * 1e3 if n > 1 else 0.0
             tot = [p["sums_ms"] + p["project_ms"] + p["residual_ms"] for p in per]
             tot_o = [p["overlap_project_k2_ms"] + p["overlap_k1_combine_ms"] for p in per]
+            tot_p = [p.get("pipelined_step_ms") for p in per]
             rows[n].append({"iteration": state["it"], "eta": eta, "max_rank_ms": max(tot),
                             "allgather_est_ms": gather_ms,
                             "step_ms": max(tot) + gather_ms,
                             "overlap_step_ms": max(tot_o) + gather_ms,
+                            "pipelined_step_ms": (max(tot_p) + gather_ms
+                                                  if None not in tot_p else None),
                             "max_sums_ms": max(p["sums_ms"] for p in per),
                             "max_project_ms": max(p["project_ms"] for p in per),
                             "ranks": per})
@@ -149,6 +198,8 @@ def main():
     for n in worlds:
         tn = float(np.mean([x["step_ms"] for x in rows[n][1:]]))
         to = float(np.mean([x["overlap_step_ms"] for x in rows[n][1:]]))
+        tp = [x["pipelined_step_ms"] for x in rows[n][1:]]
+        tp = float(np.mean(tp)) if None not in tp else None
         rec = {"config": args.config, "n_ranks": n, "groups": ops.OVERLAP_GROUPS,
                "step_ms": tn,
                "sums_ms": float(np.mean([x["max_sums_ms"] for x in rows[n][1:]])),
@@ -156,6 +207,8 @@ def main():
                "efficiency": (t1 / (n * tn)) if t1 else None,
                "overlap_step_ms": to,
                "overlap_efficiency": (t1 / (n * to)) if t1 else None,
+               "pipelined_step_ms": tp,
+               "pipelined_efficiency": (t1 / (n * tp)) if (t1 and tp) else None,
                "iterations": rows[n]}
         print(json.dumps(rec), flush=True)
 

@@ -126,13 +126,15 @@ class OverlapOracleOps(OracleOps):
         return cfg.grad_mode == "exact"
 
     def project_overlap(self, coords, cfg, grad, eta, out, pos4, nonfinite, fld, att_val,
-                        att_grad, sweeps, order):
+                        att_grad, sweeps, order, groups_out=None):
         self.overlap_calls = getattr(self, "overlap_calls", 0) + 1
         self.project(coords, cfg, grad, eta, out, pos4, nonfinite, sweeps)
         n_c, n_s, d = coords.shape
         ids = np.arange(n_c) if order is None else order.numpy()
         assert sorted(ids.tolist()) == list(range(n_c))
         for grp in np.array_split(ids, self.OVERLAP_GROUPS):
+            if groups_out is not None:
+                groups_out.append((torch.from_numpy(grp.astype(np.int32)), None))
             for c in grp:
                 t = pos4[c * n_s:(c + 1) * n_s, :d].double().numpy()
                 va, ga = orc.grid_sums(t, fld.density.grid, fld.kernel_eps ** 2)

@@ -189,6 +189,53 @@ def test_overlap_schedule_two_ranks_matches_plain(tmp_path, monkeypatch):
     assert np.abs(got["coords"] - single.pattern.coords).max() <= 1e-9
 
 
+def _worker_k1_pipe(rank, world, port, n_c, out_path):
+    from cpu_ops import OverlapOracleOps
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["SPK_OVERLAP"] = "1"
+    os.environ["SPK_K1_PIPE"] = "1"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops = OverlapOracleOps()
+        calls = []
+        orig = ops.repulsion_sums
+
+        def counted(t4, s4, cfg):
+            calls.append((t4.shape[0], s4.shape[0]))
+            return orig(t4, s4, cfg)
+
+        ops.repulsion_sums = counted
+        res = spk.optimize(_cfg(n_c), _hw(), ops=ops)
+        if rank == 0:
+            np.savez(out_path, coords=res.pattern.coords, costs=res.trace.costs(),
+                     blocks=np.array(calls, dtype=np.int64))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_k1_pipeline_two_ranks_matches_plain(tmp_path, monkeypatch):
+    """K1 under the polish (ShardedRun._k1_pipelined, opt-in SPK_K1_PIPE=1, even shards):
+    each polish group's positions are all-gathered as the group finishes and
+    the (target group, source group) blocks of K1 run as soon as both are final.  On two
+    gloo ranks (6 shots each, 3 groups of 2) the iteration equals the plain single-rank
+    loop to fp64 summation order, and the K1 work really ran as blocks."""
+    from cpu_ops import OracleOps
+
+    monkeypatch.setenv("SPK_OVERLAP", "0")
+    single = spk.optimize(_cfg(12), _hw(), ops=OracleOps())
+    out = str(tmp_path / "k.npz")
+    mp.spawn(_worker_k1_pipe, args=(2, _free_port(), 12, out), nprocs=2, join=True)
+    got = np.load(out)
+    n_s = single.pattern.coords.shape[1]
+    blocks = got["blocks"]
+    # group-sized target blocks against 1, 2, 3 gathered groups (2 ranks x 2 shots each)
+    assert (blocks[:, 0] == 2 * n_s).any() and (blocks[:, 1] == 3 * 4 * n_s).any()
+    assert np.allclose(got["costs"], single.trace.costs(), rtol=1e-12, atol=0)
+    assert np.abs(got["coords"] - single.pattern.coords).max() <= 1e-9
+
+
 def _worker_spatial(rank, world, port, n_c, out_path):
     from cpu_ops import OracleOps
 

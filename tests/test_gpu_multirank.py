@@ -27,8 +27,10 @@ def _setup(kind):
     dims = 3
     hw = spk.HardwareSpec(g_max=0.04, s_max=180.0, gamma=42.576e6, raster_dt=1e-5,
                           dwell_dt=1e-5, fov=0.192, matrix=16, dims=dims)
-    extra = {} if kind == "exact" else {"attraction_tree_precision": 1e-4}
-    cfg = spk.OptimizerConfig(n_c=25, n_s=64, dims=dims, n_decim=1, n_git=4,
+    extra = {} if kind.startswith("exact") else {"attraction_tree_precision": 1e-4}
+    # "exact_even": 36 shots = 18 per rank (even shards), with the pipelined K1
+    n_c = 36 if kind == "exact_even" else 25
+    cfg = spk.OptimizerConfig(n_c=n_c, n_s=64, dims=dims, n_decim=1, n_git=4,
                               grad_mode="exact", grid_n=12, seed=6, **extra)
     return spk, cfg, hw
 
@@ -46,7 +48,7 @@ def _worker(rank, world, port, kind, env, out_path):
         from paper_2108_02991_b200 import optimizer as om
 
         st = om.start(cfg, hw)
-        flags = (st.run.overlap, st.run.spatial)
+        flags = (st.run.overlap, st.run.spatial, st.run._use_k1_pipeline())
         res = om.finish(st)
         if rank == 0:
             np.savez(out_path, coords=res.pattern.coords, costs=res.trace.costs(),
@@ -58,6 +60,7 @@ def _worker(rank, world, port, kind, env, out_path):
 @pytest.mark.parametrize("kind,env", [
     ("exact", {"SPK_OVERLAP": "0"}),
     ("exact", {"SPK_OVERLAP": "1"}),
+    ("exact_even", {"SPK_OVERLAP": "1", "SPK_K1_PIPE": "1"}),
     ("tree", {}),
 ])
 def test_two_ranks_on_device_match_one(tmp_path, kind, env):
@@ -77,8 +80,10 @@ def test_two_ranks_on_device_match_one(tmp_path, kind, env):
     got = np.load(out)
     if kind == "tree":
         assert bool(got["flags"][1]), "two ranks with a treecode use the spatial layout"
+    if kind == "exact_even":
+        assert bool(got["flags"][2]), "even shards on two ranks pipeline K1 under the polish"
     # per-rank target sets change the fp32 chunking (exact) or the treecode groups (tree)
-    tol = 1e-6 if kind == "exact" else 1e-4
+    tol = 1e-6 if kind.startswith("exact") else 1e-4
     cs, cg = single.trace.costs(), got["costs"]
     assert np.abs(cg - cs).max() <= tol * np.abs(cs).max(), (kind, env, cg, cs)
     assert np.abs(got["coords"] - single.pattern.coords).max() <= 1e-3

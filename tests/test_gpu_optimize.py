@@ -201,6 +201,40 @@ def test_k2_under_polish_overlap_matches_plain_loop(spk, monkeypatch, dims, n_c)
     assert np.abs(ovl.pattern.coords - plain.pattern.coords).max() <= 1e-5
 
 
+@pytest.mark.parametrize("dims,n_c", [(3, 16), (2, 40)])
+def test_k1_pipeline_matches_plain_loop(spk, monkeypatch, dims, n_c):
+    """K1 block by block under the polish (engine.k1_pipelined, opt-in with SPK_K1_PIPE=1,
+    here on one GPU): per-group gathers on a side stream,
+    (target group, source group) K1 blocks on another, shot-order scatter -- the same
+    iteration as the plain fused loop to fp32 partial-sum order."""
+    hw = desk_hw(spk, dims=dims, matrix=16)
+    cfg = spk.OptimizerConfig(n_c=n_c, n_s=64, dims=dims, n_decim=1, n_git=6,
+                              grad_mode="exact", seed=4, grid_n=12)
+    monkeypatch.setenv("SPK_OVERLAP", "0")
+    plain = spk.optimize(cfg, hw)
+    monkeypatch.setenv("SPK_OVERLAP", "1")
+    monkeypatch.setenv("SPK_K1_PIPE", "1")
+    from paper_2108_02991_b200 import engine
+    from paper_2108_02991_b200 import optimizer as om
+
+    calls = []
+    orig = engine.k1_pipelined
+
+    def counted(*a, **k):
+        out = orig(*a, **k)
+        calls.append(out is not None)
+        return out
+
+    monkeypatch.setattr(engine, "k1_pipelined", counted)
+    st = om.start(cfg, hw)
+    assert st.run.overlap
+    pipe = om.finish(st)
+    assert calls and all(calls)
+    rel = np.abs(pipe.trace.costs() - plain.trace.costs()) / np.abs(plain.trace.costs())
+    assert rel.max() <= 1e-6, rel.max()
+    assert np.abs(pipe.pattern.coords - plain.pattern.coords).max() <= 1e-5
+
+
 def test_spatial_target_partition_on_device(spk, monkeypatch):
     """The treecodes' spatial layout (ShardedRun.spatial: N-body targets in Morton-order
     blocks, results returned to the shot owners; forced on a single GPU with
