@@ -413,6 +413,154 @@ __global__ void __launch_bounds__(NU_THREADS, 2) nudft_adjoint64_kernel(const Ad
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// fp64 adjoint on the FP64 tensor cores (the default; SPK_NUDFT_DMMA=0 selects the DFMA
+// kernel above).  Same tiles, chunks and fp64 generated tables; the products run as
+// mma.sync.m8n8k4.f64 (DMMA: 256 fp64 FMA per warp instruction, measured 1.86e13 FMA/s
+// vs 1.70e13 for DFMA, scripts/micro/dmma_peak.cu) with the complex product split into
+// four real MMAs, Re += Ar Br + (-Ai) Bi and Im += Ar Bi + Ai Br.  Warp w owns the
+// u-blocks 2w, 2w+1 (8 u each) against the four 8-wide v-blocks of the tile: 8 output
+// tiles, 32 DMMA per 4 samples.  Fragment rows: lane = 4 r + c reads sample 4 ks + c of
+// u (A) or v (B) = block base + r; with row strides = 2 (mod 8) double2 each quarter-warp
+// of the 128-bit fragment loads hits 8 distinct bank groups.
+constexpr int NM_AS = NU_UT + 2;  // 66: A row stride (double2)
+constexpr int NM_BS = NU_VT + 2;  // 34: B row stride (double2)
+#ifndef NM_CH_CFG
+#define NM_CH_CFG 64
+#endif
+#ifndef NM_MINB_CFG
+#define NM_MINB_CFG 2
+#endif
+constexpr int NM_CH = NM_CH_CFG;  // samples per table chunk
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
+                 "{%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(NU_THREADS, NM_MINB_CFG) nudft_adjoint_dmma_kernel(const AdjParams P) {
+    extern __shared__ __align__(16) char sm[];
+    double2* At = reinterpret_cast<double2*>(sm);        // [NM_CH][NM_AS]
+    double2* Bt = At + NM_CH * NM_AS;                    // [NM_CH][NM_BS]
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int fr = lane >> 2, fc = lane & 3;  // fragment row (u / v offset), column (sample)
+    const long long u0 = (long long)blockIdx.x * NU_UT;
+    const long long v0 = (long long)blockIdx.y * NU_VT;
+    const int slice = blockIdx.z;
+    const long long i_begin = P.p * slice / P.slices;
+    const long long i_end = P.p * (slice + 1) / P.slices;
+    double cre[2][4][2], cim[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cre[a][b][0] = cre[a][b][1] = cim[a][b][0] = cim[a][b][1] = 0.0;
+    const int h0 = P.n0 / 2, h1 = P.n1 / 2, h2 = P.n2 / 2;
+
+    for (long long c0 = i_begin; c0 < i_end; c0 += NM_CH) {
+        const int cnt = (int)min((long long)NM_CH, i_end - c0);
+        // operand tables, as in nudft_adjoint64_kernel (one row per thread)
+        for (int r = tid; r < 2 * NM_CH; r += NU_THREADS) {
+            const bool rowA = r < NM_CH;
+            const int j = rowA ? r : r - NM_CH;
+            double2* row = rowA ? At + j * NM_AS : Bt + j * NM_BS;
+            if (j >= cnt) {
+                // the MMAs read whole groups of 4 samples: zero rows past the chunk end
+                const int n = rowA ? NU_UT : NU_VT;
+                for (int q = 0; q < n; ++q) row[q] = make_double2(0.0, 0.0);
+                continue;
+            }
+            const long long i = c0 + j;
+            const double k0 = P.pts[i * P.dims];
+            const double k1 = P.pts[i * P.dims + 1];
+            const double2 wi = make_double2(P.w[2 * i], P.w[2 * i + 1]);
+            if (P.dims == 3) {
+                if (rowA) {
+                    int a = (int)(u0 / P.n1), b = (int)(u0 - (long long)a * P.n1);
+                    double2 e0 = cispi(k0 * (double)(a - h0));
+                    double2 e1 = cispi(k1 * (double)(b - h1));
+                    const double2 z1 = cispi(k1);
+                    for (int q = 0; q < NU_UT; ++q) {
+                        row[q] = cmul(e0, e1);
+                        if (++b == P.n1) {
+                            b = 0;
+                            ++a;
+                            e0 = cispi(k0 * (double)(a - h0));
+                            e1 = cispi(k1 * (double)(b - h1));
+                        } else {
+                            e1 = cmul(e1, z1);
+                        }
+                    }
+                } else {
+                    const double k2 = P.pts[i * P.dims + 2];
+                    double2 e2 = cmul(wi, cispi(k2 * (double)(v0 - h2)));
+                    const double2 z2 = cispi(k2);
+                    for (int q = 0; q < NU_VT; ++q) {
+                        row[q] = e2;
+                        e2 = cmul(e2, z2);
+                    }
+                }
+            } else if (rowA) {
+                double2 e0 = cmul(wi, cispi(k0 * (double)(u0 - h0)));
+                const double2 z0 = cispi(k0);
+                for (int q = 0; q < NU_UT; ++q) {
+                    row[q] = e0;
+                    e0 = cmul(e0, z0);
+                }
+            } else {
+                double2 e1 = cispi(k1 * (double)(v0 - h1));
+                const double2 z1 = cispi(k1);
+                for (int q = 0; q < NU_VT; ++q) {
+                    row[q] = e1;
+                    e1 = cmul(e1, z1);
+                }
+            }
+        }
+        __syncthreads();
+        const int ksteps = (cnt + 3) >> 2;
+#pragma unroll 2
+        for (int ks = 0; ks < ksteps; ++ks) {
+            const int j = 4 * ks + fc;
+            double2 a[2], b[4];
+#pragma unroll
+            for (int ub = 0; ub < 2; ++ub) a[ub] = At[j * NM_AS + (2 * warp + ub) * 8 + fr];
+#pragma unroll
+            for (int vb = 0; vb < 4; ++vb) b[vb] = Bt[j * NM_BS + vb * 8 + fr];
+#pragma unroll
+            for (int ub = 0; ub < 2; ++ub) {
+                const double nai = -a[ub].y;
+#pragma unroll
+                for (int vb = 0; vb < 4; ++vb) {
+                    dmma(cre[ub][vb][0], cre[ub][vb][1], a[ub].x, b[vb].x);
+                    dmma(cre[ub][vb][0], cre[ub][vb][1], nai, b[vb].y);
+                    dmma(cim[ub][vb][0], cim[ub][vb][1], a[ub].x, b[vb].y);
+                    dmma(cim[ub][vb][0], cim[ub][vb][1], a[ub].y, b[vb].x);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // accumulator fragment: lane holds C[row fr][cols 2 fc, 2 fc + 1] of each 8 x 8 tile
+#pragma unroll
+    for (int ub = 0; ub < 2; ++ub) {
+        const long long u = u0 + (2 * warp + ub) * 8 + fr;
+        if (u >= P.U) continue;
+        double* out = P.part + ((size_t)slice * P.U + u) * P.V * 2;
+#pragma unroll
+        for (int vb = 0; vb < 4; ++vb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long v = v0 + vb * 8 + 2 * fc + e;
+                if (v < P.V) {
+                    out[2 * v] = cre[ub][vb][e];
+                    out[2 * v + 1] = cim[ub][vb][e];
+                }
+            }
+    }
+}
+
 __global__ void __launch_bounds__(NU_THREADS) nudft_forward64_kernel(const FwdParams P) {
     extern __shared__ __align__(16) char sm[];
     double2* rows = reinterpret_cast<double2*>(sm);  // [NF_UT][V]
@@ -549,21 +697,33 @@ int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int d
     P.U = dims == 3 ? (long long)P.n0 * P.n1 : P.n0;
     P.V = dims == 3 ? P.n2 : P.n1;
     const bool f64 = mode == SPK_NUDFT_FP64;
-    const void* kern = f64 ? (const void*)nudft_adjoint64_kernel : (const void*)nudft_adjoint_kernel;
+    static int dmma_on = -1;
+    if (dmma_on < 0) {
+        const char* e = getenv("SPK_NUDFT_DMMA");
+        dmma_on = (e && e[0] == '0') ? 0 : 1;
+    }
+    const bool tc = f64 && dmma_on;
+    const void* kern = tc ? (const void*)nudft_adjoint_dmma_kernel
+                          : f64 ? (const void*)nudft_adjoint64_kernel
+                                : (const void*)nudft_adjoint_kernel;
     const size_t smem =
-        f64 ? (size_t)ND_CH * (ND_AS + ND_BS) * sizeof(double2)
-            : ((size_t)((NU_CH * NU_AS + 1) & ~1) + (size_t)NU_CH * NU_BS) * sizeof(C2);
+        tc    ? (size_t)NM_CH * (NM_AS + NM_BS) * sizeof(double2)
+        : f64 ? (size_t)ND_CH * (ND_AS + ND_BS) * sizeof(double2)
+              : ((size_t)((NU_CH * NU_AS + 1) & ~1) + (size_t)NU_CH * NU_BS) * sizeof(C2);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NU_THREADS, smem);
-    P.slices = adj_slices(P.U, P.V, p, f64 ? ND_CH : NU_CH, std::max(1, per_sm) * num_sms());
+    P.slices = adj_slices(P.U, P.V, p, tc ? NM_CH : f64 ? ND_CH : NU_CH,
+                          std::max(1, per_sm) * num_sms());
     SPK_REQUIRE(ws_bytes >= (size_t)P.slices * P.U * P.V * 16, SPK_ERR_WORKSPACE,
                 "nudft adjoint: workspace too small");
     P.part = static_cast<double*>(ws);
     dim3 grid3((unsigned)((P.U + NU_UT - 1) / NU_UT), (unsigned)((P.V + NU_VT - 1) / NU_VT),
                (unsigned)P.slices);
     cudaStream_t s = (cudaStream_t)stream;
-    if (f64)
+    if (tc)
+        nudft_adjoint_dmma_kernel<<<grid3, NU_THREADS, smem, s>>>(P);
+    else if (f64)
         nudft_adjoint64_kernel<<<grid3, NU_THREADS, smem, s>>>(P);
     else
         nudft_adjoint_kernel<<<grid3, NU_THREADS, smem, s>>>(P);
