@@ -440,7 +440,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(NU_THREADS, NM_MINB_CFG) nudft_adjoint_dmma_kernel(const AdjParams P) {
+__global__ void __launch_bounds__(NU_THREADS, NM_MINB_CFG)
+    nudft_adjoint_dmma_kernel(const AdjParams P) {
     extern __shared__ __align__(16) char sm[];
     double2* At = reinterpret_cast<double2*>(sm);        // [NM_CH][NM_AS]
     double2* Bt = At + NM_CH * NM_AS;                    // [NM_CH][NM_BS]
