@@ -197,8 +197,9 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
     The polish time of a shot varies by ~3x between shots and the iteration waits for the
     slowest, so SMs idle during that tail -- most of them on a rank with few shots
     (multi-GPU), the last waves' worth on one GPU.  Shots are
-    polished in groups, longest first by the previous iteration's sweep counts (``order``, device int32; None = shot order), each group on
-    its own high-priority stream, and each group's K2 (spk_grid_sums_shots) follows on a
+    polished in groups, longest first by the previous iteration's sweep counts
+    (``order``, device int32; None = shot order), each group on its own high-priority
+    stream, and each group's K2 (spk_grid_sums_shots) follows on a
     low-priority stream.  The projection itself is unchanged (bit-identical per shot);
     K2 writes ``att_val`` [n_shots * n_s] / ``att_grad`` [n_shots * n_s, d] for the NEW
     positions ``pos4``.  Returns ``(out, k2_events)``: the caller's stream has waited for
