@@ -420,11 +420,11 @@ __global__ void __launch_bounds__(NU_THREADS, 2) nudft_adjoint64_kernel(const Ad
 // vs 1.70e13 for DFMA, scripts/micro/dmma_peak.cu) with the complex product split into
 // four real MMAs, Re += Ar Br + (-Ai) Bi and Im += Ar Bi + Ai Br.  Warp w owns the
 // u-blocks 2w, 2w+1 (8 u each) against the four 8-wide v-blocks of the tile: 8 output
-// tiles, 32 DMMA per 4 samples.  Fragment rows: lane = 4 r + c reads sample 4 ks + c of
-// u (A) or v (B) = block base + r; with row strides = 2 (mod 8) double2 each quarter-warp
-// of the 128-bit fragment loads hits 8 distinct bank groups.
-constexpr int NM_AS = NU_UT + 2;  // 66: A row stride (double2)
-constexpr int NM_BS = NU_VT + 2;  // 34: B row stride (double2)
+// tiles, 32 DMMA per 4 samples.  The tables are stored transposed, [u][sample] and
+// [v][sample]: fragment lane = 4 r + c reads sample 4 ks + c of u (A) or v (B) = block
+// base + r, so with a row stride = 4 (mod 8) double2 each quarter-warp of the 128-bit
+// fragment loads hits 8 distinct bank groups, and the row-per-thread generation (one
+// sample per thread) writes consecutive addresses across the warp.
 #ifndef NM_CH_CFG
 #define NM_CH_CFG 64
 #endif
@@ -432,9 +432,11 @@ constexpr int NM_BS = NU_VT + 2;  // 34: B row stride (double2)
 #define NM_MINB_CFG 2
 #endif
 constexpr int NM_CH = NM_CH_CFG;  // samples per table chunk
+constexpr int NM_S = NM_CH + 4;   // table row stride (double2), = 4 (mod 8)
+static_assert(2 * NM_CH == NU_THREADS, "one thread per (sample, half) of the table chunk");
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
                  "{%0, %1};"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
@@ -443,8 +445,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 __global__ void __launch_bounds__(NU_THREADS, NM_MINB_CFG)
     nudft_adjoint_dmma_kernel(const AdjParams P) {
     extern __shared__ __align__(16) char sm[];
-    double2* At = reinterpret_cast<double2*>(sm);        // [NM_CH][NM_AS]
-    double2* Bt = At + NM_CH * NM_AS;                    // [NM_CH][NM_BS]
+    double2* At = reinterpret_cast<double2*>(sm);        // [NU_UT][NM_S]: u-major
+    double2* Bt = At + NU_UT * NM_S;                     // [NU_VT][NM_S]: v-major
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int fr = lane >> 2, fc = lane & 3;  // fragment row (u / v offset), column (sample)
@@ -462,29 +464,38 @@ __global__ void __launch_bounds__(NU_THREADS, NM_MINB_CFG)
 
     for (long long c0 = i_begin; c0 < i_end; c0 += NM_CH) {
         const int cnt = (int)min((long long)NM_CH, i_end - c0);
-        // operand tables, as in nudft_adjoint64_kernel (one row per thread)
-        for (int r = tid; r < 2 * NM_CH; r += NU_THREADS) {
-            const bool rowA = r < NM_CH;
-            const int j = rowA ? r : r - NM_CH;
-            double2* row = rowA ? At + j * NM_AS : Bt + j * NM_BS;
+        // operand tables: thread (sample j = tid mod NM_CH, half h = tid / NM_CH) writes
+        // half h of sample j's A column (32 u) and of its B column (16 v), the two fp64
+        // recurrences interleaved; each half starts from its own sincospi seed
+        {
+            const int j = tid % NM_CH, h = tid / NM_CH;
+            double2* colA = At + j;
+            double2* colB = Bt + j;
+            constexpr int QA = NU_UT / 2, QB = NU_VT / 2;
             if (j >= cnt) {
-                // the MMAs read whole groups of 4 samples: zero rows past the chunk end
-                const int n = rowA ? NU_UT : NU_VT;
-                for (int q = 0; q < n; ++q) row[q] = make_double2(0.0, 0.0);
-                continue;
-            }
-            const long long i = c0 + j;
-            const double k0 = P.pts[i * P.dims];
-            const double k1 = P.pts[i * P.dims + 1];
-            const double2 wi = make_double2(P.w[2 * i], P.w[2 * i + 1]);
-            if (P.dims == 3) {
-                if (rowA) {
-                    int a = (int)(u0 / P.n1), b = (int)(u0 - (long long)a * P.n1);
+                // the MMAs read whole groups of 4 samples: zero columns past the chunk end
+                for (int q = 0; q < QA; ++q) colA[(h * QA + q) * NM_S] = make_double2(0.0, 0.0);
+                for (int q = 0; q < QB; ++q) colB[(h * QB + q) * NM_S] = make_double2(0.0, 0.0);
+            } else {
+                const long long i = c0 + j;
+                const double k0 = P.pts[i * P.dims];
+                const double k1 = P.pts[i * P.dims + 1];
+                const double2 wi = make_double2(P.w[2 * i], P.w[2 * i + 1]);
+                if (P.dims == 3) {
+                    const long long ua = u0 + h * QA;
+                    int a = (int)(ua / P.n1), b = (int)(ua - (long long)a * P.n1);
                     double2 e0 = cispi(k0 * (double)(a - h0));
                     double2 e1 = cispi(k1 * (double)(b - h1));
                     const double2 z1 = cispi(k1);
-                    for (int q = 0; q < NU_UT; ++q) {
-                        row[q] = cmul(e0, e1);
+                    const double k2 = P.pts[i * P.dims + 2];
+                    double2 e2 = cmul(wi, cispi(k2 * (double)(v0 + h * QB - h2)));
+                    const double2 z2 = cispi(k2);
+                    for (int q = 0; q < QA; ++q) {
+                        colA[(h * QA + q) * NM_S] = cmul(e0, e1);
+                        if (q < QB) {
+                            colB[(h * QB + q) * NM_S] = e2;
+                            e2 = cmul(e2, z2);
+                        }
                         if (++b == P.n1) {
                             b = 0;
                             ++a;
@@ -495,27 +506,18 @@ __global__ void __launch_bounds__(NU_THREADS, NM_MINB_CFG)
                         }
                     }
                 } else {
-                    const double k2 = P.pts[i * P.dims + 2];
-                    double2 e2 = cmul(wi, cispi(k2 * (double)(v0 - h2)));
-                    const double2 z2 = cispi(k2);
-                    for (int q = 0; q < NU_VT; ++q) {
-                        row[q] = e2;
-                        e2 = cmul(e2, z2);
+                    double2 e0 = cmul(wi, cispi(k0 * (double)(u0 + h * QA - h0)));
+                    const double2 z0 = cispi(k0);
+                    double2 e1 = cispi(k1 * (double)(v0 + h * QB - h1));
+                    const double2 z1 = cispi(k1);
+                    for (int q = 0; q < QA; ++q) {
+                        colA[(h * QA + q) * NM_S] = e0;
+                        e0 = cmul(e0, z0);
+                        if (q < QB) {
+                            colB[(h * QB + q) * NM_S] = e1;
+                            e1 = cmul(e1, z1);
+                        }
                     }
-                }
-            } else if (rowA) {
-                double2 e0 = cmul(wi, cispi(k0 * (double)(u0 - h0)));
-                const double2 z0 = cispi(k0);
-                for (int q = 0; q < NU_UT; ++q) {
-                    row[q] = e0;
-                    e0 = cmul(e0, z0);
-                }
-            } else {
-                double2 e1 = cispi(k1 * (double)(v0 - h1));
-                const double2 z1 = cispi(k1);
-                for (int q = 0; q < NU_VT; ++q) {
-                    row[q] = e1;
-                    e1 = cmul(e1, z1);
                 }
             }
         }
@@ -526,17 +528,24 @@ __global__ void __launch_bounds__(NU_THREADS, NM_MINB_CFG)
             const int j = 4 * ks + fc;
             double2 a[2], b[4];
 #pragma unroll
-            for (int ub = 0; ub < 2; ++ub) a[ub] = At[j * NM_AS + (2 * warp + ub) * 8 + fr];
+            for (int ub = 0; ub < 2; ++ub) a[ub] = At[((2 * warp + ub) * 8 + fr) * NM_S + j];
 #pragma unroll
-            for (int vb = 0; vb < 4; ++vb) b[vb] = Bt[j * NM_BS + vb * 8 + fr];
+            for (int vb = 0; vb < 4; ++vb) b[vb] = Bt[(vb * 8 + fr) * NM_S + j];
+            // two passes over the 16 accumulators, so that the two MMAs into one
+            // accumulator are 16 instructions apart (DMMA latency)
+#pragma unroll
+            for (int ub = 0; ub < 2; ++ub)
+#pragma unroll
+                for (int vb = 0; vb < 4; ++vb) {
+                    dmma(cre[ub][vb][0], cre[ub][vb][1], a[ub].x, b[vb].x);
+                    dmma(cim[ub][vb][0], cim[ub][vb][1], a[ub].x, b[vb].y);
+                }
 #pragma unroll
             for (int ub = 0; ub < 2; ++ub) {
                 const double nai = -a[ub].y;
 #pragma unroll
                 for (int vb = 0; vb < 4; ++vb) {
-                    dmma(cre[ub][vb][0], cre[ub][vb][1], a[ub].x, b[vb].x);
                     dmma(cre[ub][vb][0], cre[ub][vb][1], nai, b[vb].y);
-                    dmma(cim[ub][vb][0], cim[ub][vb][1], a[ub].x, b[vb].y);
                     dmma(cim[ub][vb][0], cim[ub][vb][1], a[ub].y, b[vb].x);
                 }
             }
@@ -708,7 +717,7 @@ int spk_nudft_adjoint(const double* pts, const double* weights, int64_t p, int d
                           : f64 ? (const void*)nudft_adjoint64_kernel
                                 : (const void*)nudft_adjoint_kernel;
     const size_t smem =
-        tc    ? (size_t)NM_CH * (NM_AS + NM_BS) * sizeof(double2)
+        tc    ? (size_t)(NU_UT + NU_VT) * NM_S * sizeof(double2)
         : f64 ? (size_t)ND_CH * (ND_AS + ND_BS) * sizeof(double2)
               : ((size_t)((NU_CH * NU_AS + 1) & ~1) + (size_t)NU_CH * NU_BS) * sizeof(C2);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
