@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: NM_CH_CFG / NM_MINB_CFG variants predate the transposed-table kernel, which fixes 64-sample chunks)
 # DMMA adjoint variants: table chunk x CTAs per SM (built on the box with scripts/ab_build.sh).
 mkdir -p gpurun_out
 for v in "base|" "ch32_m3|-DNM_CH_CFG=32 -DNM_MINB_CFG=3" "ch32_m4|-DNM_CH_CFG=32 -DNM_MINB_CFG=4" "ch32_m2|-DNM_CH_CFG=32 -DNM_MINB_CFG=2"; do
