@@ -903,6 +903,15 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
 #define SPK_POLISH_MINB 3
 #endif
 constexpr int PL_MINB = SPK_POLISH_MINB;
+// Wider rings (> 8 warps, N_s > 1283): the instantiation's thread bound and CTAs per SM.
+#ifndef SPK_POLISH_WIDE_T
+#define SPK_POLISH_WIDE_T 1024
+#endif
+#ifndef SPK_POLISH_WIDE_MINB
+#define SPK_POLISH_WIDE_MINB 1
+#endif
+constexpr int PL_WIDE_T = SPK_POLISH_WIDE_T;
+constexpr int PL_WIDE_MINB = SPK_POLISH_WIDE_MINB;
 
 // Ring width: W warps; SPK_POLISH_WARPS overrides (fewer warps -> more shots resident
 // per SM, longer per-sweep latency).
@@ -1225,6 +1234,12 @@ static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, 
                          (int)psm);
     cudaFuncSetAttribute(polish_kernel<2, 1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)psm);
+    cudaFuncSetAttribute(polish_kernel<3, PL_WIDE_T, PL_WIDE_MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)psm);
+    cudaFuncSetAttribute(polish_kernel<2, PL_WIDE_T, PL_WIDE_MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)psm);
     double* pws = static_cast<double*>(ws);
     // <= 8 warps (N_s <= 1283): a register budget of 80 keeps the ring window in registers
     // with 3 CTAs per SM; wider rings use the 1024-thread instantiation
@@ -1237,8 +1252,13 @@ static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, 
         if (dims == 3) PL_LAUNCH(3, 256, PL_MINB);
         else PL_LAUNCH(2, 256, PL_MINB);
     } else {
-        if (dims == 3) PL_LAUNCH(3, 1024, 1);
-        else PL_LAUNCH(2, 1024, 1);
+        if (32 * pw <= PL_WIDE_T) {
+            if (dims == 3) PL_LAUNCH(3, PL_WIDE_T, PL_WIDE_MINB);
+            else PL_LAUNCH(2, PL_WIDE_T, PL_WIDE_MINB);
+        } else {
+            if (dims == 3) PL_LAUNCH(3, 1024, 1);
+            else PL_LAUNCH(2, 1024, 1);
+        }
     }
 #undef PL_LAUNCH
     SPK_CHECK_LAUNCH("polish_kernel");
