@@ -69,12 +69,15 @@ int spk_grid_sums(const void* tgt, int64_t n_tgt, const float* grid_w, const int
 /* K2 for the rows of a shot subset (the multi-GPU path's attraction of shots whose polish
  * has finished, overlapped with the polish of the others): targets are the n_s records
  * of each listed shot in tgt (shot-major), results go to the same rows of val [.] and
- * grad [.][dims] (other rows untouched).  Same arithmetic as spk_grid_sums. */
+ * grad [.][dims] (other rows untouched).  Same arithmetic as spk_grid_sums.
+ * sm_busy (optional, device int32 [256], zero-initialised, shared with spk_polish_shots):
+ * each CTA first waits until its SM holds no polish CTA, so the launch uses only the SMs
+ * the polish has left (NULL = no waiting). */
 size_t spk_grid_sums_shots_workspace_bytes(int64_t n_ids, int n_s, int64_t n_cells);
 int spk_grid_sums_shots(const void* tgt, const int32_t* shot_ids, int64_t n_ids, int n_s,
                         const float* grid_w, const int64_t* side, int dims, float eps2,
-                        double* val, double* grad, void* ws, size_t ws_bytes,
-                        spk_stream_t stream);
+                        double* val, double* grad, const int32_t* sm_busy, void* ws,
+                        size_t ws_bytes, spk_stream_t stream);
 
 /* Both sums in ONE launch (the optimize() hot loop, optimizer.py:302-303): segment 0 =
  * the density lattice (attraction), segment 1 = positions (repulsion).  Either segment
@@ -163,10 +166,12 @@ int spk_project_fista(const double* in, const double* grad, double eta,
                       int dims, double a, double b, int pin_idx, const double* pin_val,
                       int n_pit, double tau, int monotone, double* trace, int32_t* nonfinite,
                       void* ws, size_t ws_bytes, spk_stream_t stream);
+/* sm_busy (optional, see spk_grid_sums_shots): every polish CTA counts itself on its SM
+ * while it runs. */
 int spk_polish_shots(double* shots, const int32_t* shot_ids, int64_t n_ids, int64_t n_shots,
                      int n_s, int dims, double a, double b, int pin_idx, const double* pin_val,
-                     double tol, int max_sweeps, void* pos4, int32_t* sweeps, void* ws,
-                     size_t ws_bytes, spk_stream_t stream);
+                     double tol, int max_sweeps, void* pos4, int32_t* sweeps,
+                     int32_t* sm_busy, void* ws, size_t ws_bytes, spk_stream_t stream);
 
 /* feasibility_residuals (projection.py:435-452): out[0..4] = amplitude, speed,
  * acceleration, pin (0 if no pin), max -- each already clipped at 0 like the reference. */

@@ -84,6 +84,9 @@ struct NBParams {
     long long per_group;
     long long tb_per_group;
     long long src_stride;
+    // optional: CTAs wait until their SM holds no polish CTA (polish_kernel's count), so a
+    // launch beside the polish takes only the SMs the polish has left
+    const int* sm_busy;
 };
 
 constexpr int NB_TILE_W = NB_TILE;  // lattice cells per stage (fp32 partials span <= 512 cells)
@@ -288,6 +291,13 @@ __global__ void __launch_bounds__(NB_THREADS, NB_MINBLOCKS_CFG) nbody_kernel(con
     float* axes = reinterpret_cast<float*>(stages + NB_TILE_BYTES + NB_ACC_BYTES);
     __shared__ __align__(8) uint64_t bars[NB_STAGES];
     const int tid = threadIdx.x;
+    if (P.sm_busy) {
+        if (tid == 0) {
+            const volatile int* busy = P.sm_busy + sm_id();
+            while (*busy > 0) __nanosleep(20000);
+        }
+        __syncthreads();
+    }
     // Interleave the lattice (SFU-bound) and position (FMA-bound) units in launch order,
     // in proportion to their counts (Bresenham), so that the CTAs resident on an SM mix
     // both kinds and the two pipes overlap instead of running one phase after the other.
@@ -462,7 +472,8 @@ static Plan make_plan(long long n_tgt, long long n0, long long n1, long long n_g
 static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float* w0,
                        const int64_t* side, float e0, const float4* s1, long long n1, float e1,
                        double* val0, double* grad0, double* val1, double* grad1, void* ws,
-                       size_t ws_bytes, cudaStream_t stream, long long n_groups = 1) {
+                       size_t ws_bytes, cudaStream_t stream, long long n_groups = 1,
+                       const int* sm_busy = nullptr) {
     SPK_REQUIRE(n_groups >= 1 && n_tgt % n_groups == 0, SPK_ERR_ARG,
                 "targets (%lld) must split evenly into %lld groups", n_tgt, n_groups);
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
@@ -502,6 +513,7 @@ static int launch_sums(const float4* tgt, long long n_tgt, int dims, const float
     P.per_group = n_tgt / n_groups;
     P.tb_per_group = pl.n_tb / n_groups;
     P.src_stride = n_groups > 1 ? n1 : 0;
+    P.sm_busy = sm_busy;
     P.seg[0] = SegDesc{w0, n0, (n0 + NB_TILE_W - 1) / NB_TILE_W, pl.nc0, 1, e0,
                        sd[0], sd[1], dims == 3 ? sd[2] : 1};
     P.seg[1] = SegDesc{s1, n1, (n1 + NB_TILE - 1) / NB_TILE, pl.nc1, 0, e1, 0, 0, 0};
@@ -716,8 +728,8 @@ size_t spk_grid_sums_shots_workspace_bytes(int64_t n_ids, int n_s, int64_t n_cel
 
 int spk_grid_sums_shots(const void* tgt, const int32_t* shot_ids, int64_t n_ids, int n_s,
                         const float* grid_w, const int64_t* side, int dims, float eps2,
-                        double* val, double* grad, void* ws, size_t ws_bytes,
-                        spk_stream_t stream_) {
+                        double* val, double* grad, const int32_t* sm_busy, void* ws,
+                        size_t ws_bytes, spk_stream_t stream_) {
     SPK_REQUIRE(dims == 2 || dims == 3, SPK_ERR_ARG, "dims must be 2 or 3, got %d", dims);
     SPK_REQUIRE(n_ids >= 0 && n_s >= 1, SPK_ERR_ARG, "shot subset: bad sizes");
     if (n_ids == 0) return SPK_OK;
@@ -737,7 +749,7 @@ int spk_grid_sums_shots(const void* tgt, const int32_t* shot_ids, int64_t n_ids,
     gather_shot_rows_kernel<<<nb, 256, 0, stream>>>((const float4*)tgt, shot_ids, n_ids, n_s, t4);
     SPK_CHECK_LAUNCH("grid_sums_shots(gather)");
     const int rc = launch_sums(t4, n, dims, grid_w, side, eps2, nullptr, 0, 0.f, v, g, nullptr,
-                               nullptr, p + scratch, ws_bytes - scratch, stream);
+                               nullptr, p + scratch, ws_bytes - scratch, stream, 1, sm_busy);
     if (rc != SPK_OK) return rc;
     scatter_shot_rows_kernel<<<nb, 256, 0, stream>>>(v, g, shot_ids, n_ids, n_s, dims, val, grad);
     SPK_CHECK_LAUNCH("grid_sums_shots(scatter)");

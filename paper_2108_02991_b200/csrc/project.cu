@@ -803,7 +803,8 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
                                                       int max_sweeps, double* ws,
                                                       int32_t* sweeps_out, float4* pos4,
                                                       int wrap_mode,
-                                                      const int32_t* __restrict__ shot_ids) {
+                                                      const int32_t* __restrict__ shot_ids,
+                                                      int* sm_busy) {
     // wrap_mode 2: two wrap buffers in shared memory (round parity), which double as the
     // replay snapshot -- no global snapshot stores on the ring's critical path;
     // 1: one shared wrap buffer + global ping-pong snapshots; 0: wrap in the workspace.
@@ -811,6 +812,9 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
     __shared__ int stop_sh[2];
     // shot of this CTA: the launch's shot list (a subset in any order) or blockIdx.x
     const long long c = shot_ids ? (long long)shot_ids[blockIdx.x] : (long long)blockIdx.x;
+    // optional SM occupancy count: lattice-sum CTAs launched beside the polish wait for
+    // their SM to hold no polish CTA (nbody_kernel, sm_busy), so they use only idle SMs
+    if (sm_busy && threadIdx.x == 0) atomicAdd(&sm_busy[sm_id()], 1);
     const int B = blockDim.x;
     const int W = B >> 5;
     const int P = max(4 * B + RING_K * W, ns + 4);
@@ -896,6 +900,10 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
         }
     }
     if (g == 0 && sweeps_out) sweeps_out[c] = total;
+    if (sm_busy) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicSub(&sm_busy[sm_id()], 1);
+    }
 }
 
 // CTAs per SM the <= 8-warp polish instantiation is register-budgeted for.
@@ -1215,7 +1223,7 @@ static int launch_fista(const double* in, const double* grad, double eta,
 static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, int n_s,
                          int dims, double a, double b, int pin_idx, const double* pin_val,
                          double tol, int max_sweeps, void* pos4, int32_t* sweeps, void* ws,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, int* sm_busy = nullptr) {
     if (n_ids <= 0) return SPK_OK;
     const int pin = pin_idx < 0 ? -1 : pin_idx;
     double pv[3] = {0, 0, 0};
@@ -1247,7 +1255,7 @@ static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, 
 #define PL_LAUNCH(DD, TT, MB)                                                              \
     polish_kernel<DD, TT, MB><<<grid, block, psm, stream>>>(                               \
         shots, n_s, a, b, pin, pv[0], pv[1], pv[2], tol, max_sweeps, pws, sweeps,           \
-        (float4*)pos4, wrap_mode, shot_ids)
+        (float4*)pos4, wrap_mode, shot_ids, sm_busy)
     if (pw <= 8) {
         if (dims == 3) PL_LAUNCH(3, 256, PL_MINB);
         else PL_LAUNCH(2, 256, PL_MINB);
@@ -1310,8 +1318,8 @@ int spk_project_fista(const double* in, const double* grad, double eta,
 
 int spk_polish_shots(double* shots, const int32_t* shot_ids, int64_t n_ids, int64_t n_shots,
                      int n_s, int dims, double a, double b, int pin_idx, const double* pin_val,
-                     double tol, int max_sweeps, void* pos4, int32_t* sweeps, void* ws,
-                     size_t ws_bytes, spk_stream_t stream) {
+                     double tol, int max_sweeps, void* pos4, int32_t* sweeps,
+                     int32_t* sm_busy, void* ws, size_t ws_bytes, spk_stream_t stream) {
     SPK_PROJECT_CHECKS;
     SPK_REQUIRE(max_sweeps >= 1, SPK_ERR_ARG, "max_sweeps must be >= 1");
     SPK_REQUIRE(n_ids >= 0 && n_ids <= n_shots, SPK_ERR_ARG, "polish: %lld ids for %lld shots",
@@ -1321,7 +1329,7 @@ int spk_polish_shots(double* shots, const int32_t* shot_ids, int64_t n_ids, int6
     SPK_REQUIRE(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE,
                 "projection workspace too small: need %zu, got %zu", need, ws_bytes);
     return launch_polish(shots, shot_ids, n_ids, n_s, dims, a, b, pin_idx, pin_val, tol,
-                         max_sweeps, pos4, sweeps, ws, (cudaStream_t)stream);
+                         max_sweeps, pos4, sweeps, ws, (cudaStream_t)stream, sm_busy);
 }
 
 size_t spk_residuals_workspace_bytes(int64_t n_shots) {

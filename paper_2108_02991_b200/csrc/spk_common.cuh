@@ -40,6 +40,13 @@ inline int num_sms() {
     return n;
 }
 
+// The SM this thread runs on (%smid: < 256 on B200).
+__device__ __forceinline__ int sm_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return (int)r;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

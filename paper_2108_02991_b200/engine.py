@@ -126,15 +126,22 @@ class CudaOps:
         return self._ostreams
 
     def project_overlap(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, fld,
-                        att_val, att_grad, sweeps, order, groups_out=None):
+                        att_val, att_grad, sweeps, order, groups_out=None, polite=False):
         n_c = coords.shape[0]
         ps, ks = self._overlap_streams()
         g = max(1, min(len(ps), n_c // 8))
+        busy = None
+        if polite:
+            if not hasattr(self, "_sm_busy"):
+                # per-SM count of running polish CTAs (projection_overlap_device)
+                self._sm_busy = torch.zeros(256, dtype=torch.int32, device=coords.device)
+            busy = self._sm_busy
+            busy.zero_()  # stream-ordered before this call's polish (no stale counts)
         return project_overlap_device(coords, proj_cfg, grad=grad, eta=eta, out=out,
                                       pos4=pos4, nonfinite=nonfinite, field=fld,
                                       att_val=att_val, att_grad=att_grad, sweeps=sweeps,
                                       order=order, polish_streams=ps[:g], k2_streams=ks[:g],
-                                      groups_out=groups_out)
+                                      groups_out=groups_out, sm_busy=busy)
 
     def repulsion_sums(self, tgt4, src4, cfg):
         return direct_sums_device(tgt4, src4, cfg.dims, cfg.repulsion.kernel_eps ** 2)
@@ -472,6 +479,19 @@ class ShardedRun:
         mean = float(self.sweeps_prev.to(torch.float64).mean().item())
         return mean >= self.OVERLAP_MIN_SWEEPS_PER_SOURCE * n_src
 
+    def _use_polite_k2(self) -> bool:
+        """K2 CTAs only on SMs without polish CTAs (project_overlap_device sm_busy):
+        SPK_POLITE_K2=0/1 forces it; by default on when this rank's shots fit one polish
+        CTA per SM, so the polish holds a minority of the GPU and idle SMs appear as its
+        shots finish (a rank's share at N >= 8 at C2)."""
+        env = os.environ.get("SPK_POLITE_K2")
+        if env is not None:
+            return env == "1"
+        if not self.coords.is_cuda:
+            return False
+        props = torch.cuda.get_device_properties(self.coords.device)
+        return self.local <= props.multi_processor_count
+
     def _use_k1_pipeline(self) -> bool:
         """K1 block by block under the polish (_k1_pipelined), opt-in with SPK_K1_PIPE=1
         (even shards only).  Off by default: the per-rank-share projection measured it
@@ -502,7 +522,7 @@ class ShardedRun:
             out, k2_events = self.ops.project_overlap(
                 self.coords, proj_cfg, self.grad, float(eta), self.next, self._pos4_target(),
                 self.flag, self.fld, self.att_val, self.att_grad, self.sweeps, order,
-                groups_out=groups)
+                groups_out=groups, polite=self._use_polite_k2())
             self.att_pre = (self.att_val, self.att_grad, k2_events)
             self.rep_pre = self._k1_pipelined(groups) if groups else None
             self.sweeps_prev = self.sweeps.clone()

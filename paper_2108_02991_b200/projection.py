@@ -190,7 +190,8 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
                            out: torch.Tensor, pos4: torch.Tensor, nonfinite, field,
                            att_val: torch.Tensor, att_grad: torch.Tensor,
                            sweeps: torch.Tensor, order: torch.Tensor | None,
-                           polish_streams, k2_streams, eta_per_shot=None, groups_out=None):
+                           polish_streams, k2_streams, eta_per_shot=None, groups_out=None,
+                           sm_busy=None):
     """K3 with the lattice attraction (K2) of every shot started as soon as its polish
     group is done, so that K2 runs under the polish of the slower shots.
 
@@ -206,7 +207,10 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
     the projection; wait on ``k2_events`` before reading ``att_val`` / ``att_grad``.
     ``sweeps`` receives this call's sweep counts.  ``groups_out`` (a list) receives
     ``(shot ids, polished event)`` per group in launch order, for work that may start as
-    soon as a group's positions are final (the engine's pipelined K1)."""
+    soon as a group's positions are final (the engine's pipelined K1).
+    ``sm_busy`` (device int32 [256] of zeros, or None): the polish CTAs count themselves
+    per SM and the K2 CTAs wait for an SM without polish CTAs, so K2 takes only the SMs
+    the polish has left instead of sharing issue slots with it."""
     n_c, n_s, dims = coords.shape
     pin_idx, pin_val = _pin_arrays(cfg, dims)
     tau = 1.0 / stacked_operator_norm(n_s, pin_idx)
@@ -239,8 +243,8 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
         ps.wait_event(fista_done)
         _native.call("spk_polish_shots", out.data_ptr(), ids.data_ptr(), hi - lo, n_c, n_s,
                      dims, cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 0.1 * cfg.feas_tol,
-                     MAX_POLISH_SWEEPS, pos4.data_ptr(), sweeps.data_ptr(), ws.data_ptr(),
-                     ws.numel(), ps.cuda_stream)
+                     MAX_POLISH_SWEEPS, pos4.data_ptr(), sweeps.data_ptr(),
+                     _device.ptr(sm_busy), ws.data_ptr(), ws.numel(), ps.cuda_stream)
         polished = torch.cuda.Event()
         polished.record(ps)
         ks.wait_event(polished)
@@ -250,7 +254,8 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
         kws = _device.workspace(kb, f"k2_overlap_{g}")
         _native.call("spk_grid_sums_shots", pos4.data_ptr(), ids.data_ptr(), hi - lo, n_s,
                      w.data_ptr(), side_arr, dims, eps2, att_val.data_ptr(),
-                     att_grad.data_ptr(), kws.data_ptr(), kws.numel(), ks.cuda_stream)
+                     att_grad.data_ptr(), _device.ptr(sm_busy), kws.data_ptr(), kws.numel(),
+                     ks.cuda_stream)
         ev = torch.cuda.Event()
         ev.record(ks)
         # buffers used on the side streams stay reserved until that work completes, even

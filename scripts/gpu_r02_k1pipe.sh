@@ -8,5 +8,5 @@ python - <<'PY'
 import json
 for l in open("gpurun_out/rank_share_k1pipe.jsonl"):
     d = json.loads(l)
-    print(d["n_ranks"], "plain", round(d["step_ms"], 1), round(d["efficiency"] or 0, 3), "overlap", round(d["overlap_step_ms"], 1), round(d["overlap_efficiency"] or 0, 3), "pipelined", d["pipelined_step_ms"] and round(d["pipelined_step_ms"], 1), d["pipelined_efficiency"] and round(d["pipelined_efficiency"], 3))
+    print(d["n_ranks"], "polite", round(d["polite_step_ms"], 1), round(d["polite_efficiency"] or 0, 3), "plain", round(d["step_ms"], 1), round(d["efficiency"] or 0, 3), "overlap", round(d["overlap_step_ms"], 1), round(d["overlap_efficiency"] or 0, 3), "pipelined", d["pipelined_step_ms"] and round(d["pipelined_step_ms"], 1), d["pipelined_efficiency"] and round(d["pipelined_efficiency"], 3))
 PY

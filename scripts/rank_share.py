@@ -126,6 +126,21 @@ def main():
                 rec["overlap_project_k2_ms"] = f[0].elapsed_time(f[1])
                 rec["overlap_k1_combine_ms"] = f[1].elapsed_time(f[2])
                 rec["overlap_k1_ms"] = f[1].elapsed_time(f[3])
+                # the same with K2 only on SMs without polish CTAs (sm_busy, "polite")
+                sw4 = torch.empty_like(sw2)
+                h4 = [ev() for _ in range(2)]
+                torch.cuda.synchronize()
+                h4[0].record()
+                _, k2ev4 = ops.project_overlap(coords, pcfg, grad, float(eta), out, pos4, flag,
+                                               fld, av, ag, sw4, order, polite=True)
+                vr4, gr4 = ops.repulsion_sums(tgt, run.pos4_all, cfg)
+                for e_ in k2ev4:
+                    torch.cuda.current_stream().wait_event(e_)
+                ops.combine(av, ag, vr4, gr4, run.p, coords, None, None, grad.view(-1, d))
+                ops.residuals(out, pcfg)
+                h4[1].record()
+                torch.cuda.synchronize()
+                rec["polite_step_ms"] = h4[0].elapsed_time(h4[1])
                 # pipelined K1 (engine.k1_pipelined, several ranks): every polish group's
                 # block is gathered as it finishes and the K1 blocks run under the polish.
                 # The other ranks' q-th groups are taken from the current positions and
@@ -178,12 +193,14 @@ def main():
             tot = [p["sums_ms"] + p["project_ms"] + p["residual_ms"] for p in per]
             tot_o = [p["overlap_project_k2_ms"] + p["overlap_k1_combine_ms"] for p in per]
             tot_p = [p.get("pipelined_step_ms") for p in per]
+            tot_q = [p["polite_step_ms"] for p in per]
             rows[n].append({"iteration": state["it"], "eta": eta, "max_rank_ms": max(tot),
                             "allgather_est_ms": gather_ms,
                             "step_ms": max(tot) + gather_ms,
                             "overlap_step_ms": max(tot_o) + gather_ms,
                             "pipelined_step_ms": (max(tot_p) + gather_ms
                                                   if None not in tot_p else None),
+                            "polite_step_ms": max(tot_q) + gather_ms,
                             "max_sums_ms": max(p["sums_ms"] for p in per),
                             "max_project_ms": max(p["project_ms"] for p in per),
                             "ranks": per})
@@ -198,6 +215,7 @@ def main():
     for n in worlds:
         tn = float(np.mean([x["step_ms"] for x in rows[n][1:]]))
         to = float(np.mean([x["overlap_step_ms"] for x in rows[n][1:]]))
+        tq = float(np.mean([x["polite_step_ms"] for x in rows[n][1:]]))
         tp = [x["pipelined_step_ms"] for x in rows[n][1:]]
         tp = float(np.mean(tp)) if None not in tp else None
         rec = {"config": args.config, "n_ranks": n, "groups": ops.OVERLAP_GROUPS,
@@ -207,6 +225,8 @@ def main():
                "efficiency": (t1 / (n * tn)) if t1 else None,
                "overlap_step_ms": to,
                "overlap_efficiency": (t1 / (n * to)) if t1 else None,
+               "polite_step_ms": tq,
+               "polite_efficiency": (t1 / (n * tq)) if t1 else None,
                "pipelined_step_ms": tp,
                "pipelined_efficiency": (t1 / (n * tp)) if (t1 and tp) else None,
                "iterations": rows[n]}

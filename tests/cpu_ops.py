@@ -126,7 +126,7 @@ class OverlapOracleOps(OracleOps):
         return cfg.grad_mode == "exact"
 
     def project_overlap(self, coords, cfg, grad, eta, out, pos4, nonfinite, fld, att_val,
-                        att_grad, sweeps, order, groups_out=None):
+                        att_grad, sweeps, order, groups_out=None, polite=False):
         self.overlap_calls = getattr(self, "overlap_calls", 0) + 1
         self.project(coords, cfg, grad, eta, out, pos4, nonfinite, sweeps)
         n_c, n_s, d = coords.shape

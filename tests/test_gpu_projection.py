@@ -244,7 +244,7 @@ def test_fista_then_polish_subsets_equal_project_all(spk, d, ns):
     for ids, st in ((perm[:5], main), (perm[5:], side)):
         _native.call("spk_polish_shots", out.data_ptr(), ids.data_ptr(), ids.numel(), n, ns, d,
                      cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 0.1 * cfg.feas_tol,
-                     50000, pos4.data_ptr(), sw.data_ptr(), ws.data_ptr(), ws.numel(),
+                     50000, pos4.data_ptr(), sw.data_ptr(), None, ws.data_ptr(), ws.numel(),
                      st.cuda_stream)
     main.wait_stream(side)
     assert torch.equal(out, ref) and torch.equal(pos4, ref4) and torch.equal(sw, ref_sw)
@@ -252,7 +252,7 @@ def test_fista_then_polish_subsets_equal_project_all(spk, d, ns):
     with pytest.raises(ValueError):
         _native.call("spk_polish_shots", out.data_ptr(), perm.data_ptr(), n + 1, n, ns, d,
                      cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 1e-7, 50000, None, None,
-                     ws.data_ptr(), ws.numel(), _device.stream())
+                     None, ws.data_ptr(), ws.numel(), _device.stream())
 
 
 def test_grid_sums_on_shot_subset(spk):
@@ -275,7 +275,7 @@ def test_grid_sums_on_shot_subset(spk):
     ws = _device.workspace(nb, "t_gs")
     _native.call("spk_grid_sums_shots", pos4.data_ptr(), ids.data_ptr(), 3, ns, w.data_ptr(),
                  _native.i64_array(fld.sides), d, float(fld.kernel_eps ** 2), val.data_ptr(),
-                 grad.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
+                 grad.data_ptr(), None, ws.data_ptr(), ws.numel(), _device.stream())
     v, g = _device.d2h(val), _device.d2h(grad)
     rows = np.concatenate([np.arange(s * ns, (s + 1) * ns) for s in (7, 2, 4)])
     other = np.setdiff1d(np.arange(n * ns), rows)
