@@ -388,10 +388,20 @@ def _check_overflow(n: int) -> None:
         raise _native.NativeError(f"tree plan: traversal stack overflow in {n} walks")
 
 
+# Sub-walks pay while one thread per group leaves the GPU idle (a rank's Morton block,
+# the coarse levels); with many groups the serial walks already fill it and the sub-walks'
+# ancestor tests and 64x longer scans cost more (full3d level 6, 8.4M targets: plan
+# passes 6.1 ms serial vs 20.6 ms sub-walks; 2k groups: 6.1 -> 2.1 ms;
+# profiles/r02_tree_subwalk_phases.jsonl).
+SUBWALK_MAX_GROUPS = 16384
+
+
 def _sub_offsets(n_groups: int, dev) -> torch.Tensor | None:
     """Per-(group, frontier slot) list offsets of the sub-walk traversal (tree.cu
-    traverse_sub_kernel); SPK_TREE_SUBWALK=0 selects the one-thread-per-group walk."""
-    if os.environ.get("SPK_TREE_SUBWALK", "1") == "0":
+    traverse_sub_kernel), or None for the one-thread-per-group walk: sub-walks below
+    SUBWALK_MAX_GROUPS groups; SPK_TREE_SUBWALK=0/1 forces either."""
+    env = os.environ.get("SPK_TREE_SUBWALK")
+    if env == "0" or (env is None and n_groups > SUBWALK_MAX_GROUPS):
         return None
     return torch.empty(n_groups * SUB_FRONT + 1, dtype=torch.int64, device=dev)
 

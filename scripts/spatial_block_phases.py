@@ -21,12 +21,14 @@ src = fld.source_tree()
 src.static_proxies(order)
 eps2 = fld.kernel_eps ** 2
 ops = engine.CudaOps()
-for ns in (32, 128):
+NS = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "32,128").split(",")]
+RANKS = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1,8").split(",")]
+for ns in NS:
     full = spk.perturb(spk.init_radial(4096, ns, 3), 0.75, 0).points()
     pos4 = _device.pack_positions(_device.h2d(np.ascontiguousarray(full)))
     perm = ops.spatial_order(pos4, 3)
     p = pos4.shape[0]
-    for n, mode in ((1, "0"), (1, "1"), (8, "0"), (8, "1")):
+    for n, mode in [(r, m) for r in RANKS for m in ("0", "1")]:
         os.environ["SPK_TREE_SUBWALK"] = mode
         blk = pos4[perm[:p // n]].contiguous()
         for rep in range(3):

@@ -151,10 +151,13 @@ def test_optimize_with_tree_backend(spk):
 
 
 @pytest.mark.parametrize("dims", [2, 3])
-def test_device_lists_match_host_planner(spk, dims):
-    """The GPU traversal (tree.cu traverse_kernel) and the serial host planner
-    (tree_host.cpp) build identical interaction lists for the same tree and boxes."""
+def test_device_lists_match_host_planner(spk, dims, monkeypatch):
+    """The GPU traversal (tree.cu traverse_sub_kernel, the sub-walks) and the serial host
+    planner (tree_host.cpp, same merge rule) build identical interaction lists for the
+    same tree and boxes."""
     from paper_2108_02991_b200 import _device, _native, tree
+
+    monkeypatch.setenv("SPK_TREE_SUBWALK", "1")
 
     lib = _native.load()
     pts = (spk.perturb(spk.init_radial(144, 512, 3), 0.25, 4).points() if dims == 3 else
