@@ -167,11 +167,16 @@ int spk_project_fista(const double* in, const double* grad, double eta,
                       int n_pit, double tau, int monotone, double* trace, int32_t* nonfinite,
                       void* ws, size_t ws_bytes, spk_stream_t stream);
 /* sm_busy (optional, see spk_grid_sums_shots): every polish CTA counts itself on its SM
- * while it runs. */
+ * while it runs.  peer_pos4 (optional): a DEVICE array of n_peers float4 position
+ * buffers of the other ranks (peer memory, e.g. CUDA IPC over NVLink); every record
+ * written to pos4[c * n_s + n] is also written to peer_pos4[k][peer_offset + c * n_s + n]
+ * -- the position all-gather fused into the polish epilogue (the caller orders the
+ * peers' reads after a collective that follows this launch on every rank). */
 int spk_polish_shots(double* shots, const int32_t* shot_ids, int64_t n_ids, int64_t n_shots,
                      int n_s, int dims, double a, double b, int pin_idx, const double* pin_val,
                      double tol, int max_sweeps, void* pos4, int32_t* sweeps,
-                     int32_t* sm_busy, void* ws, size_t ws_bytes, spk_stream_t stream);
+                     int32_t* sm_busy, void* const* peer_pos4, int n_peers,
+                     int64_t peer_offset, void* ws, size_t ws_bytes, spk_stream_t stream);
 
 /* feasibility_residuals (projection.py:435-452): out[0..4] = amplitude, speed,
  * acceleration, pin (0 if no pin), max -- each already clipped at 0 like the reference. */

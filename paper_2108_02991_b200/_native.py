@@ -59,7 +59,7 @@ SIGNATURES = {
                                   c_vp, c_vp, c_vp, c_size, c_vp]),
     "spk_polish_shots": (c_int, [c_vp, c_vp, c_i64, c_i64, c_int, c_int, c_dbl, c_dbl, c_int,
                                  ctypes.POINTER(c_dbl), c_dbl, c_int, c_vp, c_vp, c_vp, c_vp,
-                                 c_size, c_vp]),
+                                 c_int, c_i64, c_vp, c_size, c_vp]),
     "spk_grid_sums_shots_workspace_bytes": (c_size, [c_i64, c_int, c_i64]),
     "spk_grid_sums_shots": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, ctypes.POINTER(c_i64),
                                     c_int, ctypes.c_float, c_vp, c_vp, c_vp, c_vp, c_size,

@@ -796,7 +796,7 @@ __device__ __forceinline__ void ring_step(RingLane<D>& L, int st, int ns, int B,
 // <= tol, the ring stops and sweeps j B .. k* are replayed (systolic_batch) from the
 // snapshot after sweep j B - 1 (j = k* / B), which the ring has not overwritten yet
 // because P >= ns + 4.  Bit-identical to the sequential polish.
-template <int D, int MAXT, int MINB>
+template <int D, int MAXT, int MINB, bool PEERS>
 __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int ns, double a,
                                                       double b, int pin, double pv0,
                                                       double pv1, double pv2, double tol,
@@ -804,7 +804,9 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
                                                       int32_t* sweeps_out, float4* pos4,
                                                       int wrap_mode,
                                                       const int32_t* __restrict__ shot_ids,
-                                                      int* sm_busy) {
+                                                      int* sm_busy,
+                                                      float4* const* __restrict__ peers,
+                                                      int n_peers, long long peer_off) {
     // wrap_mode 2: two wrap buffers in shared memory (round parity), which double as the
     // replay snapshot -- no global snapshot stores on the ring's critical path;
     // 1: one shared wrap buffer + global ping-pong snapshots; 0: wrap in the workspace.
@@ -898,12 +900,37 @@ __global__ void __launch_bounds__(MAXT, MINB) polish_kernel(double* shots, int n
             const double* r = res + n * D;
             pos4[c * ns + n] = pos_record(r[0], r[1], D == 3 ? r[2] : 0.0);
         }
+        if (PEERS) {
+            // multi-GPU: the shot's records into every other rank's position buffer (peer
+            // memory over NVLink) -- the all-gather of positions fused into the epilogue.
+            // Re-read from this CTA's own (L1/L2-resident) stores so the ring above keeps
+            // its register budget; a separate instantiation, so the single-GPU kernel is
+            // unchanged.
+            __syncthreads();
+            const float4* mine = pos4 + c * ns;
+            for (int k = 0; k < n_peers; ++k) {
+                float4* dst = peers[k] + peer_off + c * ns;
+                for (int n = g; n < ns; n += B) dst[n] = mine[n];
+            }
+        }
     }
     if (g == 0 && sweeps_out) sweeps_out[c] = total;
     if (sm_busy) {
         __syncthreads();
         if (threadIdx.x == 0) atomicSub(&sm_busy[sm_id()], 1);
     }
+}
+
+// Positions of the listed shots into every peer buffer (the fused gather's path for the
+// wide rings, launched right after their polish).
+__global__ void peer_copy_kernel(const float4* __restrict__ pos4,
+                                 const int32_t* __restrict__ shot_ids, int ns,
+                                 float4* const* __restrict__ peers, int n_peers,
+                                 long long peer_off) {
+    const long long c = shot_ids ? (long long)shot_ids[blockIdx.x] : (long long)blockIdx.x;
+    for (int k = 0; k < n_peers; ++k)
+        for (int n = threadIdx.x; n < ns; n += blockDim.x)
+            peers[k][peer_off + c * ns + n] = pos4[c * ns + n];
 }
 
 // CTAs per SM the <= 8-warp polish instantiation is register-budgeted for.
@@ -1223,7 +1250,9 @@ static int launch_fista(const double* in, const double* grad, double eta,
 static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, int n_s,
                          int dims, double a, double b, int pin_idx, const double* pin_val,
                          double tol, int max_sweeps, void* pos4, int32_t* sweeps, void* ws,
-                         cudaStream_t stream, int* sm_busy = nullptr) {
+                         cudaStream_t stream, int* sm_busy = nullptr,
+                         float4* const* peers = nullptr, int n_peers = 0,
+                         long long peer_off = 0) {
     if (n_ids <= 0) return SPK_OK;
     const int pin = pin_idx < 0 ? -1 : pin_idx;
     double pv[3] = {0, 0, 0};
@@ -1234,32 +1263,31 @@ static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, 
     const size_t wb = (size_t)n_s * dims * sizeof(double);
     const int wrap_mode = xb + 2 * wb <= 200 * 1024 ? 2 : xb + wb <= 200 * 1024 ? 1 : 0;
     const size_t psm = xb + (wrap_mode == 2 ? 2 * wb : wrap_mode == 1 ? wb : 0);
-    cudaFuncSetAttribute(polish_kernel<3, 256, PL_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)psm);
-    cudaFuncSetAttribute(polish_kernel<2, 256, PL_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)psm);
-    cudaFuncSetAttribute(polish_kernel<3, 1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)psm);
-    cudaFuncSetAttribute(polish_kernel<2, 1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)psm);
-    cudaFuncSetAttribute(polish_kernel<3, PL_WIDE_T, PL_WIDE_MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)psm);
-    cudaFuncSetAttribute(polish_kernel<2, PL_WIDE_T, PL_WIDE_MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)psm);
     double* pws = static_cast<double*>(ws);
     // <= 8 warps (N_s <= 1283): a register budget of 80 keeps the ring window in registers
     // with 3 CTAs per SM; wider rings use the 1024-thread instantiation
     const dim3 grid((unsigned)n_ids), block(32 * pw);
-#define PL_LAUNCH(DD, TT, MB)                                                              \
-    polish_kernel<DD, TT, MB><<<grid, block, psm, stream>>>(                               \
-        shots, n_s, a, b, pin, pv[0], pv[1], pv[2], tol, max_sweeps, pws, sweeps,           \
-        (float4*)pos4, wrap_mode, shot_ids, sm_busy)
+#define PL_LAUNCH1(DD, TT, MB, PP)                                                         \
+    do {                                                                                   \
+        cudaFuncSetAttribute(polish_kernel<DD, TT, MB, PP>,                                \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);       \
+        polish_kernel<DD, TT, MB, PP><<<grid, block, psm, stream>>>(                       \
+            shots, n_s, a, b, pin, pv[0], pv[1], pv[2], tol, max_sweeps, pws, sweeps,       \
+            (float4*)pos4, wrap_mode, shot_ids, sm_busy, peers, n_peers, peer_off);         \
+    } while (0)
+#define PL_LAUNCH(DD, TT, MB)                           \
+    do {                                                \
+        if (n_peers > 0) PL_LAUNCH1(DD, TT, MB, true);  \
+        else PL_LAUNCH1(DD, TT, MB, false);             \
+    } while (0)
     if (pw <= 8) {
         if (dims == 3) PL_LAUNCH(3, 256, PL_MINB);
         else PL_LAUNCH(2, 256, PL_MINB);
     } else {
+        // wide rings run at the 64-register edge: the peer epilogue would add spills to
+        // the ring, so they keep the single-GPU kernel and copy to the peers right after
+        const int np = n_peers;
+        n_peers = 0;
         if (32 * pw <= PL_WIDE_T) {
             if (dims == 3) PL_LAUNCH(3, PL_WIDE_T, PL_WIDE_MINB);
             else PL_LAUNCH(2, PL_WIDE_T, PL_WIDE_MINB);
@@ -1267,7 +1295,11 @@ static int launch_polish(double* shots, const int32_t* shot_ids, int64_t n_ids, 
             if (dims == 3) PL_LAUNCH(3, 1024, 1);
             else PL_LAUNCH(2, 1024, 1);
         }
+        if (np > 0)
+            peer_copy_kernel<<<(unsigned)n_ids, 256, 0, stream>>>(
+                (const float4*)pos4, shot_ids, n_s, peers, np, peer_off);
     }
+#undef PL_LAUNCH1
 #undef PL_LAUNCH
     SPK_CHECK_LAUNCH("polish_kernel");
     return SPK_OK;
@@ -1319,17 +1351,21 @@ int spk_project_fista(const double* in, const double* grad, double eta,
 int spk_polish_shots(double* shots, const int32_t* shot_ids, int64_t n_ids, int64_t n_shots,
                      int n_s, int dims, double a, double b, int pin_idx, const double* pin_val,
                      double tol, int max_sweeps, void* pos4, int32_t* sweeps,
-                     int32_t* sm_busy, void* ws, size_t ws_bytes, spk_stream_t stream) {
+                     int32_t* sm_busy, void* const* peer_pos4, int n_peers,
+                     int64_t peer_offset, void* ws, size_t ws_bytes, spk_stream_t stream) {
     SPK_PROJECT_CHECKS;
     SPK_REQUIRE(max_sweeps >= 1, SPK_ERR_ARG, "max_sweeps must be >= 1");
     SPK_REQUIRE(n_ids >= 0 && n_ids <= n_shots, SPK_ERR_ARG, "polish: %lld ids for %lld shots",
                 (long long)n_ids, (long long)n_shots);
+    SPK_REQUIRE(n_peers >= 0 && (n_peers == 0 || (peer_pos4 != nullptr && pos4 != nullptr)),
+                SPK_ERR_ARG, "polish: %d peer buffers need the peer table and pos4", n_peers);
     if (n_ids <= 0) return SPK_OK;
     const size_t need = spk_project_workspace_bytes(n_shots, n_s, dims, 0);
     SPK_REQUIRE(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE,
                 "projection workspace too small: need %zu, got %zu", need, ws_bytes);
     return launch_polish(shots, shot_ids, n_ids, n_s, dims, a, b, pin_idx, pin_val, tol,
-                         max_sweeps, pos4, sweeps, ws, (cudaStream_t)stream, sm_busy);
+                         max_sweeps, pos4, sweeps, ws, (cudaStream_t)stream, sm_busy,
+                         reinterpret_cast<float4* const*>(peer_pos4), n_peers, peer_offset);
 }
 
 size_t spk_residuals_workspace_bytes(int64_t n_shots) {

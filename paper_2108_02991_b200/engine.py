@@ -102,9 +102,10 @@ class CudaOps:
                      out.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream())
         return out
 
-    def project(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, sweeps=None):
+    def project(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, sweeps=None,
+                peers=None):
         return project_device(coords, proj_cfg, grad=grad, eta=eta, out=out, pos4=pos4,
-                              nonfinite=nonfinite, sweeps=sweeps)
+                              nonfinite=nonfinite, sweeps=sweeps, peers=peers)
 
     def residuals(self, coords, proj_cfg):
         return residuals_device(coords, proj_cfg)
@@ -126,7 +127,8 @@ class CudaOps:
         return self._ostreams
 
     def project_overlap(self, coords, proj_cfg, grad, eta, out, pos4, nonfinite, fld,
-                        att_val, att_grad, sweeps, order, groups_out=None, polite=False):
+                        att_val, att_grad, sweeps, order, groups_out=None, polite=False,
+                        peers=None):
         n_c = coords.shape[0]
         ps, ks = self._overlap_streams()
         g = max(1, min(len(ps), n_c // 8))
@@ -141,7 +143,7 @@ class CudaOps:
                                       pos4=pos4, nonfinite=nonfinite, field=fld,
                                       att_val=att_val, att_grad=att_grad, sweeps=sweeps,
                                       order=order, polish_streams=ps[:g], k2_streams=ks[:g],
-                                      groups_out=groups_out, sm_busy=busy)
+                                      groups_out=groups_out, sm_busy=busy, peers=peers)
 
     def repulsion_sums(self, tgt4, src4, cfg):
         return direct_sums_device(tgt4, src4, cfg.dims, cfg.repulsion.kernel_eps ** 2)
@@ -333,12 +335,65 @@ class ShardedRun:
         self.att_pre = None
         self.rep_pre = None
         self.sweeps_prev = None
+        self._setup_peers()
         if self.overlap:
             self.att_val = ops.empty(self.local * n_s)
             self.att_grad = ops.empty((self.local * n_s, d))
             self.sweeps = ops.empty(self.local, torch.int32)
 
     # ------------------------------------------------------------ communication
+    def _setup_peers(self):
+        """Fused position all-gather (SPK_P2P_GATHER, default on with several ranks and
+        even shards on CUDA): every rank maps the other ranks' position buffers (CUDA IPC
+        over NVLink, exchanged through the process group) and the polish epilogue writes
+        each new record into all of them (spk_polish_shots peer_pos4), so no separate
+        all-gather runs.  The first exchange of every level is checked against an NCCL
+        all-gather; any mismatch falls back to the all-gather for the rest of the run."""
+        self.peers = None
+        env = os.environ.get("SPK_P2P_GATHER")
+        if (self.world == 1 or not self.even or not self.coords.is_cuda or env == "0"
+                or getattr(self, "_p2p_failed", False)):
+            return
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        mine = reduce_tensor(self.pos4_all)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=self.group)
+        opened = []
+        for r, (fn, args) in enumerate(allh):
+            if r != self.rank:
+                opened.append(fn(*args))
+        self._peer_bufs = opened  # keeps the IPC mappings alive for this level
+        table = torch.tensor([t.data_ptr() for t in opened], dtype=torch.int64,
+                             device=self.coords.device)
+        self.peers = (table, len(opened), self.offsets[self.rank] * self.n_s)
+        self._p2p_verified = False
+
+    def _exchanged(self):
+        """Positions after a projection: with the fused gather only the first exchange of
+        a level is verified (an NCCL all-gather compared on every rank); otherwise the
+        all-gather."""
+        if self.peers is None:
+            self._gather_pos4()
+            return
+        if self._p2p_verified:
+            return
+        ref = self.ops.empty(self.pos4_all.shape, torch.float32)
+        dist.all_gather_into_tensor(ref, self.pos4_local, group=self.group)
+        ok = torch.tensor([1.0 if torch.equal(ref, self.pos4_all) else 0.0],
+                          device=self.coords.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if ok.item() == 1.0:
+            self._p2p_verified = True
+            return
+        import warnings
+
+        warnings.warn("fused position all-gather (peer memory) did not match the NCCL "
+                      "all-gather; using the all-gather for the rest of the run")
+        self.pos4_all.copy_(ref)
+        self.peers = None
+        self._p2p_failed = True
+
     def _gather_pos4(self):
         if self.world == 1:
             return
@@ -364,10 +419,11 @@ class ShardedRun:
     # --------------------------------------------------------------- iteration
     def project(self, proj_cfg):
         """Level-start projection (no step)."""
+        kw = {"peers": self.peers} if self.peers is not None else {}
         out = self.ops.project(self.coords, proj_cfg, None, 0.0, self.next,
-                               self._pos4_target(), None)
+                               self._pos4_target(), None, **kw)
         self.coords, self.next = out, self.coords
-        self._gather_pos4()
+        self._exchanged()
         self.have_prev = False
         self.host_prev = None
         self.att_pre = None
@@ -519,27 +575,32 @@ class ShardedRun:
                 order = torch.argsort(self.sweeps_prev, descending=True,
                                       stable=True).to(torch.int32)
             groups = [] if self._use_k1_pipeline() else None
+            kw = {"peers": self.peers} if self.peers is not None else {}
             out, k2_events = self.ops.project_overlap(
                 self.coords, proj_cfg, self.grad, float(eta), self.next, self._pos4_target(),
                 self.flag, self.fld, self.att_val, self.att_grad, self.sweeps, order,
-                groups_out=groups, polite=self._use_polite_k2())
+                groups_out=groups, polite=self._use_polite_k2(), **kw)
             self.att_pre = (self.att_val, self.att_grad, k2_events)
             self.rep_pre = self._k1_pipelined(groups) if groups else None
             self.sweeps_prev = self.sweeps.clone()
         elif self.overlap:
             # plain schedule, but keep the sweep counts that decide and order the overlap
+            kw = {"peers": self.peers} if self.peers is not None else {}
             out = self.ops.project(self.coords, proj_cfg, self.grad, float(eta), self.next,
-                                   self._pos4_target(), self.flag, self.sweeps)
+                                   self._pos4_target(), self.flag, self.sweeps, **kw)
             self.sweeps_prev = self.sweeps.clone()
         else:
+            kw = {"peers": self.peers} if self.peers is not None else {}
             out = self.ops.project(self.coords, proj_cfg, self.grad, float(eta), self.next,
-                                   self._pos4_target(), self.flag)
+                                   self._pos4_target(), self.flag, **kw)
         # rotate: prev <- coords, coords <- out, next <- old prev
         self.prev, self.coords, self.next = self.coords, out, self.prev
         self.prev_grad, self.grad = self.grad, self.prev_grad
         self.have_prev = True
+        # the flag all-gather completes only after every rank's projection (and so its
+        # peer writes, with the fused gather) has finished
         bad = self._all_scalars(self.flag.to(torch.float64))
-        self._gather_pos4()
+        self._exchanged()
         return not bool(bad.max() > 0)
 
     def residual_max(self, proj_cfg) -> float:

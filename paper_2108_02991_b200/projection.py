@@ -107,12 +107,16 @@ def _pin_arrays(cfg: ProjectionConfig, dims: int):
 def project_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad=None, eta=0.0,
                    out: torch.Tensor | None = None, pos4=None, sweeps=None, trace=None,
                    nonfinite=None, tau: float | None = None,
-                   max_sweeps: int = MAX_POLISH_SWEEPS, eta_per_shot=None) -> torch.Tensor:
+                   max_sweeps: int = MAX_POLISH_SWEEPS, eta_per_shot=None,
+                   peers=None) -> torch.Tensor:
     """K3 on device buffers: out = P(coords - eta * grad) for every shot.
 
     ``coords``/``grad``/``out``: (n_shots, n_s, d) fp64 CUDA tensors.  ``pos4`` (optional)
     receives the float4 positions of the result (the next N-body's sources);
-    ``eta_per_shot`` (optional device f64 [n_shots]) replaces ``eta`` shot by shot."""
+    ``eta_per_shot`` (optional device f64 [n_shots]) replaces ``eta`` shot by shot.
+    ``peers`` (optional ``(device int64 table of peer buffer addresses, count, record
+    offset)``): the polish epilogue also writes the positions into the other ranks'
+    buffers (spk_polish_shots; the engine's fused position all-gather)."""
     n_c, n_s, dims = coords.shape
     pin_idx, pin_val = _pin_arrays(cfg, dims)
     if pin_idx >= n_s:
@@ -126,6 +130,20 @@ def project_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad=None, et
     nbytes = _native.query("spk_project_workspace_bytes", n_c, n_s, dims, int(trace is not None))
     ws = _device.workspace(nbytes, "project")
     pv = _native.f64_array(list(pin_val) + [0.0] * (3 - dims))
+    if peers is not None:
+        # FISTA, then the polish of every shot with the peer-writing epilogue
+        table, n_peers, offset = peers
+        _native.call("spk_project_fista", coords.data_ptr(), _device.ptr(grad), float(eta),
+                     _device.ptr(eta_per_shot), out.data_ptr(), n_c, n_s, dims,
+                     cfg.speed_bound, cfg.accel_bound, pin_idx, pv, cfg.n_pit, float(tau),
+                     int(bool(cfg.monotone)), _device.ptr(trace), _device.ptr(nonfinite),
+                     ws.data_ptr(), ws.numel(), _device.stream())
+        _native.call("spk_polish_shots", out.data_ptr(), None, n_c, n_c, n_s, dims,
+                     cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 0.1 * cfg.feas_tol,
+                     int(max_sweeps), _device.ptr(pos4), _device.ptr(sweeps), None,
+                     table.data_ptr(), int(n_peers), int(offset), ws.data_ptr(), ws.numel(),
+                     _device.stream())
+        return out
     _native.call("spk_project_all", coords.data_ptr(), _device.ptr(grad), float(eta),
                  _device.ptr(eta_per_shot), out.data_ptr(), n_c, n_s, dims, cfg.speed_bound,
                  cfg.accel_bound, pin_idx, pv, cfg.n_pit, float(tau), int(bool(cfg.monotone)), 0.1 * cfg.feas_tol,
@@ -191,7 +209,7 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
                            att_val: torch.Tensor, att_grad: torch.Tensor,
                            sweeps: torch.Tensor, order: torch.Tensor | None,
                            polish_streams, k2_streams, eta_per_shot=None, groups_out=None,
-                           sm_busy=None):
+                           sm_busy=None, peers=None):
     """K3 with the lattice attraction (K2) of every shot started as soon as its polish
     group is done, so that K2 runs under the polish of the slower shots.
 
@@ -213,6 +231,7 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
     the polish has left instead of sharing issue slots with it."""
     n_c, n_s, dims = coords.shape
     pin_idx, pin_val = _pin_arrays(cfg, dims)
+    peer_table, n_peers, peer_offset = peers if peers is not None else (None, 0, 0)
     tau = 1.0 / stacked_operator_norm(n_s, pin_idx)
     nbytes = _native.query("spk_project_workspace_bytes", n_c, n_s, dims, 0)
     ws = _device.workspace(nbytes, "project")
@@ -244,7 +263,8 @@ def project_overlap_device(coords: torch.Tensor, cfg: ProjectionConfig, *, grad,
         _native.call("spk_polish_shots", out.data_ptr(), ids.data_ptr(), hi - lo, n_c, n_s,
                      dims, cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 0.1 * cfg.feas_tol,
                      MAX_POLISH_SWEEPS, pos4.data_ptr(), sweeps.data_ptr(),
-                     _device.ptr(sm_busy), ws.data_ptr(), ws.numel(), ps.cuda_stream)
+                     _device.ptr(sm_busy), _device.ptr(peer_table), n_peers, peer_offset,
+                     ws.data_ptr(), ws.numel(), ps.cuda_stream)
         polished = torch.cuda.Event()
         polished.record(ps)
         ks.wait_event(polished)

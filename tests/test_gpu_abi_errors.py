@@ -84,8 +84,8 @@ def test_round2_entry_point_errors(env):
     shots = _device.h2d(np.zeros((4, 8, 3)))
     with pytest.raises(_native.NativeError, match="workspace"):
         _native.call("spk_polish_shots", shots.data_ptr(), ids.data_ptr(), 2, 4, 8, 3, 0.1, 0.1,
-                     -1, _native.f64_array([0, 0, 0]), 1e-7, 100, None, None, None,
-                     tiny.data_ptr(), tiny.numel(), _device.stream())
+                     -1, _native.f64_array([0, 0, 0]), 1e-7, 100, None, None, None, None, 0,
+                     0, tiny.data_ptr(), tiny.numel(), _device.stream())
     with pytest.raises(ValueError, match="n_pit"):
         _native.call("spk_project_fista", shots.data_ptr(), None, 0.0, None, shots.data_ptr(),
                      4, 8, 3, 0.1, 0.1, -1, _native.f64_array([0, 0, 0]), 0, 0.05, 0, None,

@@ -48,8 +48,11 @@ def _worker(rank, world, port, kind, env, out_path):
         from paper_2108_02991_b200 import optimizer as om
 
         st = om.start(cfg, hw)
-        flags = (st.run.overlap, st.run.spatial, st.run._use_k1_pipeline())
+        flags = [st.run.overlap, st.run.spatial, st.run._use_k1_pipeline()]
         res = om.finish(st)
+        # the fused position all-gather (polish epilogue into the peers' buffers over
+        # CUDA IPC) ran and its per-level check against the NCCL all-gather passed
+        flags.append(st.run.peers is not None and st.run._p2p_verified)
         if rank == 0:
             np.savez(out_path, coords=res.pattern.coords, costs=res.trace.costs(),
                      flags=np.array(flags))
@@ -82,6 +85,8 @@ def test_two_ranks_on_device_match_one(tmp_path, kind, env):
         assert bool(got["flags"][1]), "two ranks with a treecode use the spatial layout"
     if kind == "exact_even":
         assert bool(got["flags"][2]), "even shards on two ranks pipeline K1 under the polish"
+    if kind == "exact_even":
+        assert bool(got["flags"][3]), "even shards use the fused (peer-memory) position gather"
     # per-rank target sets change the fp32 chunking (exact) or the treecode groups (tree)
     tol = 1e-6 if kind.startswith("exact") else 1e-4
     cs, cg = single.trace.costs(), got["costs"]

@@ -244,15 +244,15 @@ def test_fista_then_polish_subsets_equal_project_all(spk, d, ns):
     for ids, st in ((perm[:5], main), (perm[5:], side)):
         _native.call("spk_polish_shots", out.data_ptr(), ids.data_ptr(), ids.numel(), n, ns, d,
                      cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 0.1 * cfg.feas_tol,
-                     50000, pos4.data_ptr(), sw.data_ptr(), None, ws.data_ptr(), ws.numel(),
-                     st.cuda_stream)
+                     50000, pos4.data_ptr(), sw.data_ptr(), None, None, 0, 0, ws.data_ptr(),
+                     ws.numel(), st.cuda_stream)
     main.wait_stream(side)
     assert torch.equal(out, ref) and torch.equal(pos4, ref4) and torch.equal(sw, ref_sw)
     # argument errors are reported, not executed
     with pytest.raises(ValueError):
         _native.call("spk_polish_shots", out.data_ptr(), perm.data_ptr(), n + 1, n, ns, d,
                      cfg.speed_bound, cfg.accel_bound, pin_idx, pv, 1e-7, 50000, None, None,
-                     None, ws.data_ptr(), ws.numel(), _device.stream())
+                     None, None, 0, 0, ws.data_ptr(), ws.numel(), _device.stream())
 
 
 def test_grid_sums_on_shot_subset(spk):
