@@ -36,6 +36,13 @@ enum {
 };
 
 int spk_version(void);
+
+/* CUDA IPC of device buffers (the fused position all-gather between ranks): the 64-byte
+ * handle of an allocation's base, and opening a peer's handle on the caller's current
+ * device (peer access enabled lazily), closing it again. */
+int spk_ipc_handle(const void* base, void* handle_out);
+int spk_ipc_open(const void* handle, void** ptr_out);
+int spk_ipc_close(void* ptr);
 const char* spk_last_error(void);
 
 /* ---------------------------------------------------------------- K1 / K2 N-body */

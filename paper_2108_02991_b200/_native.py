@@ -26,6 +26,9 @@ c_vp = ctypes.c_void_p
 # name -> (restype, argtypes); mirrors include/sparkling_b200.h one to one.
 SIGNATURES = {
     "spk_version": (c_int, []),
+    "spk_ipc_handle": (c_int, [c_vp, c_vp]),
+    "spk_ipc_open": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "spk_ipc_close": (c_int, [c_vp]),
     "spk_last_error": (ctypes.c_char_p, []),
     "spk_nbody_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "spk_direct_sums": (c_int, [c_vp, c_i64, c_vp, c_i64, c_int, c_flt, c_vp, c_vp, c_vp,

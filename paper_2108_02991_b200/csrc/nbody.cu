@@ -684,6 +684,35 @@ int spk_version(void) { return 1; }
 
 const char* spk_last_error(void) { return g_err; }
 
+// CUDA IPC for the fused position all-gather (engine.ShardedRun._setup_peers): the other
+// ranks' buffers are opened on the CALLER's current device, so peer access from this
+// device to the owner's is enabled (cudaIpcMemLazyEnablePeerAccess).
+int spk_ipc_handle(const void* base, void* handle_out) {
+    SPK_REQUIRE(base != nullptr && handle_out != nullptr, SPK_ERR_ARG, "ipc: null pointer");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(base));
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    memcpy(handle_out, &h, sizeof(h));
+    return SPK_OK;
+}
+
+int spk_ipc_open(const void* handle, void** ptr_out) {
+    SPK_REQUIRE(handle != nullptr && ptr_out != nullptr, SPK_ERR_ARG, "ipc: null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    const cudaError_t e = cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "cudaIpcOpenMemHandle: %s",
+                cudaGetErrorString(e));
+    return SPK_OK;
+}
+
+int spk_ipc_close(void* ptr) {
+    const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    SPK_REQUIRE(e == cudaSuccess, SPK_ERR_CUDA, "cudaIpcCloseMemHandle: %s",
+                cudaGetErrorString(e));
+    return SPK_OK;
+}
+
 size_t spk_nbody_workspace_bytes(int64_t n_tgt, int64_t n_src0, int64_t n_src1) {
     return make_plan(n_tgt, n_src0, n_src1).ws_bytes + 256;
 }

@@ -19,6 +19,7 @@ the gloo backend.
 from __future__ import annotations
 
 import contextlib
+import ctypes
 import os
 
 import numpy as np
@@ -344,29 +345,61 @@ class ShardedRun:
     # ------------------------------------------------------------ communication
     def _setup_peers(self):
         """Fused position all-gather (SPK_P2P_GATHER, default on with several ranks and
-        even shards on CUDA): every rank maps the other ranks' position buffers (CUDA IPC
-        over NVLink, exchanged through the process group) and the polish epilogue writes
-        each new record into all of them (spk_polish_shots peer_pos4), so no separate
-        all-gather runs.  The first exchange of every level is checked against an NCCL
-        all-gather; any mismatch falls back to the all-gather for the rest of the run."""
+        even shards on CUDA): every rank maps the other ranks' position buffers (CUDA IPC,
+        opened on this rank's device so its kernels write over NVLink) and the polish
+        epilogue writes each new record into all of them (spk_polish_shots peer_pos4), so
+        no separate all-gather runs.  Every rank must succeed or all use the all-gather;
+        the first exchange of every level is also checked against an NCCL all-gather, and
+        a mismatch falls back to the all-gather for the rest of the run."""
+        for ptr in getattr(self, "_peer_ptrs", []):
+            _native.call("spk_ipc_close", ctypes.c_void_p(ptr))
+        self._peer_ptrs = []
         self.peers = None
         env = os.environ.get("SPK_P2P_GATHER")
         if (self.world == 1 or not self.even or not self.coords.is_cuda or env == "0"
                 or getattr(self, "_p2p_failed", False)):
             return
-        from torch.multiprocessing.reductions import reduce_tensor
-
-        mine = reduce_tensor(self.pos4_all)
+        ok = 1.0
+        mine = None
+        try:
+            info = self.pos4_all.untyped_storage()._share_cuda_()
+            off = int(info[3]) + self.pos4_all.storage_offset() * self.pos4_all.element_size()
+            raw = bytes(info[1])
+            # torch's shareable handle: [version, b"c" (cudaMalloc block)] + the 64-byte
+            # cudaIpcMemHandle_t; other kinds (expandable segments) are not IPC handles
+            if len(raw) == 66 and raw[1:2] == b"c":
+                raw = raw[2:]
+            if len(raw) != 64:
+                raise ValueError("not a cudaIpcMemHandle")
+            mine = (raw, off)
+        except Exception:  # noqa: BLE001 -- any failure means: use the all-gather
+            ok = 0.0
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=self.group)
-        opened = []
-        for r, (fn, args) in enumerate(allh):
-            if r != self.rank:
-                opened.append(fn(*args))
-        self._peer_bufs = opened  # keeps the IPC mappings alive for this level
-        table = torch.tensor([t.data_ptr() for t in opened], dtype=torch.int64,
-                             device=self.coords.device)
-        self.peers = (table, len(opened), self.offsets[self.rank] * self.n_s)
+        addrs = []
+        if ok and all(h is not None for h in allh):
+            try:
+                for r, (handle, off) in enumerate(allh):
+                    if r == self.rank:
+                        continue
+                    ptr = ctypes.c_void_p()
+                    _native.call("spk_ipc_open", handle, ctypes.byref(ptr))
+                    self._peer_ptrs.append(ptr.value)
+                    addrs.append(ptr.value + off)
+            except Exception:  # noqa: BLE001
+                ok = 0.0
+        else:
+            ok = 0.0
+        flag = torch.tensor([ok], device=self.coords.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if flag.item() != 1.0:
+            for ptr in self._peer_ptrs:
+                _native.call("spk_ipc_close", ctypes.c_void_p(ptr))
+            self._peer_ptrs = []
+            self._p2p_failed = True
+            return
+        table = torch.tensor(addrs, dtype=torch.int64, device=self.coords.device)
+        self.peers = (table, len(addrs), self.offsets[self.rank] * self.n_s)
         self._p2p_verified = False
 
     def _exchanged(self):
