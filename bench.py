@@ -607,7 +607,7 @@ def measure_exact(args, ctx, steps, warmup, with_e2e, with_cpu):
     del run, ops
     torch.cuda.empty_cache()
     if with_e2e:
-        rec["e2e"] = run_e2e_step_api(ctx, cfg, fld, steps)
+        rec["e2e"] = run_e2e_step_api(ctx, cfg, fld, max(1, min(steps, args.e2e_steps)))
         if not ctx.dist:
             rec["e2e_numpy_api"] = run_e2e(args, spk, fld, pcfg, steps)
     del fld
